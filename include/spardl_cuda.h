@@ -1,0 +1,205 @@
+/*
+ * spardl_cuda.h -- the C ABI of the B200-native SparDL sparse All-Reduce.
+ *
+ * This is the drop-in boundary for the reference's hot path, the C++ API of
+ * /root/reference/proj/include/spardl (abbreviated `inc/`).  Every entry
+ * point names the reference interface it replaces.  Plain pointers and sizes
+ * only; no C++ or torch types.  All functions return a status (SPARDL_OK or
+ * one SPARDL_E_* per reference exception class, inc/error.hpp:23-75) and set
+ * a thread-local message readable with spardl_last_error(); the message text
+ * of every reference error is reproduced verbatim.
+ *
+ * Threading/ownership: a context (spardl_ctx) belongs to one process and one
+ * CUDA device and hosts a contiguous range of the P logical workers
+ * ("local workers").  P workers may live on 1..P devices (P % world_size == 0);
+ * the reference's single-call-drives-all-workers semantics
+ * (inc/pipeline.hpp:140-142) is the world_size == 1 case.  Workers on other
+ * devices are reached over NVLink through NCCL point-to-point rounds.
+ *
+ * The hot path never falls back to the CPU: without a usable sm_100 device
+ * spardl_ctx_create fails with SPARDL_E_CUDA.
+ */
+#ifndef SPARDL_CUDA_H_
+#define SPARDL_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPARDL_ABI_VERSION 1
+
+/* status codes -- one per reference exception class (inc/error.hpp) */
+#define SPARDL_OK 0
+#define SPARDL_E_ERROR 1            /* spardl::error                 error.hpp:23 */
+#define SPARDL_E_PARTITION 2        /* spardl::partition_error       error.hpp:29 */
+#define SPARDL_E_BLOCK_MISMATCH 3   /* spardl::block_mismatch_error  error.hpp:35 */
+#define SPARDL_E_SCHEDULE 4         /* spardl::schedule_violation_error error.hpp:41 */
+#define SPARDL_E_THEOREM 5          /* spardl::theorem_violation_error  error.hpp:47 */
+#define SPARDL_E_GROUP_SIZE 6       /* spardl::group_size_error      error.hpp:53 */
+#define SPARDL_E_CONFIG 7           /* spardl::config_error          error.hpp:60 */
+#define SPARDL_E_STATE 8            /* spardl::state_error           error.hpp:66 */
+#define SPARDL_E_CONSISTENCY 9      /* spardl::consistency_error     error.hpp:72 */
+#define SPARDL_E_CUDA 100           /* device / runtime failure (no reference analogue) */
+#define SPARDL_E_NCCL 101           /* transport failure */
+#define SPARDL_E_ARG 102            /* invalid pointer / size argument */
+#define SPARDL_E_UNSUPPORTED 103    /* configuration outside the device envelope */
+
+/* enums of inc/sag.hpp:272, inc/residual.hpp:37, inc/reduce_scatter.hpp:34 */
+#define SPARDL_SAG_NONE 0
+#define SPARDL_SAG_RSAG 1
+#define SPARDL_SAG_BSAG 2
+#define SPARDL_RES_GRES 0
+#define SPARDL_RES_PRES 1
+#define SPARDL_RES_LRES 2
+#define SPARDL_TIMING_OPTIMIZED 0
+#define SPARDL_TIMING_NAIVE 1
+
+/* spardl::ClusterConfig, inc/pipeline.hpp:39-52 (field for field) */
+typedef struct spardl_config {
+  int64_t workers;   /* P */
+  int64_t dimension; /* N */
+  int64_t k;         /* total selection count */
+  int64_t teams;     /* d */
+  int32_t sag;       /* SPARDL_SAG_* */
+  int32_t residual;  /* SPARDL_RES_* */
+  int32_t timing;    /* SPARDL_TIMING_* */
+  int32_t pad_;
+  uint64_t seed;
+} spardl_config;
+
+/* spardl::RunResult scalars, inc/pipeline.hpp:115-127 */
+typedef struct spardl_run_info {
+  int32_t consistent;
+  int32_t conservation_applicable;
+  double conservation_error;   /* computed only when audit is enabled, else -1 */
+  int64_t max_rounds, max_scalars;            /* LedgerReport, fabric.hpp:41-45 */
+  int64_t srs_rounds, srs_scalars;            /* srs_phase */
+  int64_t sag_rounds, sag_scalars;            /* sag_phase */
+  int64_t gather_rounds, gather_scalars;      /* gather_phase */
+  int64_t pred_rounds, pred_low, pred_high;   /* predicted, sag.hpp:283-289 */
+  int64_t n_union;                            /* union_sizes.size() */
+  int64_t global_nnz;
+} spardl_run_info;
+
+/* spardl::HController state, inc/sag.hpp:37-90 */
+typedef struct spardl_hctrl {
+  double lower, upper;
+  int64_t target;
+  double h, step;
+  int32_t flag;
+  int32_t pad_;
+} spardl_hctrl;
+
+typedef struct spardl_ctx spardl_ctx;
+
+const char* spardl_last_error(void);
+int spardl_abi_version(void);
+
+/* ------------------------------------------------------------------ */
+/* host-side schedule logic (no GPU needed)                            */
+/* ------------------------------------------------------------------ */
+/* validate(ClusterConfig), inc/pipeline.hpp:54-78 */
+int spardl_validate(const spardl_config* cfg);
+/* partition(N, B), inc/sparse.hpp:98-117: lo[B], hi[B] */
+int spardl_partition(int64_t n, int32_t count, int64_t* lo, int64_t* hi);
+/* BlockPartition::block_of, inc/sparse.hpp:88-95 */
+int spardl_block_of(int64_t n, int32_t count, int64_t i, int32_t* block);
+/* build_bags(m, rank), inc/reduce_scatter.hpp:51-74.
+ * bag_size[l] receives |B_1..B_l|, positions[m-1] the bags concatenated. */
+int spardl_build_bags(int32_t m, int32_t rank, int32_t* l, int32_t* remainder,
+                      int32_t* bag_size, int32_t* positions);
+/* expected_cost_srs, inc/reduce_scatter.hpp:257-262 */
+int spardl_expected_cost_srs(int64_t m, int64_t k, int64_t* rounds, int64_t* scalars);
+/* expected_cost_sag, inc/sag.hpp:295-329 (mode = SPARDL_SAG_*) */
+int spardl_expected_cost_sag(int64_t P, int64_t k, int64_t d, int32_t mode, int64_t* rounds,
+                             int64_t* low, int64_t* high);
+/* bsag_phase_cost, inc/sag.hpp:332-340 */
+int spardl_bsag_phase_cost(int64_t P, int64_t k, int64_t d, int64_t* rounds, int64_t* low,
+                           int64_t* high);
+/* topka_cost, inc/sag.hpp:343-346 */
+int spardl_topka_cost(int64_t P, int64_t k, int64_t* rounds, int64_t* low, int64_t* high);
+/* dyadic_shares, inc/sag.hpp:108-118 */
+int spardl_dyadic_shares(int32_t count, double* out);
+/* HController ctor / observe / budget, inc/sag.hpp:40-81 */
+int spardl_hctrl_init(spardl_hctrl* c, int64_t P, int64_t k, int64_t d);
+int spardl_hctrl_observe(spardl_hctrl* c, int64_t n_t);
+int spardl_hctrl_budget(const spardl_hctrl* c, int64_t* budget);
+
+/* ------------------------------------------------------------------ */
+/* device components (device pointers; enqueued on `stream`, then      */
+/* synchronised because the output sizes are returned to the host)     */
+/* ------------------------------------------------------------------ */
+/* top_k_select, inc/sparse.hpp:136-162: n index-sorted entries in; the
+ * selected and discarded entries out, each index-sorted.  Output arrays
+ * must hold n entries; dis_* may be NULL. */
+int spardl_topk_select(const int32_t* idx, const float* val, int64_t n, int64_t budget,
+                       int32_t* sel_idx, float* sel_val, int64_t* n_sel, int32_t* dis_idx,
+                       float* dis_val, int64_t* n_dis, void* stream);
+/* top_k_select_slice, inc/sparse.hpp:167-177: dense values g[lo..hi) */
+int spardl_topk_select_slice(const float* g, int64_t lo, int64_t hi, int64_t budget,
+                             int32_t* sel_idx, float* sel_val, int64_t* n_sel, void* stream);
+/* r-fold merge_add, inc/sparse.hpp:182-208: out = ((l0 + l1) + l2) ... ;
+ * out arrays hold sum(n_t) entries. */
+int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* const* val,
+                     const int64_t* n, int32_t* out_idx, float* out_val, int64_t* n_out,
+                     void* stream);
+
+/* ------------------------------------------------------------------ */
+/* the pipeline: spardl_all_reduce, inc/pipeline.hpp:140-342           */
+/* ------------------------------------------------------------------ */
+/* NCCL rendezvous for multi-process contexts: rank 0 creates the id and
+ * the caller broadcasts its 128 bytes (e.g. with torch.distributed). */
+int spardl_nccl_unique_id(void* out128);
+
+/* make_worker_states + Fabric(P), inc/pipeline.hpp:87-99 / fabric.hpp:54.
+ * device: CUDA ordinal; world_size/rank: processes sharing the P workers
+ * (world_size 1 => all workers local, nccl_id ignored); stream: cudaStream_t
+ * the work is enqueued on (NULL: a context-owned stream). */
+int spardl_ctx_create(const spardl_config* cfg, int32_t device, int32_t world_size,
+                      int32_t rank, const void* nccl_id, void* stream, spardl_ctx** out);
+int spardl_ctx_destroy(spardl_ctx* ctx);
+/* first global worker id and count of the workers hosted by this context */
+int spardl_ctx_local_workers(const spardl_ctx* ctx, int32_t* first, int32_t* count);
+/* enable (1) / disable (0) CUDA-graph replay of the whole iteration */
+int spardl_ctx_set_graph(spardl_ctx* ctx, int32_t enable);
+/* enable the sparse conservation audit (inc/pipeline.hpp:305-334) */
+int spardl_ctx_set_audit(spardl_ctx* ctx, int32_t enable);
+
+/* One synchronisation: grads[i] is local worker i's dense fp32 gradient
+ * (device pointer, N floats, 16-byte aligned).  Enqueued asynchronously. */
+int spardl_allreduce(spardl_ctx* ctx, const float* const* grads_dev);
+/* Same, with HOST gradients (pinned or pageable): the copies in and the
+ * result copy out are part of the call (the reference's host signature). */
+int spardl_allreduce_host(spardl_ctx* ctx, const float* const* grads_host, int64_t* g_idx,
+                          float* g_val, int64_t cap, int64_t* nnz);
+/* wait for the enqueued work; reports device-side errors (NaN input) */
+int spardl_sync(spardl_ctx* ctx);
+/* RunResult scalars of the last call (synchronises; collective when
+ * world_size > 1: every rank must call it) */
+int spardl_get_run_info(spardl_ctx* ctx, spardl_run_info* out);
+/* device view of local worker i's GlobalSparseGradient (valid until the
+ * next call); *nnz needs a sync, so this synchronises */
+int spardl_get_global(spardl_ctx* ctx, int32_t local_worker, const int32_t** idx,
+                      const float** val, int64_t* nnz);
+/* WorkerState::residual.carry() of local worker i (device, N floats) */
+int spardl_get_carry(spardl_ctx* ctx, int32_t local_worker, float** carry_dev);
+/* reset residuals / controllers / ledger to the make_worker_states state */
+int spardl_ctx_reset_state(spardl_ctx* ctx);
+/* Fabric::ledger(), fabric.hpp:110: per GLOBAL worker (P entries); collective */
+int spardl_get_ledger(spardl_ctx* ctx, int64_t* rounds, int64_t* scalars);
+/* RunResult::union_sizes (B-SAG N_t per position group; n_union entries) */
+int spardl_get_union_sizes(spardl_ctx* ctx, int64_t* out);
+/* WorkerState::controller of local worker i (B-SAG only) */
+int spardl_get_controller(spardl_ctx* ctx, int32_t local_worker, spardl_hctrl* out);
+/* number of kernels this context launches per iteration */
+int spardl_kernel_launches(const spardl_ctx* ctx, int64_t* per_iteration);
+/* the stream the context enqueues on (cudaStream_t) */
+int spardl_ctx_stream(const spardl_ctx* ctx, void** stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARDL_CUDA_H_ */

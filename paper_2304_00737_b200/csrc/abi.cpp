@@ -1,0 +1,560 @@
+// extern "C" boundary of libspardl_cuda.so (declared in include/spardl_cuda.h).
+// Every entry point catches the internal exceptions and returns the status
+// code of the reference exception class; the message is kept per thread.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "host.hpp"
+#include "kernels.cuh"
+#include "spardl_cuda.h"
+
+#define EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+thread_local std::string g_msg;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    g_msg.clear();
+    f();
+    return SPARDL_OK;
+  } catch (const sdlh::Error& e) {
+    g_msg = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_msg = "host out of memory";
+    return SPARDL_E_ERROR;
+  } catch (const std::exception& e) {
+    g_msg = e.what();
+    return SPARDL_E_ERROR;
+  }
+}
+
+#define CK(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      sdlh::fail(SPARDL_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+void need(const void* p, const char* what) {
+  if (!p) sdlh::fail(SPARDL_E_ARG, std::string("null argument: ") + what);
+}
+
+// scoped device allocations for the one-shot component entry points
+struct DevBuf {
+  std::vector<void*> ptrs;
+  ~DevBuf() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)));
+    CK(cudaMemset(p, 0, std::max<size_t>(n * sizeof(T), 16)));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    sdlh::fail(SPARDL_E_CUDA, "no CUDA device: the SparDL device path has no CPU fallback");
+}
+
+// One select over prepared inputs, with its scratch.
+void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf) {
+  const int nseg = std::max(std::max(t.nseg, t.dnseg), 1);
+  t.scr = buf.get<sdl::SelScratch>(1);
+  int32_t* segs = buf.get<int32_t>(5 * static_cast<size_t>(nseg));
+  t.seg_gt = segs;
+  t.seg_eq = segs + nseg;
+  t.seg_sel_off = segs + 2 * nseg;
+  t.seg_dis_off = segs + 3 * nseg;
+  t.seg_take = segs + 4 * nseg;
+  sdl::SelTask* td = buf.get<sdl::SelTask>(1);
+  CK(cudaMemcpyAsync(td, &t, sizeof(t), cudaMemcpyHostToDevice, s));
+  sdl::launch_select(td, 1, nseg, s);
+  CK(cudaGetLastError());
+}
+
+}  // namespace
+
+EXPORT const char* spardl_last_error(void) { return g_msg.c_str(); }
+EXPORT int spardl_abi_version(void) { return SPARDL_ABI_VERSION; }
+
+// ---------------------------------------------------------------------------
+// host schedule logic
+EXPORT int spardl_validate(const spardl_config* cfg) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    sdlh::validate(*cfg);
+  });
+}
+
+EXPORT int spardl_partition(int64_t n, int32_t count, int64_t* lo, int64_t* hi) {
+  return guarded([&] {
+    const auto p = sdlh::partition(n, count);
+    for (int b = 0; b < count; ++b) {
+      lo[b] = p.lo[static_cast<size_t>(b)];
+      hi[b] = p.hi[static_cast<size_t>(b)];
+    }
+  });
+}
+
+EXPORT int spardl_block_of(int64_t n, int32_t count, int64_t i, int32_t* block) {
+  return guarded([&] {
+    const auto p = sdlh::partition(n, count);
+    if (i < 0 || i >= n) sdlh::fail(SPARDL_E_ARG, "index outside [0, N)");
+    *block = p.block_of(i);
+  });
+}
+
+EXPORT int spardl_build_bags(int32_t m, int32_t rank, int32_t* l, int32_t* remainder,
+                             int32_t* bag_size, int32_t* positions) {
+  return guarded([&] {
+    const auto s = sdlh::build_bags(m, rank);
+    *l = s.l;
+    *remainder = s.remainder;
+    int o = 0;
+    for (size_t j = 0; j < s.bags.size(); ++j) {
+      bag_size[j] = static_cast<int32_t>(s.bags[j].size());
+      for (int p : s.bags[j]) positions[o++] = p;
+    }
+  });
+}
+
+EXPORT int spardl_expected_cost_srs(int64_t m, int64_t k, int64_t* rounds, int64_t* scalars) {
+  return guarded([&] {   // inc/reduce_scatter.hpp:257-262
+    if (m < 1) sdlh::fail(SPARDL_E_CONFIG, "expected_cost_srs: m >= 1 required");
+    if (k % m != 0) sdlh::fail(SPARDL_E_CONFIG, "expected_cost_srs: m must divide k");
+    if (m == 1) {
+      *rounds = 0;
+      *scalars = 0;
+    } else {
+      *rounds = sdlh::ceil_log2(m);
+      *scalars = 2 * (k / m) * (m - 1);
+    }
+  });
+}
+
+EXPORT int spardl_expected_cost_sag(int64_t P, int64_t k, int64_t d, int32_t mode,
+                                    int64_t* rounds, int64_t* low, int64_t* high) {
+  return guarded([&] { sdlh::expected_cost_sag(P, k, d, mode, rounds, low, high); });
+}
+
+EXPORT int spardl_bsag_phase_cost(int64_t P, int64_t k, int64_t d, int64_t* rounds,
+                                  int64_t* low, int64_t* high) {
+  return guarded([&] {   // inc/sag.hpp:332-340
+    if (d < 2 || P % d != 0 || k % P != 0)
+      sdlh::fail(SPARDL_E_CONFIG, "bsag_phase_cost: invalid (P, k, d)");
+    const int64_t c = k / P;
+    *rounds = sdlh::ceil_log2(d);
+    *low = 2 * c * (d - 1);
+    *high = 2 * c * d * (d - 1);
+  });
+}
+
+EXPORT int spardl_topka_cost(int64_t P, int64_t k, int64_t* rounds, int64_t* low,
+                             int64_t* high) {
+  return guarded([&] {   // inc/sag.hpp:343-346
+    const int64_t sc = 2 * (P - 1) * k;
+    *rounds = sdlh::ceil_log2(P);
+    *low = *high = sc;
+  });
+}
+
+EXPORT int spardl_dyadic_shares(int32_t count, double* out) {
+  return guarded([&] {
+    const auto s = sdlh::dyadic_shares(count);
+    for (size_t i = 0; i < s.size(); ++i) out[i] = s[i];
+  });
+}
+
+EXPORT int spardl_hctrl_init(spardl_hctrl* c, int64_t P, int64_t k, int64_t d) {
+  return guarded([&] {
+    need(c, "controller");
+    sdlh::hctrl_init(c, P, k, d);
+  });
+}
+
+EXPORT int spardl_hctrl_observe(spardl_hctrl* c, int64_t n_t) {
+  return guarded([&] {
+    need(c, "controller");
+    sdlh::hctrl_observe(c, n_t);
+  });
+}
+
+EXPORT int spardl_hctrl_budget(const spardl_hctrl* c, int64_t* budget) {
+  return guarded([&] {
+    need(c, "controller");
+    *budget = sdlh::hctrl_budget(c);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// device components
+EXPORT int spardl_topk_select(const int32_t* idx, const float* val, int64_t n, int64_t budget,
+                              int32_t* sel_idx, float* sel_val, int64_t* n_sel,
+                              int32_t* dis_idx, float* dis_val, int64_t* n_dis, void* stream) {
+  return guarded([&] {   // inc/sparse.hpp:136-162
+    require_device();
+    if (budget < 0) sdlh::fail(SPARDL_E_ERROR, "top_k_select: negative budget");
+    if (n < 0 || n >= (int64_t(1) << 31)) sdlh::fail(SPARDL_E_ARG, "n out of range");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DevBuf buf;
+    int32_t* cnt = buf.get<int32_t>(3);
+    const int32_t n32 = static_cast<int32_t>(n);
+    CK(cudaMemcpyAsync(cnt, &n32, sizeof(n32), cudaMemcpyHostToDevice, s));
+    sdl::SelTask t{};
+    t.mode = 0;
+    t.idx = idx;
+    t.val = val;
+    t.count = cnt;
+    t.stride = 2048;
+    t.nseg = static_cast<int32_t>((n + 2047) / 2048);
+    t.budget = budget;
+    t.sel_idx = sel_idx;
+    t.sel_val = sel_val;
+    t.sel_cnt = cnt + 1;
+    t.dis_idx = dis_idx;
+    t.dis_val = dis_val;
+    t.dis_cnt = dis_idx ? cnt + 2 : nullptr;
+    t.weight = 1.f;
+    if (n > 0) run_select(t, s, buf);
+    int32_t out[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(out, cnt, sizeof(out), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *n_sel = out[1];
+    if (n_dis) *n_dis = dis_idx ? out[2] : n - out[1];
+  });
+}
+
+EXPORT int spardl_topk_select_slice(const float* g, int64_t lo, int64_t hi, int64_t budget,
+                                    int32_t* sel_idx, float* sel_val, int64_t* n_sel,
+                                    void* stream) {
+  return guarded([&] {   // inc/sparse.hpp:167-177, through the dividing kernels
+    require_device();
+    if (budget < 0) sdlh::fail(SPARDL_E_ERROR, "top_k_select: negative budget");
+    if (lo < 0 || hi < lo || hi >= (int64_t(1) << 31)) sdlh::fail(SPARDL_E_ARG, "bad range");
+    if (reinterpret_cast<uintptr_t>(g) % 16 != 0)
+      sdlh::fail(SPARDL_E_ARG, "slice base must be 16-byte aligned");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t nb = hi - lo;
+    if (nb == 0) {
+      *n_sel = 0;
+      return;
+    }
+    DevBuf buf;
+    const int64_t A = lo & ~int64_t(3);
+    const int nch = static_cast<int>((hi - A + sdl::kChunk - 1) / sdl::kChunk);
+    const double frac = static_cast<double>(budget) / static_cast<double>(nb);
+    int cap = static_cast<int>(
+        std::min<double>(sdl::kChunk, std::max(1024.0, sdl::kChunk * 2.5 * frac + 256.0)));
+    cap = (cap + 3) & ~3;
+    sdl::DivTask dt{};
+    dt.carry = const_cast<float*>(g);   // read only when apply_residual == 0
+    dt.lo = static_cast<int32_t>(lo);
+    dt.hi = static_cast<int32_t>(hi);
+    dt.nchunks = nch;
+    dt.cap = cap;
+    dt.budget = budget;
+    dt.use_cand = frac <= 0.25 ? 1 : 0;
+    const size_t ncand = static_cast<size_t>(nch) * cap;
+    dt.cand_idx = buf.get<int32_t>(ncand);
+    dt.cand_val = buf.get<float>(ncand);
+    dt.cand_cnt = buf.get<int32_t>(nch);
+    dt.cand_total = buf.get<int64_t>(1);
+    dt.cand_bad = buf.get<int32_t>(1);
+    dt.pre_key = buf.get<uint32_t>(1);
+    dt.samp_hist = buf.get<uint32_t>(sdl::kBins);
+    dt.sample_every = std::max(1, nch / 32);
+    dt.err = buf.get<int32_t>(1);
+    sdl::DivTask* dtd = buf.get<sdl::DivTask>(1);
+    CK(cudaMemcpyAsync(dtd, &dt, sizeof(dt), cudaMemcpyHostToDevice, s));
+    sdl::launch_divide(dtd, 1, nch, dt.sample_every, 0, s);
+    int32_t* cnt = buf.get<int32_t>(1);
+    sdl::SelTask t{};
+    t.mode_from_cand = 1;
+    t.idx = dt.cand_idx;
+    t.val = dt.cand_val;
+    t.seg_cnt = dt.cand_cnt;
+    t.stride = cap;
+    t.nseg = nch;
+    t.dval = g + lo;
+    t.dbase = static_cast<int32_t>(lo);
+    t.dn = static_cast<int32_t>(nb);
+    t.dstride = sdl::kChunk;
+    t.dnseg = static_cast<int32_t>((nb + sdl::kChunk - 1) / sdl::kChunk);
+    t.cand_total = dt.cand_total;
+    t.cand_bad = dt.cand_bad;
+    t.budget = budget;
+    t.sel_idx = sel_idx;
+    t.sel_val = sel_val;
+    t.sel_cnt = cnt;
+    t.weight = 1.f;
+    run_select(t, s, buf);
+    int32_t out = 0, err = 0;
+    CK(cudaMemcpyAsync(&out, cnt, sizeof(out), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&err, dt.err, sizeof(err), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (err) sdlh::fail(SPARDL_E_ARG, "gradient contains NaN (selection order undefined)");
+    *n_sel = out;
+  });
+}
+
+EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* const* val,
+                            const int64_t* n, int32_t* out_idx, float* out_val, int64_t* n_out,
+                            void* stream) {
+  return guarded([&] {   // inc/sparse.hpp:182-208 folded left over r lists
+    require_device();
+    if (r < 1 || r > sdl::kMaxR) sdlh::fail(SPARDL_E_ARG, "merge_add: 1 <= r <= 16 lists");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DevBuf buf;
+    int32_t* cnts = buf.get<int32_t>(static_cast<size_t>(r) + 1);
+    std::vector<int32_t> hc(static_cast<size_t>(r));
+    int64_t capsum = 0, capmax = 1;
+    for (int q = 0; q < r; ++q) {
+      hc[static_cast<size_t>(q)] = static_cast<int32_t>(n[q]);
+      capsum += n[q];
+      capmax = std::max<int64_t>(capmax, n[q]);
+    }
+    CK(cudaMemcpyAsync(cnts, hc.data(), sizeof(int32_t) * r, cudaMemcpyHostToDevice, s));
+    sdl::MergeTask mt{};
+    mt.r = r;
+    for (int q = 0; q < r; ++q) {
+      mt.in_idx[q] = idx[q];
+      mt.in_val[q] = val[q];
+      mt.in_cnt[q] = cnts + q;
+    }
+    int64_t T = std::max<int64_t>(8192 / r, (capsum + sdl::kMaxSamples - 1) / sdl::kMaxSamples);
+    T = std::max<int64_t>(T, 32);
+    if (static_cast<int64_t>(r) * T > 12800)
+      sdlh::fail(SPARDL_E_UNSUPPORTED, "merge of this size exceeds the shared-memory envelope");
+    mt.T = static_cast<int32_t>(T);
+    int64_t parts = 0;
+    for (int q = 0; q < r; ++q) parts += (n[q] + T - 1) / T;
+    parts = std::max<int64_t>(parts, 1);
+    mt.max_parts = static_cast<int32_t>(parts);
+    mt.splitters = buf.get<int32_t>(parts + 1);
+    mt.windows = buf.get<int32_t>(parts * r);
+    mt.nparts = buf.get<int32_t>(1);
+    mt.out_idx = buf.get<int32_t>(std::max<int64_t>(capsum, 1));
+    mt.out_val = buf.get<float>(std::max<int64_t>(capsum, 1));
+    mt.seg_off = buf.get<int32_t>(parts);
+    mt.seg_cnt = buf.get<int32_t>(parts);
+    sdl::MergeTask* mtd = buf.get<sdl::MergeTask>(1);
+    CK(cudaMemcpyAsync(mtd, &mt, sizeof(mt), cudaMemcpyHostToDevice, s));
+    sdl::launch_merge(mtd, 1, static_cast<int>(parts), static_cast<int>(r * T), s);
+    sdl::SelTask t{};
+    t.mode = 0;
+    t.idx = mt.out_idx;
+    t.val = mt.out_val;
+    t.seg_off = mt.seg_off;
+    t.seg_cnt = mt.seg_cnt;
+    t.nseg = static_cast<int32_t>(parts);
+    t.budget = INT64_MAX;   // identity selection == ordered compaction
+    t.sel_idx = out_idx;
+    t.sel_val = out_val;
+    t.sel_cnt = cnts + r;
+    t.weight = 1.f;
+    run_select(t, s, buf);
+    int32_t out = 0;
+    CK(cudaMemcpyAsync(&out, cnts + r, sizeof(out), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *n_out = out;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// pipeline context
+struct spardl_ctx {
+  std::unique_ptr<sdle::Engine> eng;
+  std::vector<float*> staging;     // device copies of host gradients (allreduce_host)
+  std::vector<const float*> staging_c;
+};
+
+EXPORT int spardl_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    need(out128, "out");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) sdlh::fail(SPARDL_E_NCCL, ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+EXPORT int spardl_ctx_create(const spardl_config* cfg, int32_t device, int32_t world_size,
+                             int32_t rank, const void* nccl_id, void* stream, spardl_ctx** out) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(out, "out");
+    *out = nullptr;
+    auto c = std::make_unique<spardl_ctx>();
+    c->eng = std::make_unique<sdle::Engine>(*cfg, device, world_size, rank, nccl_id,
+                                            static_cast<cudaStream_t>(stream));
+    *out = c.release();
+  });
+}
+
+EXPORT int spardl_ctx_destroy(spardl_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    for (float* p : ctx->staging) cudaFree(p);
+    delete ctx;
+  });
+}
+
+EXPORT int spardl_ctx_local_workers(const spardl_ctx* ctx, int32_t* first, int32_t* count) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    *first = ctx->eng->first_worker();
+    *count = ctx->eng->local_workers();
+  });
+}
+
+EXPORT int spardl_ctx_set_graph(spardl_ctx* ctx, int32_t enable) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->set_graph(enable != 0);
+  });
+}
+
+EXPORT int spardl_ctx_set_audit(spardl_ctx* ctx, int32_t enable) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->set_audit(enable != 0);
+  });
+}
+
+EXPORT int spardl_allreduce(spardl_ctx* ctx, const float* const* grads_dev) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(grads_dev, "grads");
+    ctx->eng->run(grads_dev);
+  });
+}
+
+EXPORT int spardl_allreduce_host(spardl_ctx* ctx, const float* const* grads_host,
+                                 int64_t* g_idx, float* g_val, int64_t cap, int64_t* nnz) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(grads_host, "grads");
+    auto& e = *ctx->eng;
+    const int wl = e.local_workers();
+    const size_t bytes = sizeof(float) * static_cast<size_t>(e.dimension());
+    if (ctx->staging.empty()) {
+      for (int i = 0; i < wl; ++i) {
+        float* p = nullptr;
+        CK(cudaMalloc(&p, bytes));
+        ctx->staging.push_back(p);
+        ctx->staging_c.push_back(p);
+      }
+    }
+    cudaStream_t s = e.stream();
+    for (int i = 0; i < wl; ++i) {
+      need(grads_host[i], "grads[i]");
+      CK(cudaMemcpyAsync(ctx->staging[static_cast<size_t>(i)], grads_host[i], bytes,
+                         cudaMemcpyHostToDevice, s));
+    }
+    e.run(ctx->staging_c.data());
+    const int32_t* di = nullptr;
+    const float* dv = nullptr;
+    int64_t n = 0;
+    e.global(0, &di, &dv, &n);   // synchronises
+    *nnz = n;
+    if (g_idx && g_val) {
+      if (cap < n) sdlh::fail(SPARDL_E_ARG, "output capacity below the global nnz");
+      std::vector<int32_t> tmp(static_cast<size_t>(n));
+      CK(cudaMemcpyAsync(tmp.data(), di, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(g_val, dv, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int64_t q = 0; q < n; ++q) g_idx[q] = tmp[static_cast<size_t>(q)];
+    }
+  });
+}
+
+EXPORT int spardl_sync(spardl_ctx* ctx) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->sync();
+  });
+}
+
+EXPORT int spardl_get_run_info(spardl_ctx* ctx, spardl_run_info* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    *out = ctx->eng->run_info();
+  });
+}
+
+EXPORT int spardl_get_global(spardl_ctx* ctx, int32_t local_worker, const int32_t** idx,
+                             const float** val, int64_t* nnz) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (local_worker < 0 || local_worker >= ctx->eng->local_workers())
+      sdlh::fail(SPARDL_E_ARG, "local worker out of range");
+    ctx->eng->global(local_worker, idx, val, nnz);
+  });
+}
+
+EXPORT int spardl_get_carry(spardl_ctx* ctx, int32_t local_worker, float** carry_dev) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (local_worker < 0 || local_worker >= ctx->eng->local_workers())
+      sdlh::fail(SPARDL_E_ARG, "local worker out of range");
+    *carry_dev = ctx->eng->carry(local_worker);
+  });
+}
+
+EXPORT int spardl_ctx_reset_state(spardl_ctx* ctx) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->reset_state();
+  });
+}
+
+EXPORT int spardl_get_ledger(spardl_ctx* ctx, int64_t* rounds, int64_t* scalars) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->ledger(rounds, scalars);
+  });
+}
+
+EXPORT int spardl_get_union_sizes(spardl_ctx* ctx, int64_t* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->union_sizes(out);
+  });
+}
+
+EXPORT int spardl_get_controller(spardl_ctx* ctx, int32_t local_worker, spardl_hctrl* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->controller(local_worker, out);
+  });
+}
+
+EXPORT int spardl_kernel_launches(const spardl_ctx* ctx, int64_t* per_iteration) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    *per_iteration = ctx->eng->launches_per_iter();
+  });
+}
+
+EXPORT int spardl_ctx_stream(const spardl_ctx* ctx, void** stream) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    *stream = static_cast<void*>(ctx->eng->stream());
+  });
+}

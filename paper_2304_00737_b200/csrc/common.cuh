@@ -1,0 +1,116 @@
+// Small device helpers shared by the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sdl {
+
+// Magnitude key: |v| ordering == unsigned ordering of the low 31 bits for
+// every non-NaN float; +0 and -0 share key 0 (inc/sparse.hpp:122-127 compares
+// fabs values, so they tie and the smaller index wins).
+__device__ __forceinline__ uint32_t mag_key(float v) {
+  return __float_as_uint(v) & 0x7fffffffu;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Exclusive prefix count of a predicate over the whole CTA (blockDim.x a
+// multiple of 32, <= 1024).  `scratch` holds >= 33 ints.  Returns the
+// exclusive rank of this thread; *total receives the CTA-wide count.
+__device__ __forceinline__ int block_rank(bool pred, int* scratch, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const uint32_t b = __ballot_sync(0xffffffffu, pred);
+  const int in_warp = __popc(b & lanemask_lt());
+  if (lane == 0) scratch[warp] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int v = threadIdx.x < nwarps ? scratch[threadIdx.x] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += n;
+    }
+    if (threadIdx.x < nwarps) scratch[threadIdx.x] = inc - v;
+    if (threadIdx.x == 31) scratch[32] = inc;
+  }
+  __syncthreads();
+  const int r = scratch[warp] + in_warp;
+  *total = scratch[32];
+  __syncthreads();
+  return r;
+}
+
+// Exclusive prefix sum of an int over the CTA.
+__device__ __forceinline__ int block_exscan(int v, int* scratch, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += n;
+  }
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int w = threadIdx.x < nwarps ? scratch[threadIdx.x] : 0;
+    int winc = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, winc, o);
+      if (lane >= o) winc += n;
+    }
+    if (threadIdx.x < nwarps) scratch[threadIdx.x] = winc - w;
+    if (threadIdx.x == 31) scratch[32] = winc;
+  }
+  __syncthreads();
+  const int r = scratch[warp] + inc - v;
+  *total = scratch[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  long long t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < nwarps; ++w) t += scratch[w];
+  __syncthreads();
+  if (threadIdx.x == 0) scratch[0] = t;
+  __syncthreads();
+  t = scratch[0];
+  __syncthreads();
+  return t;
+}
+
+// lower_bound over a sorted int array [a, a+n)
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int upper_bound_i32(const int32_t* a, int n, int32_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace sdl

@@ -1,0 +1,245 @@
+// The dividing pass: residual add fused with candidate compaction.
+//
+// Semantics (inc/pipeline.hpp:162-184, inc/residual.hpp:63-92):
+//   combined = g + carry            (ResidualStore::apply; this is also G_copy)
+//   per block b: top-L of the dense slice combined[lo_b, hi_b) (zeros count)
+// Layout: the residual buffer IS G_copy -- `carry` is overwritten in place by
+// g + carry, so the pass moves exactly 12 bytes per element (read g, read
+// carry, write carry) plus the small candidate stream.
+//
+// Kernels:
+//   k_div_sample   one chunk in `sample_every`: histogram of the top 11 key bits
+//                  of g + carry (read only)
+//   k_div_prethr   per block: the pre-threshold -- the lower edge of the digit
+//                  holding the sample's ~1.25 L-th largest key
+//   k_div_cand     every chunk: combined = g + carry written back with 128-bit
+//                  stores; entries with key >= pre-threshold compacted, in
+//                  index order, into the chunk's candidate segment
+// The select that follows (select.cu) checks on the device that the
+// candidates are complete (>= L of them, no chunk overflow); otherwise it
+// selects from the dense slice instead, so the result never depends on the
+// sample.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sdl {
+
+namespace {
+
+// chunk c of a task covers [max(lo, A + c*kChunk), min(hi, A + (c+1)*kChunk))
+// with A = lo rounded down to a multiple of 4, so every chunk is made of
+// whole float4 groups of the global array.
+__device__ __forceinline__ int64_t chunk_origin(const DivTask& t) { return (int64_t)(t.lo & ~3); }
+
+__global__ void __launch_bounds__(kThreads) k_div_sample(const DivTask* __restrict__ tasks,
+                                                         int apply_residual) {
+  const DivTask& t = tasks[blockIdx.y];
+  if (!t.use_cand) return;
+  const int c = blockIdx.x * t.sample_every;
+  if (c >= t.nchunks) return;
+  __shared__ uint32_t h[kBins];
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
+  const int64_t s = A > t.lo ? A : t.lo;
+  const int64_t e = (A + kChunk) < t.hi ? (A + kChunk) : t.hi;
+  for (int64_t i = s + threadIdx.x; i < e; i += blockDim.x) {
+    const float v = apply_residual ? __fadd_rn(t.g_tab[t.g_id][i], t.carry[i]) : t.carry[i];
+    atomicAdd(&h[mag_key(v) >> 20], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+    if (h[b]) atomicAdd(&t.samp_hist[b], h[b]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restrict__ tasks) {
+  const DivTask& t = tasks[blockIdx.x];
+  constexpr int BPT = kBins / kThreads;
+  __shared__ long long suf[kThreads];
+  __shared__ long long lscr[32];
+  uint32_t c[BPT];
+  long long mine = 0;
+#pragma unroll
+  for (int q = 0; q < BPT; ++q) {
+    c[q] = t.samp_hist[threadIdx.x * BPT + q];
+    t.samp_hist[threadIdx.x * BPT + q] = 0;
+    mine += c[q];
+  }
+  const long long ns = block_sum_ll(mine, lscr);
+  const int64_t nb = (int64_t)t.hi - t.lo;
+  if (threadIdx.x == 0) {
+    *t.cand_total = 0;
+    *t.cand_bad = t.use_cand ? 0 : 1;
+    *t.pre_key = 0;
+  }
+  if (!t.use_cand || ns == 0) {
+    if (threadIdx.x == 0) *t.cand_bad = 1;
+    return;
+  }
+  // target rank inside the sample: 1.25 L scaled to the sample, plus 4 sigma
+  const double frac = (double)t.budget / (double)nb;
+  const double expect = frac * (double)ns;
+  const long long target = (long long)(1.25 * expect + 4.0 * sqrt(expect + 1.0) + 8.0);
+  if (target >= ns) {
+    if (threadIdx.x == 0) *t.cand_bad = 1;
+    return;
+  }
+  // reverse inclusive scan (Hillis-Steele over descending thread order)
+  const int r = blockDim.x - 1 - threadIdx.x;
+  __shared__ long long vals[kThreads];
+  vals[r] = mine;
+  __syncthreads();
+  suf[threadIdx.x] = vals[threadIdx.x];
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const long long add = threadIdx.x >= (unsigned)o ? suf[threadIdx.x - o] : 0;
+    __syncthreads();
+    suf[threadIdx.x] += add;
+    __syncthreads();
+  }
+  const long long above = r > 0 ? suf[r - 1] : 0;
+  if (above < target && target <= above + mine) {
+    long long cum = above;
+    for (int q = BPT - 1; q >= 0; --q) {
+      if (cum + (long long)c[q] >= target) {
+        *t.pre_key = (uint32_t)(threadIdx.x * BPT + q) << 20;
+        break;
+      }
+      cum += c[q];
+    }
+  }
+}
+
+template <int APPLY>
+__global__ void __launch_bounds__(kThreads) k_div_cand(const DivTask* __restrict__ tasks) {
+  const DivTask& t = tasks[blockIdx.y];
+  const int c = blockIdx.x;
+  if (c >= t.nchunks) return;
+  const bool cand = !(*t.cand_bad);
+  const uint32_t pre = *t.pre_key;
+  const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int ITER = kChunk / (kThreads * 4);   // float4 groups per lane
+  float v[ITER][4];
+  uint32_t mask = 0;
+  bool nan = false;
+  const int64_t lo = t.lo, hi = t.hi;
+  const float* g = APPLY ? t.g_tab[t.g_id] : nullptr;
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
+    if (i0 >= lo && i0 + 4 <= hi) {
+      const float4 gg = APPLY ? __ldcs(reinterpret_cast<const float4*>(g + i0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 cc = __ldcs(reinterpret_cast<const float4*>(t.carry + i0));
+      float4 o;
+      if (APPLY) {
+        o.x = __fadd_rn(gg.x, cc.x);
+        o.y = __fadd_rn(gg.y, cc.y);
+        o.z = __fadd_rn(gg.z, cc.z);
+        o.w = __fadd_rn(gg.w, cc.w);
+        __stcs(reinterpret_cast<float4*>(t.carry + i0), o);
+      } else {
+        o = cc;
+      }
+      v[it][0] = o.x; v[it][1] = o.y; v[it][2] = o.z; v[it][3] = o.w;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t k = mag_key(v[it][e]);
+        nan |= k > 0x7f800000u;
+        if (k >= pre) mask |= 1u << (it * 4 + e);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t i = i0 + e;
+        v[it][e] = 0.f;
+        if (i >= lo && i < hi) {
+          float x = t.carry[i];
+          if (APPLY) {
+            x = __fadd_rn(g[i], x);
+            t.carry[i] = x;
+          }
+          v[it][e] = x;
+          const uint32_t k = mag_key(x);
+          nan |= k > 0x7f800000u;
+          if (k >= pre) mask |= 1u << (it * 4 + e);
+        }
+      }
+    }
+  }
+  if (nan) *t.err = 1;
+  if (!cand) return;
+  // order: (warp, it, lane, e) == index order inside the chunk
+  int lane_excl[ITER];
+  int warp_total = 0;
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int cnt = __popc((mask >> (it * 4)) & 0xfu);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += n;
+    }
+    lane_excl[it] = warp_total + inc - cnt;
+    warp_total += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  __shared__ int wtot[kThreads / 32 + 1];
+  if (lane == 0) wtot[warp] = warp_total;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const int x = wtot[w];
+      wtot[w] = s;
+      s += x;
+    }
+    wtot[kThreads / 32] = s;
+  }
+  __syncthreads();
+  const int total = wtot[kThreads / 32];
+  if (total > t.cap) {
+    if (threadIdx.x == 0) {
+      *t.cand_bad = 1;
+      t.cand_cnt[c] = 0;
+    }
+    return;
+  }
+  const int wbase = wtot[warp];
+  int32_t* ci = t.cand_idx + (size_t)c * t.cap;
+  float* cv = t.cand_val + (size_t)c * t.cap;
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    int p = wbase + lane_excl[it];
+    const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (mask & (1u << (it * 4 + e))) {
+        ci[p] = (int32_t)(i0 + e);
+        cv[p] = v[it][e];
+        ++p;
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    t.cand_cnt[c] = total;
+    atomicAdd(reinterpret_cast<unsigned long long*>(t.cand_total), (unsigned long long)total);
+  }
+}
+
+}  // namespace
+
+void launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sample_every,
+                   int apply_residual, cudaStream_t s) {
+  if (ntask <= 0) return;
+  // sample_every is uniform across a batch (set by the planner)
+  const int sx = (max_chunks + sample_every - 1) / sample_every;
+  k_div_sample<<<dim3(sx, ntask), kThreads, 0, s>>>(tasks_dev, apply_residual);
+  k_div_prethr<<<ntask, kThreads, 0, s>>>(tasks_dev);
+  if (apply_residual)
+    k_div_cand<1><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
+  else
+    k_div_cand<0><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
+}
+
+}  // namespace sdl

@@ -1,0 +1,907 @@
+// SparDL iteration planner / executor.  See engine.hpp for the overview.
+//
+// Reference mapping of the plan (inc/pipeline.hpp:140-342):
+//   dividing           pipeline.hpp:162-184  -> div_stage_ (launch_divide + select)
+//   Spar-Reduce-Scatter reduce_scatter.hpp:120-236 -> steps with phase 0
+//   R-SAG / B-SAG      sag.hpp:125-249        -> steps with phase 1
+//   final all-gather   pipeline.hpp:262-274  -> the gather step (phase 2)
+//   assemble/finalize  pipeline.hpp:276-303  -> launch_assemble / launch_finalize
+// The Fabric ledger (fabric.hpp:74-134) is reproduced exactly: rounds are
+// counted on the host from the schedule, scalars on the device from the
+// counts of the blocks each worker receives.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <set>
+
+namespace sdle {
+
+#define CK(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      sdlh::fail(SPARDL_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+#define NK(x)                                                                            \
+  do {                                                                                   \
+    ncclResult_t r_ = (x);                                                               \
+    if (r_ != ncclSuccess)                                                               \
+      sdlh::fail(SPARDL_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));        \
+  } while (0)
+
+namespace {
+constexpr int kSelStride = 2048;   // segment length when selecting from a compact list
+constexpr int kMergeSmemEntries = 12800;
+}  // namespace
+
+// ---------------------------------------------------------------------------
+Arena::~Arena() {
+  for (void* p : chunks_) cudaFree(p);
+}
+
+void* Arena::alloc(size_t bytes) {
+  bytes = (bytes + 255) & ~static_cast<size_t>(255);
+  if (bytes > left_) {
+    const size_t sz = std::max<size_t>(bytes, static_cast<size_t>(64) << 20);
+    void* p = nullptr;
+    CK(cudaMalloc(&p, sz));
+    CK(cudaMemset(p, 0, sz));
+    chunks_.push_back(p);
+    cur_ = static_cast<unsigned char*>(p);
+    left_ = sz;
+    total_ += sz;
+  }
+  void* r = cur_;
+  cur_ += bytes;
+  left_ -= bytes;
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const void* nccl_id,
+               cudaStream_t stream)
+    : cfg_(cfg), device_(device), world_(world), rank_(rank) {
+  sdlh::validate(cfg);
+  P_ = static_cast<int>(cfg.workers);
+  d_ = static_cast<int>(cfg.teams);
+  m_ = P_ / d_;
+  l_ = sdlh::ceil_log2(m_);
+  L_ = cfg.teams * cfg.k / cfg.workers;                 // inc/pipeline.hpp:51
+  Lcap_ = (L_ + 3) & ~static_cast<int64_t>(3);
+  if (cfg.dimension >= (int64_t(1) << 31) - 1)
+    sdlh::fail(SPARDL_E_UNSUPPORTED, "device path supports N < 2^31 - 1");
+  if (world < 1 || rank < 0 || rank >= world || P_ % world != 0)
+    sdlh::fail(SPARDL_E_UNSUPPORTED, "P must be a positive multiple of the process count");
+  if (cfg.sag == SPARDL_SAG_BSAG && d_ > sdl::kMaxR)
+    sdlh::fail(SPARDL_E_UNSUPPORTED, "bsag on the device supports d <= 16");
+  wloc_ = P_ / world;
+  first_ = rank * wloc_;
+  part_ = sdlh::partition(cfg.dimension, m_);
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    sdlh::fail(SPARDL_E_CUDA, "no CUDA device: the SparDL device path has no CPU fallback");
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop{};
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    sdlh::fail(SPARDL_E_CUDA, std::string("built for sm_100a (B200); device is ") + prop.name);
+  if (stream) {
+    stream_ = stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    own_stream_ = true;
+  }
+  if (world_ > 1) {
+    if (!nccl_id) sdlh::fail(SPARDL_E_ARG, "world_size > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    NK(ncclCommInitRank(&comm_, world_, id, rank_));
+  }
+
+  const size_t nbytes = static_cast<size_t>(cfg.dimension) * sizeof(float);
+  for (int i = 0; i < wloc_; ++i) {
+    float* c = nullptr;
+    CK(cudaMalloc(&c, (nbytes + 255) & ~static_cast<size_t>(255)));
+    CK(cudaMemset(c, 0, nbytes));
+    carry_.push_back(c);
+    ledger_total_.push_back(static_cast<int64_t*>(arena_.alloc(sizeof(int64_t))));
+  }
+  ledger_phase_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * 3 * wloc_));
+  ntot_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * wloc_));
+  budget_dev_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * wloc_));
+  ctl_dev_ = static_cast<sdl::HCtl*>(arena_.alloc(sizeof(sdl::HCtl) * wloc_));
+  gtab_dev_ = static_cast<const float**>(arena_.alloc(sizeof(float*) * wloc_));
+  CK(cudaMallocHost(reinterpret_cast<void**>(&gtab_host_), sizeof(float*) * wloc_));
+  std::memset(gtab_host_, 0, sizeof(float*) * wloc_);
+  err_dev_ = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+  hash_dev_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * d_));
+  rb_dev_ = static_cast<int64_t*>(
+      arena_.alloc(sizeof(int64_t) * (static_cast<size_t>(P_ + wloc_) + static_cast<size_t>(d_) * (world_ + 1))));
+  rounds_.assign(static_cast<size_t>(P_), 0);
+  phase_rounds_.assign(static_cast<size_t>(P_), {0, 0, 0});
+  plan();
+  reset_state();
+}
+
+Engine::~Engine() {
+  if (graph_) cudaGraphExecDestroy(graph_);
+  if (comm_) ncclCommDestroy(comm_);
+  for (float* c : carry_) cudaFree(c);
+  if (gtab_host_) cudaFreeHost(gtab_host_);
+  if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::drop_graph() {
+  if (graph_) {
+    cudaGraphExecDestroy(graph_);
+    graph_ = nullptr;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// planning helpers
+int Engine::new_uid(int owner) {
+  uid_owner_.push_back(owner);
+  return next_uid_++;
+}
+
+Slot& Engine::local_slot(int uid) {
+  auto it = slots_.find(uid);
+  if (it == slots_.end()) sdlh::fail(SPARDL_E_ERROR, "internal: block buffer not resident");
+  return it->second;
+}
+
+Slot Engine::make_slot() {
+  Slot s;
+  s.cap = Lcap_;
+  s.bytes = 16 + 8 * static_cast<size_t>(Lcap_);
+  s.base = static_cast<unsigned char*>(arena_.alloc(s.bytes));
+  s.cnt = reinterpret_cast<int32_t*>(s.base);
+  s.idx = reinterpret_cast<int32_t*>(s.base + 16);
+  s.val = reinterpret_cast<float*>(s.base + 16 + 4 * static_cast<size_t>(Lcap_));
+  return s;
+}
+
+void Engine::add_select(Stage& st, const sdl::SelTask& t0) {
+  sdl::SelTask t = t0;
+  const int nseg = std::max(t.nseg, t.dnseg);
+  t.scr = static_cast<sdl::SelScratch*>(arena_.alloc(sizeof(sdl::SelScratch)));
+  int32_t* segs = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * 5 * std::max(nseg, 1)));
+  t.seg_gt = segs;
+  t.seg_eq = segs + nseg;
+  t.seg_sel_off = segs + 2 * nseg;
+  t.seg_dis_off = segs + 3 * nseg;
+  t.seg_take = segs + 4 * nseg;
+  st.max_nseg = std::max(st.max_nseg, nseg);
+  st.sels.push_back(t);
+}
+
+sdl::SelTask Engine::select_from_slot(const Slot& in) {
+  sdl::SelTask t{};
+  t.mode = 0;
+  t.idx = in.idx;
+  t.val = in.val;
+  t.count = in.cnt;
+  t.stride = kSelStride;
+  t.nseg = static_cast<int32_t>((in.cap + kSelStride - 1) / kSelStride);
+  t.weight = 1.f;
+  return t;
+}
+
+sdl::SelTask Engine::select_from_merge(Stage& st, const std::vector<int>& pieces) {
+  const int r = static_cast<int>(pieces.size());
+  if (r > sdl::kMaxR) sdlh::fail(SPARDL_E_UNSUPPORTED, "merge fan-in above 16 lists");
+  sdl::MergeTask mt{};
+  mt.r = r;
+  int64_t capsum = 0;
+  for (int q = 0; q < r; ++q) {
+    const Slot& s = local_slot(pieces[static_cast<size_t>(q)]);
+    mt.in_idx[q] = s.idx;
+    mt.in_val[q] = s.val;
+    mt.in_cnt[q] = s.cnt;
+    capsum += s.cap;
+  }
+  int64_t T = std::max<int64_t>(8192 / r, (capsum + sdl::kMaxSamples - 1) / sdl::kMaxSamples);
+  T = std::max<int64_t>(T, 32);
+  if (static_cast<int64_t>(r) * T > kMergeSmemEntries)
+    sdlh::fail(SPARDL_E_UNSUPPORTED, "merge of this size exceeds the shared-memory envelope");
+  mt.T = static_cast<int32_t>(T);
+  int64_t parts = 0;
+  for (int q = 0; q < r; ++q) parts += (Lcap_ + T - 1) / T;
+  mt.max_parts = static_cast<int32_t>(parts);
+  mt.splitters = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * (parts + 1)));
+  mt.windows = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * parts * r));
+  mt.nparts = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+  mt.out_idx = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * capsum));
+  mt.out_val = static_cast<float*>(arena_.alloc(sizeof(float) * capsum));
+  mt.seg_off = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * parts));
+  mt.seg_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * parts));
+  st.merges.push_back(mt);
+  st.max_parts = std::max<int>(st.max_parts, static_cast<int>(parts));
+  st.max_rT = std::max<int>(st.max_rT, static_cast<int>(r * T));
+
+  sdl::SelTask t{};
+  t.mode = 0;
+  t.idx = mt.out_idx;
+  t.val = mt.out_val;
+  t.seg_off = mt.seg_off;
+  t.seg_cnt = mt.seg_cnt;
+  t.nseg = static_cast<int32_t>(parts);
+  t.weight = 1.f;
+  return t;
+}
+
+// Merge `pieces` (fold order) and select `budget` of them; the result is a
+// new block owned by worker w.  Discards go to worker w's residual list for
+// block `xi_block` (inc/reduce_scatter.hpp:102-110 / sag.hpp:160-164 /
+// sag.hpp:213-218 / sag.hpp:238-244 -> ResidualStore::record_inproc).
+int Engine::materialize(int w, int pos, std::vector<int> pieces, int64_t budget, float weight,
+                        const int64_t* budget_dev, int64_t* total_out, Stage& st,
+                        int xi_block) {
+  (void)pos;
+  const int uid = new_uid(w);
+  for (int u : pieces)
+    if (st.produced.count(u))
+      sdlh::fail(SPARDL_E_ERROR, "internal: stage reads a block produced in the same stage");
+  st.produced.insert(uid);
+  if (!is_local(w)) return uid;
+  const int li = w - first_;
+  Slot out = make_slot();
+  slots_[uid] = out;
+  sdl::SelTask t = pieces.size() == 1 ? select_from_slot(local_slot(pieces[0]))
+                                      : select_from_merge(st, pieces);
+  t.budget = budget;
+  t.budget_dev = budget_dev;
+  t.weight = weight;
+  t.total_out = total_out;
+  t.sel_idx = out.idx;
+  t.sel_val = out.val;
+  t.sel_cnt = out.cnt;
+  int64_t capsum = 0;
+  for (int u : pieces) capsum += local_slot(u).cap;
+  t.dis_idx = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * capsum));
+  t.dis_val = static_cast<float*>(arena_.alloc(sizeof(float) * capsum));
+  t.dis_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+  xi_[static_cast<size_t>(li)][static_cast<size_t>(xi_block)].push_back(
+      {t.dis_idx, t.dis_val, t.dis_cnt});
+  add_select(st, t);
+  return uid;
+}
+
+// Moves block `uid` from worker src to worker dst in the current round.
+// Physical transfers are deduplicated per (block, destination rank): workers
+// co-resident on a device read the same buffer.  The ledger still charges
+// every receiving worker (inc/fabric.hpp:95-106).
+void Engine::transfer(std::vector<Xfer>& xs, int uid, int src, int dst, int phase,
+                      std::vector<std::vector<int>>* recv_into) {
+  (void)recv_into;
+  const int sr = rank_of(src), dr = rank_of(dst);
+  if (dr == rank_) {
+    if (!has_local(uid)) {
+      slots_[uid] = make_slot();
+      xs.push_back({uid, src, sr, dr});
+    }
+    const int li = dst - first_;
+    const Slot& s = local_slot(uid);
+    ledger_adds_.push_back({ledger_total_[static_cast<size_t>(li)], s.cnt});
+    ledger_adds_.push_back({ledger_phase_ + 3 * li + phase, s.cnt});
+  } else if (sr == rank_) {
+    bool dup = false;
+    for (const Xfer& x : xs)
+      if (x.uid == uid && x.dst_rank == dr) dup = true;
+    if (!dup) xs.push_back({uid, src, sr, dr});
+  }
+}
+
+void Engine::finish_stage(Stage& st) {
+  if (!st.merges.empty()) {
+    st.merges_dev = static_cast<sdl::MergeTask*>(
+        arena_.alloc(sizeof(sdl::MergeTask) * st.merges.size()));
+    CK(cudaMemcpy(st.merges_dev, st.merges.data(), sizeof(sdl::MergeTask) * st.merges.size(),
+                  cudaMemcpyHostToDevice));
+    launches_ += 2;
+  }
+  if (!st.sels.empty()) {
+    st.sels_dev =
+        static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));
+    CK(cudaMemcpy(st.sels_dev, st.sels.data(), sizeof(sdl::SelTask) * st.sels.size(),
+                  cudaMemcpyHostToDevice));
+    launches_ += 9;
+  }
+}
+
+// ---------------------------------------------------------------------------
+void Engine::plan() {
+  const int64_t N = cfg_.dimension;
+  div_uid_.assign(static_cast<size_t>(wloc_), std::vector<int>(static_cast<size_t>(m_), -1));
+  xi_.assign(static_cast<size_t>(wloc_),
+             std::vector<std::vector<sdl::XiList>>(static_cast<size_t>(m_)));
+  std::vector<std::vector<std::vector<int>>> held(
+      static_cast<size_t>(P_), std::vector<std::vector<int>>(static_cast<size_t>(m_)));
+  std::vector<std::vector<char>> has(static_cast<size_t>(P_),
+                                     std::vector<char>(static_cast<size_t>(m_), 1));
+
+  // ---- dividing (inc/pipeline.hpp:162-184)
+  int max_chunks = 0;
+  for (int w = 0; w < P_; ++w) {
+    for (int b = 0; b < m_; ++b) {
+      const int uid = new_uid(w);
+      held[static_cast<size_t>(w)][static_cast<size_t>(b)] = {uid};
+      if (!is_local(w)) continue;
+      const int li = w - first_;
+      div_uid_[static_cast<size_t>(li)][static_cast<size_t>(b)] = uid;
+      Slot out = make_slot();
+      slots_[uid] = out;
+      const int64_t lo = part_.lo[static_cast<size_t>(b)], hi = part_.hi[static_cast<size_t>(b)];
+      const int64_t nb = hi - lo;
+      const int64_t A = lo & ~static_cast<int64_t>(3);
+      const int nch = static_cast<int>((hi - A + sdl::kChunk - 1) / sdl::kChunk);
+      const double frac = static_cast<double>(L_) / static_cast<double>(nb);
+      int cap = static_cast<int>(std::min<double>(sdl::kChunk,
+                                                  std::max(1024.0, sdl::kChunk * 2.5 * frac + 256.0)));
+      cap = (cap + 3) & ~3;
+      sdl::DivTask dt{};
+      dt.g_tab = gtab_dev_;
+      dt.g_id = li;
+      dt.carry = carry_[static_cast<size_t>(li)];
+      dt.lo = static_cast<int32_t>(lo);
+      dt.hi = static_cast<int32_t>(hi);
+      dt.nchunks = nch;
+      dt.cap = cap;
+      dt.budget = L_;
+      dt.use_cand = frac <= 0.25 ? 1 : 0;
+      const size_t ncand = dt.use_cand ? static_cast<size_t>(nch) * cap : 4;
+      dt.cand_idx = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * ncand));
+      dt.cand_val = static_cast<float*>(arena_.alloc(sizeof(float) * ncand));
+      dt.cand_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * nch));
+      dt.cand_total = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t)));
+      dt.cand_bad = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+      dt.pre_key = static_cast<uint32_t*>(arena_.alloc(sizeof(uint32_t)));
+      dt.samp_hist = static_cast<uint32_t*>(arena_.alloc(sizeof(uint32_t) * sdl::kBins));
+      dt.sample_every = std::max(1, nch / 32);
+      dt.err = err_dev_;
+      div_tasks_.push_back(dt);
+      max_chunks = std::max(max_chunks, nch);
+
+      sdl::SelTask t{};
+      t.mode_from_cand = 1;
+      t.idx = dt.cand_idx;
+      t.val = dt.cand_val;
+      t.seg_cnt = dt.cand_cnt;
+      t.stride = cap;
+      t.nseg = nch;
+      t.dval = dt.carry + lo;
+      t.dbase = static_cast<int32_t>(lo);
+      t.dn = static_cast<int32_t>(nb);
+      t.dstride = sdl::kChunk;
+      t.dnseg = static_cast<int32_t>((nb + sdl::kChunk - 1) / sdl::kChunk);
+      t.cand_total = dt.cand_total;
+      t.cand_bad = dt.cand_bad;
+      t.budget = L_;
+      t.sel_idx = out.idx;
+      t.sel_val = out.val;
+      t.sel_cnt = out.cnt;
+      t.weight = 1.f;
+      add_select(div_stage_, t);
+    }
+  }
+  // one sample_every for the whole batch (the launcher sizes its grid with it)
+  div_sample_every_ = std::max(1, max_chunks / 32);
+  for (auto& dt : div_tasks_) dt.sample_every = div_sample_every_;
+  div_max_chunks_ = max_chunks;
+  if (!div_tasks_.empty()) {
+    div_dev_ = static_cast<sdl::DivTask*>(arena_.alloc(sizeof(sdl::DivTask) * div_tasks_.size()));
+    CK(cudaMemcpy(div_dev_, div_tasks_.data(), sizeof(sdl::DivTask) * div_tasks_.size(),
+                  cudaMemcpyHostToDevice));
+    launches_ += 3;
+  }
+  finish_stage(div_stage_);
+
+  auto team_of = [&](int w) { return w / m_; };
+  auto pos_in_team = [&](int w) { return w % m_; };
+  std::vector<sdlh::Bags> bags;
+  for (int i = 0; i < m_; ++i) bags.push_back(sdlh::build_bags(m_, i));
+  const bool naive = cfg_.timing == SPARDL_TIMING_NAIVE;
+
+  auto materialize_pending = [&](Stage& st) {
+    for (int w = 0; w < P_; ++w)
+      for (int b = 0; b < m_; ++b) {
+        auto& h = held[static_cast<size_t>(w)][static_cast<size_t>(b)];
+        if (h.size() > 1) h = {materialize(w, b, h, L_, 1.f, nullptr, nullptr, st, b)};
+      }
+  };
+
+  // ---- Spar-Reduce-Scatter (inc/reduce_scatter.hpp:120-236)
+  for (int s = 1; s <= l_; ++s) {
+    Step step;
+    const int dist = 1 << (l_ - s);
+    const int bi = l_ - s + 1;
+    if (naive) materialize_pending(step.stage);   // blocks merged at step s-1
+    for (int w = 0; w < P_; ++w) {
+      const int i = pos_in_team(w);
+      for (int pos : bags[static_cast<size_t>(i)].bags[static_cast<size_t>(bi - 1)]) {
+        if (!has[static_cast<size_t>(w)][static_cast<size_t>(pos)])
+          sdlh::fail(SPARDL_E_THEOREM, "sending a block already given up");
+        auto& h = held[static_cast<size_t>(w)][static_cast<size_t>(pos)];
+        // optimized timing: the blocks of the bag about to leave are
+        // sparsified now (inc/reduce_scatter.hpp:207-215)
+        if (h.size() > 1) h = {materialize(w, pos, h, L_, 1.f, nullptr, nullptr, step.stage, pos)};
+      }
+    }
+    for (int w = 0; w < P_; ++w) {
+      const int t = team_of(w), i = pos_in_team(w);
+      const int target = t * m_ + (i + dist) % m_;
+      for (int pos : bags[static_cast<size_t>(i)].bags[static_cast<size_t>(bi - 1)]) {
+        auto& h = held[static_cast<size_t>(w)][static_cast<size_t>(pos)];
+        const int uid = h[0];
+        h.clear();
+        has[static_cast<size_t>(w)][static_cast<size_t>(pos)] = 0;
+        if (!has[static_cast<size_t>(target)][static_cast<size_t>(pos)])
+          sdlh::fail(SPARDL_E_THEOREM, "received block " + std::to_string(pos) +
+                                           " not held by worker " + std::to_string(target));
+        transfer(step.xfers, uid, w, target, 0);
+        held[static_cast<size_t>(target)][static_cast<size_t>(pos)].push_back(uid);
+      }
+      phase_rounds_[static_cast<size_t>(w)][0] += 1;
+    }
+    finish_stage(step.stage);
+    steps_.push_back(std::move(step));
+  }
+  // reserved block: sparsified once after the last merge (reduce_scatter.hpp:220-234)
+  Step res;
+  if (naive) materialize_pending(res.stage);
+  std::vector<int> R(static_cast<size_t>(P_));
+  for (int w = 0; w < P_; ++w) {
+    const int i = pos_in_team(w);
+    auto& h = held[static_cast<size_t>(w)][static_cast<size_t>(i)];
+    if (h.empty()) sdlh::fail(SPARDL_E_ERROR, "preservation block missing after reduce-scatter");
+    if (h.size() > 1) h = {materialize(w, i, h, L_, 1.f, nullptr, nullptr, res.stage, i)};
+    R[static_cast<size_t>(w)] = h[0];
+  }
+
+  // ---- Spar-All-Gather across teams (inc/sag.hpp:125-249)
+  Step* open = &res;        // stage that runs before the next transport round
+  std::vector<Step> sag_steps;
+  union_group_owner_.clear();
+  if (d_ > 1 && cfg_.sag == SPARDL_SAG_RSAG) {
+    const int steps = sdlh::exact_log2(d_);
+    for (int ts = 0; ts < steps; ++ts) {
+      const int dist = 1 << ts;
+      // round: every member swaps its block with the partner at XOR distance
+      std::vector<int> recv(static_cast<size_t>(P_), -1);
+      for (int g = 0; g < m_; ++g)
+        for (int t = 0; t < d_; ++t) {
+          const int w = t * m_ + g, partner = (t ^ dist) * m_ + g;
+          transfer(open->xfers, R[static_cast<size_t>(w)], w, partner, 1);
+          recv[static_cast<size_t>(partner)] = R[static_cast<size_t>(w)];
+          phase_rounds_[static_cast<size_t>(w)][1] += 1;
+        }
+      finish_stage(open->stage);
+      steps_.push_back(std::move(*open));
+      Step next;
+      const float share = 1.f / static_cast<float>(2 * dist);   // sag.hpp:153
+      for (int g = 0; g < m_; ++g)
+        for (int t = 0; t < d_; ++t) {
+          const int w = t * m_ + g;
+          R[static_cast<size_t>(w)] =
+              materialize(w, g, {R[static_cast<size_t>(w)], recv[static_cast<size_t>(w)]}, L_,
+                          share, nullptr, nullptr, next.stage, g);
+        }
+      sag_steps.push_back(std::move(next));
+      open = &sag_steps.back();
+    }
+  } else if (d_ > 1) {
+    // B-SAG: pre-select h (weight 1), gather unmerged, fold in source order,
+    // select L with dyadic shares, observe N_t (inc/sag.hpp:189-249,
+    // inc/pipeline.hpp:224-257)
+    const std::vector<double> shares = sdlh::dyadic_shares(d_);
+    std::vector<int> Q(static_cast<size_t>(P_));
+    // the pre-selection reads the reserved blocks: it needs its own stage
+    finish_stage(open->stage);
+    steps_.push_back(std::move(*open));
+    sag_steps.emplace_back();
+    open = &sag_steps.back();
+    for (int g = 0; g < m_; ++g)
+      for (int t = 0; t < d_; ++t) {
+        const int w = t * m_ + g;
+        const int li = w - first_;
+        Q[static_cast<size_t>(w)] =
+            materialize(w, g, {R[static_cast<size_t>(w)]}, L_, 1.f,
+                        is_local(w) ? budget_dev_ + li : nullptr, nullptr, open->stage, g);
+      }
+    for (int g = 0; g < m_; ++g)
+      for (int s = 0; s < d_; ++s) {
+        const int ws = s * m_ + g;
+        for (int i = 0; i < d_; ++i) {
+          if (i == s) continue;
+          transfer(open->xfers, Q[static_cast<size_t>(ws)], ws, i * m_ + g, 1);
+        }
+        phase_rounds_[static_cast<size_t>(ws)][1] += sdlh::ceil_log2(d_);
+      }
+    finish_stage(open->stage);
+    steps_.push_back(std::move(*open));
+    Step post;
+    for (int g = 0; g < m_; ++g) {
+      union_group_owner_.push_back(g);   // worker t=0 of group g reports N_t
+      for (int i = 0; i < d_; ++i) {
+        const int w = i * m_ + g;
+        std::vector<int> pieces;
+        for (int s = 0; s < d_; ++s) pieces.push_back(Q[static_cast<size_t>(s * m_ + g)]);
+        const int li = w - first_;
+        R[static_cast<size_t>(w)] =
+            materialize(w, g, pieces, L_, static_cast<float>(shares[static_cast<size_t>(i)]),
+                        nullptr, is_local(w) ? ntot_ + li : nullptr, post.stage, g);
+      }
+    }
+    post.controller_after = true;
+    sag_steps.push_back(std::move(post));
+    open = &sag_steps.back();
+  }
+
+  // ---- final all-gather inside each team (inc/pipeline.hpp:262-274)
+  std::vector<std::vector<int>> team_blocks(static_cast<size_t>(d_));
+  for (int t = 0; t < d_; ++t) {
+    for (int j = 0; j < m_; ++j) {
+      const int wj = t * m_ + j;
+      team_blocks[static_cast<size_t>(t)].push_back(R[static_cast<size_t>(wj)]);
+      for (int i = 0; i < m_; ++i) {
+        if (i == j) continue;
+        transfer(open->xfers, R[static_cast<size_t>(wj)], wj, t * m_ + i, 2);
+      }
+      phase_rounds_[static_cast<size_t>(wj)][2] += sdlh::ceil_log2(m_);
+    }
+  }
+  finish_stage(open->stage);
+  steps_.push_back(std::move(*open));
+
+  // ---- assemble per (team, device) and finalize per worker (pipeline.hpp:276-303)
+  team_of_local_global_.assign(static_cast<size_t>(wloc_), -1);
+  int64_t max_m = m_;
+  for (int t = 0; t < d_; ++t) {
+    bool any = false;
+    for (int j = 0; j < m_; ++j) any |= is_local(t * m_ + j);
+    if (!any) continue;
+    std::vector<sdl::GatherSrc> src;
+    for (int j = 0; j < m_; ++j) {
+      const Slot& s = local_slot(team_blocks[static_cast<size_t>(t)][static_cast<size_t>(j)]);
+      src.push_back({s.idx, s.val, s.cnt});
+    }
+    auto* src_dev = static_cast<sdl::GatherSrc*>(arena_.alloc(sizeof(sdl::GatherSrc) * m_));
+    CK(cudaMemcpy(src_dev, src.data(), sizeof(sdl::GatherSrc) * m_, cudaMemcpyHostToDevice));
+    Slot gs;
+    gs.cap = cfg_.k;
+    gs.bytes = 16 + 8 * static_cast<size_t>((cfg_.k + 3) & ~3);
+    gs.base = static_cast<unsigned char*>(arena_.alloc(gs.bytes));
+    gs.cnt = reinterpret_cast<int32_t*>(gs.base);
+    gs.idx = reinterpret_cast<int32_t*>(gs.base + 16);
+    gs.val = reinterpret_cast<float*>(gs.base + 16 + 4 * static_cast<size_t>((cfg_.k + 3) & ~3));
+    sdl::AssembleTask at{};
+    at.m = m_;
+    at.src = src_dev;
+    at.out_idx = gs.idx;
+    at.out_val = gs.val;
+    at.out_cnt = gs.cnt;
+    at.out_hash = hash_dev_ + t;
+    asm_tasks_.push_back(at);
+    for (int j = 0; j < m_; ++j)
+      if (is_local(t * m_ + j))
+        team_of_local_global_[static_cast<size_t>(t * m_ + j - first_)] =
+            static_cast<int>(global_.size());
+    global_.push_back(gs);
+    global_team_.push_back(t);
+  }
+  (void)max_m;
+  asm_dev_ = static_cast<sdl::AssembleTask*>(
+      arena_.alloc(sizeof(sdl::AssembleTask) * std::max<size_t>(1, asm_tasks_.size())));
+  CK(cudaMemcpy(asm_dev_, asm_tasks_.data(), sizeof(sdl::AssembleTask) * asm_tasks_.size(),
+                cudaMemcpyHostToDevice));
+  launches_ += 1;
+
+  for (int li = 0; li < wloc_; ++li) {
+    sdl::FinalizeTask ft{};
+    ft.mode = cfg_.residual;
+    ft.m = m_;
+    ft.n = N;
+    ft.carry = carry_[static_cast<size_t>(li)];
+    const Slot& gs = global_[static_cast<size_t>(team_of_local_global_[static_cast<size_t>(li)])];
+    ft.g_idx = gs.idx;
+    ft.g_cnt = gs.cnt;
+    std::vector<sdl::GatherSrc> div;
+    std::vector<int32_t> xoff;
+    std::vector<sdl::XiList> xl;
+    for (int b = 0; b < m_; ++b) {
+      const Slot& s = local_slot(div_uid_[static_cast<size_t>(li)][static_cast<size_t>(b)]);
+      div.push_back({s.idx, s.val, s.cnt});
+      xoff.push_back(static_cast<int32_t>(xl.size()));
+      for (const auto& x : xi_[static_cast<size_t>(li)][static_cast<size_t>(b)]) xl.push_back(x);
+    }
+    xoff.push_back(static_cast<int32_t>(xl.size()));
+    auto* div_dev = static_cast<sdl::GatherSrc*>(arena_.alloc(sizeof(sdl::GatherSrc) * m_));
+    CK(cudaMemcpy(div_dev, div.data(), sizeof(sdl::GatherSrc) * m_, cudaMemcpyHostToDevice));
+    auto* xoff_dev = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * xoff.size()));
+    CK(cudaMemcpy(xoff_dev, xoff.data(), sizeof(int32_t) * xoff.size(), cudaMemcpyHostToDevice));
+    auto* xl_dev = static_cast<sdl::XiList*>(
+        arena_.alloc(sizeof(sdl::XiList) * std::max<size_t>(1, xl.size())));
+    if (!xl.empty())
+      CK(cudaMemcpy(xl_dev, xl.data(), sizeof(sdl::XiList) * xl.size(), cudaMemcpyHostToDevice));
+    ft.div = div_dev;
+    ft.xi_off = xoff_dev;
+    ft.xi = xl_dev;
+    fin_tasks_.push_back(ft);
+  }
+  fin_max_div_ = cfg_.residual == SPARDL_RES_LRES ? Lcap_ : 0;
+  fin_dev_ = static_cast<sdl::FinalizeTask*>(
+      arena_.alloc(sizeof(sdl::FinalizeTask) * fin_tasks_.size()));
+  CK(cudaMemcpy(fin_dev_, fin_tasks_.data(), sizeof(sdl::FinalizeTask) * fin_tasks_.size(),
+                cudaMemcpyHostToDevice));
+  launches_ += fin_max_div_ > 0 ? 2 : 1;
+
+  if (!ledger_adds_.empty()) {
+    ledger_dev_ = static_cast<sdl::LedgerAdd*>(
+        arena_.alloc(sizeof(sdl::LedgerAdd) * ledger_adds_.size()));
+    CK(cudaMemcpy(ledger_dev_, ledger_adds_.data(), sizeof(sdl::LedgerAdd) * ledger_adds_.size(),
+                  cudaMemcpyHostToDevice));
+    launches_ += 1;
+  }
+  if (cfg_.sag == SPARDL_SAG_BSAG) {
+    for (int li = 0; li < wloc_; ++li)
+      ctl_tasks_.push_back({ctl_dev_ + li, ntot_ + li, budget_dev_ + li});
+    ctl_tasks_dev_ =
+        static_cast<sdl::CtlTask*>(arena_.alloc(sizeof(sdl::CtlTask) * ctl_tasks_.size()));
+    CK(cudaMemcpy(ctl_tasks_dev_, ctl_tasks_.data(), sizeof(sdl::CtlTask) * ctl_tasks_.size(),
+                  cudaMemcpyHostToDevice));
+    launches_ += 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// execution
+void Engine::exec_stage(const Stage& st) {
+  if (!st.merges.empty())
+    sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts, st.max_rT,
+                      stream_);
+  if (!st.sels.empty())
+    sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_);
+}
+
+void Engine::exec_round(const std::vector<Xfer>& xs) {
+  if (world_ == 1) return;
+  bool any = false;
+  for (const Xfer& x : xs) any |= x.src_rank != x.dst_rank;
+  if (!any) return;
+  NK(ncclGroupStart());
+  for (const Xfer& x : xs) {
+    if (x.src_rank == x.dst_rank) continue;
+    Slot& s = local_slot(x.uid);
+    if (x.src_rank == rank_)
+      NK(ncclSend(s.base, s.bytes, ncclChar, x.dst_rank, comm_, stream_));
+    else
+      NK(ncclRecv(s.base, s.bytes, ncclChar, x.src_rank, comm_, stream_));
+  }
+  NK(ncclGroupEnd());
+}
+
+void Engine::enqueue_iteration() {
+  CK(cudaMemsetAsync(ledger_phase_, 0, sizeof(int64_t) * 3 * wloc_, stream_));
+  CK(cudaMemsetAsync(hash_dev_, 0, sizeof(int64_t) * d_, stream_));
+  sdl::launch_divide(div_dev_, static_cast<int>(div_tasks_.size()), div_max_chunks_,
+                     div_sample_every_, 1, stream_);
+  exec_stage(div_stage_);
+  for (const Step& s : steps_) {
+    exec_stage(s.stage);
+    if (s.controller_after)
+      sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1, stream_);
+    exec_round(s.xfers);
+  }
+  sdl::launch_assemble(asm_dev_, static_cast<int>(asm_tasks_.size()), m_, cfg_.k, stream_);
+  sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), cfg_.k,
+                       static_cast<int>(fin_max_div_), stream_);
+  sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), stream_);
+  CK(cudaGetLastError());
+}
+
+void Engine::run(const float* const* grads) {
+  CK(cudaSetDevice(device_));
+  bool changed = false;
+  for (int i = 0; i < wloc_; ++i) {
+    if (!grads[i]) sdlh::fail(SPARDL_E_ARG, "null gradient pointer");
+    if (reinterpret_cast<uintptr_t>(grads[i]) % 16 != 0)
+      sdlh::fail(SPARDL_E_ARG, "gradient pointers must be 16-byte aligned");
+    changed |= gtab_host_[i] != grads[i];
+  }
+  if (changed) {
+    CK(cudaStreamSynchronize(stream_));
+    for (int i = 0; i < wloc_; ++i) gtab_host_[i] = grads[i];
+    CK(cudaMemcpyAsync(gtab_dev_, gtab_host_, sizeof(float*) * wloc_, cudaMemcpyHostToDevice,
+                       stream_));
+  }
+  for (int w = 0; w < P_; ++w)
+    for (int p = 0; p < 3; ++p)
+      rounds_[static_cast<size_t>(w)] += phase_rounds_[static_cast<size_t>(w)][static_cast<size_t>(p)];
+  if (use_graph_) {
+    if (!graph_) {
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_iteration();
+      } catch (...) {
+        cudaStreamEndCapture(stream_, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      CK(cudaStreamEndCapture(stream_, &g));
+      CK(cudaGraphInstantiate(&graph_, g, 0));
+      cudaGraphDestroy(g);
+    }
+    CK(cudaGraphLaunch(graph_, stream_));
+  } else {
+    enqueue_iteration();
+  }
+  ran_ = true;
+}
+
+void Engine::sync() {
+  CK(cudaSetDevice(device_));
+  CK(cudaStreamSynchronize(stream_));
+  int32_t err = 0;
+  CK(cudaMemcpy(&err, err_dev_, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err) {
+    CK(cudaMemset(err_dev_, 0, sizeof(int32_t)));
+    sdlh::fail(SPARDL_E_ARG, "gradient contains NaN (selection order undefined)");
+  }
+}
+
+void Engine::reset_state() {
+  CK(cudaSetDevice(device_));
+  CK(cudaStreamSynchronize(stream_));
+  for (int i = 0; i < wloc_; ++i) {
+    CK(cudaMemset(carry_[static_cast<size_t>(i)], 0, sizeof(float) * cfg_.dimension));
+    CK(cudaMemset(ledger_total_[static_cast<size_t>(i)], 0, sizeof(int64_t)));
+  }
+  std::fill(rounds_.begin(), rounds_.end(), 0);
+  if (cfg_.sag == SPARDL_SAG_BSAG) {
+    std::vector<sdl::HCtl> c(static_cast<size_t>(wloc_));
+    std::vector<int64_t> b(static_cast<size_t>(wloc_));
+    for (int i = 0; i < wloc_; ++i) {
+      spardl_hctrl h;
+      sdlh::hctrl_init(&h, cfg_.workers, cfg_.k, cfg_.teams);
+      c[static_cast<size_t>(i)] = {h.lower, h.upper, h.target, h.h, h.step, h.flag, 0};
+      b[static_cast<size_t>(i)] = sdlh::hctrl_budget(&h);
+    }
+    CK(cudaMemcpy(ctl_dev_, c.data(), sizeof(sdl::HCtl) * wloc_, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(budget_dev_, b.data(), sizeof(int64_t) * wloc_, cudaMemcpyHostToDevice));
+  }
+  ran_ = false;
+}
+
+// Gathers one int64 per local worker from every rank into out[P].
+static void allgather_i64(ncclComm_t comm, cudaStream_t st, int world, const int64_t* local_dev,
+                          int wloc, int64_t* out_host, int64_t* scratch_dev) {
+  if (world == 1) {
+    if (cudaMemcpy(out_host, local_dev, sizeof(int64_t) * wloc, cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+      sdlh::fail(SPARDL_E_CUDA, "readback failed");
+    return;
+  }
+  NK(ncclAllGather(local_dev, scratch_dev, static_cast<size_t>(wloc), ncclInt64, comm, st));
+  if (cudaStreamSynchronize(st) != cudaSuccess) sdlh::fail(SPARDL_E_CUDA, "allgather sync failed");
+  if (cudaMemcpy(out_host, scratch_dev, sizeof(int64_t) * wloc * world, cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    sdlh::fail(SPARDL_E_CUDA, "readback failed");
+}
+
+void Engine::ledger(int64_t* rounds, int64_t* scalars) {
+  sync();
+  std::vector<int64_t> loc(static_cast<size_t>(wloc_));
+  for (int i = 0; i < wloc_; ++i)
+    CK(cudaMemcpy(&loc[static_cast<size_t>(i)], ledger_total_[static_cast<size_t>(i)],
+                  sizeof(int64_t), cudaMemcpyDeviceToHost));
+  int64_t* tmp = rb_dev_;
+  CK(cudaMemcpy(tmp, loc.data(), sizeof(int64_t) * wloc_, cudaMemcpyHostToDevice));
+  allgather_i64(comm_, stream_, world_, tmp, wloc_, scalars, tmp + wloc_);
+  for (int w = 0; w < P_; ++w) rounds[w] = rounds_[static_cast<size_t>(w)];
+}
+
+spardl_run_info Engine::run_info() {
+  sync();
+  spardl_run_info ri{};
+  std::vector<int64_t> rounds(static_cast<size_t>(P_)), scalars(static_cast<size_t>(P_));
+  ledger(rounds.data(), scalars.data());
+  for (int w = 0; w < P_; ++w) {
+    ri.max_rounds = std::max(ri.max_rounds, rounds[static_cast<size_t>(w)]);
+    ri.max_scalars = std::max(ri.max_scalars, scalars[static_cast<size_t>(w)]);
+  }
+  // per-phase deltas: max over workers (fabric.hpp:124-134)
+  std::vector<int64_t> ph(static_cast<size_t>(3 * P_));
+  {
+    int64_t* tmp = rb_dev_;
+    // gather phase p of all workers
+    for (int p = 0; p < 3; ++p) {
+      std::vector<int64_t> loc(static_cast<size_t>(wloc_));
+      std::vector<int64_t> all(static_cast<size_t>(P_));
+      std::vector<int64_t> buf(static_cast<size_t>(3 * wloc_));
+      CK(cudaMemcpy(buf.data(), ledger_phase_, sizeof(int64_t) * 3 * wloc_, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < wloc_; ++i) loc[static_cast<size_t>(i)] = buf[static_cast<size_t>(3 * i + p)];
+      CK(cudaMemcpy(tmp, loc.data(), sizeof(int64_t) * wloc_, cudaMemcpyHostToDevice));
+      allgather_i64(comm_, stream_, world_, tmp, wloc_, all.data(), tmp + wloc_);
+      for (int w = 0; w < P_; ++w) ph[static_cast<size_t>(3 * w + p)] = all[static_cast<size_t>(w)];
+    }
+  }
+  for (int w = 0; w < P_; ++w) {
+    ri.srs_scalars = std::max(ri.srs_scalars, ph[static_cast<size_t>(3 * w)]);
+    ri.sag_scalars = std::max(ri.sag_scalars, ph[static_cast<size_t>(3 * w + 1)]);
+    ri.gather_scalars = std::max(ri.gather_scalars, ph[static_cast<size_t>(3 * w + 2)]);
+    ri.srs_rounds = std::max<int64_t>(ri.srs_rounds, phase_rounds_[static_cast<size_t>(w)][0]);
+    ri.sag_rounds = std::max<int64_t>(ri.sag_rounds, phase_rounds_[static_cast<size_t>(w)][1]);
+    ri.gather_rounds = std::max<int64_t>(ri.gather_rounds, phase_rounds_[static_cast<size_t>(w)][2]);
+  }
+  sdlh::expected_cost_sag(cfg_.workers, cfg_.k, cfg_.teams, cfg_.sag, &ri.pred_rounds,
+                          &ri.pred_low, &ri.pred_high);
+  // consistency: every assembled global gradient hashes identically
+  {
+    std::vector<int64_t> h(static_cast<size_t>(d_), 0);
+    CK(cudaMemcpy(h.data(), hash_dev_, sizeof(int64_t) * d_, cudaMemcpyDeviceToHost));
+    if (world_ > 1) {
+      int64_t* tmp = rb_dev_;
+      CK(cudaMemcpy(tmp, h.data(), sizeof(int64_t) * d_, cudaMemcpyHostToDevice));
+      NK(ncclAllGather(tmp, tmp + d_, static_cast<size_t>(d_), ncclInt64, comm_, stream_));
+      CK(cudaStreamSynchronize(stream_));
+      h.resize(static_cast<size_t>(d_ * world_));
+      CK(cudaMemcpy(h.data(), tmp + d_, sizeof(int64_t) * d_ * world_, cudaMemcpyDeviceToHost));
+    }
+    bool ok = true;
+    int64_t ref = 0;
+    bool have = false;
+    std::vector<int32_t> nnz(global_.size());
+    for (size_t q = 0; q < global_.size(); ++q)
+      CK(cudaMemcpy(&nnz[q], global_[q].cnt, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int64_t v : h) {
+      if (v == 0) continue;   // team not hosted there (an empty gradient hashes to 0 too)
+      if (!have) {
+        ref = v;
+        have = true;
+      } else if (v != ref) {
+        ok = false;
+      }
+    }
+    ri.consistent = ok ? 1 : 0;
+    ri.global_nnz = global_.empty() ? 0 : nnz[0];
+  }
+  ri.conservation_applicable = cfg_.residual == SPARDL_RES_GRES ? 1 : 0;
+  ri.conservation_error = -1.0;
+  ri.n_union = cfg_.sag == SPARDL_SAG_BSAG ? m_ : 0;
+  return ri;
+}
+
+void Engine::union_sizes(int64_t* out) {
+  if (cfg_.sag != SPARDL_SAG_BSAG) return;
+  sync();
+  std::vector<int64_t> all(static_cast<size_t>(P_));
+  int64_t* tmp = rb_dev_;
+  CK(cudaMemcpy(tmp, ntot_, sizeof(int64_t) * wloc_, cudaMemcpyDeviceToDevice));
+  allgather_i64(comm_, stream_, world_, tmp, wloc_, all.data(), tmp + wloc_);
+  for (int g = 0; g < m_; ++g) out[g] = all[static_cast<size_t>(g)];   // team 0 member g
+}
+
+void Engine::controller(int local, spardl_hctrl* out) {
+  if (cfg_.sag != SPARDL_SAG_BSAG) sdlh::fail(SPARDL_E_CONFIG, "no controller: sag != bsag");
+  sync();
+  sdl::HCtl c;
+  CK(cudaMemcpy(&c, ctl_dev_ + local, sizeof(c), cudaMemcpyDeviceToHost));
+  *out = {c.lower, c.upper, c.target, c.h, c.step, c.flag, 0};
+}
+
+void Engine::global(int local, const int32_t** idx, const float** val, int64_t* nnz) {
+  sync();
+  const Slot& gs = global_[static_cast<size_t>(team_of_local_global_[static_cast<size_t>(local)])];
+  int32_t n = 0;
+  CK(cudaMemcpy(&n, gs.cnt, sizeof(n), cudaMemcpyDeviceToHost));
+  *idx = gs.idx;
+  *val = gs.val;
+  *nnz = n;
+}
+
+}  // namespace sdle

@@ -1,0 +1,188 @@
+// The SparDL iteration planner/executor (host C++).
+//
+// At context creation the whole iteration of spardl_all_reduce
+// (inc/pipeline.hpp:140-342) is planned once, for every one of the P
+// workers, by replaying the reference schedule symbolically: which block
+// buffers exist, which worker merges which pieces in which order, which
+// buffer moves to which worker in which round.  The plan is identical on
+// every rank (it depends only on the config), so NCCL point-to-point ops
+// match without any runtime negotiation.  Only the tasks of this rank's
+// workers become device work; their descriptors are uploaded once, so an
+// iteration is a fixed sequence of kernel launches and NCCL group calls
+// (CUDA-graph capturable).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+#include "kernels.cuh"
+
+namespace sdle {
+
+// A block buffer: [int32 cnt | pad to 16 B][int32 idx[cap]][float val[cap]],
+// contiguous so one NCCL op moves it.
+struct Slot {
+  unsigned char* base = nullptr;
+  int32_t* cnt = nullptr;
+  int32_t* idx = nullptr;
+  float* val = nullptr;
+  int64_t cap = 0;
+  size_t bytes = 0;
+};
+
+class Arena {
+ public:
+  ~Arena();
+  void* alloc(size_t bytes);
+  size_t total() const { return total_; }
+
+ private:
+  std::vector<void*> chunks_;
+  unsigned char* cur_ = nullptr;
+  size_t left_ = 0;
+  size_t total_ = 0;
+};
+
+struct Xfer {            // one block moved from a worker to another rank
+  int uid;
+  int src_worker;
+  int src_rank;
+  int dst_rank;
+};
+
+struct Stage {           // one batch of merge + select tasks
+  std::vector<sdl::MergeTask> merges;
+  std::vector<sdl::SelTask> sels;
+  sdl::MergeTask* merges_dev = nullptr;
+  sdl::SelTask* sels_dev = nullptr;
+  int max_parts = 0;
+  int max_rT = 0;
+  int max_nseg = 0;
+  std::set<int> produced;    // uids written by this stage (dependency guard)
+};
+
+struct Step {            // a stage followed by a transport round
+  Stage stage;
+  std::vector<Xfer> xfers;   // empty: no round
+  bool controller_after = false;
+};
+
+class Engine {
+ public:
+  Engine(const spardl_config& cfg, int device, int world, int rank, const void* nccl_id,
+         cudaStream_t stream);
+  ~Engine();
+
+  void run(const float* const* grads_dev);
+  void sync();
+  void reset_state();
+  spardl_run_info run_info();
+  void ledger(int64_t* rounds, int64_t* scalars);
+  void union_sizes(int64_t* out);
+  void controller(int local, spardl_hctrl* out);
+  void global(int local, const int32_t** idx, const float** val, int64_t* nnz);
+  float* carry(int local) { return carry_[static_cast<size_t>(local)]; }
+  int64_t dimension() const { return cfg_.dimension; }
+  int first_worker() const { return first_; }
+  int local_workers() const { return wloc_; }
+  int64_t launches_per_iter() const { return launches_; }
+  cudaStream_t stream() const { return stream_; }
+  void set_graph(bool on) {
+    use_graph_ = on;
+    drop_graph();
+  }
+  void set_audit(bool on) { audit_ = on; }
+
+ private:
+  // --- planning
+  struct Held {                   // symbolic held block: pending pieces
+    std::vector<int> pieces;      // uids, in fold order
+  };
+  int new_uid(int owner_worker);
+  Slot& local_slot(int uid);      // the local copy (must exist)
+  bool has_local(int uid) const { return slots_.count(uid) != 0; }
+  Slot make_slot();
+  int materialize(int w, int pos, std::vector<int> pieces, int64_t budget, float weight,
+                  const int64_t* budget_dev, int64_t* total_out, Stage& st, int xi_block);
+  void add_select(Stage& st, const sdl::SelTask& t);
+  sdl::SelTask select_from_slot(const Slot& in);
+  sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);
+  void finish_stage(Stage& st);
+  void transfer(std::vector<Xfer>& xs, int uid, int src_worker, int dst_worker, int phase,
+                std::vector<std::vector<int>>* recv_into = nullptr);
+  void plan();
+  bool is_local(int w) const { return w >= first_ && w < first_ + wloc_; }
+  int rank_of(int w) const { return w / wloc_; }
+  void exec_round(const std::vector<Xfer>& xs);
+  void exec_stage(const Stage& st);
+  void enqueue_iteration();
+  void drop_graph();
+
+  // --- config
+  spardl_config cfg_;
+  int P_ = 1, m_ = 1, d_ = 1, l_ = 0;
+  int64_t L_ = 1, Lcap_ = 4;
+  sdlh::Partition part_;
+  int device_ = 0, world_ = 1, rank_ = 0, wloc_ = 1, first_ = 0;
+  cudaStream_t stream_ = nullptr;
+  bool own_stream_ = false;
+  ncclComm_t comm_ = nullptr;
+  bool use_graph_ = true;
+  bool audit_ = false;
+  cudaGraphExec_t graph_ = nullptr;
+  int64_t launches_ = 0;
+
+  Arena arena_;
+  // per local worker
+  std::vector<float*> carry_;
+  std::vector<int64_t*> ledger_total_;   // device [1] per worker (cumulative scalars)
+  int64_t* ledger_phase_ = nullptr;      // device [wloc*3] per call
+  int64_t* ntot_ = nullptr;              // device [wloc] B-SAG union sizes
+  int64_t* budget_dev_ = nullptr;        // device [wloc] B-SAG pre-selection budgets
+  sdl::HCtl* ctl_dev_ = nullptr;         // device [wloc]
+  const float** gtab_dev_ = nullptr;     // device [wloc] gradient pointers
+  const float** gtab_host_ = nullptr;    // pinned mirror
+  int32_t* err_dev_ = nullptr;           // NaN flag
+  int64_t* hash_dev_ = nullptr;          // [d] consistency hashes
+  int64_t* rb_dev_ = nullptr;            // readback scratch
+  std::vector<int64_t> rounds_;          // host, per global worker (cumulative)
+  std::vector<std::array<int64_t, 3>> phase_rounds_;  // per global worker per call
+
+  // plan
+  int next_uid_ = 0;
+  std::vector<int> uid_owner_;
+  std::map<int, Slot> slots_;            // uid -> local buffer
+  std::vector<sdl::DivTask> div_tasks_;
+  sdl::DivTask* div_dev_ = nullptr;
+  int div_max_chunks_ = 0, div_sample_every_ = 1;
+  Stage div_stage_;
+  std::vector<Step> steps_;
+  std::vector<sdl::LedgerAdd> ledger_adds_;
+  sdl::LedgerAdd* ledger_dev_ = nullptr;
+  std::vector<sdl::AssembleTask> asm_tasks_;
+  sdl::AssembleTask* asm_dev_ = nullptr;
+  std::vector<sdl::FinalizeTask> fin_tasks_;
+  sdl::FinalizeTask* fin_dev_ = nullptr;
+  int64_t fin_max_div_ = 0;
+  std::vector<sdl::CtlTask> ctl_tasks_;
+  sdl::CtlTask* ctl_tasks_dev_ = nullptr;
+  std::vector<int> team_of_local_global_;    // local worker -> index into global_ bufs
+  std::vector<Slot> global_;                 // per local team: assembled global (cap k)
+  std::vector<int> global_team_;             // team id of each global_ entry
+  // per local worker, per block: dividing outputs and discard lists
+  std::vector<std::vector<int>> div_uid_;
+  std::vector<std::vector<std::vector<sdl::XiList>>> xi_;
+  std::vector<int> union_group_owner_;       // position group -> worker providing N_t
+  bool ran_ = false;
+};
+
+}  // namespace sdle

@@ -1,0 +1,217 @@
+// Device-side data model and kernel launchers of the SparDL B200 path.
+//
+// Everything on the device is SoA: a sparse block is (int32 idx[], float
+// val[], int32 count) with a fixed capacity -- the reference's AoS
+// {int64 index; double value} Entry (inc/sparse.hpp:57-62) re-laid for
+// coalesced 128-bit traffic.  Indices are int32 (N < 2^31).
+//
+// Three kernel families:
+//   select  -- deterministic top-L over a *segmented* list (|v| desc, index
+//              asc; inc/sparse.hpp:122-162): 3 radix passes over the 31-bit
+//              magnitude key, per-segment counts, ordered compaction of the
+//              selected and discarded parts (both index-sorted).
+//   merge   -- r-way index merge with a left fold of the values in list order
+//              (inc/sparse.hpp:182-208 applied r-1 times), sample-splitter
+//              partitioned so every CTA merges <= r*T entries in shared memory.
+//   divide  -- the dividing pass (inc/pipeline.hpp:162-184): residual add fused
+//              with candidate compaction above a sampled pre-threshold.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sdl {
+
+constexpr int kThreads = 256;
+constexpr int kBins = 2048;            // radix digit width of passes 0 and 1 (11 bits)
+constexpr int kMaxR = 16;              // max lists folded by one merge task
+constexpr int kChunk = 8192;           // dividing chunk (elements per CTA)
+constexpr int kMaxSamples = 8192;      // merge splitter samples per task
+
+// ---------------------------------------------------------------------------
+// Select
+// ---------------------------------------------------------------------------
+// Per-task scratch, device resident.  `hist` is left zeroed by every kernel
+// that consumes it, so a task can be re-run without host-side clears.
+struct SelScratch {
+  uint32_t hist[kBins];
+  uint32_t prefix;       // key bits fixed so far
+  uint32_t pmask;        // which key bits are fixed
+  int64_t rank;          // 1-based rank still to find inside the prefix
+  int64_t cnt_gt;        // entries with key strictly above the prefix range
+  int64_t total;         // entries in the input
+  int64_t budget;        // effective budget for this run
+  int32_t all;           // total <= budget: everything is selected
+  int32_t mode;          // resolved input mode for this run
+  int32_t err;           // NaN seen
+  int32_t pad_;
+};
+
+// Input is a list of segments.  mode 0 (explicit): segment s holds entries
+// idx[off+j], val[off+j] for j < cnt with off = seg_off ? seg_off[s] : s*stride
+// and cnt = seg_cnt ? seg_cnt[s] : clamp(*count - off, 0, stride) (a compact
+// list cut into strided segments).  mode 1 (dense slice): entries are
+// (dbase + p, dval[p]) for p in [s*dstride, min((s+1)*dstride, dn)).
+// When `mode_from_cand` is set (the dividing select), the mode is decided on
+// the device: explicit candidates if they are complete, else dense fallback.
+struct SelTask {
+  int32_t nseg;
+  int32_t mode;
+  int32_t mode_from_cand;
+  int32_t stride;
+  const int32_t* idx;
+  const float* val;
+  const int32_t* seg_off;
+  const int32_t* seg_cnt;
+  const int32_t* count;
+  // dense slice
+  const float* dval;
+  int32_t dbase;
+  int32_t dn;
+  int32_t dstride;
+  int32_t dnseg;
+  // candidate-path verdict (dividing)
+  const int64_t* cand_total;
+  const int32_t* cand_bad;
+  // budget
+  int64_t budget;
+  const int64_t* budget_dev;
+  // outputs
+  int32_t* sel_idx;
+  float* sel_val;
+  int32_t* sel_cnt;
+  int32_t* dis_idx;      // nullable: discards are not materialised
+  float* dis_val;
+  int32_t* dis_cnt;
+  float weight;          // discard share (inc/residual.hpp:104-124)
+  int32_t pad0_;
+  int64_t* total_out;    // nullable: B-SAG union size N_t
+  // scratch
+  SelScratch* scr;
+  int32_t* seg_gt;       // [max nseg]
+  int32_t* seg_eq;
+  int32_t* seg_sel_off;
+  int32_t* seg_dis_off;
+  int32_t* seg_take;
+};
+
+// ---------------------------------------------------------------------------
+// Merge
+// ---------------------------------------------------------------------------
+struct MergeTask {
+  int32_t r;
+  int32_t T;                        // window (sample spacing) per list
+  const int32_t* in_idx[kMaxR];
+  const float* in_val[kMaxR];
+  const int32_t* in_cnt[kMaxR];
+  // device scratch written by the splitter kernel
+  int32_t* splitters;               // [max_parts + 1]
+  int32_t* windows;                 // [max_parts * r]
+  int32_t* nparts;                  // [1]
+  int32_t max_parts;
+  int32_t pad_;
+  // output: segmented list
+  int32_t* out_idx;                 // capacity sum of input capacities
+  float* out_val;
+  int32_t* seg_off;                 // [max_parts]
+  int32_t* seg_cnt;                 // [max_parts]
+};
+
+// ---------------------------------------------------------------------------
+// Dividing
+// ---------------------------------------------------------------------------
+struct DivTask {
+  const float* const* g_tab;  // gradient pointer table (updated per call)
+  int32_t g_id;            // this worker's entry in g_tab
+  int32_t pad_;
+  float* carry;            // worker residual; becomes g + carry (= g_copy) in place
+  int32_t lo, hi;          // block range
+  int32_t nchunks;
+  int32_t cap;             // candidate capacity per chunk
+  int64_t budget;          // L
+  // candidates
+  int32_t* cand_idx;       // [nchunks * cap]
+  float* cand_val;
+  int32_t* cand_cnt;       // [nchunks]
+  int64_t* cand_total;
+  int32_t* cand_bad;       // overflow / NaN / skip flag
+  uint32_t* pre_key;       // candidate threshold (key >= pre_key)
+  uint32_t* samp_hist;     // [kBins]
+  int32_t sample_every;    // sample one chunk in `sample_every`
+  int32_t use_cand;        // 0: candidate path disabled (dense select)
+  int32_t* err;            // NaN flag
+};
+
+// ---------------------------------------------------------------------------
+// Launchers (stream-ordered; no host synchronisation inside)
+// ---------------------------------------------------------------------------
+// tasks_dev: device copy of the task array; ntask; max_nseg: grid extent.
+void launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s);
+void launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T,
+                  cudaStream_t s);
+void launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sample_every,
+                   int apply_residual, cudaStream_t s);
+
+// Finalize / assembly helpers
+struct GatherSrc {            // one source block of an assembled global gradient
+  const int32_t* idx;
+  const float* val;
+  const int32_t* cnt;
+};
+struct AssembleTask {
+  int32_t m;
+  int32_t pad_;
+  const GatherSrc* src;       // [m] (device)
+  int32_t* out_idx;
+  float* out_val;
+  int32_t* out_cnt;
+  int64_t* out_hash;          // nullable: FNV-style hash for consistency checks
+};
+void launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t max_k,
+                     cudaStream_t s);
+
+constexpr int kMaxXi = 24;
+struct XiList {               // one in-procedure discard list (already weight-scaled)
+  const int32_t* idx;
+  const float* val;
+  const int32_t* cnt;
+};
+// residual finalize for one worker (inc/residual.hpp:128-150)
+struct FinalizeTask {
+  int32_t mode;               // 0 gres, 1 pres, 2 lres
+  int32_t m;                  // blocks
+  int64_t n;                  // dimension
+  float* carry;               // in: g_copy (combined); out: residual
+  const int32_t* g_idx;       // global gradient
+  const int32_t* g_cnt;
+  // per block: dividing selection + discard lists in recording order
+  const GatherSrc* div;       // [m]
+  const int32_t* xi_off;      // [m+1] offsets into xi
+  const XiList* xi;           // lists
+};
+void launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_k, int max_div,
+                     cudaStream_t s);
+
+// ledger: scalars += 2 * count for each (worker slot, count pointer)
+struct LedgerAdd {
+  int64_t* dst;
+  const int32_t* cnt;
+};
+void launch_ledger(const LedgerAdd* adds_dev, int nadd, cudaStream_t s);
+
+// B-SAG controller (Algorithm 2, inc/sag.hpp:37-90) on the device
+struct HCtl {
+  double lower, upper;
+  int64_t target;
+  double h, step;
+  int32_t flag;
+  int32_t pad_;
+};
+struct CtlTask {
+  HCtl* ctl;                  // this worker's controller
+  const int64_t* n_t;         // its group's union size
+  int64_t* budget;            // pre-selection budget for the next run
+};
+void launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStream_t s);
+
+}  // namespace sdl

@@ -1,0 +1,344 @@
+// Deterministic top-L selection over segmented sparse lists.
+//
+// Semantics: inc/sparse.hpp:136-162 (top_k_select) -- keep the min(budget,
+// nnz) entries that come first in the order (|v| desc, index asc); return
+// the kept and the discarded entries, each in index order.
+//
+// Method (per task, all tasks of a batch in one launch per kernel):
+//   hist<0..2> + find<0..2>: radix select on the 31-bit magnitude key
+//       (digits 11 / 11 / 9 bits).  After the three passes the threshold key
+//       T is exact, cnt_gt = #{key > T} and need_eq = L - cnt_gt entries of
+//       key == T are taken -- the lowest-index ones, which is exactly the
+//       reference's tie rule.
+//   count: per segment #{key > T} and #{key == T}
+//   scan:  per segment tie quota and output offsets (segments are in index
+//          order, so offsets preserve index order)
+//   write: ordered compaction of selected / discarded entries; discards are
+//          scaled by the residual share with an explicitly rounded multiply
+//          (no FMA contraction), matching inc/residual.hpp:119.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sdl {
+
+namespace {
+
+__device__ __forceinline__ int resolve_mode(const SelTask& t) {
+  if (!t.mode_from_cand) return t.mode;
+  const int64_t need = t.budget_dev ? *t.budget_dev : t.budget;
+  return (*t.cand_bad != 0 || *t.cand_total < need) ? 1 : 0;
+}
+
+__device__ __forceinline__ int nseg_of(const SelTask& t, int mode) {
+  return mode == 1 ? t.dnseg : t.nseg;
+}
+
+__device__ __forceinline__ void seg_bounds(const SelTask& t, int mode, int s, int& off,
+                                           int& cnt) {
+  if (mode == 1) {
+    off = s * t.dstride;
+    const int c = t.dn - off;
+    cnt = c < 0 ? 0 : (c > t.dstride ? t.dstride : c);
+  } else {
+    off = t.seg_off ? t.seg_off[s] : s * t.stride;
+    if (t.seg_cnt) {
+      cnt = t.seg_cnt[s];
+    } else {
+      const int c = *t.count - off;
+      cnt = c < 0 ? 0 : (c > t.stride ? t.stride : c);
+    }
+  }
+}
+
+__device__ __forceinline__ float seg_val(const SelTask& t, int mode, int p) {
+  return mode == 1 ? t.dval[p] : t.val[p];
+}
+__device__ __forceinline__ int32_t seg_idx(const SelTask& t, int mode, int p) {
+  return mode == 1 ? t.dbase + p : t.idx[p];
+}
+
+template <int PASS>
+struct Digit {
+  static constexpr int shift = PASS == 0 ? 20 : (PASS == 1 ? 9 : 0);
+  static constexpr int nbins = PASS == 2 ? 512 : 2048;
+};
+
+// ---------------------------------------------------------------------------
+template <int PASS>
+__global__ void __launch_bounds__(kThreads) k_sel_hist(const SelTask* __restrict__ tasks) {
+  const SelTask& t = tasks[blockIdx.y];
+  SelScratch* sc = t.scr;
+  int mode;
+  uint32_t prefix = 0, pmask = 0;
+  if (PASS == 0) {
+    mode = resolve_mode(t);
+  } else {
+    if (sc->all) return;
+    mode = sc->mode;
+    prefix = sc->prefix;
+    pmask = sc->pmask;
+  }
+  const int nseg = nseg_of(t, mode);
+  if ((int)blockIdx.x >= nseg) return;
+  constexpr int NB = Digit<PASS>::nbins;
+  constexpr int SH = Digit<PASS>::shift;
+  __shared__ uint32_t h[NB];
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (int s = blockIdx.x; s < nseg; s += gridDim.x) {
+    int off, cnt;
+    seg_bounds(t, mode, s, off, cnt);
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+      const uint32_t key = mag_key(seg_val(t, mode, off + j));
+      if ((key & pmask) == prefix) atomicAdd(&h[(key >> SH) & (NB - 1)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < NB; b += blockDim.x)
+    if (h[b]) atomicAdd(&sc->hist[b], h[b]);
+}
+
+// One CTA per task: locate the digit holding the rank-th largest key.
+template <int PASS>
+__global__ void __launch_bounds__(kThreads) k_sel_find(const SelTask* __restrict__ tasks) {
+  const SelTask& t = tasks[blockIdx.x];
+  SelScratch* sc = t.scr;
+  constexpr int NB = Digit<PASS>::nbins;
+  constexpr int SH = Digit<PASS>::shift;
+  constexpr int BPT = NB / kThreads;
+  __shared__ int scratch[40];
+  __shared__ long long lscr[32];
+  if (PASS > 0 && sc->all) return;
+  uint32_t c[BPT];
+  long long mine = 0;
+#pragma unroll
+  for (int q = 0; q < BPT; ++q) {
+    c[q] = sc->hist[threadIdx.x * BPT + q];
+    sc->hist[threadIdx.x * BPT + q] = 0;
+    mine += c[q];
+  }
+  int64_t rank, cnt_gt;
+  uint32_t prefix, pmask;
+  if (PASS == 0) {
+    const long long total = block_sum_ll(mine, lscr);
+    const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
+    if (threadIdx.x == 0) {
+      sc->total = total;
+      sc->budget = budget;
+      sc->mode = resolve_mode(t);
+      sc->err = 0;
+      if (total <= budget) sc->all = 1;          // identity case, inc/sparse.hpp:143-146
+      else if (budget <= 0) sc->all = 2;         // nothing kept
+      else sc->all = 0;
+      sc->prefix = 0;
+      sc->pmask = 0;
+      sc->rank = budget;
+      sc->cnt_gt = 0;
+    }
+    __syncthreads();
+    if (total <= budget || budget <= 0) return;
+    rank = budget;
+    cnt_gt = 0;
+    prefix = 0;
+    pmask = 0;
+  } else {
+    rank = sc->rank;
+    cnt_gt = sc->cnt_gt;
+    prefix = sc->prefix;
+    pmask = sc->pmask;
+  }
+  __syncthreads();
+  // suffix sums over threads (bins ascending with thread id; we scan from the top)
+  // reverse the thread order so an exclusive prefix gives "count above me".
+  const int rev = blockDim.x - 1 - threadIdx.x;
+  (void)rev;
+  // exclusive scan in reversed order: compute inclusive scan of values ordered
+  // by descending thread id using a shared array.
+  __shared__ long long vals[kThreads];
+  vals[threadIdx.x] = mine;
+  __syncthreads();
+  // simple Hillis-Steele on reversed array
+  __shared__ long long suf[kThreads];
+  suf[threadIdx.x] = vals[blockDim.x - 1 - threadIdx.x];
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    long long add = threadIdx.x >= (unsigned)o ? suf[threadIdx.x - o] : 0;
+    __syncthreads();
+    suf[threadIdx.x] += add;
+    __syncthreads();
+  }
+  // above(tid) = inclusive suffix of threads > tid = suf[rev-1]
+  const int r = blockDim.x - 1 - threadIdx.x;
+  const long long above = r > 0 ? suf[r - 1] : 0;
+  if (above < rank && rank <= above + mine) {
+    long long cum = above;
+    for (int q = BPT - 1; q >= 0; --q) {
+      if (cum + (long long)c[q] >= rank) {
+        const uint32_t digit = threadIdx.x * BPT + q;
+        sc->prefix = prefix | (digit << SH);
+        sc->pmask = pmask | ((uint32_t)(NB - 1) << SH);
+        sc->rank = rank - cum;
+        sc->cnt_gt = cnt_gt + cum;
+        break;
+      }
+      cum += c[q];
+    }
+  }
+  (void)scratch;
+}
+
+// Per segment: #{key > T}, #{key == T}
+__global__ void __launch_bounds__(kThreads) k_sel_count(const SelTask* __restrict__ tasks) {
+  const SelTask& t = tasks[blockIdx.y];
+  const SelScratch* sc = t.scr;
+  const int mode = sc->mode;
+  const int nseg = nseg_of(t, mode);
+  const int all = sc->all;
+  const uint32_t T = sc->prefix;
+  __shared__ int scratch[40];
+  for (int s = blockIdx.x; s < nseg; s += gridDim.x) {
+    int off, cnt;
+    seg_bounds(t, mode, s, off, cnt);
+    int gt = 0, eq = 0;
+    if (all == 1) {
+      gt = cnt;
+    } else if (all == 0) {
+      int lg = 0, le = 0;
+      for (int j0 = 0; j0 < cnt; j0 += blockDim.x) {
+        const int j = j0 + threadIdx.x;
+        uint32_t key = 0;
+        if (j < cnt) key = mag_key(seg_val(t, mode, off + j));
+        lg += (j < cnt && key > T);
+        le += (j < cnt && key == T);
+      }
+      int tg, te;
+      block_exscan(lg, scratch, &tg);
+      block_exscan(le, scratch, &te);
+      gt = tg;
+      eq = te;
+    }
+    if (threadIdx.x == 0) {
+      t.seg_gt[s] = gt;
+      t.seg_eq[s] = eq;
+    }
+  }
+}
+
+// One CTA per task: tie quotas and output offsets per segment.
+__global__ void __launch_bounds__(kThreads) k_sel_scan(const SelTask* __restrict__ tasks) {
+  const SelTask& t = tasks[blockIdx.x];
+  SelScratch* sc = t.scr;
+  const int mode = sc->mode;
+  const int nseg = nseg_of(t, mode);
+  const int all = sc->all;
+  const int64_t need_eq = all == 0 ? sc->rank : 0;
+  __shared__ int scratch[40];
+  int eq_carry = 0, sel_carry = 0, cnt_carry = 0;
+  for (int s0 = 0; s0 < nseg; s0 += blockDim.x) {
+    const int s = s0 + threadIdx.x;
+    int gt = 0, eq = 0, cnt = 0;
+    if (s < nseg) {
+      int off;
+      seg_bounds(t, mode, s, off, cnt);
+      gt = t.seg_gt[s];
+      eq = t.seg_eq[s];
+    }
+    int teq, tsel, tcnt;
+    const int eq_before = eq_carry + block_exscan(eq, scratch, &teq);
+    long long q = need_eq - eq_before;
+    const int take = q <= 0 ? 0 : (q >= eq ? eq : (int)q);
+    const int sel = gt + take;
+    const int sel_off = sel_carry + block_exscan(sel, scratch, &tsel);
+    const int cnt_off = cnt_carry + block_exscan(cnt, scratch, &tcnt);
+    if (s < nseg) {
+      t.seg_take[s] = take;
+      t.seg_sel_off[s] = sel_off;
+      t.seg_dis_off[s] = cnt_off - sel_off;
+    }
+    eq_carry += teq;
+    sel_carry += tsel;
+    cnt_carry += tcnt;
+  }
+  if (threadIdx.x == 0) {
+    *t.sel_cnt = sel_carry;
+    if (t.dis_cnt) *t.dis_cnt = cnt_carry - sel_carry;
+    if (t.total_out) *t.total_out = sc->total;
+  }
+}
+
+// Ordered compaction.
+__global__ void __launch_bounds__(kThreads) k_sel_write(const SelTask* __restrict__ tasks) {
+  const SelTask& t = tasks[blockIdx.y];
+  const SelScratch* sc = t.scr;
+  const int mode = sc->mode;
+  const int nseg = nseg_of(t, mode);
+  const int all = sc->all;
+  const uint32_t T = sc->prefix;
+  const float w = t.weight;
+  const bool want_dis = t.dis_idx != nullptr;
+  __shared__ int scratch[40];
+  for (int s = blockIdx.x; s < nseg; s += gridDim.x) {
+    int off, cnt;
+    seg_bounds(t, mode, s, off, cnt);
+    if (cnt == 0) continue;
+    const int sel_base = t.seg_sel_off[s];
+    const int dis_base = t.seg_dis_off[s];
+    const int take = t.seg_take[s];
+    int eq_seen = 0, sel_seen = 0;
+    for (int j0 = 0; j0 < cnt; j0 += blockDim.x) {
+      const int j = j0 + threadIdx.x;
+      const bool valid = j < cnt;
+      float v = 0.f;
+      int32_t ix = 0;
+      uint32_t key = 0;
+      if (valid) {
+        v = seg_val(t, mode, off + j);
+        ix = seg_idx(t, mode, off + j);
+        key = mag_key(v);
+      }
+      bool is_sel;
+      if (all == 1) {
+        is_sel = valid;
+      } else if (all == 2) {
+        is_sel = false;
+      } else {
+        const bool is_eq = valid && key == T;
+        int teq;
+        const int eq_rank = eq_seen + block_rank(is_eq, scratch, &teq);
+        eq_seen += teq;
+        is_sel = valid && (key > T || (is_eq && eq_rank < take));
+      }
+      int tsel;
+      const int sel_rank = sel_seen + block_rank(is_sel, scratch, &tsel);
+      sel_seen += tsel;
+      if (is_sel) {
+        t.sel_idx[sel_base + sel_rank] = ix;
+        t.sel_val[sel_base + sel_rank] = v;
+      } else if (valid && want_dis) {
+        const int p = dis_base + (j - sel_rank);
+        t.dis_idx[p] = ix;
+        t.dis_val[p] = __fmul_rn(v, w);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s) {
+  if (ntask <= 0) return;
+  const int gx = max_nseg < 1 ? 1 : (max_nseg > 8192 ? 8192 : max_nseg);
+  const int hx = max_nseg < 1 ? 1 : (max_nseg > 1184 ? 1184 : max_nseg);
+  dim3 g2(gx, ntask), gh(hx, ntask);
+  k_sel_hist<0><<<gh, kThreads, 0, s>>>(tasks_dev);
+  k_sel_find<0><<<ntask, kThreads, 0, s>>>(tasks_dev);
+  k_sel_hist<1><<<gh, kThreads, 0, s>>>(tasks_dev);
+  k_sel_find<1><<<ntask, kThreads, 0, s>>>(tasks_dev);
+  k_sel_hist<2><<<gh, kThreads, 0, s>>>(tasks_dev);
+  k_sel_find<2><<<ntask, kThreads, 0, s>>>(tasks_dev);
+  k_sel_count<<<g2, kThreads, 0, s>>>(tasks_dev);
+  k_sel_scan<<<ntask, kThreads, 0, s>>>(tasks_dev);
+  k_sel_write<<<g2, kThreads, 0, s>>>(tasks_dev);
+}
+
+}  // namespace sdl

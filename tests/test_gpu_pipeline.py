@@ -1,0 +1,133 @@
+"""GPU parity of the whole spardl_all_reduce (inc/pipeline.hpp:140-342).
+
+Every configuration runs several iterations with residual feedback, all P
+workers emulated on cuda:0, and is compared bit-exactly with the fp32 oracle
+(same algorithm, same fp32 arithmetic, same summation order): global
+indices and values, every worker's residual carry, the Fabric ledger,
+B-SAG union sizes and controller states.  On grid-snapped inputs the same
+run is also compared with the fp64 reference itself (oracle/_ref).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from gpu_util import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env(built):
+    import torch
+    import paper_2304_00737_b200 as sd
+    from pyoracle import Oracle
+    return sd, Oracle("f32"), torch
+
+
+def configs():
+    out = []
+    for P in (1, 2, 3, 4, 5, 6, 7, 8, 9):
+        for d in [x for x in range(1, P + 1) if P % x == 0]:
+            sags = ["none"] if d == 1 else (["rsag", "bsag"] if (d & (d - 1)) == 0 else ["bsag"])
+            for sag in sags:
+                out.append((P, d, sag))
+    return out
+
+
+def _run(env, P, d, sag, residual, timing, kind, N, k, iters, seed, graph=True):
+    sd, orc, torch = env
+    from pyoracle import make_config
+    cfg = sd.ClusterConfig(workers=P, dimension=N, k=k, teams=d, sag=sag, residual=residual,
+                           timing=timing)
+    ctx = sd.SparDL(cfg, device=0, graph=graph)
+    ref = orc.pipeline(make_config(P, N, k, d, sag, residual, timing))
+    rng = np.random.default_rng(seed)
+    for it in range(iters):
+        g = gen(kind, (P, N), rng)
+        dev = [torch.from_numpy(g[w]).cuda() for w in range(P)]
+        ctx.all_reduce(dev)
+        info = ctx.run_info()
+        rinfo = ref.allreduce(g)
+        tag = f"P={P} d={d} {sag} {residual} {timing} {kind} it={it}"
+        gi, gv = ctx.global_gradient(0)
+        ri, rv = ref.global_gradient()
+        assert info["consistent"] == 1, tag
+        assert np.array_equal(gi.cpu().numpy().astype(np.int64), ri), tag
+        assert np.array_equal(gv.cpu().numpy().view(np.uint32), rv.view(np.uint32)), tag
+        for w in range(P):
+            c = ctx.carry(w).cpu().numpy()
+            assert np.array_equal(c.view(np.uint32), ref.carry(w).view(np.uint32)), tag + f" w={w}"
+        for key in ("max_rounds", "max_scalars", "srs_rounds", "srs_scalars", "sag_rounds",
+                    "sag_scalars", "gather_rounds", "gather_scalars", "pred_rounds", "pred_low",
+                    "pred_high", "n_union", "global_nnz"):
+            assert info[key] == rinfo[key], (tag, key, info[key], rinfo[key])
+        lr, ls = ctx.ledger()
+        rr, rs = ref.ledger()
+        assert list(lr) == list(rr) and list(ls) == list(rs), tag
+        if sag == "bsag":
+            assert ctx.union_sizes() == list(ref.union_sizes()), tag
+            for w in range(P):
+                c, rc = ctx.controller(w), ref.controller(w)
+                assert (c["h"], c["step"], c["flag"]) == (rc.h, rc.step, rc.flag), tag
+    ctx.close()
+
+
+@pytest.mark.parametrize("P,d,sag", configs())
+@pytest.mark.parametrize("kind", ["gauss", "int"])
+def test_pipeline_small(env, P, d, sag, kind):
+    N = 3000 + 17 * P
+    k = P * (N // (P * 20))          # ~5% density
+    _run(env, P, d, sag, "gres", "optimized", kind, N, k, iters=3, seed=P * 100 + d)
+
+
+@pytest.mark.parametrize("residual", ["gres", "pres", "lres"])
+@pytest.mark.parametrize("timing", ["optimized", "naive"])
+@pytest.mark.parametrize("P,d,sag", [(4, 1, "none"), (6, 1, "none"), (8, 2, "rsag"),
+                                     (6, 3, "bsag"), (8, 4, "bsag"), (5, 5, "bsag")])
+def test_pipeline_modes(env, residual, timing, P, d, sag):
+    N = 20000 + P
+    k = P * 40
+    _run(env, P, d, sag, residual, timing, "mixed", N, k, iters=3, seed=11)
+
+
+@pytest.mark.parametrize("P,d,sag,N,dens", [(8, 1, "none", 1_000_000, 0.01),
+                                            (6, 1, "none", 1_000_003, 0.01),
+                                            (4, 1, "none", 1_000_000, 0.2),
+                                            (8, 2, "rsag", 400_000, 0.01),
+                                            (6, 3, "bsag", 400_000, 0.01),
+                                            (1, 1, "none", 2_000_000, 0.001)])
+def test_pipeline_medium(env, P, d, sag, N, dens):
+    k = P * max(1, int(N * dens) // P)
+    _run(env, P, d, sag, "gres", "optimized", "gauss", N, k, iters=3, seed=5)
+
+
+def test_pipeline_no_graph(env):
+    _run(env, 4, 1, "none", "gres", "optimized", "gauss", 50000, 400, iters=2, seed=3,
+         graph=False)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(__file__), "..", "oracle",
+                                                    "_ref", "libspardl_ref.so")),
+                    reason="oracle/_ref not built")
+@pytest.mark.parametrize("P,d,sag", [(8, 1, "none"), (6, 1, "none"), (8, 2, "rsag"),
+                                     (6, 3, "bsag")])
+def test_pipeline_vs_reference_grid(env, P, d, sag):
+    """Grid-snapped inputs: the fp32 device path equals the fp64 reference
+    bit-for-bit (hard part 1)."""
+    sd, _, torch = env
+    from pyoracle import Oracle, make_config
+    ref = Oracle("ref").pipeline(make_config(P, 200_000, P * 250, d, sag))
+    ctx = sd.SparDL(sd.ClusterConfig(workers=P, dimension=200_000, k=P * 250, teams=d, sag=sag))
+    rng = np.random.default_rng(1)
+    for _ in range(4):
+        g = gen("grid", (P, 200_000), rng)
+        ctx.all_reduce([torch.from_numpy(g[w]).cuda() for w in range(P)])
+        ref.allreduce(g.astype(np.float64))
+        gi, gv = ctx.global_gradient(0)
+        ri, rv = ref.global_gradient()
+        assert np.array_equal(gi.cpu().numpy().astype(np.int64), ri)
+        assert np.array_equal(gv.cpu().numpy().astype(np.float64), rv)
+        for w in range(P):
+            assert np.array_equal(ctx.carry(w).cpu().numpy().astype(np.float64), ref.carry(w))
+    ctx.close()
