@@ -174,6 +174,14 @@ int spardl_allreduce(spardl_ctx* ctx, const float* const* grads_dev);
  * result copy out are part of the call (the reference's host signature). */
 int spardl_allreduce_host(spardl_ctx* ctx, const float* const* grads_host, int64_t* g_idx,
                           float* g_val, int64_t cap, int64_t* nnz);
+/* Measurement hook (bench.py): runs `iters` extra iterations outside any
+ * CUDA graph with events on the context stream at the phase boundaries and
+ * returns the mean device time per phase in ms: [0] sampling + pre-threshold,
+ * [1] fused residual-add/candidate pass, [2] dividing select, [3] SRS/SAG
+ * stages and rounds, [4] final gather + assemble + finalize + ledger.
+ * The iterations advance the residual state like ordinary calls. */
+int spardl_profile(spardl_ctx* ctx, const float* const* grads_dev, int32_t iters,
+                   double* phase_ms);
 /* wait for the enqueued work; reports device-side errors (NaN input) */
 int spardl_sync(spardl_ctx* ctx);
 /* RunResult scalars of the last call (synchronises; collective when

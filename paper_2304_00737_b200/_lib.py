@@ -135,7 +135,8 @@ EXPORTS = [
     "spardl_topk_select", "spardl_topk_select_slice", "spardl_merge_add",
     "spardl_nccl_unique_id", "spardl_ctx_create", "spardl_ctx_destroy",
     "spardl_ctx_local_workers", "spardl_ctx_set_graph", "spardl_ctx_set_audit",
-    "spardl_allreduce", "spardl_allreduce_host", "spardl_sync", "spardl_get_run_info",
+    "spardl_allreduce", "spardl_allreduce_host", "spardl_profile", "spardl_sync",
+    "spardl_get_run_info",
     "spardl_get_global", "spardl_get_carry", "spardl_ctx_reset_state", "spardl_get_ledger",
     "spardl_get_union_sizes", "spardl_get_controller", "spardl_kernel_launches",
     "spardl_ctx_stream",

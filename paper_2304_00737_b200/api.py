@@ -313,6 +313,14 @@ class SparDL:
                                           C.byref(nnz)))
         return idx[: nnz.value], val[: nnz.value]
 
+    def profile(self, grads, iters: int = 10):
+        """Mean device ms per phase over `iters` non-graph iterations:
+        sample+prethr, candidate pass, dividing select, SRS/SAG, gather+finalize."""
+        ptrs = (C.c_void_p * self.local_workers)(*[g.data_ptr() for g in grads])
+        out = (C.c_double * 5)()
+        check(lib().spardl_profile(self._h, ptrs, C.c_int32(iters), out))
+        return list(out)
+
     def sync(self):
         check(lib().spardl_sync(self._h))
 

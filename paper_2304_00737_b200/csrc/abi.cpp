@@ -484,6 +484,16 @@ EXPORT int spardl_allreduce_host(spardl_ctx* ctx, const float* const* grads_host
   });
 }
 
+EXPORT int spardl_profile(spardl_ctx* ctx, const float* const* grads_dev, int32_t iters,
+                          double* phase_ms) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(grads_dev, "grads");
+    need(phase_ms, "phase_ms");
+    ctx->eng->profile(grads_dev, iters, phase_ms);
+  });
+}
+
 EXPORT int spardl_sync(spardl_ctx* ctx) {
   return guarded([&] {
     need(ctx, "ctx");

@@ -229,17 +229,25 @@ __global__ void __launch_bounds__(kThreads) k_div_cand(const DivTask* __restrict
 
 }  // namespace
 
-void launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sample_every,
-                   int apply_residual, cudaStream_t s) {
-  if (ntask <= 0) return;
-  // sample_every is uniform across a batch (set by the planner)
-  const int sx = (max_chunks + sample_every - 1) / sample_every;
-  k_div_sample<<<dim3(sx, ntask), kThreads, 0, s>>>(tasks_dev, apply_residual);
-  k_div_prethr<<<ntask, kThreads, 0, s>>>(tasks_dev);
-  if (apply_residual)
-    k_div_cand<1><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
-  else
-    k_div_cand<0><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
+int launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sample_every,
+                  int apply_residual, cudaStream_t s, int part) {
+  if (ntask <= 0) return 0;
+  int n = 0;
+  if (part != 2) {
+    // sample_every is uniform across a batch (set by the planner)
+    const int sx = (max_chunks + sample_every - 1) / sample_every;
+    k_div_sample<<<dim3(sx, ntask), kThreads, 0, s>>>(tasks_dev, apply_residual);
+    k_div_prethr<<<ntask, kThreads, 0, s>>>(tasks_dev);
+    n += 2;
+  }
+  if (part != 1) {
+    if (apply_residual)
+      k_div_cand<1><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
+    else
+      k_div_cand<0><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
+    n += 1;
+  }
+  return n;
 }
 
 }  // namespace sdl

@@ -659,12 +659,14 @@ void Engine::plan() {
 
 // ---------------------------------------------------------------------------
 // execution
-void Engine::exec_stage(const Stage& st) {
+int Engine::exec_stage(const Stage& st) {
+  int n = 0;
   if (!st.merges.empty())
-    sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts, st.max_rT,
-                      stream_);
+    n += sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts,
+                           st.max_rT, stream_);
   if (!st.sels.empty())
-    sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_);
+    n += sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_);
+  return n;
 }
 
 void Engine::exec_round(const std::vector<Xfer>& xs) {
@@ -684,23 +686,67 @@ void Engine::exec_round(const std::vector<Xfer>& xs) {
   NK(ncclGroupEnd());
 }
 
-void Engine::enqueue_iteration() {
+// One iteration.  When `ev` is given (profiling, never inside a graph), an
+// event is recorded at each phase boundary:
+//   ev[0] | sample+pre-threshold | ev[1] | candidate pass | ev[2] | dividing
+//   select | ev[3] | SRS + SAG stages and rounds | ev[4] | final gather,
+//   assemble, finalize, ledger | ev[5]
+void Engine::enqueue_iteration(cudaEvent_t* ev) {
+  int n = 0;
+  auto mark = [&](int i) {
+    if (ev) CK(cudaEventRecord(ev[i], stream_));
+  };
   CK(cudaMemsetAsync(ledger_phase_, 0, sizeof(int64_t) * 3 * wloc_, stream_));
   CK(cudaMemsetAsync(hash_dev_, 0, sizeof(int64_t) * d_, stream_));
-  sdl::launch_divide(div_dev_, static_cast<int>(div_tasks_.size()), div_max_chunks_,
-                     div_sample_every_, 1, stream_);
-  exec_stage(div_stage_);
-  for (const Step& s : steps_) {
-    exec_stage(s.stage);
+  mark(0);
+  n += sdl::launch_divide(div_dev_, static_cast<int>(div_tasks_.size()), div_max_chunks_,
+                          div_sample_every_, 1, stream_, 1);
+  mark(1);
+  n += sdl::launch_divide(div_dev_, static_cast<int>(div_tasks_.size()), div_max_chunks_,
+                          div_sample_every_, 1, stream_, 2);
+  mark(2);
+  n += exec_stage(div_stage_);
+  mark(3);
+  for (size_t i = 0; i < steps_.size(); ++i) {
+    const Step& s = steps_[i];
+    n += exec_stage(s.stage);
     if (s.controller_after)
-      sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1, stream_);
+      n += sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1,
+                                  stream_);
+    if (i + 1 == steps_.size()) mark(4);
     exec_round(s.xfers);
   }
-  sdl::launch_assemble(asm_dev_, static_cast<int>(asm_tasks_.size()), m_, cfg_.k, stream_);
-  sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), cfg_.k,
-                       static_cast<int>(fin_max_div_), stream_);
-  sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), stream_);
+  if (steps_.empty()) mark(4);
+  n += sdl::launch_assemble(asm_dev_, static_cast<int>(asm_tasks_.size()), m_, cfg_.k, stream_);
+  n += sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), cfg_.k,
+                            static_cast<int>(fin_max_div_), stream_);
+  n += sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), stream_);
+  mark(5);
   CK(cudaGetLastError());
+  launches_ = n;
+}
+
+void Engine::profile(const float* const* grads, int iters, double* phase_ms) {
+  CK(cudaSetDevice(device_));
+  run(grads);   // refresh pointer table + warm
+  cudaEvent_t ev[6];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  double acc[5] = {0, 0, 0, 0, 0};
+  for (int it = 0; it < iters; ++it) {
+    for (int w = 0; w < P_; ++w)
+      for (int p = 0; p < 3; ++p)
+        rounds_[static_cast<size_t>(w)] +=
+            phase_rounds_[static_cast<size_t>(w)][static_cast<size_t>(p)];
+    enqueue_iteration(ev);
+    CK(cudaEventSynchronize(ev[5]));
+    for (int p = 0; p < 5; ++p) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ev[p], ev[p + 1]));
+      acc[p] += ms;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int p = 0; p < 5; ++p) phase_ms[p] = acc[p] / std::max(iters, 1);
 }
 
 void Engine::run(const float* const* grads) {

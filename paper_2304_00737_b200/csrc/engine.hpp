@@ -83,6 +83,9 @@ class Engine {
   ~Engine();
 
   void run(const float* const* grads_dev);
+  // per-phase device time of `iters` profiled (non-graph) iterations, ms:
+  // [sample+prethr, candidate pass, dividing select, SRS/SAG, gather+finalize]
+  void profile(const float* const* grads_dev, int iters, double* phase_ms);
   void sync();
   void reset_state();
   spardl_run_info run_info();
@@ -123,8 +126,8 @@ class Engine {
   bool is_local(int w) const { return w >= first_ && w < first_ + wloc_; }
   int rank_of(int w) const { return w / wloc_; }
   void exec_round(const std::vector<Xfer>& xs);
-  void exec_stage(const Stage& st);
-  void enqueue_iteration();
+  int exec_stage(const Stage& st);
+  void enqueue_iteration(cudaEvent_t* ev = nullptr);
   void drop_graph();
 
   // --- config

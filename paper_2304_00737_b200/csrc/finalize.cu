@@ -153,18 +153,19 @@ __global__ void k_controller(const CtlTask* __restrict__ tasks, int n, int obser
 
 }  // namespace
 
-void launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t max_k,
-                     cudaStream_t s) {
+int launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t max_k,
+                    cudaStream_t s) {
   (void)max_m;
-  if (ntask <= 0) return;
+  if (ntask <= 0) return 0;
   int gx = (int)((max_k + kThreads - 1) / kThreads);
   gx = gx < 1 ? 1 : (gx > 1184 ? 1184 : gx);
   k_assemble<<<dim3(gx, ntask), kThreads, 0, s>>>(tasks_dev);
+  return 1;
 }
 
-void launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_k, int max_div,
-                     cudaStream_t s) {
-  if (ntask <= 0) return;
+int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_k, int max_div,
+                    cudaStream_t s) {
+  if (ntask <= 0) return 0;
   int gx = (int)((max_k + kThreads - 1) / kThreads);
   gx = gx < 1 ? 1 : (gx > 2368 ? 2368 : gx);
   k_finalize<<<dim3(gx, ntask), kThreads, 0, s>>>(tasks_dev);
@@ -172,18 +173,22 @@ void launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_k, in
     int lx = (max_div + kThreads - 1) / kThreads;
     lx = lx < 1 ? 1 : (lx > 1184 ? 1184 : lx);
     k_finalize_lres<<<dim3(lx, ntask), kThreads, 0, s>>>(tasks_dev);
+    return 2;
   }
+  return 1;
 }
 
-void launch_ledger(const LedgerAdd* adds_dev, int nadd, cudaStream_t s) {
-  if (nadd <= 0) return;
+int launch_ledger(const LedgerAdd* adds_dev, int nadd, cudaStream_t s) {
+  if (nadd <= 0) return 0;
   const int gx = (nadd + kThreads - 1) / kThreads;
   k_ledger<<<gx, kThreads, 0, s>>>(adds_dev, nadd);
+  return 1;
 }
 
-void launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStream_t s) {
-  if (ntask <= 0) return;
+int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStream_t s) {
+  if (ntask <= 0) return 0;
   k_controller<<<(ntask + 127) / 128, 128, 0, s>>>(tasks_dev, ntask, observe);
+  return 1;
 }
 
 }  // namespace sdl

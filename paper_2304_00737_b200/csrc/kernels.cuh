@@ -146,11 +146,12 @@ struct DivTask {
 // Launchers (stream-ordered; no host synchronisation inside)
 // ---------------------------------------------------------------------------
 // tasks_dev: device copy of the task array; ntask; max_nseg: grid extent.
-void launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s);
-void launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T,
+int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s);
+int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T,
                   cudaStream_t s);
-void launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sample_every,
-                   int apply_residual, cudaStream_t s);
+// part: 0 = whole pass, 1 = sample + pre-threshold only, 2 = candidate pass only
+int launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sample_every,
+                  int apply_residual, cudaStream_t s, int part = 0);
 
 // Finalize / assembly helpers
 struct GatherSrc {            // one source block of an assembled global gradient
@@ -167,7 +168,7 @@ struct AssembleTask {
   int32_t* out_cnt;
   int64_t* out_hash;          // nullable: FNV-style hash for consistency checks
 };
-void launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t max_k,
+int launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t max_k,
                      cudaStream_t s);
 
 constexpr int kMaxXi = 24;
@@ -189,7 +190,7 @@ struct FinalizeTask {
   const int32_t* xi_off;      // [m+1] offsets into xi
   const XiList* xi;           // lists
 };
-void launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_k, int max_div,
+int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_k, int max_div,
                      cudaStream_t s);
 
 // ledger: scalars += 2 * count for each (worker slot, count pointer)
@@ -197,7 +198,7 @@ struct LedgerAdd {
   int64_t* dst;
   const int32_t* cnt;
 };
-void launch_ledger(const LedgerAdd* adds_dev, int nadd, cudaStream_t s);
+int launch_ledger(const LedgerAdd* adds_dev, int nadd, cudaStream_t s);
 
 // B-SAG controller (Algorithm 2, inc/sag.hpp:37-90) on the device
 struct HCtl {
@@ -212,6 +213,6 @@ struct CtlTask {
   const int64_t* n_t;         // its group's union size
   int64_t* budget;            // pre-selection budget for the next run
 };
-void launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStream_t s);
+int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStream_t s);
 
 }  // namespace sdl

@@ -190,9 +190,9 @@ __global__ void __launch_bounds__(kThreads) k_merge_part(const MergeTask* __rest
 
 }  // namespace
 
-void launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T,
-                  cudaStream_t s) {
-  if (ntask <= 0 || max_parts <= 0) return;
+int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T,
+                 cudaStream_t s) {
+  if (ntask <= 0 || max_parts <= 0) return 0;
   const int rx = (max_parts + kThreads - 1) / kThreads;
   k_merge_rank<<<dim3(rx, ntask), kThreads, 0, s>>>(tasks_dev);
   const size_t smem = (size_t)max_r_T * 16;
@@ -203,6 +203,7 @@ void launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_
     configured = smem;
   }
   k_merge_part<<<dim3(max_parts, ntask), kThreads, smem, s>>>(tasks_dev);
+  return 2;
 }
 
 }  // namespace sdl

@@ -325,8 +325,8 @@ __global__ void __launch_bounds__(kThreads) k_sel_write(const SelTask* __restric
 
 }  // namespace
 
-void launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s) {
-  if (ntask <= 0) return;
+int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s) {
+  if (ntask <= 0) return 0;
   const int gx = max_nseg < 1 ? 1 : (max_nseg > 8192 ? 8192 : max_nseg);
   const int hx = max_nseg < 1 ? 1 : (max_nseg > 1184 ? 1184 : max_nseg);
   dim3 g2(gx, ntask), gh(hx, ntask);
@@ -339,6 +339,7 @@ void launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream
   k_sel_count<<<g2, kThreads, 0, s>>>(tasks_dev);
   k_sel_scan<<<ntask, kThreads, 0, s>>>(tasks_dev);
   k_sel_write<<<g2, kThreads, 0, s>>>(tasks_dev);
+  return 9;
 }
 
 }  // namespace sdl
