@@ -291,6 +291,7 @@ def main():
         out["launches"] = ctx.kernel_launches()
         info = ctx.run_info()
         out["consistent"] = info["consistent"]
+        out["dense_fallbacks"] = ctx.dense_fallbacks()
         out["ledger"] = (info["max_rounds"], info["max_scalars"])
         if extras:
             ph = ctx.profile(grads, iters=min(20, max(3, steps)))
@@ -406,6 +407,7 @@ def main():
         "clocks": r.get("clocks"),
         "gpu_launches": int(r["launches"]) * steps * world,
         "consistent": bool(r["consistent"]),
+        "dense_fallbacks_last_step": r["dense_fallbacks"],
         "ledger": {"max_rounds": r["ledger"][0], "max_scalars": r["ledger"][1]},
     }
     if "e2e_ms" in r:

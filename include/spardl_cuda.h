@@ -201,6 +201,12 @@ int spardl_get_ledger(spardl_ctx* ctx, int64_t* rounds, int64_t* scalars);
 int spardl_get_union_sizes(spardl_ctx* ctx, int64_t* out);
 /* WorkerState::controller of local worker i (B-SAG only) */
 int spardl_get_controller(spardl_ctx* ctx, int32_t local_worker, spardl_hctrl* out);
+/* diagnostics: dividing selections of the last call that could not use the
+ * candidate fast path and selected from the dense slice (synchronises) */
+int spardl_dense_fallbacks(spardl_ctx* ctx, int64_t* count);
+/* diagnostics of local dividing task i (= local_worker * m + block):
+ * [resolved mode, candidate flags, candidate total, list length, pre-key, capacity] */
+int spardl_div_diag(spardl_ctx* ctx, int32_t task, int64_t* out6);
 /* number of kernels this context launches per iteration */
 int spardl_kernel_launches(const spardl_ctx* ctx, int64_t* per_iteration);
 /* the stream the context enqueues on (cudaStream_t) */

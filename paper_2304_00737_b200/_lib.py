@@ -138,7 +138,8 @@ EXPORTS = [
     "spardl_allreduce", "spardl_allreduce_host", "spardl_profile", "spardl_sync",
     "spardl_get_run_info",
     "spardl_get_global", "spardl_get_carry", "spardl_ctx_reset_state", "spardl_get_ledger",
-    "spardl_get_union_sizes", "spardl_get_controller", "spardl_kernel_launches",
+    "spardl_get_union_sizes", "spardl_get_controller", "spardl_dense_fallbacks",
+    "spardl_kernel_launches",
     "spardl_ctx_stream",
 ]
 
@@ -170,3 +171,4 @@ def check(rc: int) -> None:
     if rc != 0:
         msg = lib().spardl_last_error().decode()
         raise _BY_CODE.get(rc, SpardlError)(msg, rc)
+EXPORTS.append("spardl_div_diag")

@@ -369,6 +369,11 @@ class SparDL:
         check(lib().spardl_get_controller(self._h, C.c_int32(local), C.byref(c)))
         return {"h": c.h, "step": c.step, "flag": c.flag, "target": c.target}
 
+    def dense_fallbacks(self) -> int:
+        n = C.c_int64()
+        check(lib().spardl_dense_fallbacks(self._h, C.byref(n)))
+        return n.value
+
     def kernel_launches(self) -> int:
         n = C.c_int64()
         check(lib().spardl_kernel_launches(self._h, C.byref(n)))

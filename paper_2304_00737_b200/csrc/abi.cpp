@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "divplan.hpp"
 #include "engine.hpp"
 #include "host.hpp"
 #include "kernels.cuh"
@@ -73,7 +74,8 @@ void require_device() {
 
 // One select over prepared inputs, with its scratch.
 void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf) {
-  const int nseg = std::max(std::max(t.nseg, t.dnseg), 1);
+  sdl::sel_prepare(t, t.stride);
+  const int nseg = std::max(1, sdl::sel_scratch_segments(t));
   t.scr = buf.get<sdl::SelScratch>(1);
   int32_t* segs = buf.get<int32_t>(5 * static_cast<size_t>(nseg));
   t.seg_gt = segs;
@@ -83,7 +85,7 @@ void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf) {
   t.seg_take = segs + 4 * nseg;
   sdl::SelTask* td = buf.get<sdl::SelTask>(1);
   CK(cudaMemcpyAsync(td, &t, sizeof(t), cudaMemcpyHostToDevice, s));
-  sdl::launch_select(td, 1, nseg, s);
+  sdl::launch_select(td, 1, std::max(1, sdl::sel_grid_segments(t)), s);
   CK(cudaGetLastError());
 }
 
@@ -220,8 +222,8 @@ EXPORT int spardl_topk_select(const int32_t* idx, const float* val, int64_t n, i
     t.idx = idx;
     t.val = val;
     t.count = cnt;
-    t.stride = 2048;
-    t.nseg = static_cast<int32_t>((n + 2047) / 2048);
+    t.stride = sdl::kTile;
+    t.nseg = static_cast<int32_t>((n + sdl::kTile - 1) / sdl::kTile);
     t.budget = budget;
     t.sel_idx = sel_idx;
     t.sel_val = sel_val;
@@ -255,53 +257,20 @@ EXPORT int spardl_topk_select_slice(const float* g, int64_t lo, int64_t hi, int6
       return;
     }
     DevBuf buf;
-    const int64_t A = lo & ~int64_t(3);
-    const int nch = static_cast<int>((hi - A + sdl::kChunk - 1) / sdl::kChunk);
-    const double frac = static_cast<double>(budget) / static_cast<double>(nb);
-    int cap = static_cast<int>(
-        std::min<double>(sdl::kChunk, std::max(1024.0, sdl::kChunk * 2.5 * frac + 256.0)));
-    cap = (cap + 3) & ~3;
     sdl::DivTask dt{};
+    sdl::SelTask t{};
+    sdl::div_plan(dt, t, lo, hi, budget,
+                  [&](size_t n) { return static_cast<void*>(buf.get<unsigned char>(n)); });
     dt.carry = const_cast<float*>(g);   // read only when apply_residual == 0
-    dt.lo = static_cast<int32_t>(lo);
-    dt.hi = static_cast<int32_t>(hi);
-    dt.nchunks = nch;
-    dt.cap = cap;
-    dt.budget = budget;
-    dt.use_cand = frac <= 0.25 ? 1 : 0;
-    const size_t ncand = static_cast<size_t>(nch) * cap;
-    dt.cand_idx = buf.get<int32_t>(ncand);
-    dt.cand_val = buf.get<float>(ncand);
-    dt.cand_cnt = buf.get<int32_t>(nch);
-    dt.cand_total = buf.get<int64_t>(1);
-    dt.cand_bad = buf.get<int32_t>(1);
-    dt.pre_key = buf.get<uint32_t>(1);
-    dt.samp_hist = buf.get<uint32_t>(sdl::kBins);
-    dt.sample_every = std::max(1, nch / 32);
     dt.err = buf.get<int32_t>(1);
     sdl::DivTask* dtd = buf.get<sdl::DivTask>(1);
     CK(cudaMemcpyAsync(dtd, &dt, sizeof(dt), cudaMemcpyHostToDevice, s));
-    sdl::launch_divide(dtd, 1, nch, dt.sample_every, 0, s);
+    sdl::launch_divide(dtd, 1, dt.nchunks, dt.sample_every, 0, s);
     int32_t* cnt = buf.get<int32_t>(1);
-    sdl::SelTask t{};
-    t.mode_from_cand = 1;
-    t.idx = dt.cand_idx;
-    t.val = dt.cand_val;
-    t.seg_cnt = dt.cand_cnt;
-    t.stride = cap;
-    t.nseg = nch;
     t.dval = g + lo;
-    t.dbase = static_cast<int32_t>(lo);
-    t.dn = static_cast<int32_t>(nb);
-    t.dstride = sdl::kChunk;
-    t.dnseg = static_cast<int32_t>((nb + sdl::kChunk - 1) / sdl::kChunk);
-    t.cand_total = dt.cand_total;
-    t.cand_bad = dt.cand_bad;
-    t.budget = budget;
     t.sel_idx = sel_idx;
     t.sel_val = sel_val;
     t.sel_cnt = cnt;
-    t.weight = 1.f;
     run_select(t, s, buf);
     int32_t out = 0, err = 0;
     CK(cudaMemcpyAsync(&out, cnt, sizeof(out), cudaMemcpyDeviceToHost, s));
@@ -336,7 +305,7 @@ EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* c
       mt.in_val[q] = val[q];
       mt.in_cnt[q] = cnts + q;
     }
-    int64_t T = std::max<int64_t>(8192 / r, (capsum + sdl::kMaxSamples - 1) / sdl::kMaxSamples);
+    int64_t T = std::max<int64_t>(2048 / r, (capsum + sdl::kMaxSamples - 1) / sdl::kMaxSamples);
     T = std::max<int64_t>(T, 32);
     if (static_cast<int64_t>(r) * T > 12800)
       sdlh::fail(SPARDL_E_UNSUPPORTED, "merge of this size exceeds the shared-memory envelope");
@@ -362,6 +331,7 @@ EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* c
     t.seg_off = mt.seg_off;
     t.seg_cnt = mt.seg_cnt;
     t.nseg = static_cast<int32_t>(parts);
+    t.stride = static_cast<int32_t>(r * T);
     t.budget = INT64_MAX;   // identity selection == ordered compaction
     t.sel_idx = out_idx;
     t.sel_val = out_val;
@@ -552,6 +522,20 @@ EXPORT int spardl_get_controller(spardl_ctx* ctx, int32_t local_worker, spardl_h
   return guarded([&] {
     need(ctx, "ctx");
     ctx->eng->controller(local_worker, out);
+  });
+}
+
+EXPORT int spardl_dense_fallbacks(spardl_ctx* ctx, int64_t* count) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    *count = ctx->eng->dense_fallbacks();
+  });
+}
+
+EXPORT int spardl_div_diag(spardl_ctx* ctx, int32_t task, int64_t* out6) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->div_diag(task, out6);
   });
 }
 

@@ -37,34 +37,51 @@ __global__ void __launch_bounds__(kThreads) k_div_sample(const DivTask* __restri
   if (!t.use_cand) return;
   const int c = blockIdx.x * t.sample_every;
   if (c >= t.nchunks) return;
-  __shared__ uint32_t h[kBins];
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
+  // 13-bit key histogram (8 exponent + 5 mantissa bits: 1/32-octave bins)
+  extern __shared__ uint32_t h[];
+  __shared__ unsigned int bmin, bmax;
+  for (int b = threadIdx.x; b < kSampBins; b += blockDim.x) h[b] = 0;
+  if (threadIdx.x == 0) {
+    bmin = kSampBins;
+    bmax = 0;
+  }
   __syncthreads();
   const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
   const int64_t s = A > t.lo ? A : t.lo;
   const int64_t e = (A + kChunk) < t.hi ? (A + kChunk) : t.hi;
-  for (int64_t i = s + threadIdx.x; i < e; i += blockDim.x) {
-    const float v = apply_residual ? __fadd_rn(t.g_tab[t.g_id][i], t.carry[i]) : t.carry[i];
-    atomicAdd(&h[mag_key(v) >> 20], 1u);
+  const float* g = apply_residual ? t.g_tab[t.g_id] : nullptr;
+  for (int64_t i0 = s; i0 < e; i0 += blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool in = i < e;
+    float v = 0.f;
+    if (in) v = apply_residual ? __fadd_rn(__ldcs(g + i), __ldcs(t.carry + i)) : t.carry[i];
+    // warp-aggregated: sampled keys crowd into a few top-bit bins
+    const uint32_t bin = mag_key(v) >> kSampShift;
+    const uint32_t am = __ballot_sync(0xffffffffu, in);
+    if (in) {
+      const uint32_t peers = __match_any_sync(am, bin);
+      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+    }
+    const unsigned lo_b = __reduce_min_sync(0xffffffffu, in ? bin : (unsigned)kSampBins);
+    const unsigned hi_b = __reduce_max_sync(0xffffffffu, in ? bin : 0u);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&bmin, lo_b);
+      atomicMax(&bmax, hi_b);
+    }
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+  for (int b = bmin + threadIdx.x; b <= (int)bmax; b += blockDim.x)
     if (h[b]) atomicAdd(&t.samp_hist[b], h[b]);
 }
 
 __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restrict__ tasks) {
   const DivTask& t = tasks[blockIdx.x];
-  constexpr int BPT = kBins / kThreads;
+  constexpr int BPT = kSampBins / kThreads;
   __shared__ long long suf[kThreads];
   __shared__ long long lscr[32];
-  uint32_t c[BPT];
+  uint32_t* hist = t.samp_hist + threadIdx.x * BPT;
   long long mine = 0;
-#pragma unroll
-  for (int q = 0; q < BPT; ++q) {
-    c[q] = t.samp_hist[threadIdx.x * BPT + q];
-    t.samp_hist[threadIdx.x * BPT + q] = 0;
-    mine += c[q];
-  }
+  for (int q = 0; q < BPT; ++q) mine += hist[q];
   const long long ns = block_sum_ll(mine, lscr);
   const int64_t nb = (int64_t)t.hi - t.lo;
   if (threadIdx.x == 0) {
@@ -72,16 +89,13 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
     *t.cand_bad = t.use_cand ? 0 : 1;
     *t.pre_key = 0;
   }
-  if (!t.use_cand || ns == 0) {
-    if (threadIdx.x == 0) *t.cand_bad = 1;
-    return;
-  }
   // target rank inside the sample: 1.25 L scaled to the sample, plus 4 sigma
   const double frac = (double)t.budget / (double)nb;
   const double expect = frac * (double)ns;
   const long long target = (long long)(1.25 * expect + 4.0 * sqrt(expect + 1.0) + 8.0);
-  if (target >= ns) {
+  if (!t.use_cand || ns == 0 || target >= ns) {
     if (threadIdx.x == 0) *t.cand_bad = 1;
+    for (int q = 0; q < BPT; ++q) hist[q] = 0;   // leave the histogram zeroed
     return;
   }
   // reverse inclusive scan (Hillis-Steele over descending thread order)
@@ -101,13 +115,15 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
   if (above < target && target <= above + mine) {
     long long cum = above;
     for (int q = BPT - 1; q >= 0; --q) {
-      if (cum + (long long)c[q] >= target) {
-        *t.pre_key = (uint32_t)(threadIdx.x * BPT + q) << 20;
+      const uint32_t cq = hist[q];
+      if (cum + (long long)cq >= target) {
+        *t.pre_key = (uint32_t)(threadIdx.x * BPT + q) << kSampShift;
         break;
       }
-      cum += c[q];
+      cum += cq;
     }
   }
+  for (int q = 0; q < BPT; ++q) hist[q] = 0;   // leave the histogram zeroed
 }
 
 template <int APPLY>
@@ -115,7 +131,9 @@ __global__ void __launch_bounds__(kThreads) k_div_cand(const DivTask* __restrict
   const DivTask& t = tasks[blockIdx.y];
   const int c = blockIdx.x;
   if (c >= t.nchunks) return;
-  const bool cand = !(*t.cand_bad);
+  // participation in the look-back is decided by the pre-threshold kernel
+  // only (bit 0), never by an overflow seen later in this kernel (bit 1)
+  const bool cand = !(*t.cand_bad & 1);
   const uint32_t pre = *t.pre_key;
   const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -198,9 +216,9 @@ __global__ void __launch_bounds__(kThreads) k_div_cand(const DivTask* __restrict
   }
   __syncthreads();
   const int total = wtot[kThreads / 32];
-  if (total > t.cap) {
+  if (total > t.cap) {   // chunk segment overflow: the select falls back to the dense slice
     if (threadIdx.x == 0) {
-      *t.cand_bad = 1;
+      atomicOr(t.cand_bad, 2);
       t.cand_cnt[c] = 0;
     }
     return;
@@ -221,9 +239,38 @@ __global__ void __launch_bounds__(kThreads) k_div_cand(const DivTask* __restrict
       }
     }
   }
+  if (threadIdx.x == 0) t.cand_cnt[c] = total;
+}
+
+// One CTA per task: the work list of the dividing select -- every chunk
+// segment cut into tiles of <= kTile candidates, in chunk (= index) order --
+// and the candidate total.  Unused tile slots get count 0.
+__global__ void __launch_bounds__(1024) k_div_tiles(const DivTask* __restrict__ tasks) {
+  const DivTask& t = tasks[blockIdx.x];
+  __shared__ int scratch[40];
+  if (*t.cand_bad & 1) return;
+  int tile_carry = 0, cand_carry = 0;
+  for (int c0 = 0; c0 < t.nchunks; c0 += blockDim.x) {
+    const int c = c0 + threadIdx.x;
+    const int cnt = c < t.nchunks ? t.cand_cnt[c] : 0;
+    const int nt = (cnt + kTile - 1) / kTile;
+    int ttot, ctot;
+    const int tbase = tile_carry + block_exscan(nt, scratch, &ttot);
+    block_exscan(cnt, scratch, &ctot);
+    for (int j = 0; j < nt; ++j) {
+      const int q = tbase + j;
+      if (q < t.max_tiles) {
+        t.tile_off[q] = c * t.cap + j * kTile;
+        t.tile_cnt[q] = min(kTile, cnt - j * kTile);
+      }
+    }
+    tile_carry += ttot;
+    cand_carry += ctot;
+  }
+  for (int q = tile_carry + threadIdx.x; q < t.max_tiles; q += blockDim.x) t.tile_cnt[q] = 0;
   if (threadIdx.x == 0) {
-    t.cand_cnt[c] = total;
-    atomicAdd(reinterpret_cast<unsigned long long*>(t.cand_total), (unsigned long long)total);
+    *t.cand_total = cand_carry;
+    if (tile_carry > t.max_tiles) *t.cand_bad |= 2;   // work list capacity: dense fallback
   }
 }
 
@@ -236,7 +283,13 @@ int launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sampl
   if (part != 2) {
     // sample_every is uniform across a batch (set by the planner)
     const int sx = (max_chunks + sample_every - 1) / sample_every;
-    k_div_sample<<<dim3(sx, ntask), kThreads, 0, s>>>(tasks_dev, apply_residual);
+    const int smem = kSampBins * (int)sizeof(uint32_t);
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(k_div_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      configured = true;
+    }
+    k_div_sample<<<dim3(sx, ntask), kThreads, smem, s>>>(tasks_dev, apply_residual);
     k_div_prethr<<<ntask, kThreads, 0, s>>>(tasks_dev);
     n += 2;
   }
@@ -245,7 +298,8 @@ int launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sampl
       k_div_cand<1><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
     else
       k_div_cand<0><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
-    n += 1;
+    k_div_tiles<<<ntask, 1024, 0, s>>>(tasks_dev);
+    n += 2;
   }
   return n;
 }

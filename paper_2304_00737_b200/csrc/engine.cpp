@@ -11,6 +11,8 @@
 // counts of the blocks each worker receives.
 #include "engine.hpp"
 
+#include "divplan.hpp"
+
 #include <algorithm>
 #include <array>
 #include <cstring>
@@ -32,7 +34,6 @@ namespace sdle {
   } while (0)
 
 namespace {
-constexpr int kSelStride = 2048;   // segment length when selecting from a compact list
 constexpr int kMergeSmemEntries = 12800;
 }  // namespace
 
@@ -167,7 +168,9 @@ Slot Engine::make_slot() {
 
 void Engine::add_select(Stage& st, const sdl::SelTask& t0) {
   sdl::SelTask t = t0;
-  const int nseg = std::max(t.nseg, t.dnseg);
+  // t.stride carries the longest possible input segment (see callers)
+  sdl::sel_prepare(t, t.stride);
+  const int nseg = std::max(1, sdl::sel_scratch_segments(t));
   t.scr = static_cast<sdl::SelScratch*>(arena_.alloc(sizeof(sdl::SelScratch)));
   int32_t* segs = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * 5 * std::max(nseg, 1)));
   t.seg_gt = segs;
@@ -175,7 +178,7 @@ void Engine::add_select(Stage& st, const sdl::SelTask& t0) {
   t.seg_sel_off = segs + 2 * nseg;
   t.seg_dis_off = segs + 3 * nseg;
   t.seg_take = segs + 4 * nseg;
-  st.max_nseg = std::max(st.max_nseg, nseg);
+  st.max_nseg = std::max(st.max_nseg, sdl::sel_grid_segments(t));
   st.sels.push_back(t);
 }
 
@@ -185,8 +188,8 @@ sdl::SelTask Engine::select_from_slot(const Slot& in) {
   t.idx = in.idx;
   t.val = in.val;
   t.count = in.cnt;
-  t.stride = kSelStride;
-  t.nseg = static_cast<int32_t>((in.cap + kSelStride - 1) / kSelStride);
+  t.stride = sdl::kTile;
+  t.nseg = static_cast<int32_t>((in.cap + sdl::kTile - 1) / sdl::kTile);
   t.weight = 1.f;
   return t;
 }
@@ -204,7 +207,7 @@ sdl::SelTask Engine::select_from_merge(Stage& st, const std::vector<int>& pieces
     mt.in_cnt[q] = s.cnt;
     capsum += s.cap;
   }
-  int64_t T = std::max<int64_t>(8192 / r, (capsum + sdl::kMaxSamples - 1) / sdl::kMaxSamples);
+  int64_t T = std::max<int64_t>(2048 / r, (capsum + sdl::kMaxSamples - 1) / sdl::kMaxSamples);
   T = std::max<int64_t>(T, 32);
   if (static_cast<int64_t>(r) * T > kMergeSmemEntries)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "merge of this size exceeds the shared-memory envelope");
@@ -230,6 +233,7 @@ sdl::SelTask Engine::select_from_merge(Stage& st, const std::vector<int>& pieces
   t.seg_off = mt.seg_off;
   t.seg_cnt = mt.seg_cnt;
   t.nseg = static_cast<int32_t>(parts);
+  t.stride = static_cast<int32_t>(r * T);   // longest partition (offsets come from seg_off)
   t.weight = 1.f;
   return t;
 }
@@ -317,6 +321,8 @@ void Engine::finish_stage(Stage& st) {
 void Engine::plan() {
   const int64_t N = cfg_.dimension;
   div_uid_.assign(static_cast<size_t>(wloc_), std::vector<int>(static_cast<size_t>(m_), -1));
+  div_scr_.assign(static_cast<size_t>(wloc_),
+                  std::vector<const sdl::SelScratch*>(static_cast<size_t>(m_), nullptr));
   xi_.assign(static_cast<size_t>(wloc_),
              std::vector<std::vector<sdl::XiList>>(static_cast<size_t>(m_)));
   std::vector<std::vector<std::vector<int>>> held(
@@ -336,60 +342,27 @@ void Engine::plan() {
       Slot out = make_slot();
       slots_[uid] = out;
       const int64_t lo = part_.lo[static_cast<size_t>(b)], hi = part_.hi[static_cast<size_t>(b)];
-      const int64_t nb = hi - lo;
-      const int64_t A = lo & ~static_cast<int64_t>(3);
-      const int nch = static_cast<int>((hi - A + sdl::kChunk - 1) / sdl::kChunk);
-      const double frac = static_cast<double>(L_) / static_cast<double>(nb);
-      int cap = static_cast<int>(std::min<double>(sdl::kChunk,
-                                                  std::max(1024.0, sdl::kChunk * 2.5 * frac + 256.0)));
-      cap = (cap + 3) & ~3;
       sdl::DivTask dt{};
+      sdl::SelTask t{};
+      sdl::div_plan(dt, t, lo, hi, L_, [&](size_t n) { return arena_.alloc(n); });
       dt.g_tab = gtab_dev_;
       dt.g_id = li;
       dt.carry = carry_[static_cast<size_t>(li)];
-      dt.lo = static_cast<int32_t>(lo);
-      dt.hi = static_cast<int32_t>(hi);
-      dt.nchunks = nch;
-      dt.cap = cap;
-      dt.budget = L_;
-      dt.use_cand = frac <= 0.25 ? 1 : 0;
-      const size_t ncand = dt.use_cand ? static_cast<size_t>(nch) * cap : 4;
-      dt.cand_idx = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * ncand));
-      dt.cand_val = static_cast<float*>(arena_.alloc(sizeof(float) * ncand));
-      dt.cand_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * nch));
-      dt.cand_total = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t)));
-      dt.cand_bad = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
-      dt.pre_key = static_cast<uint32_t*>(arena_.alloc(sizeof(uint32_t)));
-      dt.samp_hist = static_cast<uint32_t*>(arena_.alloc(sizeof(uint32_t) * sdl::kBins));
-      dt.sample_every = std::max(1, nch / 32);
       dt.err = err_dev_;
       div_tasks_.push_back(dt);
-      max_chunks = std::max(max_chunks, nch);
-
-      sdl::SelTask t{};
-      t.mode_from_cand = 1;
-      t.idx = dt.cand_idx;
-      t.val = dt.cand_val;
-      t.seg_cnt = dt.cand_cnt;
-      t.stride = cap;
-      t.nseg = nch;
+      max_chunks = std::max(max_chunks, dt.nchunks);
       t.dval = dt.carry + lo;
-      t.dbase = static_cast<int32_t>(lo);
-      t.dn = static_cast<int32_t>(nb);
-      t.dstride = sdl::kChunk;
-      t.dnseg = static_cast<int32_t>((nb + sdl::kChunk - 1) / sdl::kChunk);
-      t.cand_total = dt.cand_total;
-      t.cand_bad = dt.cand_bad;
-      t.budget = L_;
       t.sel_idx = out.idx;
       t.sel_val = out.val;
       t.sel_cnt = out.cnt;
-      t.weight = 1.f;
       add_select(div_stage_, t);
+      div_scr_[static_cast<size_t>(li)][static_cast<size_t>(b)] = div_stage_.sels.back().scr;
     }
   }
   // one sample_every for the whole batch (the launcher sizes its grid with it)
-  div_sample_every_ = std::max(1, max_chunks / 32);
+  // ~8 sampled chunks (65k elements) per block: ~650 expected top-L samples
+  // at 1% density whatever the block size (the 4-sigma margin is ~15%)
+  div_sample_every_ = std::max(1, max_chunks / 8);
   for (auto& dt : div_tasks_) dt.sample_every = div_sample_every_;
   div_max_chunks_ = max_chunks;
   if (!div_tasks_.empty()) {
@@ -592,6 +565,7 @@ void Engine::plan() {
             static_cast<int>(global_.size());
     global_.push_back(gs);
     global_team_.push_back(t);
+    team_src_.push_back(src_dev);
   }
   (void)max_m;
   asm_dev_ = static_cast<sdl::AssembleTask*>(
@@ -606,9 +580,12 @@ void Engine::plan() {
     ft.m = m_;
     ft.n = N;
     ft.carry = carry_[static_cast<size_t>(li)];
-    const Slot& gs = global_[static_cast<size_t>(team_of_local_global_[static_cast<size_t>(li)])];
-    ft.g_idx = gs.idx;
-    ft.g_cnt = gs.cnt;
+    ft.gblk = team_src_[static_cast<size_t>(team_of_local_global_[static_cast<size_t>(li)])];
+    auto* sc_dev = static_cast<const sdl::SelScratch**>(
+        arena_.alloc(sizeof(sdl::SelScratch*) * m_));
+    CK(cudaMemcpy(sc_dev, div_scr_[static_cast<size_t>(li)].data(), sizeof(sdl::SelScratch*) * m_,
+                  cudaMemcpyHostToDevice));
+    ft.div_sc = sc_dev;
     std::vector<sdl::GatherSrc> div;
     std::vector<int32_t> xoff;
     std::vector<sdl::XiList> xl;
@@ -718,7 +695,7 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   }
   if (steps_.empty()) mark(4);
   n += sdl::launch_assemble(asm_dev_, static_cast<int>(asm_tasks_.size()), m_, cfg_.k, stream_);
-  n += sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), cfg_.k,
+  n += sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), Lcap_, m_,
                             static_cast<int>(fin_max_div_), stream_);
   n += sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), stream_);
   mark(5);
@@ -920,6 +897,39 @@ spardl_run_info Engine::run_info() {
   ri.conservation_error = -1.0;
   ri.n_union = cfg_.sag == SPARDL_SAG_BSAG ? m_ : 0;
   return ri;
+}
+
+void Engine::div_diag(int task, int64_t* out) {
+  sync();
+  const sdl::DivTask& dt = div_tasks_.at(static_cast<size_t>(task));
+  int32_t bad = 0, cnt = 0, mode = 0;
+  int64_t tot = 0;
+  uint32_t pre = 0;
+  CK(cudaMemcpy(&bad, dt.cand_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+  cnt = dt.max_tiles;
+  CK(cudaMemcpy(&tot, dt.cand_total, sizeof(tot), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&pre, dt.pre_key, sizeof(pre), cudaMemcpyDeviceToHost));
+  const int li = task / m_, b = task % m_;
+  CK(cudaMemcpy(&mode, &div_scr_[static_cast<size_t>(li)][static_cast<size_t>(b)]->mode,
+                sizeof(mode), cudaMemcpyDeviceToHost));
+  out[0] = mode;
+  out[1] = bad;
+  out[2] = tot;
+  out[3] = cnt;
+  out[4] = pre;
+  out[5] = dt.cap;
+}
+
+int64_t Engine::dense_fallbacks() {
+  sync();
+  int64_t n = 0;
+  for (const auto& row : div_scr_)
+    for (const sdl::SelScratch* sc : row) {
+      int32_t mode = 0;
+      CK(cudaMemcpy(&mode, &sc->mode, sizeof(mode), cudaMemcpyDeviceToHost));
+      n += mode == 1;
+    }
+  return n;
 }
 
 void Engine::union_sizes(int64_t* out) {

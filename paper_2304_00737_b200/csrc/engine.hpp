@@ -91,6 +91,10 @@ class Engine {
   spardl_run_info run_info();
   void ledger(int64_t* rounds, int64_t* scalars);
   void union_sizes(int64_t* out);
+  // dividing selects of the last iteration that fell back to the dense path
+  int64_t dense_fallbacks();
+  // [mode, cand_bad, cand_total, cand_count, pre_key, cap] of dividing task i
+  void div_diag(int task, int64_t* out);
   void controller(int local, spardl_hctrl* out);
   void global(int local, const int32_t** idx, const float** val, int64_t* nnz);
   float* carry(int local) { return carry_[static_cast<size_t>(local)]; }
@@ -183,6 +187,8 @@ class Engine {
   std::vector<int> global_team_;             // team id of each global_ entry
   // per local worker, per block: dividing outputs and discard lists
   std::vector<std::vector<int>> div_uid_;
+  std::vector<std::vector<const sdl::SelScratch*>> div_scr_;
+  std::vector<const sdl::GatherSrc*> team_src_;   // per global_ entry: the m reserved blocks
   std::vector<std::vector<std::vector<sdl::XiList>>> xi_;
   std::vector<int> union_group_owner_;       // position group -> worker providing N_t
   bool ran_ = false;

@@ -1,5 +1,7 @@
 // Global-gradient assembly, residual finalize, ledger and the B-SAG
 // controller on the device.
+#include <climits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -70,33 +72,113 @@ __device__ __forceinline__ int block_of_dev(int64_t n, int m, int64_t i) {
   return (int)(rem + (i - split) / base);
 }
 
-__global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __restrict__ tasks) {
-  const FinalizeTask& t = tasks[blockIdx.y];
-  if (t.mode == 2) return;   // lres ignores the global gradient
-  const int gn = *t.g_cnt;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < gn; e += gridDim.x * blockDim.x) {
-    const int32_t j = t.g_idx[e];
-    if (t.mode == 1) {
-      t.carry[j] = 0.f;
-      continue;
+// Warp-cooperative lower/upper bound over a sorted global array (32-ary
+// search: ~log32(n) rounds of one load per lane instead of log2(n)
+// dependent loads).  Must be called by a full warp.
+__device__ __forceinline__ int warp_bound(const int32_t* a, int n, int32_t x, bool upper) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = n;   // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) / 32;
+    const int p = lo + lane * step;
+    const int32_t v = p < hi ? a[p] : INT_MAX;
+    const bool below = upper ? (v <= x) : (v < x);
+    const int c = __popc(__ballot_sync(0xffffffffu, below && p < hi));
+    if (c == 0) {
+      hi = lo;
+    } else {
+      const int nlo = lo + (c - 1) * step + 1;
+      const int nhi = lo + c * step;
+      lo = nlo;
+      hi = nhi < hi ? nhi : hi;
     }
-    const int b = block_of_dev(t.n, t.m, j);
-    const GatherSrc d = t.div[b];
-    const int dn = *d.cnt;
-    const int p = lower_bound_i32(d.idx, dn, j);
-    bool present = !(p < dn && d.idx[p] == j);
-    float acc = present ? t.carry[j] : 0.f;
-    for (int q = t.xi_off[b]; q < t.xi_off[b + 1]; ++q) {
-      const XiList x = t.xi[q];
-      const int xn = *x.cnt;
-      const int r = lower_bound_i32(x.idx, xn, j);
-      if (r < xn && x.idx[r] == j) {
-        const float xv = x.val[r];
-        acc = present ? __fadd_rn(acc, xv) : xv;
-        present = true;
+  }
+  const int p = lo + lane;
+  const int32_t v = p < hi ? a[p] : INT_MAX;
+  const bool below = p < hi && (upper ? (v <= x) : (v < x));
+  return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
+
+// One CTA per (worker, block b, chunk of 256 global entries of block b).
+// The dividing-selection membership comes from the dividing select's
+// threshold (no search); each in-procedure discard list is joined with the
+// chunk through a shared-memory binary search over the chunk's indices.
+constexpr int kFinChunk = 1024;              // global entries per CTA
+constexpr int kFinPer = kFinChunk / kThreads;
+
+__global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __restrict__ tasks) {
+  const FinalizeTask& t = tasks[blockIdx.z];
+  if (t.mode == 2) return;   // lres ignores the global gradient
+  const int b = blockIdx.y;
+  const GatherSrc G = t.gblk[b];
+  const int gn = *G.cnt;
+  const int c0 = blockIdx.x * kFinChunk;
+  if (c0 >= gn) return;
+  const int nloc = min(kFinChunk, gn - c0);
+  const int tid = threadIdx.x;
+  if (t.mode == 1) {   // pres: zero at the global indices
+    for (int e = tid; e < nloc; e += kThreads) t.carry[G.idx[c0 + e]] = 0.f;
+    return;
+  }
+  __shared__ int32_t gi[kFinChunk];
+  __shared__ float sv[kFinChunk];
+  __shared__ unsigned char sf[kFinChunk];
+  __shared__ int range[2];
+  const SelScratch* dsc = t.div_sc[b];
+  float acc[kFinPer];
+  bool present[kFinPer];
+#pragma unroll
+  for (int q = 0; q < kFinPer; ++q) {
+    const int e = tid + q * kThreads;
+    const bool valid = e < nloc;
+    const int32_t j = valid ? G.idx[c0 + e] : INT_MAX;
+    gi[e] = j;
+    acc[q] = 0.f;
+    present[q] = false;
+    if (valid) {
+      const float x = t.carry[j];   // combined == g_copy, in place
+      present[q] = !sel_member(dsc, mag_key(x), j);
+      acc[q] = present[q] ? x : 0.f;
+    }
+  }
+  __syncthreads();
+  const int32_t jlo = gi[0], jhi = gi[nloc - 1];
+  for (int xq = t.xi_off[b]; xq < t.xi_off[b + 1]; ++xq) {
+    const XiList X = t.xi[xq];
+    const int xn = *X.cnt;
+    if (tid < 32) {
+      const int r = warp_bound(X.idx, xn, jlo, false);
+      if (tid == 0) range[0] = r;
+    } else if (tid < 64) {
+      const int r = warp_bound(X.idx, xn, jhi, true);
+      if (tid == 32) range[1] = r;
+    }
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) sf[tid + q * kThreads] = 0;
+    __syncthreads();
+    for (int p = range[0] + tid; p < range[1]; p += kThreads) {
+      const int32_t xi = X.idx[p];
+      const int pos = lower_bound_i32(gi, nloc, xi);
+      if (pos < nloc && gi[pos] == xi) {
+        sv[pos] = X.val[p];
+        sf[pos] = 1;
       }
     }
-    t.carry[j] = present ? acc : 0.f;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) {
+      const int e = tid + q * kThreads;
+      if (e < nloc && sf[e]) {
+        acc[q] = present[q] ? __fadd_rn(acc[q], sv[e]) : sv[e];
+        present[q] = true;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < kFinPer; ++q) {
+    const int e = tid + q * kThreads;
+    if (e < nloc) t.carry[gi[e]] = present[q] ? acc[q] : 0.f;
   }
 }
 
@@ -163,12 +245,12 @@ int launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t
   return 1;
 }
 
-int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_k, int max_div,
-                    cudaStream_t s) {
+int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_blk, int m,
+                    int max_div, cudaStream_t s) {
   if (ntask <= 0) return 0;
-  int gx = (int)((max_k + kThreads - 1) / kThreads);
-  gx = gx < 1 ? 1 : (gx > 2368 ? 2368 : gx);
-  k_finalize<<<dim3(gx, ntask), kThreads, 0, s>>>(tasks_dev);
+  int gx = (int)((max_blk + kFinChunk - 1) / kFinChunk);
+  gx = gx < 1 ? 1 : gx;
+  k_finalize<<<dim3(gx, m, ntask), kThreads, 0, s>>>(tasks_dev);
   if (max_div > 0) {
     int lx = (max_div + kThreads - 1) / kThreads;
     lx = lx < 1 ? 1 : (lx > 1184 ? 1184 : lx);

@@ -27,6 +27,17 @@ constexpr int kBins = 2048;            // radix digit width of passes 0 and 1 (1
 constexpr int kMaxR = 16;              // max lists folded by one merge task
 constexpr int kChunk = 8192;           // dividing chunk (elements per CTA)
 constexpr int kMaxSamples = 8192;      // merge splitter samples per task
+constexpr int kTile = 256;             // select work item (entries per warp task)
+constexpr int kSampShift = 18;         // dividing sample histogram: key >> 18
+constexpr int kSampBins = 1 << (31 - kSampShift);   // 8192 bins (1/32 octave)
+
+struct SelTask;
+// Host helper: fills the derived work-decomposition fields of a select task
+// (tiles per input segment; dense tiles) given the largest possible length of
+// one input segment.  Returns the number of work segments of the task.
+int sel_prepare(SelTask& t, int max_seg_len);
+int sel_scratch_segments(const SelTask& t);   // per-segment scratch entries needed
+int sel_grid_segments(const SelTask& t);      // segments the launch grid is sized for
 
 // ---------------------------------------------------------------------------
 // Select
@@ -41,11 +52,19 @@ struct SelScratch {
   int64_t cnt_gt;        // entries with key strictly above the prefix range
   int64_t total;         // entries in the input
   int64_t budget;        // effective budget for this run
-  int32_t all;           // total <= budget: everything is selected
+  int32_t all;           // 1: total <= budget, all selected; 2: budget 0; 0: threshold
   int32_t mode;          // resolved input mode for this run
-  int32_t err;           // NaN seen
+  int32_t cut_idx;       // largest selected index among entries with key == T
   int32_t pad_;
 };
+
+// Membership in a finished selection without searching its output:
+// selected  <=>  key > T  or  (key == T and index <= cut_idx).
+__device__ __forceinline__ bool sel_member(const SelScratch* sc, uint32_t key, int32_t idx) {
+  if (sc->all == 1) return true;
+  if (sc->all == 2) return false;
+  return key > sc->prefix || (key == sc->prefix && idx <= sc->cut_idx);
+}
 
 // Input is a list of segments.  mode 0 (explicit): segment s holds entries
 // idx[off+j], val[off+j] for j < cnt with off = seg_off ? seg_off[s] : s*stride
@@ -55,10 +74,12 @@ struct SelScratch {
 // When `mode_from_cand` is set (the dividing select), the mode is decided on
 // the device: explicit candidates if they are complete, else dense fallback.
 struct SelTask {
-  int32_t nseg;
+  int32_t nseg;          // input segments (explicit mode)
   int32_t mode;
   int32_t mode_from_cand;
   int32_t stride;
+  int32_t tiles;         // kTile-entry tiles per input segment (set by sel_prepare)
+  int32_t pad1_;
   const int32_t* idx;
   const float* val;
   const int32_t* seg_off;
@@ -73,6 +94,7 @@ struct SelTask {
   // candidate-path verdict (dividing)
   const int64_t* cand_total;
   const int32_t* cand_bad;
+  uint32_t* cand_hist;   // nullable: pass-0 histogram built by the candidate pass
   // budget
   int64_t budget;
   const int64_t* budget_dev;
@@ -127,16 +149,21 @@ struct DivTask {
   float* carry;            // worker residual; becomes g + carry (= g_copy) in place
   int32_t lo, hi;          // block range
   int32_t nchunks;
-  int32_t cap;             // candidate capacity per chunk
+  int32_t cap;             // candidate capacity per chunk segment
   int64_t budget;          // L
-  // candidates
+  // candidates: one index-ordered segment per chunk, then a tile work list
   int32_t* cand_idx;       // [nchunks * cap]
   float* cand_val;
   int32_t* cand_cnt;       // [nchunks]
+  int32_t* tile_off;       // [max_tiles] work list for the select (k_div_tiles)
+  int32_t* tile_cnt;       // [max_tiles]
+  int32_t max_tiles;
+  int32_t pad2_;
   int64_t* cand_total;
-  int32_t* cand_bad;       // overflow / NaN / skip flag
+  int32_t* cand_bad;       // bit 0: candidate path off for this run, bit 1: overflow
   uint32_t* pre_key;       // candidate threshold (key >= pre_key)
-  uint32_t* samp_hist;     // [kBins]
+  uint32_t* samp_hist;     // [kSampBins]
+  uint32_t* cand_hist;     // [kBins] pass-0 histogram of the candidates (for the select)
   int32_t sample_every;    // sample one chunk in `sample_every`
   int32_t use_cand;        // 0: candidate path disabled (dense select)
   int32_t* err;            // NaN flag
@@ -183,15 +210,15 @@ struct FinalizeTask {
   int32_t m;                  // blocks
   int64_t n;                  // dimension
   float* carry;               // in: g_copy (combined); out: residual
-  const int32_t* g_idx;       // global gradient
-  const int32_t* g_cnt;
+  const GatherSrc* gblk;      // [m] the global gradient, block by block
+  const SelScratch* const* div_sc;  // [m] dividing-select state (membership test)
   // per block: dividing selection + discard lists in recording order
   const GatherSrc* div;       // [m]
   const int32_t* xi_off;      // [m+1] offsets into xi
   const XiList* xi;           // lists
 };
-int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_k, int max_div,
-                     cudaStream_t s);
+int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_blk, int m,
+                    int max_div, cudaStream_t s);
 
 // ledger: scalars += 2 * count for each (worker slot, count pointer)
 struct LedgerAdd {

@@ -9,13 +9,15 @@
 //       (digits 11 / 11 / 9 bits).  After the three passes the threshold key
 //       T is exact, cnt_gt = #{key > T} and need_eq = L - cnt_gt entries of
 //       key == T are taken -- the lowest-index ones, which is exactly the
-//       reference's tie rule.
-//   count: per segment #{key > T} and #{key == T}
+//       reference's tie rule.  For the dividing select the first histogram is
+//       built by the candidate pass itself (divide.cu), so hist<0> skips it.
+//   count: per segment (one warp each) #{key > T} and #{key == T}
 //   scan:  per segment tie quota and output offsets (segments are in index
 //          order, so offsets preserve index order)
-//   write: ordered compaction of selected / discarded entries; discards are
-//          scaled by the residual share with an explicitly rounded multiply
-//          (no FMA contraction), matching inc/residual.hpp:119.
+//   write: ordered compaction (one warp per segment, ballots) of selected and
+//          discarded entries; discards are scaled by the residual share with
+//          an explicitly rounded multiply (no FMA contraction), matching
+//          inc/residual.hpp:119.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -23,16 +25,31 @@ namespace sdl {
 
 namespace {
 
+constexpr int kWarps = kThreads / 32;
+
 __device__ __forceinline__ int resolve_mode(const SelTask& t) {
   if (!t.mode_from_cand) return t.mode;
   const int64_t need = t.budget_dev ? *t.budget_dev : t.budget;
   return (*t.cand_bad != 0 || *t.cand_total < need) ? 1 : 0;
 }
 
-__device__ __forceinline__ int nseg_of(const SelTask& t, int mode) {
-  return mode == 1 ? t.dnseg : t.nseg;
+// Is the pass-0 histogram already built by the dividing candidate pass?  In
+// candidate mode yes; after a candidate-list overflow (flags == 2) too: every
+// chunk histogrammed its candidates before the overflow was detected, and
+// the L-th largest key lies above the pre-threshold because more than the
+// capacity (> L) of entries passed it.
+__device__ __forceinline__ bool hist0_ready(const SelTask& t, int mode) {
+  if (!t.cand_hist) return false;
+  return mode == 0 || *t.cand_bad == 2;
 }
 
+__device__ __forceinline__ int nseg_of(const SelTask& t, int mode) {
+  return mode == 1 ? t.dnseg : t.nseg * t.tiles;
+}
+
+// Segment s of a task.  Explicit inputs are cut further into `tiles` tiles
+// of <= kTile entries per input segment (tile order == index order), so every
+// warp-level work item is small regardless of how the input was segmented.
 __device__ __forceinline__ void seg_bounds(const SelTask& t, int mode, int s, int& off,
                                            int& cnt) {
   if (mode == 1) {
@@ -40,13 +57,19 @@ __device__ __forceinline__ void seg_bounds(const SelTask& t, int mode, int s, in
     const int c = t.dn - off;
     cnt = c < 0 ? 0 : (c > t.dstride ? t.dstride : c);
   } else {
-    off = t.seg_off ? t.seg_off[s] : s * t.stride;
+    const int tiles = t.tiles;
+    const int si = s / tiles, ti = s - si * tiles;
+    int o, c;
+    o = t.seg_off ? t.seg_off[si] : si * t.stride;
     if (t.seg_cnt) {
-      cnt = t.seg_cnt[s];
+      c = t.seg_cnt[si];
     } else {
-      const int c = *t.count - off;
-      cnt = c < 0 ? 0 : (c > t.stride ? t.stride : c);
+      c = *t.count - o;
+      c = c < 0 ? 0 : (c > t.stride ? t.stride : c);
     }
+    off = o + ti * kTile;
+    c -= ti * kTile;
+    cnt = c < 0 ? 0 : (c > kTile ? kTile : c);
   }
 }
 
@@ -63,6 +86,15 @@ struct Digit {
   static constexpr int nbins = PASS == 2 ? 512 : 2048;
 };
 
+// warp-aggregated shared-memory histogram increment
+__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t bin, bool active) {
+  const uint32_t am = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  const uint32_t peers = __match_any_sync(am, bin);
+  const int leader = __ffs(peers) - 1;
+  if ((int)(threadIdx.x & 31) == leader) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+}
+
 // ---------------------------------------------------------------------------
 template <int PASS>
 __global__ void __launch_bounds__(kThreads) k_sel_hist(const SelTask* __restrict__ tasks) {
@@ -72,6 +104,7 @@ __global__ void __launch_bounds__(kThreads) k_sel_hist(const SelTask* __restrict
   uint32_t prefix = 0, pmask = 0;
   if (PASS == 0) {
     mode = resolve_mode(t);
+    if (hist0_ready(t, mode)) return;   // built by the candidate pass
   } else {
     if (sc->all) return;
     mode = sc->mode;
@@ -79,18 +112,25 @@ __global__ void __launch_bounds__(kThreads) k_sel_hist(const SelTask* __restrict
     pmask = sc->pmask;
   }
   const int nseg = nseg_of(t, mode);
-  if ((int)blockIdx.x >= nseg) return;
+  const int per = (nseg + gridDim.x - 1) / gridDim.x;
+  const int s0 = blockIdx.x * per;
+  if (s0 >= nseg) return;
+  const int s1 = min(nseg, s0 + per);
   constexpr int NB = Digit<PASS>::nbins;
   constexpr int SH = Digit<PASS>::shift;
   __shared__ uint32_t h[NB];
   for (int b = threadIdx.x; b < NB; b += blockDim.x) h[b] = 0;
   __syncthreads();
-  for (int s = blockIdx.x; s < nseg; s += gridDim.x) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int s = s0 + warp; s < s1; s += kWarps) {
     int off, cnt;
     seg_bounds(t, mode, s, off, cnt);
-    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-      const uint32_t key = mag_key(seg_val(t, mode, off + j));
-      if ((key & pmask) == prefix) atomicAdd(&h[(key >> SH) & (NB - 1)], 1u);
+    for (int j0 = 0; j0 < cnt; j0 += 32) {
+      const int j = j0 + lane;
+      uint32_t key = 0;
+      if (j < cnt) key = mag_key(seg_val(t, mode, off + j));
+      const bool in = j < cnt && (key & pmask) == prefix;
+      hist_add(h, (key >> SH) & (NB - 1), in);
     }
   }
   __syncthreads();
@@ -106,16 +146,26 @@ __global__ void __launch_bounds__(kThreads) k_sel_find(const SelTask* __restrict
   constexpr int NB = Digit<PASS>::nbins;
   constexpr int SH = Digit<PASS>::shift;
   constexpr int BPT = NB / kThreads;
-  __shared__ int scratch[40];
   __shared__ long long lscr[32];
+  __shared__ long long suf[kThreads];
   if (PASS > 0 && sc->all) return;
+  int mode = 0;
+  const uint32_t* src = sc->hist;
+  if (PASS == 0) {
+    mode = resolve_mode(t);
+    if (hist0_ready(t, mode)) src = t.cand_hist;
+  }
   uint32_t c[BPT];
   long long mine = 0;
 #pragma unroll
   for (int q = 0; q < BPT; ++q) {
-    c[q] = sc->hist[threadIdx.x * BPT + q];
-    sc->hist[threadIdx.x * BPT + q] = 0;
+    c[q] = src[threadIdx.x * BPT + q];
     mine += c[q];
+  }
+#pragma unroll
+  for (int q = 0; q < BPT; ++q) {
+    sc->hist[threadIdx.x * BPT + q] = 0;
+    if (PASS == 0 && t.cand_hist) t.cand_hist[threadIdx.x * BPT + q] = 0;
   }
   int64_t rank, cnt_gt;
   uint32_t prefix, pmask;
@@ -125,8 +175,8 @@ __global__ void __launch_bounds__(kThreads) k_sel_find(const SelTask* __restrict
     if (threadIdx.x == 0) {
       sc->total = total;
       sc->budget = budget;
-      sc->mode = resolve_mode(t);
-      sc->err = 0;
+      sc->mode = mode;
+      sc->cut_idx = -1;
       if (total <= budget) sc->all = 1;          // identity case, inc/sparse.hpp:143-146
       else if (budget <= 0) sc->all = 2;         // nothing kept
       else sc->all = 0;
@@ -148,27 +198,16 @@ __global__ void __launch_bounds__(kThreads) k_sel_find(const SelTask* __restrict
     pmask = sc->pmask;
   }
   __syncthreads();
-  // suffix sums over threads (bins ascending with thread id; we scan from the top)
-  // reverse the thread order so an exclusive prefix gives "count above me".
-  const int rev = blockDim.x - 1 - threadIdx.x;
-  (void)rev;
-  // exclusive scan in reversed order: compute inclusive scan of values ordered
-  // by descending thread id using a shared array.
-  __shared__ long long vals[kThreads];
-  vals[threadIdx.x] = mine;
-  __syncthreads();
-  // simple Hillis-Steele on reversed array
-  __shared__ long long suf[kThreads];
-  suf[threadIdx.x] = vals[blockDim.x - 1 - threadIdx.x];
+  // above(tid) = count in the bins of all threads > tid (bins ascend with tid)
+  const int r = blockDim.x - 1 - threadIdx.x;
+  suf[r] = mine;
   __syncthreads();
   for (int o = 1; o < (int)blockDim.x; o <<= 1) {
-    long long add = threadIdx.x >= (unsigned)o ? suf[threadIdx.x - o] : 0;
+    const long long add = threadIdx.x >= (unsigned)o ? suf[threadIdx.x - o] : 0;
     __syncthreads();
     suf[threadIdx.x] += add;
     __syncthreads();
   }
-  // above(tid) = inclusive suffix of threads > tid = suf[rev-1]
-  const int r = blockDim.x - 1 - threadIdx.x;
   const long long above = r > 0 ? suf[r - 1] : 0;
   if (above < rank && rank <= above + mine) {
     long long cum = above;
@@ -184,10 +223,9 @@ __global__ void __launch_bounds__(kThreads) k_sel_find(const SelTask* __restrict
       cum += c[q];
     }
   }
-  (void)scratch;
 }
 
-// Per segment: #{key > T}, #{key == T}
+// Per segment (one warp): #{key > T}, #{key == T}
 __global__ void __launch_bounds__(kThreads) k_sel_count(const SelTask* __restrict__ tasks) {
   const SelTask& t = tasks[blockIdx.y];
   const SelScratch* sc = t.scr;
@@ -195,29 +233,23 @@ __global__ void __launch_bounds__(kThreads) k_sel_count(const SelTask* __restric
   const int nseg = nseg_of(t, mode);
   const int all = sc->all;
   const uint32_t T = sc->prefix;
-  __shared__ int scratch[40];
-  for (int s = blockIdx.x; s < nseg; s += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int s = blockIdx.x * kWarps + (threadIdx.x >> 5); s < nseg; s += gridDim.x * kWarps) {
     int off, cnt;
     seg_bounds(t, mode, s, off, cnt);
     int gt = 0, eq = 0;
     if (all == 1) {
       gt = cnt;
     } else if (all == 0) {
-      int lg = 0, le = 0;
-      for (int j0 = 0; j0 < cnt; j0 += blockDim.x) {
-        const int j = j0 + threadIdx.x;
-        uint32_t key = 0;
-        if (j < cnt) key = mag_key(seg_val(t, mode, off + j));
-        lg += (j < cnt && key > T);
-        le += (j < cnt && key == T);
+      for (int j = lane; j < cnt; j += 32) {
+        const uint32_t key = mag_key(seg_val(t, mode, off + j));
+        gt += key > T;
+        eq += key == T;
       }
-      int tg, te;
-      block_exscan(lg, scratch, &tg);
-      block_exscan(le, scratch, &te);
-      gt = tg;
-      eq = te;
+      gt = __reduce_add_sync(0xffffffffu, gt);
+      eq = __reduce_add_sync(0xffffffffu, eq);
     }
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       t.seg_gt[s] = gt;
       t.seg_eq[s] = eq;
     }
@@ -225,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) k_sel_count(const SelTask* __restric
 }
 
 // One CTA per task: tie quotas and output offsets per segment.
-__global__ void __launch_bounds__(kThreads) k_sel_scan(const SelTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(1024) k_sel_scan(const SelTask* __restrict__ tasks) {
   const SelTask& t = tasks[blockIdx.x];
   SelScratch* sc = t.scr;
   const int mode = sc->mode;
@@ -266,18 +298,20 @@ __global__ void __launch_bounds__(kThreads) k_sel_scan(const SelTask* __restrict
   }
 }
 
-// Ordered compaction.
+// Ordered compaction, one warp per segment.
 __global__ void __launch_bounds__(kThreads) k_sel_write(const SelTask* __restrict__ tasks) {
   const SelTask& t = tasks[blockIdx.y];
-  const SelScratch* sc = t.scr;
+  SelScratch* sc = t.scr;
   const int mode = sc->mode;
   const int nseg = nseg_of(t, mode);
   const int all = sc->all;
   const uint32_t T = sc->prefix;
   const float w = t.weight;
   const bool want_dis = t.dis_idx != nullptr;
-  __shared__ int scratch[40];
-  for (int s = blockIdx.x; s < nseg; s += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  int cut = -1;
+  for (int s = blockIdx.x * kWarps + (threadIdx.x >> 5); s < nseg; s += gridDim.x * kWarps) {
     int off, cnt;
     seg_bounds(t, mode, s, off, cnt);
     if (cnt == 0) continue;
@@ -285,8 +319,8 @@ __global__ void __launch_bounds__(kThreads) k_sel_write(const SelTask* __restric
     const int dis_base = t.seg_dis_off[s];
     const int take = t.seg_take[s];
     int eq_seen = 0, sel_seen = 0;
-    for (int j0 = 0; j0 < cnt; j0 += blockDim.x) {
-      const int j = j0 + threadIdx.x;
+    for (int j0 = 0; j0 < cnt; j0 += 32) {
+      const int j = j0 + lane;
       const bool valid = j < cnt;
       float v = 0.f;
       int32_t ix = 0;
@@ -303,14 +337,15 @@ __global__ void __launch_bounds__(kThreads) k_sel_write(const SelTask* __restric
         is_sel = false;
       } else {
         const bool is_eq = valid && key == T;
-        int teq;
-        const int eq_rank = eq_seen + block_rank(is_eq, scratch, &teq);
-        eq_seen += teq;
+        const uint32_t be = __ballot_sync(0xffffffffu, is_eq);
+        const int eq_rank = eq_seen + __popc(be & lt);
+        eq_seen += __popc(be);
         is_sel = valid && (key > T || (is_eq && eq_rank < take));
+        if (is_sel && is_eq) cut = max(cut, ix);
       }
-      int tsel;
-      const int sel_rank = sel_seen + block_rank(is_sel, scratch, &tsel);
-      sel_seen += tsel;
+      const uint32_t bs = __ballot_sync(0xffffffffu, is_sel);
+      const int sel_rank = sel_seen + __popc(bs & lt);
+      sel_seen += __popc(bs);
       if (is_sel) {
         t.sel_idx[sel_base + sel_rank] = ix;
         t.sel_val[sel_base + sel_rank] = v;
@@ -321,24 +356,52 @@ __global__ void __launch_bounds__(kThreads) k_sel_write(const SelTask* __restric
       }
     }
   }
+  if (all == 0) {
+    cut = __reduce_max_sync(0xffffffffu, cut);
+    if (lane == 0 && cut >= 0) atomicMax(&sc->cut_idx, cut);
+  }
 }
+
+inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 }  // namespace
 
+int sel_prepare(SelTask& t, int max_seg_len) {
+  t.tiles = max_seg_len <= kTile ? 1 : (max_seg_len + kTile - 1) / kTile;
+  if (t.dn > 0) {
+    t.dstride = kTile;
+    t.dnseg = (t.dn + kTile - 1) / kTile;
+  }
+  return t.nseg * t.tiles;
+}
+
+int sel_scratch_segments(const SelTask& t) {
+  const int ne = t.nseg * t.tiles;
+  return ne > t.dnseg ? ne : t.dnseg;
+}
+
+int sel_grid_segments(const SelTask& t) {
+  // grids are sized for the expected (explicit / candidate) input; the dense
+  // fallback of the dividing select grid-strides over its larger range
+  if (t.mode == 1 && !t.mode_from_cand) return t.dnseg;
+  return t.nseg * t.tiles;
+}
+
 int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s) {
   if (ntask <= 0) return 0;
-  const int gx = max_nseg < 1 ? 1 : (max_nseg > 8192 ? 8192 : max_nseg);
-  const int hx = max_nseg < 1 ? 1 : (max_nseg > 1184 ? 1184 : max_nseg);
-  dim3 g2(gx, ntask), gh(hx, ntask);
+  // histogram CTAs cover ~16 segments each; count/write use a warp per segment
+  const int hx = clampi((max_nseg + 15) / 16, 1, 1184);
+  const int wx = clampi((max_nseg + kWarps - 1) / kWarps, 1, 4096);
+  dim3 gh(hx, ntask), gw(wx, ntask);
   k_sel_hist<0><<<gh, kThreads, 0, s>>>(tasks_dev);
   k_sel_find<0><<<ntask, kThreads, 0, s>>>(tasks_dev);
   k_sel_hist<1><<<gh, kThreads, 0, s>>>(tasks_dev);
   k_sel_find<1><<<ntask, kThreads, 0, s>>>(tasks_dev);
   k_sel_hist<2><<<gh, kThreads, 0, s>>>(tasks_dev);
   k_sel_find<2><<<ntask, kThreads, 0, s>>>(tasks_dev);
-  k_sel_count<<<g2, kThreads, 0, s>>>(tasks_dev);
-  k_sel_scan<<<ntask, kThreads, 0, s>>>(tasks_dev);
-  k_sel_write<<<g2, kThreads, 0, s>>>(tasks_dev);
+  k_sel_count<<<gw, kThreads, 0, s>>>(tasks_dev);
+  k_sel_scan<<<ntask, 1024, 0, s>>>(tasks_dev);
+  k_sel_write<<<gw, kThreads, 0, s>>>(tasks_dev);
   return 9;
 }
 
