@@ -160,6 +160,13 @@ int spardl_nccl_unique_id(void* out128);
 int spardl_ctx_create(const spardl_config* cfg, int32_t device, int32_t world_size,
                       int32_t rank, const void* nccl_id, void* stream, spardl_ctx** out);
 int spardl_ctx_destroy(spardl_ctx* ctx);
+/* Host-only schedule inspection (no GPU): the NCCL point-to-point ops rank
+ * `rank` of `world_size` issues per iteration, in issue order, 5 int64 each:
+ * (round, peer rank, is_send, block id, bytes).  ops may be NULL to query
+ * the count.  Every rank derives the same plan, so sends and receives of a
+ * rank pair match one to one in order (tested with a gloo process group). */
+int spardl_plan_ops(const spardl_config* cfg, int32_t world_size, int32_t rank, int64_t* ops,
+                    int64_t cap, int64_t* n_ops);
 /* first global worker id and count of the workers hosted by this context */
 int spardl_ctx_local_workers(const spardl_ctx* ctx, int32_t* first, int32_t* count);
 /* enable (1) / disable (0) CUDA-graph replay of the whole iteration */

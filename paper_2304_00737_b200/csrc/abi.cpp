@@ -377,6 +377,27 @@ EXPORT int spardl_ctx_create(const spardl_config* cfg, int32_t device, int32_t w
   });
 }
 
+EXPORT int spardl_plan_ops(const spardl_config* cfg, int32_t world_size, int32_t rank,
+                           int64_t* ops, int64_t cap, int64_t* n_ops) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(n_ops, "n_ops");
+    sdle::Engine e(*cfg, 0, world_size, rank, nullptr, nullptr, /*plan_only=*/true);
+    const auto v = e.plan_ops();
+    *n_ops = static_cast<int64_t>(v.size());
+    if (ops) {
+      if (cap < *n_ops) sdlh::fail(SPARDL_E_ARG, "ops capacity too small");
+      for (size_t i = 0; i < v.size(); ++i) {
+        ops[5 * i + 0] = v[i].round;
+        ops[5 * i + 1] = v[i].peer;
+        ops[5 * i + 2] = v[i].is_send;
+        ops[5 * i + 3] = v[i].uid;
+        ops[5 * i + 4] = v[i].bytes;
+      }
+    }
+  });
+}
+
 EXPORT int spardl_ctx_destroy(spardl_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;

@@ -50,11 +50,19 @@ __global__ void __launch_bounds__(kThreads) k_div_sample(const DivTask* __restri
   const int64_t s = A > t.lo ? A : t.lo;
   const int64_t e = (A + kChunk) < t.hi ? (A + kChunk) : t.hi;
   const float* g = apply_residual ? t.g_tab[t.g_id] : nullptr;
-  for (int64_t i0 = s; i0 < e; i0 += blockDim.x) {
-    const int64_t i = i0 + threadIdx.x;
+  constexpr int PER = kChunk / kThreads;   // elements per thread, all loads issued first
+  float vals[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int64_t i = s + (int64_t)q * kThreads + threadIdx.x;
+    vals[q] = 0.f;
+    if (i < e) vals[q] = apply_residual ? __fadd_rn(__ldcs(g + i), __ldcs(t.carry + i)) : t.carry[i];
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int64_t i = s + (int64_t)q * kThreads + threadIdx.x;
     const bool in = i < e;
-    float v = 0.f;
-    if (in) v = apply_residual ? __fadd_rn(__ldcs(g + i), __ldcs(t.carry + i)) : t.carry[i];
+    const float v = vals[q];
     // warp-aggregated: sampled keys crowd into a few top-bit bins
     const uint32_t bin = mag_key(v) >> kSampShift;
     const uint32_t am = __ballot_sync(0xffffffffu, in);

@@ -44,6 +44,10 @@ Arena::~Arena() {
 
 void* Arena::alloc(size_t bytes) {
   bytes = (bytes + 255) & ~static_cast<size_t>(255);
+  if (dry) {   // plan-only: distinct, aligned, never dereferenced addresses
+    total_ += bytes;
+    return reinterpret_cast<void*>(static_cast<uintptr_t>(0x1000) + total_ - bytes);
+  }
   if (bytes > left_) {
     const size_t sz = std::max<size_t>(bytes, static_cast<size_t>(64) << 20);
     void* p = nullptr;
@@ -62,8 +66,10 @@ void* Arena::alloc(size_t bytes) {
 
 // ---------------------------------------------------------------------------
 Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const void* nccl_id,
-               cudaStream_t stream)
+               cudaStream_t stream, bool plan_only)
     : cfg_(cfg), device_(device), world_(world), rank_(rank) {
+  dry_ = plan_only;
+  arena_.dry = plan_only;
   sdlh::validate(cfg);
   P_ = static_cast<int>(cfg.workers);
   d_ = static_cast<int>(cfg.teams);
@@ -80,6 +86,24 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   wloc_ = P_ / world;
   first_ = rank * wloc_;
   part_ = sdlh::partition(cfg.dimension, m_);
+  if (plan_only) {   // schedule inspection only: no device, no communicator
+    for (int i = 0; i < wloc_; ++i) {
+      carry_.push_back(static_cast<float*>(arena_.alloc(sizeof(float) * cfg.dimension)));
+      ledger_total_.push_back(static_cast<int64_t*>(arena_.alloc(sizeof(int64_t))));
+    }
+    ledger_phase_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * 3 * wloc_));
+    ntot_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * wloc_));
+    budget_dev_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * wloc_));
+    ctl_dev_ = static_cast<sdl::HCtl*>(arena_.alloc(sizeof(sdl::HCtl) * wloc_));
+    gtab_dev_ = static_cast<const float**>(arena_.alloc(sizeof(float*) * wloc_));
+    err_dev_ = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+    hash_dev_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * d_));
+    rounds_.assign(static_cast<size_t>(P_), 0);
+    phase_rounds_.assign(static_cast<size_t>(P_), {0, 0, 0});
+    plan();
+    carry_.clear();
+    return;
+  }
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -133,6 +157,22 @@ Engine::~Engine() {
   for (float* c : carry_) cudaFree(c);
   if (gtab_host_) cudaFreeHost(gtab_host_);
   if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+std::vector<PlanOp> Engine::plan_ops() const {
+  std::vector<PlanOp> ops;
+  int round = 0;
+  for (const Step& s : steps_) {
+    if (s.xfers.empty()) continue;
+    for (const Xfer& x : s.xfers) {
+      if (x.src_rank == x.dst_rank) continue;
+      const bool send = x.src_rank == rank_;
+      ops.push_back({round, send ? x.dst_rank : x.src_rank, send ? 1 : 0, x.uid,
+                     static_cast<int64_t>(16 + 8 * Lcap_)});
+    }
+    ++round;
+  }
+  return ops;
 }
 
 void Engine::drop_graph() {
@@ -304,14 +344,14 @@ void Engine::finish_stage(Stage& st) {
   if (!st.merges.empty()) {
     st.merges_dev = static_cast<sdl::MergeTask*>(
         arena_.alloc(sizeof(sdl::MergeTask) * st.merges.size()));
-    CK(cudaMemcpy(st.merges_dev, st.merges.data(), sizeof(sdl::MergeTask) * st.merges.size(),
+    CK(mcpy(st.merges_dev, st.merges.data(), sizeof(sdl::MergeTask) * st.merges.size(),
                   cudaMemcpyHostToDevice));
     launches_ += 2;
   }
   if (!st.sels.empty()) {
     st.sels_dev =
         static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));
-    CK(cudaMemcpy(st.sels_dev, st.sels.data(), sizeof(sdl::SelTask) * st.sels.size(),
+    CK(mcpy(st.sels_dev, st.sels.data(), sizeof(sdl::SelTask) * st.sels.size(),
                   cudaMemcpyHostToDevice));
     launches_ += 9;
   }
@@ -367,7 +407,7 @@ void Engine::plan() {
   div_max_chunks_ = max_chunks;
   if (!div_tasks_.empty()) {
     div_dev_ = static_cast<sdl::DivTask*>(arena_.alloc(sizeof(sdl::DivTask) * div_tasks_.size()));
-    CK(cudaMemcpy(div_dev_, div_tasks_.data(), sizeof(sdl::DivTask) * div_tasks_.size(),
+    CK(mcpy(div_dev_, div_tasks_.data(), sizeof(sdl::DivTask) * div_tasks_.size(),
                   cudaMemcpyHostToDevice));
     launches_ += 3;
   }
@@ -543,7 +583,7 @@ void Engine::plan() {
       src.push_back({s.idx, s.val, s.cnt});
     }
     auto* src_dev = static_cast<sdl::GatherSrc*>(arena_.alloc(sizeof(sdl::GatherSrc) * m_));
-    CK(cudaMemcpy(src_dev, src.data(), sizeof(sdl::GatherSrc) * m_, cudaMemcpyHostToDevice));
+    CK(mcpy(src_dev, src.data(), sizeof(sdl::GatherSrc) * m_, cudaMemcpyHostToDevice));
     Slot gs;
     gs.cap = cfg_.k;
     gs.bytes = 16 + 8 * static_cast<size_t>((cfg_.k + 3) & ~3);
@@ -570,7 +610,7 @@ void Engine::plan() {
   (void)max_m;
   asm_dev_ = static_cast<sdl::AssembleTask*>(
       arena_.alloc(sizeof(sdl::AssembleTask) * std::max<size_t>(1, asm_tasks_.size())));
-  CK(cudaMemcpy(asm_dev_, asm_tasks_.data(), sizeof(sdl::AssembleTask) * asm_tasks_.size(),
+  CK(mcpy(asm_dev_, asm_tasks_.data(), sizeof(sdl::AssembleTask) * asm_tasks_.size(),
                 cudaMemcpyHostToDevice));
   launches_ += 1;
 
@@ -583,7 +623,7 @@ void Engine::plan() {
     ft.gblk = team_src_[static_cast<size_t>(team_of_local_global_[static_cast<size_t>(li)])];
     auto* sc_dev = static_cast<const sdl::SelScratch**>(
         arena_.alloc(sizeof(sdl::SelScratch*) * m_));
-    CK(cudaMemcpy(sc_dev, div_scr_[static_cast<size_t>(li)].data(), sizeof(sdl::SelScratch*) * m_,
+    CK(mcpy(sc_dev, div_scr_[static_cast<size_t>(li)].data(), sizeof(sdl::SelScratch*) * m_,
                   cudaMemcpyHostToDevice));
     ft.div_sc = sc_dev;
     std::vector<sdl::GatherSrc> div;
@@ -597,13 +637,13 @@ void Engine::plan() {
     }
     xoff.push_back(static_cast<int32_t>(xl.size()));
     auto* div_dev = static_cast<sdl::GatherSrc*>(arena_.alloc(sizeof(sdl::GatherSrc) * m_));
-    CK(cudaMemcpy(div_dev, div.data(), sizeof(sdl::GatherSrc) * m_, cudaMemcpyHostToDevice));
+    CK(mcpy(div_dev, div.data(), sizeof(sdl::GatherSrc) * m_, cudaMemcpyHostToDevice));
     auto* xoff_dev = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * xoff.size()));
-    CK(cudaMemcpy(xoff_dev, xoff.data(), sizeof(int32_t) * xoff.size(), cudaMemcpyHostToDevice));
+    CK(mcpy(xoff_dev, xoff.data(), sizeof(int32_t) * xoff.size(), cudaMemcpyHostToDevice));
     auto* xl_dev = static_cast<sdl::XiList*>(
         arena_.alloc(sizeof(sdl::XiList) * std::max<size_t>(1, xl.size())));
     if (!xl.empty())
-      CK(cudaMemcpy(xl_dev, xl.data(), sizeof(sdl::XiList) * xl.size(), cudaMemcpyHostToDevice));
+      CK(mcpy(xl_dev, xl.data(), sizeof(sdl::XiList) * xl.size(), cudaMemcpyHostToDevice));
     ft.div = div_dev;
     ft.xi_off = xoff_dev;
     ft.xi = xl_dev;
@@ -612,14 +652,14 @@ void Engine::plan() {
   fin_max_div_ = cfg_.residual == SPARDL_RES_LRES ? Lcap_ : 0;
   fin_dev_ = static_cast<sdl::FinalizeTask*>(
       arena_.alloc(sizeof(sdl::FinalizeTask) * fin_tasks_.size()));
-  CK(cudaMemcpy(fin_dev_, fin_tasks_.data(), sizeof(sdl::FinalizeTask) * fin_tasks_.size(),
+  CK(mcpy(fin_dev_, fin_tasks_.data(), sizeof(sdl::FinalizeTask) * fin_tasks_.size(),
                 cudaMemcpyHostToDevice));
   launches_ += fin_max_div_ > 0 ? 2 : 1;
 
   if (!ledger_adds_.empty()) {
     ledger_dev_ = static_cast<sdl::LedgerAdd*>(
         arena_.alloc(sizeof(sdl::LedgerAdd) * ledger_adds_.size()));
-    CK(cudaMemcpy(ledger_dev_, ledger_adds_.data(), sizeof(sdl::LedgerAdd) * ledger_adds_.size(),
+    CK(mcpy(ledger_dev_, ledger_adds_.data(), sizeof(sdl::LedgerAdd) * ledger_adds_.size(),
                   cudaMemcpyHostToDevice));
     launches_ += 1;
   }
@@ -628,7 +668,7 @@ void Engine::plan() {
       ctl_tasks_.push_back({ctl_dev_ + li, ntot_ + li, budget_dev_ + li});
     ctl_tasks_dev_ =
         static_cast<sdl::CtlTask*>(arena_.alloc(sizeof(sdl::CtlTask) * ctl_tasks_.size()));
-    CK(cudaMemcpy(ctl_tasks_dev_, ctl_tasks_.data(), sizeof(sdl::CtlTask) * ctl_tasks_.size(),
+    CK(mcpy(ctl_tasks_dev_, ctl_tasks_.data(), sizeof(sdl::CtlTask) * ctl_tasks_.size(),
                   cudaMemcpyHostToDevice));
     launches_ += 1;
   }
@@ -770,7 +810,7 @@ void Engine::sync() {
   CK(cudaSetDevice(device_));
   CK(cudaStreamSynchronize(stream_));
   int32_t err = 0;
-  CK(cudaMemcpy(&err, err_dev_, sizeof(err), cudaMemcpyDeviceToHost));
+  CK(mcpy(&err, err_dev_, sizeof(err), cudaMemcpyDeviceToHost));
   if (err) {
     CK(cudaMemset(err_dev_, 0, sizeof(int32_t)));
     sdlh::fail(SPARDL_E_ARG, "gradient contains NaN (selection order undefined)");
@@ -794,8 +834,8 @@ void Engine::reset_state() {
       c[static_cast<size_t>(i)] = {h.lower, h.upper, h.target, h.h, h.step, h.flag, 0};
       b[static_cast<size_t>(i)] = sdlh::hctrl_budget(&h);
     }
-    CK(cudaMemcpy(ctl_dev_, c.data(), sizeof(sdl::HCtl) * wloc_, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(budget_dev_, b.data(), sizeof(int64_t) * wloc_, cudaMemcpyHostToDevice));
+    CK(mcpy(ctl_dev_, c.data(), sizeof(sdl::HCtl) * wloc_, cudaMemcpyHostToDevice));
+    CK(mcpy(budget_dev_, b.data(), sizeof(int64_t) * wloc_, cudaMemcpyHostToDevice));
   }
   ran_ = false;
 }
@@ -820,10 +860,10 @@ void Engine::ledger(int64_t* rounds, int64_t* scalars) {
   sync();
   std::vector<int64_t> loc(static_cast<size_t>(wloc_));
   for (int i = 0; i < wloc_; ++i)
-    CK(cudaMemcpy(&loc[static_cast<size_t>(i)], ledger_total_[static_cast<size_t>(i)],
+    CK(mcpy(&loc[static_cast<size_t>(i)], ledger_total_[static_cast<size_t>(i)],
                   sizeof(int64_t), cudaMemcpyDeviceToHost));
   int64_t* tmp = rb_dev_;
-  CK(cudaMemcpy(tmp, loc.data(), sizeof(int64_t) * wloc_, cudaMemcpyHostToDevice));
+  CK(mcpy(tmp, loc.data(), sizeof(int64_t) * wloc_, cudaMemcpyHostToDevice));
   allgather_i64(comm_, stream_, world_, tmp, wloc_, scalars, tmp + wloc_);
   for (int w = 0; w < P_; ++w) rounds[w] = rounds_[static_cast<size_t>(w)];
 }
@@ -846,9 +886,9 @@ spardl_run_info Engine::run_info() {
       std::vector<int64_t> loc(static_cast<size_t>(wloc_));
       std::vector<int64_t> all(static_cast<size_t>(P_));
       std::vector<int64_t> buf(static_cast<size_t>(3 * wloc_));
-      CK(cudaMemcpy(buf.data(), ledger_phase_, sizeof(int64_t) * 3 * wloc_, cudaMemcpyDeviceToHost));
+      CK(mcpy(buf.data(), ledger_phase_, sizeof(int64_t) * 3 * wloc_, cudaMemcpyDeviceToHost));
       for (int i = 0; i < wloc_; ++i) loc[static_cast<size_t>(i)] = buf[static_cast<size_t>(3 * i + p)];
-      CK(cudaMemcpy(tmp, loc.data(), sizeof(int64_t) * wloc_, cudaMemcpyHostToDevice));
+      CK(mcpy(tmp, loc.data(), sizeof(int64_t) * wloc_, cudaMemcpyHostToDevice));
       allgather_i64(comm_, stream_, world_, tmp, wloc_, all.data(), tmp + wloc_);
       for (int w = 0; w < P_; ++w) ph[static_cast<size_t>(3 * w + p)] = all[static_cast<size_t>(w)];
     }
@@ -866,21 +906,21 @@ spardl_run_info Engine::run_info() {
   // consistency: every assembled global gradient hashes identically
   {
     std::vector<int64_t> h(static_cast<size_t>(d_), 0);
-    CK(cudaMemcpy(h.data(), hash_dev_, sizeof(int64_t) * d_, cudaMemcpyDeviceToHost));
+    CK(mcpy(h.data(), hash_dev_, sizeof(int64_t) * d_, cudaMemcpyDeviceToHost));
     if (world_ > 1) {
       int64_t* tmp = rb_dev_;
-      CK(cudaMemcpy(tmp, h.data(), sizeof(int64_t) * d_, cudaMemcpyHostToDevice));
+      CK(mcpy(tmp, h.data(), sizeof(int64_t) * d_, cudaMemcpyHostToDevice));
       NK(ncclAllGather(tmp, tmp + d_, static_cast<size_t>(d_), ncclInt64, comm_, stream_));
       CK(cudaStreamSynchronize(stream_));
       h.resize(static_cast<size_t>(d_ * world_));
-      CK(cudaMemcpy(h.data(), tmp + d_, sizeof(int64_t) * d_ * world_, cudaMemcpyDeviceToHost));
+      CK(mcpy(h.data(), tmp + d_, sizeof(int64_t) * d_ * world_, cudaMemcpyDeviceToHost));
     }
     bool ok = true;
     int64_t ref = 0;
     bool have = false;
     std::vector<int32_t> nnz(global_.size());
     for (size_t q = 0; q < global_.size(); ++q)
-      CK(cudaMemcpy(&nnz[q], global_[q].cnt, sizeof(int32_t), cudaMemcpyDeviceToHost));
+      CK(mcpy(&nnz[q], global_[q].cnt, sizeof(int32_t), cudaMemcpyDeviceToHost));
     for (int64_t v : h) {
       if (v == 0) continue;   // team not hosted there (an empty gradient hashes to 0 too)
       if (!have) {
@@ -905,12 +945,12 @@ void Engine::div_diag(int task, int64_t* out) {
   int32_t bad = 0, cnt = 0, mode = 0;
   int64_t tot = 0;
   uint32_t pre = 0;
-  CK(cudaMemcpy(&bad, dt.cand_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+  CK(mcpy(&bad, dt.cand_bad, sizeof(bad), cudaMemcpyDeviceToHost));
   cnt = dt.max_tiles;
-  CK(cudaMemcpy(&tot, dt.cand_total, sizeof(tot), cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(&pre, dt.pre_key, sizeof(pre), cudaMemcpyDeviceToHost));
+  CK(mcpy(&tot, dt.cand_total, sizeof(tot), cudaMemcpyDeviceToHost));
+  CK(mcpy(&pre, dt.pre_key, sizeof(pre), cudaMemcpyDeviceToHost));
   const int li = task / m_, b = task % m_;
-  CK(cudaMemcpy(&mode, &div_scr_[static_cast<size_t>(li)][static_cast<size_t>(b)]->mode,
+  CK(mcpy(&mode, &div_scr_[static_cast<size_t>(li)][static_cast<size_t>(b)]->mode,
                 sizeof(mode), cudaMemcpyDeviceToHost));
   out[0] = mode;
   out[1] = bad;
@@ -926,7 +966,7 @@ int64_t Engine::dense_fallbacks() {
   for (const auto& row : div_scr_)
     for (const sdl::SelScratch* sc : row) {
       int32_t mode = 0;
-      CK(cudaMemcpy(&mode, &sc->mode, sizeof(mode), cudaMemcpyDeviceToHost));
+      CK(mcpy(&mode, &sc->mode, sizeof(mode), cudaMemcpyDeviceToHost));
       n += mode == 1;
     }
   return n;
@@ -937,7 +977,7 @@ void Engine::union_sizes(int64_t* out) {
   sync();
   std::vector<int64_t> all(static_cast<size_t>(P_));
   int64_t* tmp = rb_dev_;
-  CK(cudaMemcpy(tmp, ntot_, sizeof(int64_t) * wloc_, cudaMemcpyDeviceToDevice));
+  CK(mcpy(tmp, ntot_, sizeof(int64_t) * wloc_, cudaMemcpyDeviceToDevice));
   allgather_i64(comm_, stream_, world_, tmp, wloc_, all.data(), tmp + wloc_);
   for (int g = 0; g < m_; ++g) out[g] = all[static_cast<size_t>(g)];   // team 0 member g
 }
@@ -946,7 +986,7 @@ void Engine::controller(int local, spardl_hctrl* out) {
   if (cfg_.sag != SPARDL_SAG_BSAG) sdlh::fail(SPARDL_E_CONFIG, "no controller: sag != bsag");
   sync();
   sdl::HCtl c;
-  CK(cudaMemcpy(&c, ctl_dev_ + local, sizeof(c), cudaMemcpyDeviceToHost));
+  CK(mcpy(&c, ctl_dev_ + local, sizeof(c), cudaMemcpyDeviceToHost));
   *out = {c.lower, c.upper, c.target, c.h, c.step, c.flag, 0};
 }
 
@@ -954,7 +994,7 @@ void Engine::global(int local, const int32_t** idx, const float** val, int64_t* 
   sync();
   const Slot& gs = global_[static_cast<size_t>(team_of_local_global_[static_cast<size_t>(local)])];
   int32_t n = 0;
-  CK(cudaMemcpy(&n, gs.cnt, sizeof(n), cudaMemcpyDeviceToHost));
+  CK(mcpy(&n, gs.cnt, sizeof(n), cudaMemcpyDeviceToHost));
   *idx = gs.idx;
   *val = gs.val;
   *nnz = n;

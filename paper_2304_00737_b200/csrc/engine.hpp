@@ -44,6 +44,7 @@ class Arena {
   ~Arena();
   void* alloc(size_t bytes);
   size_t total() const { return total_; }
+  bool dry = false;   // plan-only mode: hand out fake addresses, touch no device
 
  private:
   std::vector<void*> chunks_;
@@ -76,10 +77,21 @@ struct Step {            // a stage followed by a transport round
   bool controller_after = false;
 };
 
+// One NCCL point-to-point op of a rank's iteration (plan-only inspection).
+struct PlanOp {
+  int32_t round;
+  int32_t peer;       // other rank
+  int32_t is_send;
+  int32_t uid;        // block buffer id (identical numbering on every rank)
+  int64_t bytes;
+};
+
 class Engine {
  public:
   Engine(const spardl_config& cfg, int device, int world, int rank, const void* nccl_id,
-         cudaStream_t stream);
+         cudaStream_t stream, bool plan_only = false);
+  // the NCCL ops this rank issues per iteration, in issue order
+  std::vector<PlanOp> plan_ops() const;
   ~Engine();
 
   void run(const float* const* grads_dev);
@@ -131,6 +143,10 @@ class Engine {
   int rank_of(int w) const { return w / wloc_; }
   void exec_round(const std::vector<Xfer>& xs);
   int exec_stage(const Stage& st);
+  cudaError_t mcpy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    return dry_ ? cudaSuccess : cudaMemcpy(dst, src, bytes, kind);
+  }
+  bool dry_ = false;
   void enqueue_iteration(cudaEvent_t* ev = nullptr);
   void drop_graph();
 

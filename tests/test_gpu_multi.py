@@ -1,0 +1,113 @@
+"""Multi-GPU parity (one process per GPU, NCCL point-to-point over NVLink).
+
+The P workers are spread over the available GPUs; every rank checks its
+own workers' residuals, the global gradient and the full ledger bit-exactly
+against the fp32 oracle.  Skipped with fewer than 2 GPUs (run under
+`gpurun --gpus 2` / `--gpus 4`).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+CASES = [(8, 1, "none", "gres", "optimized"), (6, 1, "none", "gres", "naive"),
+         (8, 2, "rsag", "gres", "optimized"), (8, 4, "bsag", "gres", "optimized"),
+         (6, 3, "bsag", "pres", "optimized"), (4, 2, "rsag", "lres", "optimized"),
+         (8, 8, "rsag", "gres", "optimized")]
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    import torch.distributed as dist
+    import paper_2304_00737_b200 as sd
+    from gpu_util import gen
+    from pyoracle import Oracle, make_config
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    errors = []
+    try:
+        orc = Oracle("f32")
+        for P, d, sag, residual, timing in CASES:
+            if P % world:
+                continue
+            N, k = 300_000 + P, P * 1000
+            cfg = sd.ClusterConfig(workers=P, dimension=N, k=k, teams=d, sag=sag,
+                                   residual=residual, timing=timing)
+            ctx = sd.SparDL.from_process_group(cfg, device=rank)
+            ref = orc.pipeline(make_config(P, N, k, d, sag, residual, timing))
+            rng = np.random.default_rng(P * 7 + d)
+            for it in range(3):
+                g = gen("gauss" if it != 1 else "int", (P, N), rng)
+                dev = [torch.from_numpy(g[ctx.first_worker + i]).cuda()
+                       for i in range(ctx.local_workers)]
+                ctx.all_reduce(dev)
+                info = ctx.run_info()           # collective
+                lr, ls = ctx.ledger()           # collective
+                rinfo = ref.allreduce(g)
+                tag = f"rank{rank} P={P} d={d} {sag} {residual} {timing} it={it}"
+                gi, gv = ctx.global_gradient(0)
+                ri, rv = ref.global_gradient()
+                if not (np.array_equal(gi.cpu().numpy().astype(np.int64), ri)
+                        and np.array_equal(gv.cpu().numpy().view(np.uint32), rv.view(np.uint32))):
+                    errors.append(tag + " global")
+                for i in range(ctx.local_workers):
+                    w = ctx.first_worker + i
+                    if not np.array_equal(ctx.carry(i).cpu().numpy().view(np.uint32),
+                                          ref.carry(w).view(np.uint32)):
+                        errors.append(tag + f" carry w={w}")
+                rr, rs = ref.ledger()
+                if list(lr) != list(rr) or list(ls) != list(rs):
+                    errors.append(tag + " ledger")
+                for key in ("max_rounds", "max_scalars", "srs_scalars", "sag_scalars",
+                            "gather_scalars", "consistent"):
+                    if info[key] != rinfo[key]:
+                        errors.append(tag + f" {key} {info[key]} != {rinfo[key]}")
+                if sag == "bsag" and ctx.union_sizes() != list(ref.union_sizes()):
+                    errors.append(tag + " union sizes")
+            ctx.close()
+    except Exception as e:  # report, do not hang the peer
+        errors.append(f"rank{rank} exception {e!r}")
+    q.put((rank, errors))
+    try:
+        dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_parity(built, world):
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=840) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(not v for v in res.values()), res

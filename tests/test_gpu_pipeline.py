@@ -131,3 +131,28 @@ def test_pipeline_vs_reference_grid(env, P, d, sag):
         for w in range(P):
             assert np.array_equal(ctx.carry(w).cpu().numpy().astype(np.float64), ref.carry(w))
     ctx.close()
+
+
+GOLDEN = sorted(__import__("glob").glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_pipeline_golden_fixture(env, path):
+    """The device path reproduces the reference-generated fixtures exactly."""
+    sd, _, torch = env
+    z = np.load(path)
+    P, N, k, d = (int(x) for x in z["cfg"][:4])
+    sag, residual, timing = (str(x) for x in z["modes"])
+    ctx = sd.SparDL(sd.ClusterConfig(workers=P, dimension=N, k=k, teams=d, sag=sag,
+                                     residual=residual, timing=timing))
+    for it in range(int(z["iters"])):
+        g = z[f"g{it}"].astype(np.float32)
+        ctx.all_reduce([torch.from_numpy(g[w]).cuda() for w in range(P)])
+        info = ctx.run_info()
+        gi, gv = ctx.global_gradient(0)
+        assert np.array_equal(gi.cpu().numpy().astype(np.int64), z[f"gi{it}"])
+        assert np.array_equal(gv.cpu().numpy().astype(np.float64), z[f"gv{it}"])
+        for w in range(P):
+            assert np.array_equal(ctx.carry(w).cpu().numpy().astype(np.float64), z[f"carry{it}_{w}"])
+        assert [info["max_rounds"], info["max_scalars"]] == z[f"ledger{it}"].tolist()
+    ctx.close()
