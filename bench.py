@@ -273,21 +273,22 @@ def main():
         e1.record(stream)
         e1.synchronize()
         ms = e0.elapsed_time(e1) / steps
-        if sampler:
-            # keep the GPU loaded until the sampler has seen enough of it
-            t_end = time.time() + 3.0
-            while len(sampler.rows) < 8 and time.time() < t_end:
-                for _ in range(20):
-                    ctx.all_reduce(grads)
-                ctx.sync()
-            sampler.recording = False
-            sampler.stop()
-            out["clocks"] = sampler.summary()
-        ctx.sync()
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         out["ms"] = float(t.item())
+        if extras:
+            # keep every GPU loaded (all ranks in lockstep: the iterations are
+            # collective) until the clock sampler has seen >= ~1.5 s of load
+            soak = max(0, min(4000, int((1500.0 - out["ms"] * steps) / max(out["ms"], 1e-3))))
+            for _ in range(soak):
+                ctx.all_reduce(grads)
+            ctx.sync()
+        if sampler:
+            sampler.recording = False
+            sampler.stop()
+            out["clocks"] = sampler.summary()
+        ctx.sync()
         out["launches"] = ctx.kernel_launches()
         info = ctx.run_info()
         out["consistent"] = info["consistent"]
