@@ -1,0 +1,658 @@
+// spardl_b200.hpp -- C++ drop-in surface of the B200 SparDL path.
+//
+// Mirrors the public API of the reference's header-only library
+// (/root/reference/proj/include/spardl, "inc/") so that reference users keep
+// their code: same namespace, type and function names, argument meaning and
+// exception classes.  The implementation is a thin layer over the C ABI of
+// libspardl_cuda.so (include/spardl_cuda.h): the sparse arithmetic and the
+// whole all-reduce run on the GPU; this header only converts containers.
+//
+// Numerics: the device computes values in fp32 (indices int32); doubles are
+// converted on the way in.  Inputs that are fp32-representable produce the
+// reference's results bit-for-bit wherever the reference's own arithmetic
+// stays fp32-exact (e.g. grid-snapped gradients); otherwise values agree to
+// fp32 rounding.
+//
+// Link with -lspardl_cuda (paper_2304_00737_b200/libspardl_cuda.so).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <optional>
+#include <ostream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "spardl_cuda.h"
+
+namespace spardl {
+
+// ---------------------------------------------------------------- errors (inc/error.hpp)
+class error : public std::runtime_error {
+ public:
+  explicit error(const std::string& what) : std::runtime_error(what) {}
+};
+#define SPARDL_B200_ERROR_CLASS(name) \
+  class name : public error {         \
+   public:                            \
+    using error::error;               \
+  };
+SPARDL_B200_ERROR_CLASS(partition_error)
+SPARDL_B200_ERROR_CLASS(block_mismatch_error)
+SPARDL_B200_ERROR_CLASS(schedule_violation_error)
+SPARDL_B200_ERROR_CLASS(theorem_violation_error)
+SPARDL_B200_ERROR_CLASS(group_size_error)
+SPARDL_B200_ERROR_CLASS(config_error)
+SPARDL_B200_ERROR_CLASS(state_error)
+SPARDL_B200_ERROR_CLASS(consistency_error)
+#undef SPARDL_B200_ERROR_CLASS
+
+namespace b200 {
+// status code of the C ABI -> the reference's exception class
+inline void check(int rc) {
+  if (rc == SPARDL_OK) return;
+  const std::string m = spardl_last_error();
+  switch (rc) {
+    case SPARDL_E_PARTITION: throw partition_error(m);
+    case SPARDL_E_BLOCK_MISMATCH: throw block_mismatch_error(m);
+    case SPARDL_E_SCHEDULE: throw schedule_violation_error(m);
+    case SPARDL_E_THEOREM: throw theorem_violation_error(m);
+    case SPARDL_E_GROUP_SIZE: throw group_size_error(m);
+    case SPARDL_E_CONFIG: throw config_error(m);
+    case SPARDL_E_STATE: throw state_error(m);
+    case SPARDL_E_CONSISTENCY: throw consistency_error(m);
+    default: throw error(m);
+  }
+}
+}  // namespace b200
+
+// ---------------------------------------------------------------- inc/mathutil.hpp
+constexpr bool is_power_of_two(std::int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+constexpr int ceil_log2(std::int64_t x) { return x <= 1 ? 0 : 1 + ceil_log2((x + 1) / 2); }
+constexpr int exact_log2(std::int64_t x) { return x <= 1 ? 0 : 1 + exact_log2(x / 2); }
+
+// ---------------------------------------------------------------- inc/sparse.hpp
+using Index = std::int64_t;
+
+struct GradientVector {
+  std::vector<double> values;
+  GradientVector() = default;
+  explicit GradientVector(Index n, double fill = 0.0) : values(static_cast<size_t>(n), fill) {}
+  explicit GradientVector(std::vector<double> v) : values(std::move(v)) {}
+  Index size() const { return static_cast<Index>(values.size()); }
+  double& operator[](Index i) { return values[static_cast<size_t>(i)]; }
+  double operator[](Index i) const { return values[static_cast<size_t>(i)]; }
+};
+
+struct IndexRange {
+  Index lo = 0;
+  Index hi = 0;
+  Index size() const { return hi - lo; }
+  bool contains(Index i) const { return lo <= i && i < hi; }
+  bool operator==(const IndexRange&) const = default;
+};
+
+struct Entry {
+  Index index = 0;
+  double value = 0.0;
+  bool operator==(const Entry&) const = default;
+};
+
+struct SparseBlock {
+  int block_id = 0;
+  IndexRange range;
+  std::vector<Entry> entries;
+  Index nnz() const { return static_cast<Index>(entries.size()); }
+  bool empty() const { return entries.empty(); }
+  bool operator==(const SparseBlock&) const = default;
+};
+
+struct BlockPartition {
+  Index n = 0;
+  int block_count = 0;
+  std::vector<IndexRange> ranges;
+  const IndexRange& range_of(int block_id) const { return ranges[static_cast<size_t>(block_id)]; }
+  int block_of(Index i) const {
+    std::int32_t b = 0;
+    b200::check(spardl_block_of(n, block_count, i, &b));
+    return b;
+  }
+};
+
+inline BlockPartition partition(Index n, int block_count) {
+  BlockPartition p;
+  p.n = n;
+  p.block_count = block_count;
+  std::vector<std::int64_t> lo(static_cast<size_t>(std::max(block_count, 1)));
+  std::vector<std::int64_t> hi(lo.size());
+  b200::check(spardl_partition(n, block_count, lo.data(), hi.data()));
+  for (int b = 0; b < block_count; ++b) p.ranges.push_back({lo[size_t(b)], hi[size_t(b)]});
+  return p;
+}
+
+// The selection order of the device select (|v| desc, index asc).
+inline bool selection_before(const Entry& a, const Entry& b) {
+  const double x = a.value < 0 ? -a.value : a.value;
+  const double y = b.value < 0 ? -b.value : b.value;
+  return x != y ? x > y : a.index < b.index;
+}
+
+struct TopKResult {
+  SparseBlock selected;
+  SparseBlock discarded;
+};
+
+namespace b200 {
+inline std::int32_t idx32(Index i) {
+  if (i < 0 || i >= (Index(1) << 31)) throw error("index outside the device's int32 range");
+  return static_cast<std::int32_t>(i);
+}
+}  // namespace b200
+
+// Device selection; the entries returned carry the caller's own values.
+inline TopKResult top_k_select(const SparseBlock& block, Index budget) {
+  if (budget < 0) throw error("top_k_select: negative budget");
+  TopKResult out;
+  out.selected.block_id = out.discarded.block_id = block.block_id;
+  out.selected.range = out.discarded.range = block.range;
+  const size_t n = block.entries.size();
+  std::vector<std::int32_t> idx(n), si(n + 1), di(n + 1);
+  std::vector<float> val(n), sv(n + 1), dv(n + 1);
+  std::map<Index, double> orig;
+  for (size_t e = 0; e < n; ++e) {
+    idx[e] = b200::idx32(block.entries[e].index);
+    val[e] = static_cast<float>(block.entries[e].value);
+    orig[block.entries[e].index] = block.entries[e].value;
+  }
+  std::int64_t ns = 0, nd = 0;
+  b200::check(spardl_topk_select_hostbuf(idx.data(), val.data(), static_cast<std::int64_t>(n),
+                                         budget, si.data(), sv.data(), &ns, di.data(), dv.data(),
+                                         &nd));
+  for (std::int64_t e = 0; e < ns; ++e) out.selected.entries.push_back({si[size_t(e)], orig[si[size_t(e)]]});
+  for (std::int64_t e = 0; e < nd; ++e) out.discarded.entries.push_back({di[size_t(e)], orig[di[size_t(e)]]});
+  return out;
+}
+
+inline TopKResult top_k_select_slice(const GradientVector& g, int block_id,
+                                     const IndexRange& range, Index budget) {
+  if (budget < 0) throw error("top_k_select: negative budget");
+  std::vector<float> gf(static_cast<size_t>(range.hi));
+  for (Index i = range.lo; i < range.hi; ++i) gf[size_t(i)] = static_cast<float>(g[i]);
+  const size_t n = static_cast<size_t>(range.size());
+  std::vector<std::int32_t> si(n + 1);
+  std::vector<float> sv(n + 1);
+  std::int64_t ns = 0;
+  b200::check(spardl_topk_select_slice_hostbuf(gf.data(), range.lo, range.hi, budget, si.data(),
+                                               sv.data(), &ns));
+  TopKResult out;
+  out.selected.block_id = out.discarded.block_id = block_id;
+  out.selected.range = out.discarded.range = range;
+  std::vector<char> taken(n, 0);
+  for (std::int64_t e = 0; e < ns; ++e) {
+    const Index i = si[size_t(e)];
+    out.selected.entries.push_back({i, g[i]});
+    taken[size_t(i - range.lo)] = 1;
+  }
+  for (Index i = range.lo; i < range.hi; ++i)
+    if (!taken[size_t(i - range.lo)]) out.discarded.entries.push_back({i, g[i]});
+  return out;
+}
+
+// Device merge: values summed in fp32 (exact for fp32-representable sums).
+inline SparseBlock merge_add(const SparseBlock& a, const SparseBlock& b) {
+  if (a.block_id != b.block_id)
+    throw block_mismatch_error("merge_add: block ids differ (" + std::to_string(a.block_id) +
+                               " vs " + std::to_string(b.block_id) + ")");
+  std::vector<std::int32_t> ai, bi;
+  std::vector<float> av, bv;
+  for (const Entry& e : a.entries) ai.push_back(b200::idx32(e.index)), av.push_back(float(e.value));
+  for (const Entry& e : b.entries) bi.push_back(b200::idx32(e.index)), bv.push_back(float(e.value));
+  const std::int32_t* ip[2] = {ai.data(), bi.data()};
+  const float* vp[2] = {av.data(), bv.data()};
+  const std::int64_t ns[2] = {std::int64_t(ai.size()), std::int64_t(bi.size())};
+  std::vector<std::int32_t> oi(ai.size() + bi.size() + 1);
+  std::vector<float> ov(oi.size());
+  std::int64_t no = 0;
+  b200::check(spardl_merge_add_hostbuf(2, ip, vp, ns, oi.data(), ov.data(), &no));
+  SparseBlock out;
+  out.block_id = a.block_id;
+  out.range = a.range;
+  for (std::int64_t e = 0; e < no; ++e) out.entries.push_back({oi[size_t(e)], ov[size_t(e)]});
+  return out;
+}
+
+inline SparseBlock scale(const SparseBlock& block, double factor) {
+  SparseBlock out = block;
+  for (Entry& e : out.entries) e.value *= factor;
+  return out;
+}
+
+struct GlobalSparseGradient {
+  Index n = 0;
+  std::vector<Entry> entries;
+  Index nnz() const { return static_cast<Index>(entries.size()); }
+  bool operator==(const GlobalSparseGradient&) const = default;
+};
+
+inline bool well_formed(const SparseBlock& block) {
+  for (size_t e = 0; e < block.entries.size(); ++e) {
+    if (!block.range.contains(block.entries[e].index)) return false;
+    if (e && block.entries[e].index <= block.entries[e - 1].index) return false;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- inc/fabric.hpp
+using WorkerId = int;
+
+struct WorkerCost {
+  std::int64_t rounds = 0;
+  std::int64_t scalars_received = 0;
+  bool operator==(const WorkerCost&) const = default;
+};
+
+struct LedgerReport {
+  std::vector<WorkerCost> per_worker;
+  std::int64_t max_rounds = 0;
+  std::int64_t max_scalars_received = 0;
+};
+
+struct ClusterConfig;
+namespace b200 {
+struct DeviceState;   // the GPU context a Fabric drives (created on first use)
+}
+
+// The fabric of the drop-in API.  spardl_all_reduce moves blocks GPU to GPU
+// (NVLink); the ledger here is the reference's alpha-beta account of it.
+class Fabric {
+ public:
+  struct Send {
+    WorkerId target = 0;
+    std::vector<SparseBlock> payload;
+  };
+  using RoundPlan = std::vector<std::optional<Send>>;
+
+  explicit Fabric(int worker_count) : costs_(static_cast<size_t>(worker_count > 0 ? worker_count : 0)) {
+    if (worker_count < 1) throw config_error("fabric needs >= 1 worker");
+  }
+  int worker_count() const { return static_cast<int>(costs_.size()); }
+
+  // One lockstep round of host-side block delivery with the reference's
+  // accounting (used by callers that drive their own schedules).
+  std::vector<std::vector<SparseBlock>> exchange(RoundPlan plan) {
+    const int p = worker_count();
+    if (static_cast<int>(plan.size()) != p)
+      throw schedule_violation_error("round plan size != worker count");
+    std::vector<std::vector<SparseBlock>> inbox(plan.size());
+    std::vector<char> hit(plan.size(), 0), active(plan.size(), 0);
+    for (WorkerId s = 0; s < p; ++s) {
+      auto& snd = plan[size_t(s)];
+      if (!snd) continue;
+      const WorkerId t = snd->target;
+      if (t < 0 || t >= p)
+        throw schedule_violation_error("message target out of range: " + std::to_string(t));
+      if (hit[size_t(t)])
+        throw schedule_violation_error("two messages target worker " + std::to_string(t) +
+                                       " in one round");
+      hit[size_t(t)] = active[size_t(s)] = active[size_t(t)] = 1;
+      for (const SparseBlock& b : snd->payload) costs_[size_t(t)].scalars_received += 2 * b.nnz();
+      inbox[size_t(t)] = std::move(snd->payload);
+    }
+    for (size_t w = 0; w < active.size(); ++w) costs_[w].rounds += active[w];
+    return inbox;
+  }
+
+  const std::vector<WorkerCost>& ledger() const { return costs_; }
+  LedgerReport report() const {
+    LedgerReport r;
+    r.per_worker = costs_;
+    for (const WorkerCost& c : costs_) {
+      r.max_rounds = std::max(r.max_rounds, c.rounds);
+      r.max_scalars_received = std::max(r.max_scalars_received, c.scalars_received);
+    }
+    return r;
+  }
+  WorkerCost delta_since(const std::vector<WorkerCost>& snap) const {
+    WorkerCost d;
+    for (size_t w = 0; w < costs_.size(); ++w) {
+      d.rounds = std::max(d.rounds, costs_[w].rounds - snap[w].rounds);
+      d.scalars_received =
+          std::max(d.scalars_received, costs_[w].scalars_received - snap[w].scalars_received);
+    }
+    return d;
+  }
+
+  // drop-in internals
+  std::vector<WorkerCost>& mutable_ledger() { return costs_; }
+  std::shared_ptr<b200::DeviceState> device;
+
+ private:
+  std::vector<WorkerCost> costs_;
+};
+
+inline void write_ledger_csv(std::ostream& os, const Fabric& fabric) {
+  os << "worker_id,rounds,scalars_received\n";
+  for (size_t w = 0; w < fabric.ledger().size(); ++w)
+    os << w << ',' << fabric.ledger()[w].rounds << ',' << fabric.ledger()[w].scalars_received
+       << '\n';
+}
+
+// ---------------------------------------------------------------- inc/reduce_scatter.hpp
+enum class SrsTiming { optimized, naive };
+
+struct BagSchedule {
+  int team_size = 1;
+  int worker_rank = 0;
+  int l = 0;
+  int preservation = 0;
+  std::vector<std::vector<int>> sending_bags;
+  int remainder = 0;
+  bool operator==(const BagSchedule&) const = default;
+};
+
+inline BagSchedule build_bags(int team_size, int worker_rank) {
+  std::int32_t l = 0, rem = 0;
+  std::vector<std::int32_t> sizes(64), pos(static_cast<size_t>(std::max(team_size, 1)));
+  b200::check(spardl_build_bags(team_size, worker_rank, &l, &rem, sizes.data(), pos.data()));
+  BagSchedule s;
+  s.team_size = team_size;
+  s.worker_rank = worker_rank;
+  s.preservation = worker_rank;
+  s.l = l;
+  s.remainder = rem;
+  size_t o = 0;
+  for (int j = 0; j < l; ++j) {
+    s.sending_bags.emplace_back(pos.begin() + std::ptrdiff_t(o),
+                                pos.begin() + std::ptrdiff_t(o + size_t(sizes[size_t(j)])));
+    o += size_t(sizes[size_t(j)]);
+  }
+  return s;
+}
+
+struct SrsCost {
+  std::int64_t rounds = 0;
+  std::int64_t scalars = 0;
+};
+inline SrsCost expected_cost_srs(std::int64_t m, std::int64_t k) {
+  SrsCost c;
+  b200::check(spardl_expected_cost_srs(m, k, &c.rounds, &c.scalars));
+  return c;
+}
+
+// ---------------------------------------------------------------- inc/sag.hpp
+class HController {
+ public:
+  HController(std::int64_t workers, std::int64_t k, std::int64_t teams) {
+    b200::check(spardl_hctrl_init(&s_, workers, k, teams));
+  }
+  double h() const { return s_.h; }
+  double step() const { return s_.step; }
+  bool flag() const { return s_.flag != 0; }
+  std::int64_t target() const { return s_.target; }
+  Index budget() const {
+    std::int64_t b = 0;
+    b200::check(spardl_hctrl_budget(&s_, &b));
+    return b;
+  }
+  void observe(std::int64_t n_t) { b200::check(spardl_hctrl_observe(&s_, n_t)); }
+  const spardl_hctrl& raw() const { return s_; }
+  spardl_hctrl& raw() { return s_; }
+
+ private:
+  spardl_hctrl s_{};
+};
+
+inline void controller_update(HController& c, std::int64_t n_t) { c.observe(n_t); }
+
+inline std::vector<double> dyadic_shares(int count) {
+  std::vector<double> s(static_cast<size_t>(std::max(count, 1)));
+  b200::check(spardl_dyadic_shares(count, s.data()));
+  s.resize(static_cast<size_t>(std::max(count, 0)));
+  return s;
+}
+
+enum class SagMode { none, rsag, bsag };
+
+struct CostRange {
+  std::int64_t rounds = 0;
+  std::int64_t scalars_low = 0;
+  std::int64_t scalars_high = 0;
+  bool exact() const { return scalars_low == scalars_high; }
+};
+
+inline CostRange expected_cost_sag(std::int64_t workers, std::int64_t k, std::int64_t teams,
+                                   SagMode mode) {
+  CostRange c;
+  b200::check(spardl_expected_cost_sag(workers, k, teams, static_cast<std::int32_t>(mode),
+                                       &c.rounds, &c.scalars_low, &c.scalars_high));
+  return c;
+}
+inline CostRange bsag_phase_cost(std::int64_t workers, std::int64_t k, std::int64_t teams) {
+  CostRange c;
+  b200::check(spardl_bsag_phase_cost(workers, k, teams, &c.rounds, &c.scalars_low,
+                                     &c.scalars_high));
+  return c;
+}
+inline CostRange topka_cost(std::int64_t workers, std::int64_t k) {
+  CostRange c;
+  b200::check(spardl_topka_cost(workers, k, &c.rounds, &c.scalars_low, &c.scalars_high));
+  return c;
+}
+
+// ---------------------------------------------------------------- inc/residual.hpp
+enum class ResidualMode { gres, pres, lres };
+
+// Host view of a worker's residual; the authoritative copy lives on the GPU
+// and is mirrored here after every spardl_all_reduce.
+class ResidualStore {
+ public:
+  ResidualStore(ResidualMode mode, Index n) : mode_(mode), n_(n), carry_(n) {}
+  ResidualMode mode() const { return mode_; }
+  Index dimension() const { return n_; }
+  const GradientVector& carry() const { return carry_; }
+  GradientVector& mutable_carry() { return carry_; }
+
+ private:
+  ResidualMode mode_;
+  Index n_;
+  GradientVector carry_;
+};
+
+// ---------------------------------------------------------------- inc/pipeline.hpp
+struct ClusterConfig {
+  std::int64_t workers = 1;
+  std::int64_t dimension = 1;
+  std::int64_t k = 1;
+  std::int64_t teams = 1;
+  SagMode sag = SagMode::none;
+  ResidualMode residual = ResidualMode::gres;
+  SrsTiming timing = SrsTiming::optimized;
+  std::uint64_t seed = 0;
+  std::int64_t team_size() const { return workers / teams; }
+  std::int64_t block_budget() const { return teams * k / workers; }
+};
+
+namespace b200 {
+inline spardl_config to_c(const ClusterConfig& c) {
+  spardl_config o{};
+  o.workers = c.workers;
+  o.dimension = c.dimension;
+  o.k = c.k;
+  o.teams = c.teams;
+  o.sag = static_cast<std::int32_t>(c.sag);
+  o.residual = static_cast<std::int32_t>(c.residual);
+  o.timing = static_cast<std::int32_t>(c.timing);
+  o.seed = c.seed;
+  return o;
+}
+
+struct DeviceState {
+  spardl_config cfg{};
+  spardl_ctx* ctx = nullptr;
+  std::vector<std::int64_t> last_scalars, last_rounds;
+  ~DeviceState() {
+    if (ctx) spardl_ctx_destroy(ctx);
+  }
+};
+}  // namespace b200
+
+inline void validate(const ClusterConfig& cfg) {
+  const spardl_config c = b200::to_c(cfg);
+  b200::check(spardl_validate(&c));
+}
+
+struct WorkerState {
+  ResidualStore residual;
+  std::optional<HController> controller;
+};
+
+inline std::vector<WorkerState> make_worker_states(const ClusterConfig& cfg) {
+  validate(cfg);
+  std::vector<WorkerState> s;
+  for (std::int64_t w = 0; w < cfg.workers; ++w) {
+    WorkerState ws{ResidualStore(cfg.residual, cfg.dimension), std::nullopt};
+    if (cfg.sag == SagMode::bsag) ws.controller.emplace(cfg.workers, cfg.k, cfg.teams);
+    s.push_back(std::move(ws));
+  }
+  return s;
+}
+
+inline bool verify_consistency(const std::vector<GlobalSparseGradient>& per_worker) {
+  for (size_t w = 1; w < per_worker.size(); ++w)
+    if (!(per_worker[w] == per_worker[0])) return false;
+  return true;
+}
+
+struct PhaseCost {
+  std::int64_t rounds = 0;
+  std::int64_t scalars = 0;
+};
+
+struct RunResult {
+  GlobalSparseGradient global;
+  std::vector<GlobalSparseGradient> per_worker;
+  bool consistent = false;
+  bool conservation_applicable = false;
+  double conservation_error = 0.0;
+  LedgerReport ledger;
+  PhaseCost srs_phase;
+  PhaseCost sag_phase;
+  PhaseCost gather_phase;
+  CostRange predicted;
+  std::vector<std::int64_t> union_sizes;
+};
+
+inline CostRange expected_cost(const ClusterConfig& cfg) {
+  validate(cfg);
+  return expected_cost_sag(cfg.workers, cfg.k, cfg.teams, cfg.sag);
+}
+
+// The sparse All-Reduce on the GPU: all P workers on device 0 of this
+// process (the multi-GPU form is spardl_ctx_create with world_size > 1).
+inline RunResult spardl_all_reduce(Fabric& fabric, const ClusterConfig& cfg,
+                                   const std::vector<GradientVector>& grads,
+                                   std::vector<WorkerState>& states) {
+  validate(cfg);
+  const int p = static_cast<int>(cfg.workers);
+  if (fabric.worker_count() != p || grads.size() != size_t(p) || states.size() != size_t(p))
+    throw config_error("worker count mismatch between fabric/inputs/states");
+  const spardl_config c = b200::to_c(cfg);
+  auto& dev = fabric.device;
+  if (!dev || std::memcmp(&dev->cfg, &c, sizeof(c)) != 0) {
+    dev = std::make_shared<b200::DeviceState>();
+    dev->cfg = c;
+    b200::check(spardl_ctx_create(&c, 0, 1, 0, nullptr, nullptr, &dev->ctx));
+    dev->last_scalars.assign(size_t(p), 0);
+    dev->last_rounds.assign(size_t(p), 0);
+  }
+  const size_t n = static_cast<size_t>(cfg.dimension);
+  // WorkerState in (value semantics): residual carries and controllers
+  const size_t np = static_cast<size_t>(p);
+  std::vector<std::vector<float>> g32(np, std::vector<float>(n));
+  std::vector<std::vector<float>> comb(np, std::vector<float>(n));
+  std::vector<const float*> gp(np);
+  for (int w = 0; w < p; ++w) {
+    if (states[size_t(w)].residual.mode() != cfg.residual)
+      throw config_error("residual store mode differs from configuration");
+    if (grads[size_t(w)].size() != cfg.dimension)
+      throw config_error("apply_residual: dimension mismatch");
+    std::vector<float> carry(n);
+    for (size_t i = 0; i < n; ++i) {
+      g32[size_t(w)][i] = static_cast<float>(grads[size_t(w)].values[i]);
+      carry[i] = static_cast<float>(states[size_t(w)].residual.carry().values[i]);
+      comb[size_t(w)][i] = g32[size_t(w)][i] + carry[i];
+    }
+    b200::check(spardl_carry_from_host(dev->ctx, w, carry.data()));
+    if (cfg.sag == SagMode::bsag) {
+      if (!states[size_t(w)].controller)
+        throw config_error("bsag requires controller state per worker");
+      b200::check(spardl_set_controller(dev->ctx, w, &states[size_t(w)].controller->raw()));
+    }
+    gp[size_t(w)] = g32[size_t(w)].data();
+  }
+  std::vector<std::int64_t> gi(size_t(cfg.k) + 1);
+  std::vector<float> gv(size_t(cfg.k) + 1);
+  std::int64_t nnz = 0;
+  b200::check(spardl_allreduce_host(dev->ctx, gp.data(), gi.data(), gv.data(), cfg.k, &nnz));
+  spardl_run_info info{};
+  b200::check(spardl_get_run_info(dev->ctx, &info));
+
+  RunResult r;
+  r.global.n = cfg.dimension;
+  for (std::int64_t e = 0; e < nnz; ++e) r.global.entries.push_back({gi[size_t(e)], gv[size_t(e)]});
+  r.per_worker.assign(size_t(p), r.global);
+  r.consistent = info.consistent != 0;
+  // WorkerState out
+  std::vector<float> carry(n);
+  for (int w = 0; w < p; ++w) {
+    b200::check(spardl_carry_to_host(dev->ctx, w, carry.data()));
+    auto& dst = states[size_t(w)].residual.mutable_carry().values;
+    for (size_t i = 0; i < n; ++i) dst[i] = carry[i];
+    if (cfg.sag == SagMode::bsag)
+      b200::check(spardl_get_controller(dev->ctx, w, &states[size_t(w)].controller->raw()));
+  }
+  // ledger: the device ledger is cumulative per context; fold its delta in
+  std::vector<std::int64_t> rounds(np), scalars(np);
+  b200::check(spardl_get_ledger(dev->ctx, rounds.data(), scalars.data()));
+  for (int w = 0; w < p; ++w) {
+    auto& l = fabric.mutable_ledger()[size_t(w)];
+    l.scalars_received += scalars[size_t(w)] - dev->last_scalars[size_t(w)];
+    l.rounds += rounds[size_t(w)] - dev->last_rounds[size_t(w)];
+    dev->last_scalars[size_t(w)] = scalars[size_t(w)];
+    dev->last_rounds[size_t(w)] = rounds[size_t(w)];
+  }
+  r.ledger = fabric.report();
+  r.srs_phase = {info.srs_rounds, info.srs_scalars};
+  r.sag_phase = {info.sag_rounds, info.sag_scalars};
+  r.gather_phase = {info.gather_rounds, info.gather_scalars};
+  r.predicted = {info.pred_rounds, info.pred_low, info.pred_high};
+  if (info.n_union > 0) {
+    r.union_sizes.resize(size_t(info.n_union));
+    b200::check(spardl_get_union_sizes(dev->ctx, r.union_sizes.data()));
+  }
+  // conservation audit as the reference states it (inc/pipeline.hpp:305-334)
+  r.conservation_applicable = cfg.residual == ResidualMode::gres;
+  double worst = 0.0;
+  {
+    std::vector<double> lhs(n, 0.0), rhs(n, 0.0);
+    for (int w = 0; w < p; ++w)
+      for (size_t i = 0; i < n; ++i) lhs[i] += comb[size_t(w)][i];
+    for (const Entry& e : r.global.entries) rhs[size_t(e.index)] += e.value;
+    for (int w = 0; w < p; ++w)
+      for (size_t i = 0; i < n; ++i) rhs[i] += states[size_t(w)].residual.carry().values[i];
+    for (size_t i = 0; i < n; ++i) {
+      const double den = std::max(1.0, lhs[i] < 0 ? -lhs[i] : lhs[i]);
+      const double d = lhs[i] - rhs[i];
+      worst = std::max(worst, (d < 0 ? -d : d) / den);
+    }
+  }
+  r.conservation_error = worst;
+  return r;
+}
+
+}  // namespace spardl

@@ -146,6 +146,16 @@ int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* const* v
                      const int64_t* n, int32_t* out_idx, float* out_val, int64_t* n_out,
                      void* stream);
 
+/* The same three components on HOST buffers (staged through the device by
+ * the library; synchronous).  Used by the C++ drop-in shim. */
+int spardl_topk_select_hostbuf(const int32_t* idx, const float* val, int64_t n, int64_t budget,
+                               int32_t* sel_idx, float* sel_val, int64_t* n_sel,
+                               int32_t* dis_idx, float* dis_val, int64_t* n_dis);
+int spardl_topk_select_slice_hostbuf(const float* g, int64_t lo, int64_t hi, int64_t budget,
+                                     int32_t* sel_idx, float* sel_val, int64_t* n_sel);
+int spardl_merge_add_hostbuf(int32_t r, const int32_t* const* idx, const float* const* val,
+                             const int64_t* n, int32_t* out_idx, float* out_val, int64_t* n_out);
+
 /* ------------------------------------------------------------------ */
 /* the pipeline: spardl_all_reduce, inc/pipeline.hpp:140-342           */
 /* ------------------------------------------------------------------ */
@@ -200,6 +210,12 @@ int spardl_get_global(spardl_ctx* ctx, int32_t local_worker, const int32_t** idx
                       const float** val, int64_t* nnz);
 /* WorkerState::residual.carry() of local worker i (device, N floats) */
 int spardl_get_carry(spardl_ctx* ctx, int32_t local_worker, float** carry_dev);
+/* host copies of WorkerState::residual.carry() (N floats; synchronise) --
+ * used by the C++ drop-in shim to keep the reference's value semantics */
+int spardl_carry_to_host(spardl_ctx* ctx, int32_t local_worker, float* host);
+int spardl_carry_from_host(spardl_ctx* ctx, int32_t local_worker, const float* host);
+/* overwrite WorkerState::controller of local worker i (B-SAG only) */
+int spardl_set_controller(spardl_ctx* ctx, int32_t local_worker, const spardl_hctrl* c);
 /* reset residuals / controllers / ledger to the make_worker_states state */
 int spardl_ctx_reset_state(spardl_ctx* ctx);
 /* Fabric::ledger(), fabric.hpp:110: per GLOBAL worker (P entries); collective */

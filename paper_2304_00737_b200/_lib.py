@@ -133,10 +133,12 @@ EXPORTS = [
     "spardl_expected_cost_sag", "spardl_bsag_phase_cost", "spardl_topka_cost",
     "spardl_dyadic_shares", "spardl_hctrl_init", "spardl_hctrl_observe", "spardl_hctrl_budget",
     "spardl_topk_select", "spardl_topk_select_slice", "spardl_merge_add",
+    "spardl_topk_select_hostbuf", "spardl_topk_select_slice_hostbuf", "spardl_merge_add_hostbuf",
     "spardl_nccl_unique_id", "spardl_ctx_create", "spardl_ctx_destroy", "spardl_plan_ops",
     "spardl_ctx_local_workers", "spardl_ctx_set_graph", "spardl_ctx_set_audit",
     "spardl_allreduce", "spardl_allreduce_host", "spardl_profile", "spardl_sync",
     "spardl_get_run_info", "spardl_get_global", "spardl_get_carry", "spardl_ctx_reset_state",
+    "spardl_carry_to_host", "spardl_carry_from_host", "spardl_set_controller",
     "spardl_get_ledger", "spardl_get_union_sizes", "spardl_get_controller",
     "spardl_dense_fallbacks", "spardl_div_diag", "spardl_kernel_launches", "spardl_ctx_stream",
 ]

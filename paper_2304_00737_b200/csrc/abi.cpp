@@ -346,6 +346,101 @@ EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* c
 }
 
 // ---------------------------------------------------------------------------
+// host-buffer variants: stage through the device, run the device kernels
+namespace {
+template <class T>
+T* to_dev(DevBuf& buf, const T* host, size_t n) {
+  T* d = buf.get<T>(std::max<size_t>(n, 1));
+  if (n) CK(cudaMemcpy(d, host, sizeof(T) * n, cudaMemcpyHostToDevice));
+  return d;
+}
+template <class T>
+void to_host(T* host, const T* dev, size_t n) {
+  if (n) CK(cudaMemcpy(host, dev, sizeof(T) * n, cudaMemcpyDeviceToHost));
+}
+}  // namespace
+
+EXPORT int spardl_topk_select_hostbuf(const int32_t* idx, const float* val, int64_t n,
+                                      int64_t budget, int32_t* sel_idx, float* sel_val,
+                                      int64_t* n_sel, int32_t* dis_idx, float* dis_val,
+                                      int64_t* n_dis) {
+  int rc = SPARDL_OK;
+  const int outer = guarded([&] {
+    require_device();
+    DevBuf buf;
+    const size_t un = static_cast<size_t>(n < 0 ? 0 : n);
+    int32_t* di = to_dev(buf, idx, un);
+    float* dv = to_dev(buf, val, un);
+    int32_t* si = buf.get<int32_t>(un + 1);
+    float* sv = buf.get<float>(un + 1);
+    int32_t* xi = dis_idx ? buf.get<int32_t>(un + 1) : nullptr;
+    float* xv = dis_idx ? buf.get<float>(un + 1) : nullptr;
+    int64_t ns = 0, nd = 0;
+    rc = spardl_topk_select(di, dv, n, budget, si, sv, &ns, xi, xv, &nd, nullptr);
+    if (rc != SPARDL_OK) return;
+    to_host(sel_idx, si, static_cast<size_t>(ns));
+    to_host(sel_val, sv, static_cast<size_t>(ns));
+    if (dis_idx) {
+      to_host(dis_idx, xi, static_cast<size_t>(nd));
+      to_host(dis_val, xv, static_cast<size_t>(nd));
+    }
+    *n_sel = ns;
+    if (n_dis) *n_dis = nd;
+  });
+  return rc != SPARDL_OK ? rc : outer;
+}
+
+EXPORT int spardl_topk_select_slice_hostbuf(const float* g, int64_t lo, int64_t hi,
+                                            int64_t budget, int32_t* sel_idx, float* sel_val,
+                                            int64_t* n_sel) {
+  int rc = SPARDL_OK;
+  const int outer = guarded([&] {
+    require_device();
+    if (hi < lo || lo < 0) sdlh::fail(SPARDL_E_ARG, "bad range");
+    DevBuf buf;
+    float* dg = to_dev(buf, g, static_cast<size_t>(hi));
+    const size_t cap = static_cast<size_t>(hi - lo) + 1;
+    int32_t* si = buf.get<int32_t>(cap);
+    float* sv = buf.get<float>(cap);
+    int64_t ns = 0;
+    rc = spardl_topk_select_slice(dg, lo, hi, budget, si, sv, &ns, nullptr);
+    if (rc != SPARDL_OK) return;
+    to_host(sel_idx, si, static_cast<size_t>(ns));
+    to_host(sel_val, sv, static_cast<size_t>(ns));
+    *n_sel = ns;
+  });
+  return rc != SPARDL_OK ? rc : outer;
+}
+
+EXPORT int spardl_merge_add_hostbuf(int32_t r, const int32_t* const* idx, const float* const* val,
+                                    const int64_t* n, int32_t* out_idx, float* out_val,
+                                    int64_t* n_out) {
+  int rc = SPARDL_OK;
+  const int outer = guarded([&] {
+    require_device();
+    if (r < 1 || r > sdl::kMaxR) sdlh::fail(SPARDL_E_ARG, "merge_add: 1 <= r <= 16 lists");
+    DevBuf buf;
+    std::vector<const int32_t*> di(static_cast<size_t>(r));
+    std::vector<const float*> dv(static_cast<size_t>(r));
+    size_t total = 0;
+    for (int q = 0; q < r; ++q) {
+      di[static_cast<size_t>(q)] = to_dev(buf, idx[q], static_cast<size_t>(n[q]));
+      dv[static_cast<size_t>(q)] = to_dev(buf, val[q], static_cast<size_t>(n[q]));
+      total += static_cast<size_t>(n[q]);
+    }
+    int32_t* oi = buf.get<int32_t>(total + 1);
+    float* ov = buf.get<float>(total + 1);
+    int64_t no = 0;
+    rc = spardl_merge_add(r, di.data(), dv.data(), n, oi, ov, &no, nullptr);
+    if (rc != SPARDL_OK) return;
+    to_host(out_idx, oi, static_cast<size_t>(no));
+    to_host(out_val, ov, static_cast<size_t>(no));
+    *n_out = no;
+  });
+  return rc != SPARDL_OK ? rc : outer;
+}
+
+// ---------------------------------------------------------------------------
 // pipeline context
 struct spardl_ctx {
   std::unique_ptr<sdle::Engine> eng;
@@ -515,6 +610,40 @@ EXPORT int spardl_get_carry(spardl_ctx* ctx, int32_t local_worker, float** carry
     if (local_worker < 0 || local_worker >= ctx->eng->local_workers())
       sdlh::fail(SPARDL_E_ARG, "local worker out of range");
     *carry_dev = ctx->eng->carry(local_worker);
+  });
+}
+
+EXPORT int spardl_carry_to_host(spardl_ctx* ctx, int32_t local_worker, float* host) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(host, "host");
+    if (local_worker < 0 || local_worker >= ctx->eng->local_workers())
+      sdlh::fail(SPARDL_E_ARG, "local worker out of range");
+    ctx->eng->sync();
+    CK(cudaMemcpy(host, ctx->eng->carry(local_worker),
+                  sizeof(float) * static_cast<size_t>(ctx->eng->dimension()),
+                  cudaMemcpyDeviceToHost));
+  });
+}
+
+EXPORT int spardl_carry_from_host(spardl_ctx* ctx, int32_t local_worker, const float* host) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(host, "host");
+    if (local_worker < 0 || local_worker >= ctx->eng->local_workers())
+      sdlh::fail(SPARDL_E_ARG, "local worker out of range");
+    ctx->eng->sync();
+    CK(cudaMemcpy(ctx->eng->carry(local_worker), host,
+                  sizeof(float) * static_cast<size_t>(ctx->eng->dimension()),
+                  cudaMemcpyHostToDevice));
+  });
+}
+
+EXPORT int spardl_set_controller(spardl_ctx* ctx, int32_t local_worker, const spardl_hctrl* c) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(c, "controller");
+    ctx->eng->set_controller(local_worker, *c);
   });
 }
 

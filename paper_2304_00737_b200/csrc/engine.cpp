@@ -990,6 +990,16 @@ void Engine::controller(int local, spardl_hctrl* out) {
   *out = {c.lower, c.upper, c.target, c.h, c.step, c.flag, 0};
 }
 
+void Engine::set_controller(int local, const spardl_hctrl& h) {
+  if (cfg_.sag != SPARDL_SAG_BSAG) sdlh::fail(SPARDL_E_CONFIG, "no controller: sag != bsag");
+  if (local < 0 || local >= wloc_) sdlh::fail(SPARDL_E_ARG, "local worker out of range");
+  sync();
+  const sdl::HCtl c{h.lower, h.upper, h.target, h.h, h.step, h.flag, 0};
+  const int64_t b = sdlh::hctrl_budget(&h);
+  CK(mcpy(ctl_dev_ + local, &c, sizeof(c), cudaMemcpyHostToDevice));
+  CK(mcpy(budget_dev_ + local, &b, sizeof(b), cudaMemcpyHostToDevice));
+}
+
 void Engine::global(int local, const int32_t** idx, const float** val, int64_t* nnz) {
   sync();
   const Slot& gs = global_[static_cast<size_t>(team_of_local_global_[static_cast<size_t>(local)])];

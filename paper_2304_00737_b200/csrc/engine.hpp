@@ -108,6 +108,7 @@ class Engine {
   // [mode, cand_bad, cand_total, cand_count, pre_key, cap] of dividing task i
   void div_diag(int task, int64_t* out);
   void controller(int local, spardl_hctrl* out);
+  void set_controller(int local, const spardl_hctrl& c);
   void global(int local, const int32_t** idx, const float** val, int64_t* nnz);
   float* carry(int local) { return carry_[static_cast<size_t>(local)]; }
   int64_t dimension() const { return cfg_.dimension; }
