@@ -3,18 +3,20 @@ sys.path.insert(0, '.')
 import paper_2304_00737_b200 as sd
 from paper_2304_00737_b200._lib import lib
 P, N, k = 8, 25_600_000, 256_000
-def diag(ctx, tag):
-    out = (C.c_int64 * 6)()
-    rows = []
-    for t in (0, 1, 63):
-        lib().spardl_div_diag(ctx._h, t, out); rows.append(list(out))
-    print(tag, rows, 'fallbacks', ctx.dense_fallbacks())
-ctx = sd.SparDL(sd.ClusterConfig(workers=P, dimension=N, k=k), device=0, graph=True)
+ctx = sd.SparDL(sd.ClusterConfig(workers=P, dimension=N, k=k), device=0, graph=False)
 gen = torch.Generator(device='cuda')
 grads = []
 for i in range(P):
     gen.manual_seed(1000 + i)
     grads.append(torch.randn(N, device='cuda', generator=gen))
-for it in range(60):
+for it in range(5):
     ctx.all_reduce(grads); ctx.sync()
-    if it % 4 == 0: diag(ctx, f'it={it}')
+out = (C.c_int64 * 12)()
+names = ['p1','p0h','p0s','p0f','p1h','p1s','p1f','p2h','p2s','p2f','cnt+scan','write']
+for step in (-1, 0, 1, 2, 3):
+    for task in (0,):
+        rc = lib().spardl_debug_select_timestamps(ctx._h, step, task, out)
+        if rc: print(step, 'rc', rc, lib().spardl_last_error()); continue
+        ts = list(out)
+        d = [(names[i], round((ts[i+1]-ts[i])/1000, 1)) for i in range(11)]
+        print('step', step, 'total us', round((ts[11]-ts[0])/1000,1), d)

@@ -75,8 +75,10 @@ void require_device() {
 // One select over prepared inputs, with its scratch.
 void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf) {
   sdl::sel_prepare(t, t.stride);
-  const int nseg = std::max(1, sdl::sel_scratch_segments(t));
+  if (t.nseg > sdl::kMaxSegPerTask || t.dnseg > sdl::kMaxSegPerTask)
+    sdlh::fail(SPARDL_E_UNSUPPORTED, "selection larger than the device work-item bound");
   t.scr = buf.get<sdl::SelScratch>(1);
+  const int nseg = std::max(1, sdl::sel_scratch_segments(t));
   int32_t* segs = buf.get<int32_t>(5 * static_cast<size_t>(nseg));
   t.seg_gt = segs;
   t.seg_eq = segs + nseg;
@@ -222,8 +224,10 @@ EXPORT int spardl_topk_select(const int32_t* idx, const float* val, int64_t n, i
     t.idx = idx;
     t.val = val;
     t.count = cnt;
-    t.stride = sdl::kTile;
-    t.nseg = static_cast<int32_t>((n + sdl::kTile - 1) / sdl::kTile);
+    int64_t stride = sdl::kTile;
+    while ((n + stride - 1) / stride > sdl::kMaxSegPerTask) stride += sdl::kTile;
+    t.stride = static_cast<int32_t>(stride);
+    t.nseg = static_cast<int32_t>((n + stride - 1) / stride);
     t.budget = budget;
     t.sel_idx = sel_idx;
     t.sel_val = sel_val;
@@ -686,6 +690,14 @@ EXPORT int spardl_div_diag(spardl_ctx* ctx, int32_t task, int64_t* out6) {
   return guarded([&] {
     need(ctx, "ctx");
     ctx->eng->div_diag(task, out6);
+  });
+}
+
+EXPORT int spardl_debug_select_timestamps(spardl_ctx* ctx, int32_t step, int32_t task,
+                                          int64_t* out12) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->select_timestamps(step, task, out12);
   });
 }
 

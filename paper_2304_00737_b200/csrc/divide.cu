@@ -58,24 +58,24 @@ __global__ void __launch_bounds__(kThreads) k_div_sample(const DivTask* __restri
     vals[q] = 0.f;
     if (i < e) vals[q] = apply_residual ? __fadd_rn(__ldcs(g + i), __ldcs(t.carry + i)) : t.carry[i];
   }
+  // 1/32-octave bins spread a warp's keys over many bins: plain shared
+  // atomics; the occupied bin range is tracked in registers
+  unsigned lo_b = kSampBins, hi_b = 0;
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int64_t i = s + (int64_t)q * kThreads + threadIdx.x;
-    const bool in = i < e;
-    const float v = vals[q];
-    // warp-aggregated: sampled keys crowd into a few top-bit bins
-    const uint32_t bin = mag_key(v) >> kSampShift;
-    const uint32_t am = __ballot_sync(0xffffffffu, in);
-    if (in) {
-      const uint32_t peers = __match_any_sync(am, bin);
-      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+    if (i < e) {
+      const uint32_t bin = mag_key(vals[q]) >> kSampShift;
+      atomicAdd(&h[bin], 1u);
+      lo_b = min(lo_b, bin);
+      hi_b = max(hi_b, bin);
     }
-    const unsigned lo_b = __reduce_min_sync(0xffffffffu, in ? bin : (unsigned)kSampBins);
-    const unsigned hi_b = __reduce_max_sync(0xffffffffu, in ? bin : 0u);
-    if ((threadIdx.x & 31) == 0) {
-      atomicMin(&bmin, lo_b);
-      atomicMax(&bmax, hi_b);
-    }
+  }
+  lo_b = __reduce_min_sync(0xffffffffu, lo_b);
+  hi_b = __reduce_max_sync(0xffffffffu, hi_b);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&bmin, lo_b);
+    atomicMax(&bmax, hi_b);
   }
   __syncthreads();
   for (int b = bmin + threadIdx.x; b <= (int)bmax; b += blockDim.x)
@@ -261,15 +261,16 @@ __global__ void __launch_bounds__(1024) k_div_tiles(const DivTask* __restrict__ 
   for (int c0 = 0; c0 < t.nchunks; c0 += blockDim.x) {
     const int c = c0 + threadIdx.x;
     const int cnt = c < t.nchunks ? t.cand_cnt[c] : 0;
-    const int nt = (cnt + kTile - 1) / kTile;
+    const int tl = t.tile_len;
+    const int nt = (cnt + tl - 1) / tl;
     int ttot, ctot;
     const int tbase = tile_carry + block_exscan(nt, scratch, &ttot);
     block_exscan(cnt, scratch, &ctot);
     for (int j = 0; j < nt; ++j) {
       const int q = tbase + j;
       if (q < t.max_tiles) {
-        t.tile_off[q] = c * t.cap + j * kTile;
-        t.tile_cnt[q] = min(kTile, cnt - j * kTile);
+        t.tile_off[q] = c * t.cap + j * tl;
+        t.tile_cnt[q] = min(tl, cnt - j * tl);
       }
     }
     tile_carry += ttot;
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__(1024) k_div_tiles(const DivTask* __restrict__ 
   for (int q = tile_carry + threadIdx.x; q < t.max_tiles; q += blockDim.x) t.tile_cnt[q] = 0;
   if (threadIdx.x == 0) {
     *t.cand_total = cand_carry;
+    *t.ntiles = min(tile_carry, t.max_tiles);
     if (tile_carry > t.max_tiles) *t.cand_bad |= 2;   // work list capacity: dense fallback
   }
 }

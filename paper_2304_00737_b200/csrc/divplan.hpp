@@ -22,8 +22,13 @@ void div_plan(DivTask& dt, SelTask& t, int64_t lo, int64_t hi, int64_t budget, A
   // ~1.4-2.3 L) before the dense fallback takes over
   int cap = static_cast<int>(std::min<double>(kChunk, std::max(1024.0, 8.0 * kChunk * frac)));
   cap = (cap + kTile - 1) / kTile * kTile;
-  const int max_tiles =
-      nch + static_cast<int>((std::min<int64_t>(nb, 4 * budget + 4096) + kTile - 1) / kTile);
+  // work-list tiles: as small as kTile while the list fits the select's
+  // per-task work-item bound
+  const int64_t cand_cap = std::min<int64_t>(nb, 4 * budget + 4096);
+  int tile_len = kTile;
+  while (nch + (cand_cap + tile_len - 1) / tile_len > kMaxSegPerTask) tile_len += kTile;
+  const int max_tiles = nch + static_cast<int>((cand_cap + tile_len - 1) / tile_len);
+  dt.tile_len = tile_len;
   dt.lo = static_cast<int32_t>(lo);
   dt.hi = static_cast<int32_t>(hi);
   dt.nchunks = nch;
@@ -37,6 +42,8 @@ void div_plan(DivTask& dt, SelTask& t, int64_t lo, int64_t hi, int64_t budget, A
   dt.max_tiles = max_tiles;
   dt.tile_off = static_cast<int32_t*>(alloc(sizeof(int32_t) * max_tiles));
   dt.tile_cnt = static_cast<int32_t*>(alloc(sizeof(int32_t) * max_tiles));
+  dt.ntiles = static_cast<int32_t*>(alloc(sizeof(int32_t)));
+  t.nseg_dev = dt.ntiles;
   dt.cand_total = static_cast<int64_t*>(alloc(sizeof(int64_t)));
   dt.cand_bad = static_cast<int32_t*>(alloc(sizeof(int32_t)));
   dt.pre_key = static_cast<uint32_t*>(alloc(sizeof(uint32_t)));
@@ -51,7 +58,7 @@ void div_plan(DivTask& dt, SelTask& t, int64_t lo, int64_t hi, int64_t budget, A
   t.val = dt.cand_val;
   t.seg_off = dt.tile_off;
   t.seg_cnt = dt.tile_cnt;
-  t.stride = kTile;
+  t.stride = tile_len;
   t.nseg = dt.use_cand ? max_tiles : 1;
   t.dbase = static_cast<int32_t>(lo);
   t.dn = static_cast<int32_t>(nb);

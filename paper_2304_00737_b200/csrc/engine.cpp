@@ -210,9 +210,11 @@ void Engine::add_select(Stage& st, const sdl::SelTask& t0) {
   sdl::SelTask t = t0;
   // t.stride carries the longest possible input segment (see callers)
   sdl::sel_prepare(t, t.stride);
-  const int nseg = std::max(1, sdl::sel_scratch_segments(t));
+  if (t.nseg > sdl::kMaxSegPerTask || t.dnseg > sdl::kMaxSegPerTask)
+    sdlh::fail(SPARDL_E_UNSUPPORTED, "selection larger than the device work-item bound");
   t.scr = static_cast<sdl::SelScratch*>(arena_.alloc(sizeof(sdl::SelScratch)));
-  int32_t* segs = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * 5 * std::max(nseg, 1)));
+  const int nseg = std::max(1, sdl::sel_scratch_segments(t));
+  int32_t* segs = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * 5 * nseg));
   t.seg_gt = segs;
   t.seg_eq = segs + nseg;
   t.seg_sel_off = segs + 2 * nseg;
@@ -228,8 +230,10 @@ sdl::SelTask Engine::select_from_slot(const Slot& in) {
   t.idx = in.idx;
   t.val = in.val;
   t.count = in.cnt;
-  t.stride = sdl::kTile;
-  t.nseg = static_cast<int32_t>((in.cap + sdl::kTile - 1) / sdl::kTile);
+  int64_t stride = sdl::kTile;
+  while ((in.cap + stride - 1) / stride > sdl::kMaxSegPerTask) stride += sdl::kTile;
+  t.stride = static_cast<int32_t>(stride);
+  t.nseg = static_cast<int32_t>((in.cap + stride - 1) / stride);
   t.weight = 1.f;
   return t;
 }
@@ -958,6 +962,13 @@ void Engine::div_diag(int task, int64_t* out) {
   out[3] = cnt;
   out[4] = pre;
   out[5] = dt.cap;
+}
+
+void Engine::select_timestamps(int step, int task, int64_t* out12) {
+  sync();
+  const Stage& st = step < 0 ? div_stage_ : steps_.at(static_cast<size_t>(step)).stage;
+  const sdl::SelScratch* sc = st.sels.at(static_cast<size_t>(task)).scr;
+  CK(mcpy(out12, sc->tstamp, sizeof(long long) * 12, cudaMemcpyDeviceToHost));
 }
 
 int64_t Engine::dense_fallbacks() {

@@ -105,6 +105,8 @@ class Engine {
   void union_sizes(int64_t* out);
   // dividing selects of the last iteration that fell back to the dense path
   int64_t dense_fallbacks();
+  // device timestamps (ns) of the phases of one select of the last run
+  void select_timestamps(int step, int task, int64_t* out12);
   // [mode, cand_bad, cand_total, cand_count, pre_key, cap] of dividing task i
   void div_diag(int task, int64_t* out);
   void controller(int local, spardl_hctrl* out);

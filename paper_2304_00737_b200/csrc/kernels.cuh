@@ -26,8 +26,10 @@ constexpr int kThreads = 256;
 constexpr int kBins = 2048;            // radix digit width of passes 0 and 1 (11 bits)
 constexpr int kMaxR = 16;              // max lists folded by one merge task
 constexpr int kChunk = 8192;           // dividing chunk (elements per CTA)
-constexpr int kMaxSamples = 8192;      // merge splitter samples per task
+constexpr int kMaxSamples = 8000;      // merge splitter samples per task (< kMaxSegPerTask)
 constexpr int kTile = 256;             // select work item (entries per warp task)
+constexpr int kCl = 16;                // CTAs per select cluster (one cluster per task)
+constexpr int kMaxSegPerTask = 8192;   // select work items per task (smem bound)
 constexpr int kSampShift = 18;         // dividing sample histogram: key >> 18
 constexpr int kSampBins = 1 << (31 - kSampShift);   // 8192 bins (1/32 octave)
 
@@ -56,6 +58,7 @@ struct SelScratch {
   int32_t mode;          // resolved input mode for this run
   int32_t cut_idx;       // largest selected index among entries with key == T
   int32_t pad_;
+  long long tstamp[12];  // phase timestamps (globaltimer ns) of the last run, CTA 0
 };
 
 // Membership in a finished selection without searching its output:
@@ -78,8 +81,9 @@ struct SelTask {
   int32_t mode;
   int32_t mode_from_cand;
   int32_t stride;
-  int32_t tiles;         // kTile-entry tiles per input segment (set by sel_prepare)
+  int32_t tiles;         // unused (kept for layout stability)
   int32_t pad1_;
+  const int32_t* nseg_dev;  // nullable: segments actually in use (device-decided)
   const int32_t* idx;
   const float* val;
   const int32_t* seg_off;
@@ -158,7 +162,8 @@ struct DivTask {
   int32_t* tile_off;       // [max_tiles] work list for the select (k_div_tiles)
   int32_t* tile_cnt;       // [max_tiles]
   int32_t max_tiles;
-  int32_t pad2_;
+  int32_t tile_len;        // candidates per work-list tile (multiple of kTile)
+  int32_t* ntiles;         // tiles in use (written by k_div_tiles)
   int64_t* cand_total;
   int32_t* cand_bad;       // bit 0: candidate path off for this run, bit 1: overflow
   uint32_t* pre_key;       // candidate threshold (key >= pre_key)

@@ -1,31 +1,41 @@
-// Deterministic top-L selection over segmented sparse lists.
+// Deterministic top-L selection over segmented sparse lists -- one kernel.
 //
 // Semantics: inc/sparse.hpp:136-162 (top_k_select) -- keep the min(budget,
 // nnz) entries that come first in the order (|v| desc, index asc); return
 // the kept and the discarded entries, each in index order.
 //
-// Method (per task, all tasks of a batch in one launch per kernel):
-//   hist<0..2> + find<0..2>: radix select on the 31-bit magnitude key
-//       (digits 11 / 11 / 9 bits).  After the three passes the threshold key
-//       T is exact, cnt_gt = #{key > T} and need_eq = L - cnt_gt entries of
-//       key == T are taken -- the lowest-index ones, which is exactly the
-//       reference's tie rule.  For the dividing select the first histogram is
-//       built by the candidate pass itself (divide.cu), so hist<0> skips it.
-//   count: per segment (one warp each) #{key > T} and #{key == T}
-//   scan:  per segment tie quota and output offsets (segments are in index
-//          order, so offsets preserve index order)
-//   write: ordered compaction (one warp per segment, ballots) of selected and
-//          discarded entries; discards are scaled by the residual share with
-//          an explicitly rounded multiply (no FMA contraction), matching
-//          inc/residual.hpp:119.
+// Method: one thread-block cluster of kCl CTAs per task (Blackwell clusters,
+// distributed shared memory).  Every CTA owns a contiguous range of the
+// task's segments (segments are in index order, so CTA order == index order).
+//   1. counts: CTA totals exchanged through DSMEM -> total, identity case.
+//   2. radix select on the 31-bit magnitude key, digits 11/11/9 bits: each
+//      CTA histograms its entries matching the current prefix in shared
+//      memory, adds the non-zero bins into CTA 0's histogram through DSMEM,
+//      CTA 0 locates the digit holding the rank-th largest key and the other
+//      CTAs read the new prefix from CTA 0 -- two cluster barriers per pass,
+//      no global atomics, no kernel boundaries.  After the three passes the
+//      threshold key T is exact, and need_eq = L - #{key > T} entries of key
+//      T are kept: the lowest-index ones (the reference's tie rule).
+//   3. per segment (one warp each) #{key > T}, #{key == T}; CTA totals go
+//      through DSMEM so every CTA knows the tie quota and the output offsets
+//      of the CTAs before it; a CTA-wide scan places each segment.
+//   4. ordered compaction with warp ballots of the selected entries and of
+//      the discarded ones, the latter scaled by the residual share with an
+//      explicitly rounded multiply (no FMA contraction, inc/residual.hpp:119).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sdl {
 
 namespace {
 
-constexpr int kWarps = kThreads / 32;
+constexpr int kSelThreads = 512;   // 16 warps per CTA
+constexpr int kWarps = kSelThreads / 32;
+constexpr int kIlp = 8;   // 32-entry groups loaded per warp step (memory-level parallelism)
 
 __device__ __forceinline__ int resolve_mode(const SelTask& t) {
   if (!t.mode_from_cand) return t.mode;
@@ -33,44 +43,28 @@ __device__ __forceinline__ int resolve_mode(const SelTask& t) {
   return (*t.cand_bad != 0 || *t.cand_total < need) ? 1 : 0;
 }
 
-// Is the pass-0 histogram already built by the dividing candidate pass?  In
-// candidate mode yes; after a candidate-list overflow (flags == 2) too: every
-// chunk histogrammed its candidates before the overflow was detected, and
-// the L-th largest key lies above the pre-threshold because more than the
-// capacity (> L) of entries passed it.
-__device__ __forceinline__ bool hist0_ready(const SelTask& t, int mode) {
-  if (!t.cand_hist) return false;
-  return mode == 0 || *t.cand_bad == 2;
-}
-
+// segments actually in use (the planner sizes nseg for the worst case)
 __device__ __forceinline__ int nseg_of(const SelTask& t, int mode) {
-  return mode == 1 ? t.dnseg : t.nseg * t.tiles;
+  if (mode == 1) return t.dnseg;
+  if (t.nseg_dev) return min(*t.nseg_dev, t.nseg);
+  if (!t.seg_cnt) return min(t.nseg, (*t.count + t.stride - 1) / t.stride);
+  return t.nseg;
 }
 
-// Segment s of a task.  Explicit inputs are cut further into `tiles` tiles
-// of <= kTile entries per input segment (tile order == index order), so every
-// warp-level work item is small regardless of how the input was segmented.
+// segment s: entries [off, off + cnt) of the task's input
 __device__ __forceinline__ void seg_bounds(const SelTask& t, int mode, int s, int& off,
                                            int& cnt) {
+  int c;
   if (mode == 1) {
     off = s * t.dstride;
-    const int c = t.dn - off;
-    cnt = c < 0 ? 0 : (c > t.dstride ? t.dstride : c);
+    c = t.dn - off;
+    c = c > t.dstride ? t.dstride : c;
   } else {
-    const int tiles = t.tiles;
-    const int si = s / tiles, ti = s - si * tiles;
-    int o, c;
-    o = t.seg_off ? t.seg_off[si] : si * t.stride;
-    if (t.seg_cnt) {
-      c = t.seg_cnt[si];
-    } else {
-      c = *t.count - o;
-      c = c < 0 ? 0 : (c > t.stride ? t.stride : c);
-    }
-    off = o + ti * kTile;
-    c -= ti * kTile;
-    cnt = c < 0 ? 0 : (c > kTile ? kTile : c);
+    off = t.seg_off ? t.seg_off[s] : s * t.stride;
+    c = t.seg_cnt ? t.seg_cnt[s] : *t.count - off;
+    c = c > t.stride ? t.stride : c;
   }
+  cnt = c < 0 ? 0 : c;
 }
 
 __device__ __forceinline__ float seg_val(const SelTask& t, int mode, int p) {
@@ -80,256 +74,340 @@ __device__ __forceinline__ int32_t seg_idx(const SelTask& t, int mode, int p) {
   return mode == 1 ? t.dbase + p : t.idx[p];
 }
 
-template <int PASS>
-struct Digit {
-  static constexpr int shift = PASS == 0 ? 20 : (PASS == 1 ? 9 : 0);
-  static constexpr int nbins = PASS == 2 ? 512 : 2048;
+// shared-memory histogram increment (the keys of a warp spread over many bins,
+// so plain shared atomics beat warp aggregation with match.any)
+__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t bin, bool active) {
+  if (active) atomicAdd(&h[bin], 1u);
+}
+
+struct RadixState {     // lives in CTA 0, read by the cluster through DSMEM
+  uint32_t prefix;
+  uint32_t pmask;
+  int64_t rank;         // rank still to find inside the prefix
+  int64_t total;
+  int64_t budget;
+  int32_t all;          // 1: everything kept, 2: nothing kept, 0: threshold
+  int32_t pad_;
 };
 
-// warp-aggregated shared-memory histogram increment
-__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t bin, bool active) {
-  const uint32_t am = __ballot_sync(0xffffffffu, active);
-  if (!active) return;
-  const uint32_t peers = __match_any_sync(am, bin);
-  const int leader = __ffs(peers) - 1;
-  if ((int)(threadIdx.x & 31) == leader) atomicAdd(&h[bin], (uint32_t)__popc(peers));
-}
+struct CtaTotals {      // per-CTA counters exchanged through DSMEM
+  long long cnt, gt, eq;
+};
 
-// ---------------------------------------------------------------------------
-template <int PASS>
-__global__ void __launch_bounds__(kThreads) k_sel_hist(const SelTask* __restrict__ tasks) {
-  const SelTask& t = tasks[blockIdx.y];
-  SelScratch* sc = t.scr;
-  int mode;
-  uint32_t prefix = 0, pmask = 0;
-  if (PASS == 0) {
-    mode = resolve_mode(t);
-    if (hist0_ready(t, mode)) return;   // built by the candidate pass
-  } else {
-    if (sc->all) return;
-    mode = sc->mode;
-    prefix = sc->prefix;
-    pmask = sc->pmask;
-  }
-  const int nseg = nseg_of(t, mode);
-  const int per = (nseg + gridDim.x - 1) / gridDim.x;
-  const int s0 = blockIdx.x * per;
-  if (s0 >= nseg) return;
-  const int s1 = min(nseg, s0 + per);
-  constexpr int NB = Digit<PASS>::nbins;
-  constexpr int SH = Digit<PASS>::shift;
-  __shared__ uint32_t h[NB];
-  for (int b = threadIdx.x; b < NB; b += blockDim.x) h[b] = 0;
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int s = s0 + warp; s < s1; s += kWarps) {
-    int off, cnt;
-    seg_bounds(t, mode, s, off, cnt);
-    for (int j0 = 0; j0 < cnt; j0 += 32) {
-      const int j = j0 + lane;
-      uint32_t key = 0;
-      if (j < cnt) key = mag_key(seg_val(t, mode, off + j));
-      const bool in = j < cnt && (key & pmask) == prefix;
-      hist_add(h, (key >> SH) & (NB - 1), in);
-    }
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < NB; b += blockDim.x)
-    if (h[b]) atomicAdd(&sc->hist[b], h[b]);
-}
-
-// One CTA per task: locate the digit holding the rank-th largest key.
-template <int PASS>
-__global__ void __launch_bounds__(kThreads) k_sel_find(const SelTask* __restrict__ tasks) {
-  const SelTask& t = tasks[blockIdx.x];
-  SelScratch* sc = t.scr;
-  constexpr int NB = Digit<PASS>::nbins;
-  constexpr int SH = Digit<PASS>::shift;
-  constexpr int BPT = NB / kThreads;
-  __shared__ long long lscr[32];
-  __shared__ long long suf[kThreads];
-  if (PASS > 0 && sc->all) return;
-  int mode = 0;
-  const uint32_t* src = sc->hist;
-  if (PASS == 0) {
-    mode = resolve_mode(t);
-    if (hist0_ready(t, mode)) src = t.cand_hist;
-  }
-  uint32_t c[BPT];
+// CTA 0: locate the digit holding the rank-th largest key in agg[0..nb).
+__device__ void find_digit(uint32_t* agg, int nb, int shift, RadixState* st, long long* suf) {
+  const int bpt = nb / kSelThreads;
   long long mine = 0;
-#pragma unroll
-  for (int q = 0; q < BPT; ++q) {
-    c[q] = src[threadIdx.x * BPT + q];
-    mine += c[q];
-  }
-#pragma unroll
-  for (int q = 0; q < BPT; ++q) {
-    sc->hist[threadIdx.x * BPT + q] = 0;
-    if (PASS == 0 && t.cand_hist) t.cand_hist[threadIdx.x * BPT + q] = 0;
-  }
-  int64_t rank, cnt_gt;
-  uint32_t prefix, pmask;
-  if (PASS == 0) {
-    const long long total = block_sum_ll(mine, lscr);
-    const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
-    if (threadIdx.x == 0) {
-      sc->total = total;
-      sc->budget = budget;
-      sc->mode = mode;
-      sc->cut_idx = -1;
-      if (total <= budget) sc->all = 1;          // identity case, inc/sparse.hpp:143-146
-      else if (budget <= 0) sc->all = 2;         // nothing kept
-      else sc->all = 0;
-      sc->prefix = 0;
-      sc->pmask = 0;
-      sc->rank = budget;
-      sc->cnt_gt = 0;
-    }
-    __syncthreads();
-    if (total <= budget || budget <= 0) return;
-    rank = budget;
-    cnt_gt = 0;
-    prefix = 0;
-    pmask = 0;
-  } else {
-    rank = sc->rank;
-    cnt_gt = sc->cnt_gt;
-    prefix = sc->prefix;
-    pmask = sc->pmask;
-  }
-  __syncthreads();
-  // above(tid) = count in the bins of all threads > tid (bins ascend with tid)
-  const int r = blockDim.x - 1 - threadIdx.x;
+  for (int q = 0; q < bpt; ++q) mine += agg[threadIdx.x * bpt + q];
+  const int r = kSelThreads - 1 - threadIdx.x;     // bins ascend with tid; scan from the top
   suf[r] = mine;
   __syncthreads();
-  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+  for (int o = 1; o < kSelThreads; o <<= 1) {
     const long long add = threadIdx.x >= (unsigned)o ? suf[threadIdx.x - o] : 0;
     __syncthreads();
     suf[threadIdx.x] += add;
     __syncthreads();
   }
   const long long above = r > 0 ? suf[r - 1] : 0;
+  const int64_t rank = st->rank;
+  __syncthreads();
   if (above < rank && rank <= above + mine) {
     long long cum = above;
-    for (int q = BPT - 1; q >= 0; --q) {
-      if (cum + (long long)c[q] >= rank) {
-        const uint32_t digit = threadIdx.x * BPT + q;
-        sc->prefix = prefix | (digit << SH);
-        sc->pmask = pmask | ((uint32_t)(NB - 1) << SH);
-        sc->rank = rank - cum;
-        sc->cnt_gt = cnt_gt + cum;
+    for (int q = bpt - 1; q >= 0; --q) {
+      const uint32_t c = agg[threadIdx.x * bpt + q];
+      if (cum + (long long)c >= rank) {
+        const uint32_t digit = threadIdx.x * bpt + q;
+        st->prefix |= digit << shift;
+        st->pmask |= (uint32_t)(nb - 1) << shift;
+        st->rank = rank - cum;
         break;
       }
-      cum += c[q];
+      cum += c;
     }
   }
+  __syncthreads();
+  for (int q = 0; q < bpt; ++q) agg[threadIdx.x * bpt + q] = 0;   // ready for the next pass
 }
 
-// Per segment (one warp): #{key > T}, #{key == T}
-__global__ void __launch_bounds__(kThreads) k_sel_count(const SelTask* __restrict__ tasks) {
-  const SelTask& t = tasks[blockIdx.y];
-  const SelScratch* sc = t.scr;
-  const int mode = sc->mode;
+template <int CL>
+__global__ void __launch_bounds__(kSelThreads)
+    k_select(const SelTask* __restrict__ tasks) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = (int)cluster.block_rank();
+  const SelTask t = tasks[blockIdx.y];   // by value: fields live in registers, not re-read
+  SelScratch* sc = t.scr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  __shared__ uint32_t hist[kBins];
+  __shared__ uint32_t agg[kBins];                   // meaningful in CTA 0
+  __shared__ RadixState st;                         // meaningful in CTA 0
+  __shared__ CtaTotals tot[CL];                     // meaningful in CTA 0
+  __shared__ long long suf[kSelThreads];
+  __shared__ int scratch[40];
+  __shared__ long long lscr[32];
+  __shared__ RadixState my;                         // this CTA's copy of CTA 0's state
+
+  RadixState* st0 = cluster.map_shared_rank(&st, 0);
+  uint32_t* agg0 = cluster.map_shared_rank(agg, 0);
+  CtaTotals* tot0 = cluster.map_shared_rank(tot, 0);
+
+  const int mode = resolve_mode(t);
   const int nseg = nseg_of(t, mode);
-  const int all = sc->all;
-  const uint32_t T = sc->prefix;
-  const int lane = threadIdx.x & 31;
-  for (int s = blockIdx.x * kWarps + (threadIdx.x >> 5); s < nseg; s += gridDim.x * kWarps) {
-    int off, cnt;
-    seg_bounds(t, mode, s, off, cnt);
+
+  auto stamp = [&](int i) {
+    if (cr == 0 && threadIdx.x == 0) {
+      long long ts;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+      sc->tstamp[i] = ts;
+    }
+  };
+  stamp(0);
+  // ---- 1. totals and an entry-balanced split of the segments over the
+  // cluster: every CTA scans all segment lengths (cheap: <= 8192 counts) and
+  // owns the segments whose first entry falls in its 1/kCl of the entries.
+  __shared__ int s_lo, s_hi;
+  long long total = 0;
+  {
+    if (threadIdx.x == 0) {
+      s_lo = 0;
+      s_hi = 0;
+    }
+    // pass A: the total
+    long long part = 0;
+    for (int s = threadIdx.x; s < nseg; s += kSelThreads) {
+      int off, c;
+      seg_bounds(t, mode, s, off, c);
+      part += c;
+    }
+    total = block_sum_ll(part, lscr);
+    const long long lo_t = total * cr / CL, hi_t = total * (cr + 1) / CL;
+    // pass B: s0 = #{s : start(s) < lo_t}, s1 = #{s : start(s) < hi_t}
+    int carry = 0, n_lo = 0, n_hi = 0;
+    for (int b0 = 0; b0 < nseg; b0 += kSelThreads) {
+      const int s = b0 + threadIdx.x;
+      int c = 0;
+      if (s < nseg) {
+        int off;
+        seg_bounds(t, mode, s, off, c);
+      }
+      int tt;
+      const long long start = carry + block_exscan(c, scratch, &tt);
+      n_lo += __syncthreads_count(s < nseg && start < lo_t);
+      n_hi += __syncthreads_count(s < nseg && start < hi_t);
+      carry += tt;
+    }
+    if (threadIdx.x == 0) {
+      s_lo = cr == 0 ? 0 : n_lo;
+      s_hi = cr == CL - 1 ? nseg : n_hi;
+    }
+  }
+  for (int b = threadIdx.x; b < kBins; b += kSelThreads) agg[b] = 0;
+  const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
+  if (cr == 0 && threadIdx.x == 0) {
+    st.total = total;
+    st.budget = budget;
+    st.prefix = 0;
+    st.pmask = 0;
+    st.rank = budget;
+    st.all = total <= budget ? 1 : (budget <= 0 ? 2 : 0);   // identity case, sparse.hpp:143-146
+    sc->cut_idx = -1;
+  }
+  if (threadIdx.x == 0) {
+    my.total = total;
+    my.budget = budget;
+    my.prefix = 0;
+    my.pmask = 0;
+    my.rank = budget;
+    my.all = total <= budget ? 1 : (budget <= 0 ? 2 : 0);
+  }
+  cluster.sync();   // CTA 0's aggregation histogram is zeroed
+  stamp(1);
+  const int s0 = s_lo, s1 = s_hi;
+  const int nloc = s1 - s0;
+  // per-segment counters of this CTA's range (task scratch, L2 resident)
+  int* s_gt = t.seg_gt + s0;
+  int* s_eq = t.seg_eq + s0;
+  int* s_take = t.seg_take + s0;
+  int* s_sel = t.seg_sel_off + s0;
+  int* s_dis = t.seg_dis_off + s0;
+
+  // ---- 2. radix passes
+  if (my.all == 0) {
+#pragma unroll 1
+    for (int pass = 0; pass < 3; ++pass) {
+      const int shift = pass == 0 ? 20 : (pass == 1 ? 9 : 0);
+      const int nb = pass == 2 ? 512 : kBins;
+      for (int b = threadIdx.x; b < nb; b += kSelThreads) hist[b] = 0;
+      __syncthreads();
+      const uint32_t prefix = my.prefix, pmask = my.pmask;
+      for (int s = s0 + warp; s < s1; s += kWarps) {
+        int off, c;
+        seg_bounds(t, mode, s, off, c);
+        const float* __restrict__ vp = (mode == 1 ? t.dval : t.val) + off;
+        for (int j0 = 0; j0 < c; j0 += 32 * kIlp) {
+          uint32_t key[kIlp];
+#pragma unroll
+          for (int u = 0; u < kIlp; ++u) {   // all loads in flight first
+            const int j = j0 + u * 32 + lane;
+            key[u] = j < c ? mag_key(__ldg(vp + j)) : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < kIlp; ++u) {
+            const int j = j0 + u * 32 + lane;
+            hist_add(hist, (key[u] >> shift) & (nb - 1), j < c && (key[u] & pmask) == prefix);
+          }
+        }
+      }
+      __syncthreads();
+      stamp(2 + 3 * pass);
+      // distributed reduction: CTA r sums its 1/CL slice of the bins over
+      // all CTAs' histograms (DSMEM loads) and stores it into CTA 0's copy
+      cluster.sync();
+      {
+        const int per = nb / CL;
+        for (int b = cr * per + threadIdx.x; b < (cr + 1) * per; b += kSelThreads) {
+          uint32_t sum = 0;
+#pragma unroll
+          for (int q = 0; q < CL; ++q) sum += cluster.map_shared_rank(hist, q)[b];
+          agg0[b] = sum;
+        }
+      }
+      cluster.sync();
+      stamp(3 + 3 * pass);
+      if (cr == 0) find_digit(agg, nb, shift, &st, suf);
+      cluster.sync();
+      if (threadIdx.x == 0) my = *st0;
+      __syncthreads();
+      stamp(4 + 3 * pass);
+    }
+  }
+  const int all = my.all;
+  const uint32_t T = my.prefix;
+  const int64_t need_eq = all == 0 ? my.rank : 0;
+
+  // ---- 3. per-segment counts, offsets
+  long long g_loc = 0, e_loc = 0, c_loc = 0;
+  for (int ls = warp; ls < nloc; ls += kWarps) {
+    int off, c;
+    seg_bounds(t, mode, s0 + ls, off, c);
     int gt = 0, eq = 0;
     if (all == 1) {
-      gt = cnt;
+      gt = c;
     } else if (all == 0) {
-      for (int j = lane; j < cnt; j += 32) {
-        const uint32_t key = mag_key(seg_val(t, mode, off + j));
-        gt += key > T;
-        eq += key == T;
+      const float* __restrict__ vp = (mode == 1 ? t.dval : t.val) + off;
+      for (int j0 = 0; j0 < c; j0 += 32 * kIlp) {
+        uint32_t key[kIlp];
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+          const int j = j0 + u * 32 + lane;
+          key[u] = j < c ? mag_key(__ldg(vp + j)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+          const bool in = j0 + u * 32 + lane < c;
+          gt += in && key[u] > T;
+          eq += in && key[u] == T;
+        }
       }
       gt = __reduce_add_sync(0xffffffffu, gt);
       eq = __reduce_add_sync(0xffffffffu, eq);
     }
     if (lane == 0) {
-      t.seg_gt[s] = gt;
-      t.seg_eq[s] = eq;
+      s_gt[ls] = gt;
+      s_eq[ls] = eq;
+      s_sel[ls] = c;   // segment length, temporarily
+      g_loc += gt;
+      e_loc += eq;
+      c_loc += c;
     }
   }
-}
-
-// One CTA per task: tie quotas and output offsets per segment.
-__global__ void __launch_bounds__(1024) k_sel_scan(const SelTask* __restrict__ tasks) {
-  const SelTask& t = tasks[blockIdx.x];
-  SelScratch* sc = t.scr;
-  const int mode = sc->mode;
-  const int nseg = nseg_of(t, mode);
-  const int all = sc->all;
-  const int64_t need_eq = all == 0 ? sc->rank : 0;
-  __shared__ int scratch[40];
-  int eq_carry = 0, sel_carry = 0, cnt_carry = 0;
-  for (int s0 = 0; s0 < nseg; s0 += blockDim.x) {
-    const int s = s0 + threadIdx.x;
-    int gt = 0, eq = 0, cnt = 0;
-    if (s < nseg) {
-      int off;
-      seg_bounds(t, mode, s, off, cnt);
-      gt = t.seg_gt[s];
-      eq = t.seg_eq[s];
-    }
-    int teq, tsel, tcnt;
-    const int eq_before = eq_carry + block_exscan(eq, scratch, &teq);
-    long long q = need_eq - eq_before;
-    const int take = q <= 0 ? 0 : (q >= eq ? eq : (int)q);
-    const int sel = gt + take;
-    const int sel_off = sel_carry + block_exscan(sel, scratch, &tsel);
-    const int cnt_off = cnt_carry + block_exscan(cnt, scratch, &tcnt);
-    if (s < nseg) {
-      t.seg_take[s] = take;
-      t.seg_sel_off[s] = sel_off;
-      t.seg_dis_off[s] = cnt_off - sel_off;
-    }
-    eq_carry += teq;
-    sel_carry += tsel;
-    cnt_carry += tcnt;
-  }
+  g_loc = block_sum_ll(g_loc, lscr);
+  e_loc = block_sum_ll(e_loc, lscr);
+  c_loc = block_sum_ll(c_loc, lscr);
+  if (threadIdx.x == 0) tot0[cr] = {c_loc, g_loc, e_loc};
+  cluster.sync();
+  __shared__ long long base_eq, base_sel, base_cnt, all_sel, all_cnt;
   if (threadIdx.x == 0) {
-    *t.sel_cnt = sel_carry;
-    if (t.dis_cnt) *t.dis_cnt = cnt_carry - sel_carry;
-    if (t.total_out) *t.total_out = sc->total;
+    long long be = 0, bs = 0, bc = 0, ts = 0, tc = 0;
+    for (int q = 0; q < CL; ++q) {
+      const CtaTotals x = tot0[q];
+      long long take = need_eq - be;
+      take = take < 0 ? 0 : (take > x.eq ? x.eq : take);
+      if (q == cr) {
+        base_eq = be;
+        base_sel = bs;
+        base_cnt = bc;
+      }
+      be += x.eq;
+      bs += x.gt + take;
+      bc += x.cnt;
+      ts += x.gt + take;
+      tc += x.cnt;
+    }
+    all_sel = ts;
+    all_cnt = tc;
   }
-}
+  cluster.sync();   // every CTA has read CTA 0's totals
+  __syncthreads();
+  {
+    int eq_carry = (int)base_eq, sel_carry = (int)base_sel, cnt_carry = (int)base_cnt;
+    for (int l0 = 0; l0 < nloc; l0 += kSelThreads) {
+      const int ls = l0 + threadIdx.x;
+      int gt = 0, eq = 0, c = 0;
+      if (ls < nloc) {
+        gt = s_gt[ls];
+        eq = s_eq[ls];
+        c = s_sel[ls];
+      }
+      int teq, tsel, tcnt;
+      const int eq_before = eq_carry + block_exscan(eq, scratch, &teq);
+      const long long q = need_eq - eq_before;
+      const int take = q <= 0 ? 0 : (q >= eq ? eq : (int)q);
+      const int sel = gt + take;
+      const int sel_off = sel_carry + block_exscan(sel, scratch, &tsel);
+      const int cnt_off = cnt_carry + block_exscan(c, scratch, &tcnt);
+      if (ls < nloc) {
+        s_take[ls] = take;
+        s_sel[ls] = sel_off;
+        s_dis[ls] = cnt_off - sel_off;
+      }
+      eq_carry += teq;
+      sel_carry += tsel;
+      cnt_carry += tcnt;
+    }
+  }
+  __syncthreads();
 
-// Ordered compaction, one warp per segment.
-__global__ void __launch_bounds__(kThreads) k_sel_write(const SelTask* __restrict__ tasks) {
-  const SelTask& t = tasks[blockIdx.y];
-  SelScratch* sc = t.scr;
-  const int mode = sc->mode;
-  const int nseg = nseg_of(t, mode);
-  const int all = sc->all;
-  const uint32_t T = sc->prefix;
+  stamp(10);
+  // ---- 4. ordered compaction
   const float w = t.weight;
   const bool want_dis = t.dis_idx != nullptr;
-  const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   int cut = -1;
-  for (int s = blockIdx.x * kWarps + (threadIdx.x >> 5); s < nseg; s += gridDim.x * kWarps) {
-    int off, cnt;
-    seg_bounds(t, mode, s, off, cnt);
-    if (cnt == 0) continue;
-    const int sel_base = t.seg_sel_off[s];
-    const int dis_base = t.seg_dis_off[s];
-    const int take = t.seg_take[s];
+  for (int ls = warp; ls < nloc; ls += kWarps) {
+    int off, c;
+    seg_bounds(t, mode, s0 + ls, off, c);
+    const int sel_base = s_sel[ls], dis_base = s_dis[ls], take = s_take[ls];
     int eq_seen = 0, sel_seen = 0;
-    for (int j0 = 0; j0 < cnt; j0 += 32) {
-      const int j = j0 + lane;
-      const bool valid = j < cnt;
-      float v = 0.f;
-      int32_t ix = 0;
-      uint32_t key = 0;
-      if (valid) {
-        v = seg_val(t, mode, off + j);
-        ix = seg_idx(t, mode, off + j);
-        key = mag_key(v);
+    const float* __restrict__ vp = (mode == 1 ? t.dval : t.val) + off;
+    const int32_t* __restrict__ ip = mode == 1 ? nullptr : t.idx + off;
+    const int32_t ibase = t.dbase + off;
+    for (int j00 = 0; j00 < c; j00 += 32 * kIlp) {
+      float vv[kIlp];
+      int32_t iv[kIlp];
+#pragma unroll
+      for (int u = 0; u < kIlp; ++u) {   // all loads in flight first
+        const int j = j00 + u * 32 + lane;
+        vv[u] = j < c ? __ldg(vp + j) : 0.f;
+        iv[u] = j < c ? (ip ? __ldg(ip + j) : ibase + j) : 0;
       }
+#pragma unroll
+    for (int u = 0; u < kIlp; ++u) {
+      const int j = j00 + u * 32 + lane;
+      const bool valid = j < c;
+      const float v = vv[u];
+      const int32_t ix = iv[u];
+      const uint32_t key = mag_key(v);
       bool is_sel;
       if (all == 1) {
         is_sel = valid;
@@ -355,54 +433,80 @@ __global__ void __launch_bounds__(kThreads) k_sel_write(const SelTask* __restric
         t.dis_val[p] = __fmul_rn(v, w);
       }
     }
+    }
   }
   if (all == 0) {
     cut = __reduce_max_sync(0xffffffffu, cut);
     if (lane == 0 && cut >= 0) atomicMax(&sc->cut_idx, cut);
   }
+  if (cr == 0 && threadIdx.x == 0) {
+    *t.sel_cnt = (int32_t)all_sel;
+    if (t.dis_cnt) *t.dis_cnt = (int32_t)(all_cnt - all_sel);
+    if (t.total_out) *t.total_out = my.total;
+    // the finished selection, for membership tests (sel_member)
+    sc->prefix = T;
+    sc->all = all;
+    sc->mode = mode;
+    sc->total = my.total;
+  }
+  stamp(11);
+  cluster.sync();   // keep CTA 0's shared memory alive until every reader is done
 }
-
-inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 }  // namespace
 
 int sel_prepare(SelTask& t, int max_seg_len) {
-  t.tiles = max_seg_len <= kTile ? 1 : (max_seg_len + kTile - 1) / kTile;
+  (void)max_seg_len;
   if (t.dn > 0) {
-    t.dstride = kTile;
-    t.dnseg = (t.dn + kTile - 1) / kTile;
+    // dense slices: tiles of >= 256 entries, at most kMaxSegPerTask of them
+    int stride = kTile;
+    while ((int64_t)(t.dn + stride - 1) / stride > kMaxSegPerTask) stride += kTile;
+    t.dstride = stride;
+    t.dnseg = (t.dn + stride - 1) / stride;
   }
-  return t.nseg * t.tiles;
+  return t.nseg;
 }
 
-int sel_scratch_segments(const SelTask& t) {
-  const int ne = t.nseg * t.tiles;
-  return ne > t.dnseg ? ne : t.dnseg;
-}
+int sel_scratch_segments(const SelTask& t) { return t.nseg > t.dnseg ? t.nseg : t.dnseg; }
 
 int sel_grid_segments(const SelTask& t) {
-  // grids are sized for the expected (explicit / candidate) input; the dense
-  // fallback of the dividing select grid-strides over its larger range
   if (t.mode == 1 && !t.mode_from_cand) return t.dnseg;
-  return t.nseg * t.tiles;
+  return t.nseg;
 }
 
+namespace {
+template <int CL>
+void launch_cl(const SelTask* tasks_dev, int ntask, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {   // 16 is a non-portable cluster size on sm_100
+    cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    configured = true;
+  }
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(CL, ntask);
+  lc.blockDim = dim3(kSelThreads);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  cudaLaunchKernelEx(&lc, k_select<CL>, tasks_dev);
+}
+}  // namespace
+
 int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s) {
+  (void)max_nseg;
   if (ntask <= 0) return 0;
-  // histogram CTAs cover ~16 segments each; count/write use a warp per segment
-  const int hx = clampi((max_nseg + 15) / 16, 1, 1184);
-  const int wx = clampi((max_nseg + kWarps - 1) / kWarps, 1, 4096);
-  dim3 gh(hx, ntask), gw(wx, ntask);
-  k_sel_hist<0><<<gh, kThreads, 0, s>>>(tasks_dev);
-  k_sel_find<0><<<ntask, kThreads, 0, s>>>(tasks_dev);
-  k_sel_hist<1><<<gh, kThreads, 0, s>>>(tasks_dev);
-  k_sel_find<1><<<ntask, kThreads, 0, s>>>(tasks_dev);
-  k_sel_hist<2><<<gh, kThreads, 0, s>>>(tasks_dev);
-  k_sel_find<2><<<ntask, kThreads, 0, s>>>(tasks_dev);
-  k_sel_count<<<gw, kThreads, 0, s>>>(tasks_dev);
-  k_sel_scan<<<ntask, 1024, 0, s>>>(tasks_dev);
-  k_sel_write<<<gw, kThreads, 0, s>>>(tasks_dev);
-  return 9;
+  // about one 512-thread CTA per SM in total: few tasks get wide clusters
+  if (ntask > 96) launch_cl<2>(tasks_dev, ntask, s);
+  else if (ntask > 48) launch_cl<4>(tasks_dev, ntask, s);
+  else if (ntask > 24) launch_cl<8>(tasks_dev, ntask, s);
+  else launch_cl<16>(tasks_dev, ntask, s);
+  return 1;
 }
 
 }  // namespace sdl
