@@ -20,3 +20,16 @@ for step in (-1, 0, 1, 2, 3):
         ts = list(out)
         d = [(names[i], round((ts[i+1]-ts[i])/1000, 1)) for i in range(11)]
         print('step', step, 'total us', round((ts[11]-ts[0])/1000,1), d)
+# per-task spread of the dividing select and the SRS selects (CTA 0 of each cluster)
+for step, ntask in ((-1, 64), (0, 16), (1, 8), (2, 8)):
+    rows = []
+    for task in range(ntask):
+        rc = lib().spardl_debug_select_timestamps(ctx._h, step, task, out)
+        if rc: break
+        rows.append((out[0], out[11]))
+    if not rows: continue
+    t0 = min(r[0] for r in rows)
+    s = sorted(((a - t0) / 1000, (b - t0) / 1000) for a, b in rows)
+    print('step', step, 'n', len(rows), 'span us', round(max(b for a, b in s), 1),
+          'starts', [round(a, 1) for a, b in s][::max(1, len(s) // 8)],
+          'durs', [round(b - a, 1) for a, b in s][::max(1, len(s) // 8)])

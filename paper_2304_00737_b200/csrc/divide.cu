@@ -22,6 +22,10 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#ifndef SPARDL_DIV_MINB
+#define SPARDL_DIV_MINB 2
+#endif
+
 namespace sdl {
 
 namespace {
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
 }
 
 template <int APPLY>
-__global__ void __launch_bounds__(kThreads) k_div_cand(const DivTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const DivTask* __restrict__ tasks) {
   const DivTask& t = tasks[blockIdx.y];
   const int c = blockIdx.x;
   if (c >= t.nchunks) return;
@@ -150,20 +154,33 @@ __global__ void __launch_bounds__(kThreads) k_div_cand(const DivTask* __restrict
   uint32_t mask = 0;
   bool nan = false;
   const int64_t lo = t.lo, hi = t.hi;
-  const float* g = APPLY ? t.g_tab[t.g_id] : nullptr;
+  // gradient and carry never alias; telling the compiler so lets every load
+  // of the chunk issue before the first store (one memory latency per CTA
+  // instead of one per float4 group)
+  const float* __restrict__ g = APPLY ? t.g_tab[t.g_id] : nullptr;
+  float* __restrict__ carry = t.carry;
+  float4 gv[ITER], cv4[ITER];
 #pragma unroll
   for (int it = 0; it < ITER; ++it) {
     const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
     if (i0 >= lo && i0 + 4 <= hi) {
-      const float4 gg = APPLY ? __ldcs(reinterpret_cast<const float4*>(g + i0)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 cc = __ldcs(reinterpret_cast<const float4*>(t.carry + i0));
+      if (APPLY) gv[it] = __ldcs(reinterpret_cast<const float4*>(g + i0));
+      cv4[it] = __ldcs(reinterpret_cast<const float4*>(carry + i0));
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
+    if (i0 >= lo && i0 + 4 <= hi) {
+      const float4 cc = cv4[it];
       float4 o;
       if (APPLY) {
+        const float4 gg = gv[it];
         o.x = __fadd_rn(gg.x, cc.x);
         o.y = __fadd_rn(gg.y, cc.y);
         o.z = __fadd_rn(gg.z, cc.z);
         o.w = __fadd_rn(gg.w, cc.w);
-        __stcs(reinterpret_cast<float4*>(t.carry + i0), o);
+        __stcs(reinterpret_cast<float4*>(carry + i0), o);
       } else {
         o = cc;
       }
@@ -180,10 +197,10 @@ __global__ void __launch_bounds__(kThreads) k_div_cand(const DivTask* __restrict
         const int64_t i = i0 + e;
         v[it][e] = 0.f;
         if (i >= lo && i < hi) {
-          float x = t.carry[i];
+          float x = carry[i];
           if (APPLY) {
             x = __fadd_rn(g[i], x);
-            t.carry[i] = x;
+            carry[i] = x;
           }
           v[it][e] = x;
           const uint32_t k = mag_key(x);
@@ -196,19 +213,22 @@ __global__ void __launch_bounds__(kThreads) k_div_cand(const DivTask* __restrict
   if (nan) *t.err = 1;
   if (!cand) return;
   // order: (warp, it, lane, e) == index order inside the chunk
+  // per group: a lane's offset = candidates of the lower lanes, from four
+  // ballots (one per float4 component)
   int lane_excl[ITER];
   int warp_total = 0;
+  const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int it = 0; it < ITER; ++it) {
-    const int cnt = __popc((mask >> (it * 4)) & 0xfu);
-    int inc = cnt;
+    int below = 0, all = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int n = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += n;
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t b = __ballot_sync(0xffffffffu, (mask >> (it * 4 + e)) & 1u);
+      below += __popc(b & lt);
+      all += __popc(b);
     }
-    lane_excl[it] = warp_total + inc - cnt;
-    warp_total += __shfl_sync(0xffffffffu, inc, 31);
+    lane_excl[it] = warp_total + below;
+    warp_total += all;
   }
   __shared__ int wtot[kThreads / 32 + 1];
   if (lane == 0) wtot[warp] = warp_total;

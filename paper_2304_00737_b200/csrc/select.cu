@@ -24,6 +24,9 @@
 //      explicitly rounded multiply (no FMA contraction, inc/residual.hpp:119).
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -130,7 +133,10 @@ __device__ void find_digit(uint32_t* agg, int nb, int shift, RadixState* st, lon
 }
 
 template <int CL>
-__global__ void __launch_bounds__(kSelThreads)
+#ifndef SPARDL_SEL_MINB
+#define SPARDL_SEL_MINB 1
+#endif
+__global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     k_select(const SelTask* __restrict__ tasks) {
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank();
@@ -476,36 +482,81 @@ int sel_grid_segments(const SelTask& t) {
 
 namespace {
 template <int CL>
-void launch_cl(const SelTask* tasks_dev, int ntask, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {   // 16 is a non-portable cluster size on sm_100
-    cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    configured = true;
-  }
+cudaLaunchConfig_t cl_config(int ntask, cudaStream_t s, cudaLaunchAttribute* attr) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(CL, ntask);
   lc.blockDim = dim3(kSelThreads);
   lc.dynamicSmemBytes = 0;
   lc.stream = s;
-  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
+  return lc;
+}
+
+// clusters of width CL that can be resident at once on this device (a
+// cluster must fit in one GPC, so wide clusters leave SMs unused)
+template <int CL>
+int max_clusters() {
+  static int n = -1;
+  if (n < 0) {   // 16 is a non-portable cluster size on sm_100
+    cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t lc = cl_config<CL>(1, nullptr, attr);
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, k_select<CL>, &lc) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    n = c;
+    if (getenv("SPARDL_DEBUG")) fprintf(stderr, "k_select<%d>: %d resident clusters\n", CL, n);
+  }
+  return n;
+}
+
+template <int CL>
+void launch_cl(const SelTask* tasks_dev, int ntask, cudaStream_t s) {
+  max_clusters<CL>();
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t lc = cl_config<CL>(ntask, s, attr);
   cudaLaunchKernelEx(&lc, k_select<CL>, tasks_dev);
+}
+
+int forced_cl() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("SPARDL_SELECT_CLUSTER");   // tuning experiments only
+    f = e ? atoi(e) : 0;
+  }
+  return f;
 }
 }  // namespace
 
 int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s) {
   (void)max_nseg;
   if (ntask <= 0) return 0;
-  // about one 512-thread CTA per SM in total: few tasks get wide clusters
-  if (ntask > 96) launch_cl<2>(tasks_dev, ntask, s);
-  else if (ntask > 48) launch_cl<4>(tasks_dev, ntask, s);
-  else if (ntask > 24) launch_cl<8>(tasks_dev, ntask, s);
-  else launch_cl<16>(tasks_dev, ntask, s);
+  // the widest cluster for which every task's cluster is resident in one
+  // wave (a second wave would double the latency of the whole batch)
+  int cl = forced_cl();
+  if (cl == 0) {
+    if (max_clusters<16>() >= ntask) cl = 16;
+    else if (max_clusters<8>() >= ntask) cl = 8;
+    else if (max_clusters<4>() >= ntask) cl = 4;
+    else cl = 2;
+  }
+  static int dbg = 0;
+  if (dbg < 8 && getenv("SPARDL_DEBUG")) {
+    ++dbg;
+    fprintf(stderr, "select batch: %d tasks -> cluster %d\n", ntask, cl);
+  }
+  if (cl >= 16) launch_cl<16>(tasks_dev, ntask, s);
+  else if (cl >= 8) launch_cl<8>(tasks_dev, ntask, s);
+  else if (cl >= 4) launch_cl<4>(tasks_dev, ntask, s);
+  else launch_cl<2>(tasks_dev, ntask, s);
   return 1;
 }
 
