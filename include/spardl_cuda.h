@@ -179,6 +179,10 @@ int spardl_plan_ops(const spardl_config* cfg, int32_t world_size, int32_t rank, 
                     int64_t cap, int64_t* n_ops);
 /* first global worker id and count of the workers hosted by this context */
 int spardl_ctx_local_workers(const spardl_ctx* ctx, int32_t* first, int32_t* count);
+/* *peer = 1 when blocks move by direct peer-memory reads over NVLink (CUDA
+ * IPC mappings; all ranks on one node), 0 when by NCCL send/recv.  The
+ * environment variable SPARDL_TRANSPORT=nccl forces NCCL at creation. */
+int spardl_ctx_transport(const spardl_ctx* ctx, int32_t* peer);
 /* enable (1) / disable (0) CUDA-graph replay of the whole iteration */
 int spardl_ctx_set_graph(spardl_ctx* ctx, int32_t enable);
 /* enable the sparse conservation audit (inc/pipeline.hpp:305-334) */

@@ -256,6 +256,10 @@ class SparDL:
         check(lib().spardl_ctx_local_workers(self._h, C.byref(f), C.byref(n)))
         self.first_worker, self.local_workers = f.value, n.value
         self.device = device
+        pv = C.c_int32(0)
+        check(lib().spardl_ctx_transport(self._h, C.byref(pv)))
+        #: "peer" (direct NVLink reads of the producer's buffers), "nccl" or "local"
+        self.transport = "peer" if pv.value else ("nccl" if self.local_workers < cfg.workers else "local")
         if not graph:
             check(lib().spardl_ctx_set_graph(self._h, 0))
 

@@ -513,6 +513,14 @@ EXPORT int spardl_ctx_local_workers(const spardl_ctx* ctx, int32_t* first, int32
   });
 }
 
+EXPORT int spardl_ctx_transport(const spardl_ctx* ctx, int32_t* peer) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(peer, "peer");
+    *peer = ctx->eng->peer_transport() ? 1 : 0;
+  });
+}
+
 EXPORT int spardl_ctx_set_graph(spardl_ctx* ctx, int32_t enable) {
   return guarded([&] {
     need(ctx, "ctx");

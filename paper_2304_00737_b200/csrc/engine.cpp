@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 
@@ -147,12 +148,19 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
       arena_.alloc(sizeof(int64_t) * (static_cast<size_t>(P_ + wloc_) + static_cast<size_t>(d_) * (world_ + 1))));
   rounds_.assign(static_cast<size_t>(P_), 0);
   phase_rounds_.assign(static_cast<size_t>(P_), {0, 0, 0});
+  epoch_ = static_cast<long long*>(arena_.alloc(sizeof(long long)));
+  peer_err_ = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+  setup_peer();
   plan();
+  plan_peer();
   reset_state();
 }
 
 Engine::~Engine() {
   if (graph_) cudaGraphExecDestroy(graph_);
+  for (size_t q = 0; q < peer_base_.size(); ++q)
+    if (peer_base_[q] && peer_base_[q] != sym_) cudaIpcCloseMemHandle(peer_base_[q]);
+  if (sym_) cudaFree(sym_);
   if (comm_) ncclCommDestroy(comm_);
   for (float* c : carry_) cudaFree(c);
   if (gtab_host_) cudaFreeHost(gtab_host_);
@@ -186,6 +194,8 @@ void Engine::drop_graph() {
 // planning helpers
 int Engine::new_uid(int owner) {
   uid_owner_.push_back(owner);
+  if (rank_slots_.size() != static_cast<size_t>(world_)) rank_slots_.assign(static_cast<size_t>(world_), 0);
+  uid_slot_.push_back(rank_slots_[static_cast<size_t>(rank_of(owner))]++);
   return next_uid_++;
 }
 
@@ -195,7 +205,24 @@ Slot& Engine::local_slot(int uid) {
   return it->second;
 }
 
-Slot Engine::make_slot() {
+Slot Engine::sym_slot(int uid) const {
+  const int r = uid_owner_[static_cast<size_t>(uid)] / wloc_;
+  Slot s;
+  s.cap = Lcap_;
+  s.bytes = 16 + 8 * static_cast<size_t>(Lcap_);
+  s.base = peer_base_[static_cast<size_t>(r)] + slot_stride_ * static_cast<size_t>(uid_slot_[static_cast<size_t>(uid)]);
+  s.cnt = reinterpret_cast<int32_t*>(s.base);
+  s.idx = reinterpret_cast<int32_t*>(s.base + 16);
+  s.val = reinterpret_cast<float*>(s.base + 16 + 4 * static_cast<size_t>(Lcap_));
+  return s;
+}
+
+// A block buffer.  Peer transport: the buffer lives at a fixed place of its
+// owner's symmetric region (the same numbering on every rank), so a consumer
+// on another GPU addresses it directly; otherwise a private buffer that a
+// transport round fills.
+Slot Engine::make_slot(int uid) {
+  if (peer_) return sym_slot(uid);
   Slot s;
   s.cap = Lcap_;
   s.bytes = 16 + 8 * static_cast<size_t>(Lcap_);
@@ -297,7 +324,7 @@ int Engine::materialize(int w, int pos, std::vector<int> pieces, int64_t budget,
   st.produced.insert(uid);
   if (!is_local(w)) return uid;
   const int li = w - first_;
-  Slot out = make_slot();
+  Slot out = make_slot(uid);
   slots_[uid] = out;
   sdl::SelTask t = pieces.size() == 1 ? select_from_slot(local_slot(pieces[0]))
                                       : select_from_merge(st, pieces);
@@ -327,9 +354,10 @@ void Engine::transfer(std::vector<Xfer>& xs, int uid, int src, int dst, int phas
                       std::vector<std::vector<int>>* recv_into) {
   (void)recv_into;
   const int sr = rank_of(src), dr = rank_of(dst);
+  deliveries_.push_back({uid, dr});
   if (dr == rank_) {
     if (!has_local(uid)) {
-      slots_[uid] = make_slot();
+      slots_[uid] = make_slot(uid);
       xs.push_back({uid, src, sr, dr});
     }
     const int li = dst - first_;
@@ -380,10 +408,11 @@ void Engine::plan() {
     for (int b = 0; b < m_; ++b) {
       const int uid = new_uid(w);
       held[static_cast<size_t>(w)][static_cast<size_t>(b)] = {uid};
+      div_stage_.produced.insert(uid);
       if (!is_local(w)) continue;
       const int li = w - first_;
       div_uid_[static_cast<size_t>(li)][static_cast<size_t>(b)] = uid;
-      Slot out = make_slot();
+      Slot out = make_slot(uid);
       slots_[uid] = out;
       const int64_t lo = part_.lo[static_cast<size_t>(b)], hi = part_.hi[static_cast<size_t>(b)];
       sdl::DivTask dt{};
@@ -679,6 +708,131 @@ void Engine::plan() {
 }
 
 // ---------------------------------------------------------------------------
+// peer-memory transport setup
+void Engine::setup_peer() {
+  if (world_ == 1) return;
+  const char* env = std::getenv("SPARDL_TRANSPORT");
+  if (env && std::strcmp(env, "nccl") == 0) return;
+  // the plan numbers every rank's buffers identically: a plan-only replay
+  // gives the region size each rank needs
+  int max_slots = 0, nuid = 0;
+  {
+    Engine dry(cfg_, 0, world_, rank_, nullptr, nullptr, true);
+    for (int c : dry.rank_slots_) max_slots = std::max(max_slots, c);
+    nuid = dry.next_uid_;
+  }
+  auto align = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+  slot_stride_ = align(16 + 8 * static_cast<size_t>(Lcap_));
+  flags_off_ = slot_stride_ * static_cast<size_t>(max_slots);
+  done_off_ = flags_off_ + align(sizeof(long long) * static_cast<size_t>(nuid));
+  const size_t bytes = done_off_ + align(sizeof(long long) * static_cast<size_t>(world_));
+  CK(cudaMalloc(&sym_, bytes));
+  CK(cudaMemset(sym_, 0, bytes));
+  cudaIpcMemHandle_t mine{};
+  int32_t ok = cudaIpcGetMemHandle(&mine, sym_) == cudaSuccess ? 1 : 0;
+  cudaGetLastError();
+  // exchange the handles over the communicator
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  unsigned char* dbuf = nullptr;
+  CK(cudaMalloc(&dbuf, hb * static_cast<size_t>(world_ + 1) + 16));
+  CK(cudaMemcpy(dbuf, &mine, hb, cudaMemcpyHostToDevice));
+  NK(ncclAllGather(dbuf, dbuf + hb, hb, ncclChar, comm_, stream_));
+  std::vector<cudaIpcMemHandle_t> hs(static_cast<size_t>(world_));
+  CK(cudaStreamSynchronize(stream_));
+  CK(cudaMemcpy(hs.data(), dbuf + hb, hb * static_cast<size_t>(world_), cudaMemcpyDeviceToHost));
+  peer_base_.assign(static_cast<size_t>(world_), nullptr);
+  peer_base_[static_cast<size_t>(rank_)] = sym_;
+  for (int q = 0; q < world_ && ok; ++q) {
+    if (q == rank_) continue;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hs[static_cast<size_t>(q)], cudaIpcMemLazyEnablePeerAccess) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+    } else {
+      peer_base_[static_cast<size_t>(q)] = static_cast<unsigned char*>(p);
+    }
+  }
+  // every rank must agree, or all use NCCL
+  int32_t* dok = reinterpret_cast<int32_t*>(dbuf + hb * static_cast<size_t>(world_ + 1));
+  CK(cudaMemcpy(dok, &ok, sizeof(ok), cudaMemcpyHostToDevice));
+  NK(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, comm_, stream_));
+  CK(cudaStreamSynchronize(stream_));
+  CK(cudaMemcpy(&ok, dok, sizeof(ok), cudaMemcpyDeviceToHost));
+  CK(cudaFree(dbuf));
+  if (!ok) {
+    for (int q = 0; q < world_; ++q)
+      if (q != rank_ && peer_base_[static_cast<size_t>(q)])
+        cudaIpcCloseMemHandle(peer_base_[static_cast<size_t>(q)]);
+    peer_base_.clear();
+    cudaFree(sym_);
+    sym_ = nullptr;
+    return;
+  }
+  peer_ = true;
+}
+
+// Readiness flags: the owner of a block publishes it to every rank it is
+// delivered to right after the stage that produces it; a consumer waits at the
+// round of the schedule that delivers it.
+void Engine::plan_peer() {
+  if (!peer_) return;
+  auto flag_at = [&](int rank, int uid) {
+    return reinterpret_cast<long long*>(peer_base_[static_cast<size_t>(rank)] + flags_off_) + uid;
+  };
+  auto upload = [&](const auto& v) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    T* d = static_cast<T*>(arena_.alloc(sizeof(T) * std::max<size_t>(1, v.size())));
+    if (!v.empty()) CK(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    return d;
+  };
+  std::set<std::pair<int, int>> seen;
+  std::vector<long long*> div_pub;
+  std::vector<std::vector<long long*>> pub(steps_.size());
+  for (const auto& dl : deliveries_) {
+    const int uid = dl.first, dst = dl.second;
+    if (rank_of(uid_owner_[static_cast<size_t>(uid)]) != rank_ || dst == rank_) continue;
+    if (!seen.insert(dl).second) continue;
+    if (div_stage_.produced.count(uid)) {
+      div_pub.push_back(flag_at(dst, uid));
+      continue;
+    }
+    bool found = false;
+    for (size_t i = 0; i < steps_.size() && !found; ++i)
+      if (steps_[i].stage.produced.count(uid)) {
+        pub[i].push_back(flag_at(dst, uid));
+        found = true;
+      }
+    if (!found) sdlh::fail(SPARDL_E_ERROR, "internal: delivered block has no producing stage");
+  }
+  div_peer_.pub = upload(div_pub);
+  div_peer_.npub = static_cast<int>(div_pub.size());
+  step_peer_.assign(steps_.size(), PeerLists{});
+  for (size_t i = 0; i < steps_.size(); ++i) {
+    std::vector<const long long*> w;
+    std::set<int> uids;
+    for (const Xfer& x : steps_[i].xfers)
+      if (x.dst_rank == rank_ && rank_of(uid_owner_[static_cast<size_t>(x.uid)]) != rank_ &&
+          uids.insert(x.uid).second)
+        w.push_back(flag_at(rank_, x.uid));
+    step_peer_[i].pub = upload(pub[i]);
+    step_peer_[i].npub = static_cast<int>(pub[i].size());
+    step_peer_[i].wait = upload(w);
+    step_peer_[i].nwait = static_cast<int>(w.size());
+  }
+  std::vector<const long long*> begin;
+  std::vector<long long*> done;
+  for (int q = 0; q < world_; ++q) {
+    if (q == rank_) continue;
+    begin.push_back(reinterpret_cast<const long long*>(sym_ + done_off_) + q);
+    done.push_back(reinterpret_cast<long long*>(peer_base_[static_cast<size_t>(q)] + done_off_) + rank_);
+  }
+  begin_dev_ = upload(begin);
+  done_dev_ = upload(done);
+  npeer_ = static_cast<int>(begin.size());
+}
+
+// ---------------------------------------------------------------------------
 // execution
 int Engine::exec_stage(const Stage& st) {
   int n = 0;
@@ -691,7 +845,7 @@ int Engine::exec_stage(const Stage& st) {
 }
 
 void Engine::exec_round(const std::vector<Xfer>& xs) {
-  if (world_ == 1) return;
+  if (world_ == 1 || peer_) return;
   bool any = false;
   for (const Xfer& x : xs) any |= x.src_rank != x.dst_rank;
   if (!any) return;
@@ -719,6 +873,8 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   };
   CK(cudaMemsetAsync(ledger_phase_, 0, sizeof(int64_t) * 3 * wloc_, stream_));
   CK(cudaMemsetAsync(hash_dev_, 0, sizeof(int64_t) * d_, stream_));
+  // peers may read our block buffers until they finish the previous iteration
+  if (peer_) n += sdl::launch_begin(epoch_, begin_dev_, npeer_, peer_err_, stream_);
   mark(0);
   n += sdl::launch_divide(div_dev_, static_cast<int>(div_tasks_.size()), div_max_chunks_,
                           div_sample_every_, 1, stream_, 1);
@@ -727,14 +883,18 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
                           div_sample_every_, 1, stream_, 2);
   mark(2);
   n += exec_stage(div_stage_);
+  if (peer_) n += sdl::launch_publish(div_peer_.pub, div_peer_.npub, epoch_, stream_);
   mark(3);
   for (size_t i = 0; i < steps_.size(); ++i) {
     const Step& s = steps_[i];
     n += exec_stage(s.stage);
+    if (peer_) n += sdl::launch_publish(step_peer_[i].pub, step_peer_[i].npub, epoch_, stream_);
     if (s.controller_after)
       n += sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1,
                                   stream_);
     if (i + 1 == steps_.size()) mark(4);
+    if (peer_)
+      n += sdl::launch_wait(step_peer_[i].wait, step_peer_[i].nwait, epoch_, peer_err_, stream_);
     exec_round(s.xfers);
   }
   if (steps_.empty()) mark(4);
@@ -742,6 +902,8 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   n += sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), Lcap_, m_,
                             static_cast<int>(fin_max_div_), stream_);
   n += sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), stream_);
+  // last remote read of the iteration done: peers may overwrite their buffers
+  if (peer_) n += sdl::launch_publish(done_dev_, npeer_, epoch_, stream_);
   mark(5);
   CK(cudaGetLastError());
   launches_ = n;
@@ -814,6 +976,13 @@ void Engine::sync() {
   CK(cudaSetDevice(device_));
   CK(cudaStreamSynchronize(stream_));
   int32_t err = 0;
+  if (peer_) {
+    CK(cudaMemcpy(&err, peer_err_, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err) {
+      CK(cudaMemset(peer_err_, 0, sizeof(int32_t)));
+      sdlh::fail(SPARDL_E_CUDA, "peer transport: a peer did not arrive within 10 s");
+    }
+  }
   CK(mcpy(&err, err_dev_, sizeof(err), cudaMemcpyDeviceToHost));
   if (err) {
     CK(cudaMemset(err_dev_, 0, sizeof(int32_t)));

@@ -132,7 +132,8 @@ class Engine {
   int new_uid(int owner_worker);
   Slot& local_slot(int uid);      // the local copy (must exist)
   bool has_local(int uid) const { return slots_.count(uid) != 0; }
-  Slot make_slot();
+  Slot make_slot(int uid);
+  Slot sym_slot(int uid) const;   // uid's buffer in its owner's symmetric region
   int materialize(int w, int pos, std::vector<int> pieces, int64_t budget, float weight,
                   const int64_t* budget_dev, int64_t* total_out, Stage& st, int xi_block);
   void add_select(Stage& st, const sdl::SelTask& t);
@@ -211,6 +212,33 @@ class Engine {
   std::vector<std::vector<std::vector<sdl::XiList>>> xi_;
   std::vector<int> union_group_owner_;       // position group -> worker providing N_t
   bool ran_ = false;
+
+  // --- peer-memory transport (transport.cu); NCCL send/recv when off
+  struct PeerLists {
+    long long** pub = nullptr;          // device: remote flags to publish after the stage
+    int npub = 0;
+    const long long** wait = nullptr;   // device: local flags to wait for at the round
+    int nwait = 0;
+  };
+  void setup_peer();                    // before plan(): symmetric region + IPC mappings
+  void plan_peer();                     // after plan(): publish / wait lists
+  bool peer_ = false;
+  unsigned char* sym_ = nullptr;
+  std::vector<unsigned char*> peer_base_;   // per rank; own entry is sym_
+  size_t slot_stride_ = 0, flags_off_ = 0, done_off_ = 0;
+  std::vector<int> uid_slot_;               // owner-rank-local buffer index of each uid
+  std::vector<int> rank_slots_;             // buffers numbered so far, per rank
+  std::vector<std::pair<int, int>> deliveries_;   // (uid, destination rank), whole plan
+  long long* epoch_ = nullptr;
+  int32_t* peer_err_ = nullptr;
+  PeerLists div_peer_;
+  std::vector<PeerLists> step_peer_;
+  const long long** begin_dev_ = nullptr;
+  long long** done_dev_ = nullptr;
+  int npeer_ = 0;
+
+ public:
+  bool peer_transport() const { return peer_; }
 };
 
 }  // namespace sdle

@@ -65,13 +65,6 @@ __global__ void __launch_bounds__(kThreads) k_assemble(const AssembleTask* __res
 //   lres: carry = dividing remainder, i.e. combined with the dividing
 //         selections zeroed (handled by k_finalize_lres).
 // Off the global gradient the carry already holds g_copy (in place).
-__device__ __forceinline__ int block_of_dev(int64_t n, int m, int64_t i) {
-  const int64_t base = n / m, rem = n % m;
-  const int64_t split = rem * (base + 1);
-  if (i < split) return (int)(i / (base + 1));
-  return (int)(rem + (i - split) / base);
-}
-
 // Warp-cooperative lower/upper bound over a sorted global array (32-ary
 // search: ~log32(n) rounds of one load per lane instead of log2(n)
 // dependent loads).  Must be called by a full warp.

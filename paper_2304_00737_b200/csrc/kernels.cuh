@@ -247,4 +247,11 @@ struct CtlTask {
 };
 int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStream_t s);
 
+// peer-memory transport (transport.cu): iteration epoch, readiness flags
+int launch_begin(long long* epoch, const long long* const* done, int n, int32_t* err,
+                 cudaStream_t s);
+int launch_publish(long long* const* targets, int n, const long long* epoch, cudaStream_t s);
+int launch_wait(const long long* const* flags, int n, const long long* epoch, int32_t* err,
+                cudaStream_t s);
+
 }  // namespace sdl

@@ -31,12 +31,10 @@ __global__ void __launch_bounds__(kThreads) k_merge_rank(const MergeTask* __rest
   const int r = t.r, T = t.T;
   __shared__ int32_t samp[kMaxSamples];
   __shared__ int base[kMaxR + 1];
-  __shared__ int ns[kMaxR];
   if (threadIdx.x == 0) {
     int b = 0;
     for (int l = 0; l < r; ++l) {
       const int n = *t.in_cnt[l];
-      ns[l] = n;
       base[l] = b;
       b += (n + T - 1) / T;
     }

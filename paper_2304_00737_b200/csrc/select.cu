@@ -70,13 +70,6 @@ __device__ __forceinline__ void seg_bounds(const SelTask& t, int mode, int s, in
   cnt = c < 0 ? 0 : c;
 }
 
-__device__ __forceinline__ float seg_val(const SelTask& t, int mode, int p) {
-  return mode == 1 ? t.dval[p] : t.val[p];
-}
-__device__ __forceinline__ int32_t seg_idx(const SelTask& t, int mode, int p) {
-  return mode == 1 ? t.dbase + p : t.idx[p];
-}
-
 // shared-memory histogram increment (the keys of a warp spread over many bins,
 // so plain shared atomics beat warp aggregation with match.any)
 __device__ __forceinline__ void hist_add(uint32_t* h, uint32_t bin, bool active) {

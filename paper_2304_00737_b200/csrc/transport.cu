@@ -1,0 +1,102 @@
+// Peer-memory transport: block buffers are read by their consumers straight
+// out of the producing GPU's memory over NVLink (CUDA IPC mappings of a
+// symmetric buffer region), so a transport round of the schedule
+// (inc/fabric.hpp:95-106 -- one Fabric::deliver per block) costs one
+// readiness flag instead of a copy: the merge or assembly that consumes a
+// block reads it remotely, overlapping the transfer with its own work.
+//
+// Protocol, per iteration e (a device-resident counter, so CUDA-graph replays
+// see fresh values):
+//   k_begin    e = ++epoch; wait until every peer finished iteration e-1
+//              (peers may still read our block buffers until then)
+//   k_publish  after the stage producing a block: fence, then store e into
+//              the consumer's flag for that block (remote store)
+//   k_wait     at the round that delivers a block: spin (acquire, system
+//              scope) until the local flag for the block reaches e
+//   k_done     after the last remote read of the iteration: store e into
+//              every peer's done[rank] flag
+// Waits are bounded (~10 s): a peer that never arrives sets *err and the next
+// sync() reports it instead of hanging the device.
+#include "kernels.cuh"
+
+namespace sdl {
+
+namespace {
+
+constexpr unsigned long long kTimeoutNs = 10ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(long long* p, long long v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+__device__ void spin_until(const long long* flag, long long target, int32_t* err) {
+  if (ld_acquire_sys(flag) >= target) return;
+  const unsigned long long t0 = gtime();
+  unsigned ns = 32;
+  while (ld_acquire_sys(flag) < target) {
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+    if (gtime() - t0 > kTimeoutNs) {
+      atomicExch(err, 1);
+      return;
+    }
+  }
+}
+
+__global__ void k_begin(long long* epoch, const long long* const* done, int n, int32_t* err) {
+  __shared__ long long e;
+  if (threadIdx.x == 0) {
+    e = *epoch + 1;
+    *epoch = e;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) spin_until(done[i], e - 1, err);
+}
+
+__global__ void k_publish(long long* const* targets, int n, const long long* epoch) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long e = *epoch;
+  __threadfence_system();
+  st_release_sys(targets[i], e);
+}
+
+__global__ void k_wait(const long long* const* flags, int n, const long long* epoch, int32_t* err) {
+  const long long e = *epoch;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) spin_until(flags[i], e, err);
+}
+
+}  // namespace
+
+int launch_begin(long long* epoch, const long long* const* done, int n, int32_t* err,
+                 cudaStream_t s) {
+  k_begin<<<1, 32, 0, s>>>(epoch, done, n, err);
+  return 1;
+}
+
+int launch_publish(long long* const* targets, int n, const long long* epoch, cudaStream_t s) {
+  if (n <= 0) return 0;
+  k_publish<<<(n + 127) / 128, 128, 0, s>>>(targets, n, epoch);
+  return 1;
+}
+
+int launch_wait(const long long* const* flags, int n, const long long* epoch, int32_t* err,
+                cudaStream_t s) {
+  if (n <= 0) return 0;
+  k_wait<<<1, 128, 0, s>>>(flags, n, epoch, err);
+  return 1;
+}
+
+}  // namespace sdl

@@ -1,4 +1,5 @@
-"""Multi-GPU parity (one process per GPU, NCCL point-to-point over NVLink).
+"""Multi-GPU parity (one process per GPU), for both transports: direct
+peer-memory reads over NVLink (default) and NCCL send/recv.
 
 The P workers are spread over the available GPUs; every rank checks its
 own workers' residuals, the global gradient and the full ledger bit-exactly
@@ -30,7 +31,7 @@ CASES = [(8, 1, "none", "gres", "optimized"), (6, 1, "none", "gres", "naive"),
          (8, 8, "rsag", "gres", "optimized")]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, transport):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -40,6 +41,7 @@ def _worker(rank, world, port, q):
     import paper_2304_00737_b200 as sd
     from gpu_util import gen
     from pyoracle import Oracle, make_config
+    os.environ["SPARDL_TRANSPORT"] = transport
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
@@ -54,6 +56,8 @@ def _worker(rank, world, port, q):
             cfg = sd.ClusterConfig(workers=P, dimension=N, k=k, teams=d, sag=sag,
                                    residual=residual, timing=timing)
             ctx = sd.SparDL.from_process_group(cfg, device=rank)
+            if ctx.transport != transport:
+                errors.append(f"rank{rank} transport {ctx.transport} != {transport}")
             ref = orc.pipeline(make_config(P, N, k, d, sag, residual, timing))
             rng = np.random.default_rng(P * 7 + d)
             for it in range(3):
@@ -95,8 +99,9 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(900)
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_multi_gpu_parity(built, world):
+def test_multi_gpu_parity(built, world, transport):
     import torch
     import torch.multiprocessing as mp
     if torch.cuda.device_count() < world:
@@ -104,7 +109,7 @@ def test_multi_gpu_parity(built, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=840) for _ in procs)
