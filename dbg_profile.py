@@ -11,7 +11,7 @@ for i in range(P):
     grads.append(torch.randn(N, device='cuda', generator=gen))
 for it in range(5):
     ctx.all_reduce(grads); ctx.sync()
-out = (C.c_int64 * 12)()
+out = (C.c_int64 * 44)()
 names = ['p1','p0h','p0s','p0f','p1h','p1s','p1f','p2h','p2s','p2f','cnt+scan','write']
 for step in (-1, 0, 1, 2, 3):
     for task in (0,):
@@ -33,3 +33,12 @@ for step, ntask in ((-1, 64), (0, 16), (1, 8), (2, 8)):
     print('step', step, 'n', len(rows), 'span us', round(max(b for a, b in s), 1),
           'starts', [round(a, 1) for a, b in s][::max(1, len(s) // 8)],
           'durs', [round(b - a, 1) for a, b in s][::max(1, len(s) // 8)])
+
+# per-CTA view of one task per step: start offsets and pass-0 histogram ends (us, rel. CTA 0 start)
+for step in (-1, 1, 2, 3):
+    rc = lib().spardl_debug_select_timestamps(ctx._h, step, 0, out)
+    if rc: continue
+    ts = list(out); t0 = ts[0]
+    starts = [round((x - t0) / 1000, 1) for x in ts[12:28] if x]
+    ends = [round((x - t0) / 1000, 1) for x in ts[28:44] if x]
+    print('step', step, 'cta starts', starts, 'hist0 ends', ends)

@@ -1137,7 +1137,7 @@ void Engine::select_timestamps(int step, int task, int64_t* out12) {
   sync();
   const Stage& st = step < 0 ? div_stage_ : steps_.at(static_cast<size_t>(step)).stage;
   const sdl::SelScratch* sc = st.sels.at(static_cast<size_t>(task)).scr;
-  CK(mcpy(out12, sc->tstamp, sizeof(long long) * 12, cudaMemcpyDeviceToHost));
+  CK(mcpy(out12, sc->tstamp, sizeof(long long) * 44, cudaMemcpyDeviceToHost));
 }
 
 int64_t Engine::dense_fallbacks() {

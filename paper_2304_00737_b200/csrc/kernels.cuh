@@ -59,6 +59,7 @@ struct SelScratch {
   int32_t cut_idx;       // largest selected index among entries with key == T
   int32_t pad_;
   long long tstamp[12];  // phase timestamps (globaltimer ns) of the last run, CTA 0
+  long long cta_ts[2][16];   // per CTA: start, end of the pass-0 histogram
 };
 
 // Membership in a finished selection without searching its output:
@@ -81,8 +82,8 @@ struct SelTask {
   int32_t mode;
   int32_t mode_from_cand;
   int32_t stride;
-  int32_t tiles;         // unused (kept for layout stability)
   int32_t pad1_;
+  int32_t pad2_;
   const int32_t* nseg_dev;  // nullable: segments actually in use (device-decided)
   const int32_t* idx;
   const float* val;

@@ -161,6 +161,14 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     }
   };
   stamp(0);
+  auto cta_stamp = [&](int k) {
+    if (threadIdx.x == 0 && cr < 16) {
+      long long ts;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+      sc->cta_ts[k][cr] = ts;
+    }
+  };
+  cta_stamp(0);
   // ---- 1. totals and an entry-balanced split of the segments over the
   // cluster: every CTA scans all segment lengths (cheap: <= 8192 counts) and
   // owns the segments whose first entry falls in its 1/kCl of the entries.
@@ -259,6 +267,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       }
       __syncthreads();
       stamp(2 + 3 * pass);
+      if (pass == 0) cta_stamp(1);
       // distributed reduction: CTA r sums its 1/CL slice of the bins over
       // all CTAs' histograms (DSMEM loads) and stores it into CTA 0's copy
       cluster.sync();
