@@ -240,14 +240,15 @@ void Engine::add_select(Stage& st, const sdl::SelTask& t0) {
   if (t.nseg > sdl::kMaxSegPerTask || t.dnseg > sdl::kMaxSegPerTask)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "selection larger than the device work-item bound");
   t.scr = static_cast<sdl::SelScratch*>(arena_.alloc(sizeof(sdl::SelScratch)));
-  const int nseg = std::max(1, sdl::sel_scratch_segments(t));
-  int32_t* segs = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * 5 * nseg));
+  const int nck = std::max(1, sdl::sel_chunk_capacity(t));
+  int32_t* segs = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * 5 * nck));
   t.seg_gt = segs;
-  t.seg_eq = segs + nseg;
-  t.seg_sel_off = segs + 2 * nseg;
-  t.seg_dis_off = segs + 3 * nseg;
-  t.seg_take = segs + 4 * nseg;
-  st.max_nseg = std::max(st.max_nseg, sdl::sel_grid_segments(t));
+  t.seg_eq = segs + nck;
+  t.seg_sel_off = segs + 2 * nck;
+  t.seg_dis_off = segs + 3 * nck;
+  t.seg_take = segs + 4 * nck;
+  // the select's per-CTA segment table is sized for a whole task's segments
+  st.max_nseg = std::max(st.max_nseg, sdl::sel_scratch_segments(t));
   st.sels.push_back(t);
 }
 

@@ -40,6 +40,7 @@ struct SelTask;
 int sel_prepare(SelTask& t, int max_seg_len);
 int sel_scratch_segments(const SelTask& t);   // per-segment scratch entries needed
 int sel_grid_segments(const SelTask& t);      // segments the launch grid is sized for
+int sel_chunk_capacity(const SelTask& t);     // per-chunk scratch entries needed
 
 // ---------------------------------------------------------------------------
 // Select
@@ -115,7 +116,7 @@ struct SelTask {
   int64_t* total_out;    // nullable: B-SAG union size N_t
   // scratch
   SelScratch* scr;
-  int32_t* seg_gt;       // [max nseg]
+  int32_t* seg_gt;       // [sel_chunk_capacity] per work chunk
   int32_t* seg_eq;
   int32_t* seg_sel_off;
   int32_t* seg_dis_off;

@@ -39,6 +39,7 @@ namespace {
 constexpr int kSelThreads = 512;   // 16 warps per CTA
 constexpr int kWarps = kSelThreads / 32;
 constexpr int kIlp = 8;   // 32-entry groups loaded per warp step (memory-level parallelism)
+constexpr int kChunkE = 32 * kIlp;   // flat entries per work chunk (one warp step)
 
 __device__ __forceinline__ int resolve_mode(const SelTask& t) {
   if (!t.mode_from_cand) return t.mode;
@@ -125,12 +126,12 @@ __device__ void find_digit(uint32_t* agg, int nb, int shift, RadixState* st, lon
   for (int q = 0; q < bpt; ++q) agg[threadIdx.x * bpt + q] = 0;   // ready for the next pass
 }
 
-template <int CL>
 #ifndef SPARDL_SEL_MINB
 #define SPARDL_SEL_MINB 1
 #endif
+template <int CL>
 __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
-    k_select(const SelTask* __restrict__ tasks) {
+    k_select(const SelTask* __restrict__ tasks, int tab_cap) {
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank();
   const SelTask t = tasks[blockIdx.y];   // by value: fields live in registers, not re-read
@@ -145,6 +146,12 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   __shared__ int scratch[40];
   __shared__ long long lscr[32];
   __shared__ RadixState my;                         // this CTA's copy of CTA 0's state
+  // this CTA's work items: contiguous pieces of its segments, <= plen long
+  // (item i = input elements [iof[i], iof[i] + ilen[i])), so the warps share
+  // long merge partitions evenly and never re-read segment bounds
+  extern __shared__ int32_t dyn[];
+  int32_t* iof = dyn;
+  int32_t* ilen = dyn + tab_cap;
 
   RadixState* st0 = cluster.map_shared_rank(&st, 0);
   uint32_t* agg0 = cluster.map_shared_rank(agg, 0);
@@ -171,14 +178,10 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   cta_stamp(0);
   // ---- 1. totals and an entry-balanced split of the segments over the
   // cluster: every CTA scans all segment lengths (cheap: <= 8192 counts) and
-  // owns the segments whose first entry falls in its 1/kCl of the entries.
-  __shared__ int s_lo, s_hi;
+  // owns the segments whose first entry falls in its 1/CL of the entries.
+  __shared__ int s_lo, s_hi, s_F, s_before;
   long long total = 0;
   {
-    if (threadIdx.x == 0) {
-      s_lo = 0;
-      s_hi = 0;
-    }
     // pass A: the total
     long long part = 0;
     for (int s = threadIdx.x; s < nseg; s += kSelThreads) {
@@ -207,6 +210,46 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       s_lo = cr == 0 ? 0 : n_lo;
       s_hi = cr == CL - 1 ? nseg : n_hi;
     }
+    __syncthreads();
+  }
+  const int s0 = s_lo, s1 = s_hi;
+  const int nloc = s1 - s0;
+  // ---- 1b. the work items of this CTA; its per-item scratch starts at
+  // s0 + (entries before it) / kChunkE + cr (disjoint across the cluster)
+  __shared__ int s_nit, s_plen;
+  {
+    long long before = 0, here = 0;
+    for (int s = threadIdx.x; s < s1; s += kSelThreads) {
+      int off, c;
+      seg_bounds(t, mode, s, off, c);
+      if (s < s0) before += c;
+      else here += c;
+    }
+    before = block_sum_ll(before, lscr);
+    here = block_sum_ll(here, lscr);
+    // smallest piece length (kChunkE * 2^j) whose items fit the table
+    long long plen = kChunkE;
+    while (nloc + (here + plen - 1) / plen > tab_cap && plen < (1ll << 30)) plen <<= 1;
+    int carry = 0;
+    for (int b0 = 0; b0 < nloc; b0 += kSelThreads) {
+      const int ls = b0 + threadIdx.x;
+      int off = 0, c = 0;
+      if (ls < nloc) seg_bounds(t, mode, s0 + ls, off, c);
+      const int np = (int)((c + plen - 1) / plen);
+      int tt;
+      int it = carry + block_exscan(np, scratch, &tt);
+      for (int j = 0; j < np && it < tab_cap; ++j, ++it) {
+        iof[it] = off + j * (int)plen;
+        ilen[it] = min((int)plen, c - j * (int)plen);
+      }
+      carry += tt;
+    }
+    if (threadIdx.x == 0) {
+      s_nit = min(carry, tab_cap);
+      s_plen = (int)plen;
+      s_F = (int)here;
+      s_before = s0 + (int)(before / kChunkE) + cr;
+    }
   }
   for (int b = threadIdx.x; b < kBins; b += kSelThreads) agg[b] = 0;
   const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
@@ -227,18 +270,19 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     my.rank = budget;
     my.all = total <= budget ? 1 : (budget <= 0 ? 2 : 0);
   }
-  cluster.sync();   // CTA 0's aggregation histogram is zeroed
+  cluster.sync();   // CTA 0's aggregation histogram is zeroed; tables are visible
   stamp(1);
-  const int s0 = s_lo, s1 = s_hi;
-  const int nloc = s1 - s0;
-  // per-segment counters of this CTA's range (task scratch, L2 resident)
-  int* s_gt = t.seg_gt + s0;
-  int* s_eq = t.seg_eq + s0;
-  int* s_take = t.seg_take + s0;
-  int* s_sel = t.seg_sel_off + s0;
-  int* s_dis = t.seg_dis_off + s0;
+  const int nit = s_nit;
+  // per-item counters of this CTA (task scratch, L2 resident)
+  int* c_gt = t.seg_gt + s_before;
+  int* c_eq = t.seg_eq + s_before;
+  int* c_take = t.seg_take + s_before;
+  int* c_sel = t.seg_sel_off + s_before;
+  int* c_dis = t.seg_dis_off + s_before;
+  const float* __restrict__ vbase = mode == 1 ? t.dval : t.val;
+  const int32_t* __restrict__ ibase = mode == 1 ? nullptr : t.idx;
 
-  // ---- 2. radix passes
+  // ---- 2. radix passes: warp w histograms chunks w, w + kWarps, ...
   if (my.all == 0) {
 #pragma unroll 1
     for (int pass = 0; pass < 3; ++pass) {
@@ -247,11 +291,10 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       for (int b = threadIdx.x; b < nb; b += kSelThreads) hist[b] = 0;
       __syncthreads();
       const uint32_t prefix = my.prefix, pmask = my.pmask;
-      for (int s = s0 + warp; s < s1; s += kWarps) {
-        int off, c;
-        seg_bounds(t, mode, s, off, c);
-        const float* __restrict__ vp = (mode == 1 ? t.dval : t.val) + off;
-        for (int j0 = 0; j0 < c; j0 += 32 * kIlp) {
+      for (int k = warp; k < nit; k += kWarps) {
+        const int c = ilen[k];
+        const float* __restrict__ vp = vbase + iof[k];
+        for (int j0 = 0; j0 < c; j0 += kChunkE) {
           uint32_t key[kIlp];
 #pragma unroll
           for (int u = 0; u < kIlp; ++u) {   // all loads in flight first
@@ -293,17 +336,16 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   const uint32_t T = my.prefix;
   const int64_t need_eq = all == 0 ? my.rank : 0;
 
-  // ---- 3. per-segment counts, offsets
-  long long g_loc = 0, e_loc = 0, c_loc = 0;
-  for (int ls = warp; ls < nloc; ls += kWarps) {
-    int off, c;
-    seg_bounds(t, mode, s0 + ls, off, c);
+  // ---- 3. per-chunk counts, offsets
+  long long g_loc = 0, e_loc = 0;
+  for (int k = warp; k < nit; k += kWarps) {
+    const int c = ilen[k];
     int gt = 0, eq = 0;
     if (all == 1) {
       gt = c;
     } else if (all == 0) {
-      const float* __restrict__ vp = (mode == 1 ? t.dval : t.val) + off;
-      for (int j0 = 0; j0 < c; j0 += 32 * kIlp) {
+      const float* __restrict__ vp = vbase + iof[k];
+      for (int j0 = 0; j0 < c; j0 += kChunkE) {
         uint32_t key[kIlp];
 #pragma unroll
         for (int u = 0; u < kIlp; ++u) {
@@ -321,18 +363,15 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       eq = __reduce_add_sync(0xffffffffu, eq);
     }
     if (lane == 0) {
-      s_gt[ls] = gt;
-      s_eq[ls] = eq;
-      s_sel[ls] = c;   // segment length, temporarily
+      c_gt[k] = gt;
+      c_eq[k] = eq;
       g_loc += gt;
       e_loc += eq;
-      c_loc += c;
     }
   }
   g_loc = block_sum_ll(g_loc, lscr);
   e_loc = block_sum_ll(e_loc, lscr);
-  c_loc = block_sum_ll(c_loc, lscr);
-  if (threadIdx.x == 0) tot0[cr] = {c_loc, g_loc, e_loc};
+  if (threadIdx.x == 0) tot0[cr] = {(long long)s_F, g_loc, e_loc};
   cluster.sync();
   __shared__ long long base_eq, base_sel, base_cnt, all_sel, all_cnt;
   if (threadIdx.x == 0) {
@@ -359,13 +398,13 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   __syncthreads();
   {
     int eq_carry = (int)base_eq, sel_carry = (int)base_sel, cnt_carry = (int)base_cnt;
-    for (int l0 = 0; l0 < nloc; l0 += kSelThreads) {
-      const int ls = l0 + threadIdx.x;
+    for (int l0 = 0; l0 < nit; l0 += kSelThreads) {
+      const int k = l0 + threadIdx.x;
       int gt = 0, eq = 0, c = 0;
-      if (ls < nloc) {
-        gt = s_gt[ls];
-        eq = s_eq[ls];
-        c = s_sel[ls];
+      if (k < nit) {
+        gt = c_gt[k];
+        eq = c_eq[k];
+        c = ilen[k];
       }
       int teq, tsel, tcnt;
       const int eq_before = eq_carry + block_exscan(eq, scratch, &teq);
@@ -374,10 +413,10 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       const int sel = gt + take;
       const int sel_off = sel_carry + block_exscan(sel, scratch, &tsel);
       const int cnt_off = cnt_carry + block_exscan(c, scratch, &tcnt);
-      if (ls < nloc) {
-        s_take[ls] = take;
-        s_sel[ls] = sel_off;
-        s_dis[ls] = cnt_off - sel_off;
+      if (k < nit) {
+        c_take[k] = take;
+        c_sel[k] = sel_off;
+        c_dis[k] = cnt_off - sel_off;
       }
       eq_carry += teq;
       sel_carry += tsel;
@@ -387,60 +426,59 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   __syncthreads();
 
   stamp(10);
-  // ---- 4. ordered compaction
+  // ---- 4. ordered compaction, chunk by chunk
   const float w = t.weight;
   const bool want_dis = t.dis_idx != nullptr;
   const uint32_t lt = lanemask_lt();
   int cut = -1;
-  for (int ls = warp; ls < nloc; ls += kWarps) {
-    int off, c;
-    seg_bounds(t, mode, s0 + ls, off, c);
-    const int sel_base = s_sel[ls], dis_base = s_dis[ls], take = s_take[ls];
+  for (int k = warp; k < nit; k += kWarps) {
+    const int c = ilen[k], e0 = iof[k];
+    const int sel_base = c_sel[k], dis_base = c_dis[k], take = c_take[k];
     int eq_seen = 0, sel_seen = 0;
-    const float* __restrict__ vp = (mode == 1 ? t.dval : t.val) + off;
-    const int32_t* __restrict__ ip = mode == 1 ? nullptr : t.idx + off;
-    const int32_t ibase = t.dbase + off;
-    for (int j00 = 0; j00 < c; j00 += 32 * kIlp) {
+    const float* __restrict__ vp = vbase + e0;
+    const int32_t* __restrict__ ip = ibase ? ibase + e0 : nullptr;
+    const int32_t ib = t.dbase + e0;
+    for (int j00 = 0; j00 < c; j00 += kChunkE) {
       float vv[kIlp];
       int32_t iv[kIlp];
 #pragma unroll
       for (int u = 0; u < kIlp; ++u) {   // all loads in flight first
         const int j = j00 + u * 32 + lane;
         vv[u] = j < c ? __ldg(vp + j) : 0.f;
-        iv[u] = j < c ? (ip ? __ldg(ip + j) : ibase + j) : 0;
+        iv[u] = j < c ? (ip ? __ldg(ip + j) : ib + j) : 0;
       }
 #pragma unroll
-    for (int u = 0; u < kIlp; ++u) {
-      const int j = j00 + u * 32 + lane;
-      const bool valid = j < c;
-      const float v = vv[u];
-      const int32_t ix = iv[u];
-      const uint32_t key = mag_key(v);
-      bool is_sel;
-      if (all == 1) {
-        is_sel = valid;
-      } else if (all == 2) {
-        is_sel = false;
-      } else {
-        const bool is_eq = valid && key == T;
-        const uint32_t be = __ballot_sync(0xffffffffu, is_eq);
-        const int eq_rank = eq_seen + __popc(be & lt);
-        eq_seen += __popc(be);
-        is_sel = valid && (key > T || (is_eq && eq_rank < take));
-        if (is_sel && is_eq) cut = max(cut, ix);
+      for (int u = 0; u < kIlp; ++u) {
+        const int j = j00 + u * 32 + lane;
+        const bool valid = j < c;
+        const float v = vv[u];
+        const int32_t ix = iv[u];
+        const uint32_t key = mag_key(v);
+        bool is_sel;
+        if (all == 1) {
+          is_sel = valid;
+        } else if (all == 2) {
+          is_sel = false;
+        } else {
+          const bool is_eq = valid && key == T;
+          const uint32_t be = __ballot_sync(0xffffffffu, is_eq);
+          const int eq_rank = eq_seen + __popc(be & lt);
+          eq_seen += __popc(be);
+          is_sel = valid && (key > T || (is_eq && eq_rank < take));
+          if (is_sel && is_eq) cut = max(cut, ix);
+        }
+        const uint32_t bs = __ballot_sync(0xffffffffu, is_sel);
+        const int sel_rank = sel_seen + __popc(bs & lt);
+        sel_seen += __popc(bs);
+        if (is_sel) {
+          t.sel_idx[sel_base + sel_rank] = ix;
+          t.sel_val[sel_base + sel_rank] = v;
+        } else if (valid && want_dis) {
+          const int p = dis_base + (j - sel_rank);
+          t.dis_idx[p] = ix;
+          t.dis_val[p] = __fmul_rn(v, w);
+        }
       }
-      const uint32_t bs = __ballot_sync(0xffffffffu, is_sel);
-      const int sel_rank = sel_seen + __popc(bs & lt);
-      sel_seen += __popc(bs);
-      if (is_sel) {
-        t.sel_idx[sel_base + sel_rank] = ix;
-        t.sel_val[sel_base + sel_rank] = v;
-      } else if (valid && want_dis) {
-        const int p = dis_base + (j - sel_rank);
-        t.dis_idx[p] = ix;
-        t.dis_val[p] = __fmul_rn(v, w);
-      }
-    }
     }
   }
   if (all == 0) {
@@ -484,11 +522,11 @@ int sel_grid_segments(const SelTask& t) {
 
 namespace {
 template <int CL>
-cudaLaunchConfig_t cl_config(int ntask, cudaStream_t s, cudaLaunchAttribute* attr) {
+cudaLaunchConfig_t cl_config(int ntask, size_t smem, cudaStream_t s, cudaLaunchAttribute* attr) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(CL, ntask);
   lc.blockDim = dim3(kSelThreads);
-  lc.dynamicSmemBytes = 0;
+  lc.dynamicSmemBytes = smem;
   lc.stream = s;
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
@@ -499,33 +537,45 @@ cudaLaunchConfig_t cl_config(int ntask, cudaStream_t s, cudaLaunchAttribute* att
   return lc;
 }
 
+size_t table_bytes(int tab_cap) { return sizeof(int32_t) * 2 * static_cast<size_t>(tab_cap); }
+
 // clusters of width CL that can be resident at once on this device (a
 // cluster must fit in one GPC, so wide clusters leave SMs unused)
 template <int CL>
-int max_clusters() {
-  static int n = -1;
-  if (n < 0) {   // 16 is a non-portable cluster size on sm_100
+int max_clusters(size_t smem) {
+  static bool configured = false;
+  static size_t last_smem = ~size_t(0);
+  static int n = 0;
+  if (!configured) {   // 16 is a non-portable cluster size on sm_100
     cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)table_bytes(kMaxSegPerTask));
+    configured = true;
+  }
+  if (smem != last_smem) {
     cudaLaunchAttribute attr[1];
-    cudaLaunchConfig_t lc = cl_config<CL>(1, nullptr, attr);
+    cudaLaunchConfig_t lc = cl_config<CL>(1, smem, nullptr, attr);
     int c = 0;
     if (cudaOccupancyMaxActiveClusters(&c, k_select<CL>, &lc) != cudaSuccess) {
       cudaGetLastError();
       c = 0;
     }
     n = c;
-    if (getenv("SPARDL_DEBUG")) fprintf(stderr, "k_select<%d>: %d resident clusters\n", CL, n);
+    last_smem = smem;
+    if (getenv("SPARDL_DEBUG"))
+      fprintf(stderr, "k_select<%d>: %d resident clusters (%zu B tables)\n", CL, n, smem);
   }
   return n;
 }
 
 template <int CL>
-void launch_cl(const SelTask* tasks_dev, int ntask, cudaStream_t s) {
-  max_clusters<CL>();
+void launch_cl(const SelTask* tasks_dev, int ntask, int tab_cap, cudaStream_t s) {
+  const size_t smem = table_bytes(tab_cap);
+  max_clusters<CL>(smem);
   cudaLaunchAttribute attr[1];
-  cudaLaunchConfig_t lc = cl_config<CL>(ntask, s, attr);
-  cudaLaunchKernelEx(&lc, k_select<CL>, tasks_dev);
+  cudaLaunchConfig_t lc = cl_config<CL>(ntask, smem, s, attr);
+  cudaLaunchKernelEx(&lc, k_select<CL>, tasks_dev, tab_cap);
 }
 
 int forced_cl() {
@@ -538,16 +588,25 @@ int forced_cl() {
 }
 }  // namespace
 
+int sel_chunk_capacity(const SelTask& t) {
+  const int64_t ex = (int64_t)t.nseg * t.stride;
+  const int64_t mx = ex > t.dn ? ex : t.dn;
+  const int ns = t.nseg > t.dnseg ? t.nseg : t.dnseg;
+  return ns + (int)((mx + kChunkE - 1) / kChunkE) + kCl + 2;
+}
+
 int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s) {
-  (void)max_nseg;
   if (ntask <= 0) return 0;
+  // item table: at least 2048 entries so long inputs split into short pieces
+  const int tab_cap = max_nseg < 2048 ? 2048 : max_nseg;
+  const size_t smem = table_bytes(tab_cap);
   // the widest cluster for which every task's cluster is resident in one
   // wave (a second wave would double the latency of the whole batch)
   int cl = forced_cl();
   if (cl == 0) {
-    if (max_clusters<16>() >= ntask) cl = 16;
-    else if (max_clusters<8>() >= ntask) cl = 8;
-    else if (max_clusters<4>() >= ntask) cl = 4;
+    if (max_clusters<16>(smem) >= ntask) cl = 16;
+    else if (max_clusters<8>(smem) >= ntask) cl = 8;
+    else if (max_clusters<4>(smem) >= ntask) cl = 4;
     else cl = 2;
   }
   static int dbg = 0;
@@ -555,10 +614,10 @@ int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_
     ++dbg;
     fprintf(stderr, "select batch: %d tasks -> cluster %d\n", ntask, cl);
   }
-  if (cl >= 16) launch_cl<16>(tasks_dev, ntask, s);
-  else if (cl >= 8) launch_cl<8>(tasks_dev, ntask, s);
-  else if (cl >= 4) launch_cl<4>(tasks_dev, ntask, s);
-  else launch_cl<2>(tasks_dev, ntask, s);
+  if (cl >= 16) launch_cl<16>(tasks_dev, ntask, tab_cap, s);
+  else if (cl >= 8) launch_cl<8>(tasks_dev, ntask, tab_cap, s);
+  else if (cl >= 4) launch_cl<4>(tasks_dev, ntask, tab_cap, s);
+  else launch_cl<2>(tasks_dev, ntask, tab_cap, s);
   return 1;
 }
 
