@@ -232,8 +232,9 @@ int spardl_get_controller(spardl_ctx* ctx, int32_t local_worker, spardl_hctrl* o
  * candidate fast path and selected from the dense slice (synchronises) */
 int spardl_dense_fallbacks(spardl_ctx* ctx, int64_t* count);
 /* diagnostics of local dividing task i (= local_worker * m + block):
- * [resolved mode, candidate flags, candidate total, list length, pre-key, capacity] */
-int spardl_div_diag(spardl_ctx* ctx, int32_t task, int64_t* out6);
+ * [resolved mode, candidate flags, candidate total, list length, pre-key, capacity,
+ *  selection threshold key, carried next pre-key (-1: none), carried margin] */
+int spardl_div_diag(spardl_ctx* ctx, int32_t task, int64_t* out9);
 /* diagnostics: device timestamps (ns) of the phases of select `task` of
  * planner step `step` (-1: the dividing stage) in the last iteration:
  * out44[0..12) CTA 0's phase stamps, [12..28) each cluster CTA's start,

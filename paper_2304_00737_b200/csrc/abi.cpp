@@ -694,10 +694,10 @@ EXPORT int spardl_dense_fallbacks(spardl_ctx* ctx, int64_t* count) {
   });
 }
 
-EXPORT int spardl_div_diag(spardl_ctx* ctx, int32_t task, int64_t* out6) {
+EXPORT int spardl_div_diag(spardl_ctx* ctx, int32_t task, int64_t* out9) {
   return guarded([&] {
     need(ctx, "ctx");
-    ctx->eng->div_diag(task, out6);
+    ctx->eng->div_diag(task, out9);
   });
 }
 

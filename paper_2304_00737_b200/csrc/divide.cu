@@ -38,7 +38,7 @@ __device__ __forceinline__ int64_t chunk_origin(const DivTask& t) { return (int6
 __global__ void __launch_bounds__(kThreads) k_div_sample(const DivTask* __restrict__ tasks,
                                                          int apply_residual) {
   const DivTask& t = tasks[blockIdx.y];
-  if (!t.use_cand) return;
+  if (!t.use_cand || t.hist->valid) return;   // no sample needed: carried threshold
   const int c = blockIdx.x * t.sample_every;
   if (c >= t.nchunks) return;
   // 13-bit key histogram (8 exponent + 5 mantissa bits: 1/32-octave bins)
@@ -96,6 +96,14 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
   for (int q = 0; q < BPT; ++q) mine += hist[q];
   const long long ns = block_sum_ll(mine, lscr);
   const int64_t nb = (int64_t)t.hi - t.lo;
+  if (t.use_cand && t.hist->valid) {   // threshold carried from the last iteration
+    if (threadIdx.x == 0) {
+      *t.cand_total = 0;
+      *t.cand_bad = 0;
+      *t.pre_key = t.hist->next_pre;
+    }
+    return;   // the sample histogram was not touched: still zero
+  }
   if (threadIdx.x == 0) {
     *t.cand_total = 0;
     *t.cand_bad = t.use_cand ? 0 : 1;

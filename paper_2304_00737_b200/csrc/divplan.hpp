@@ -48,6 +48,7 @@ void div_plan(DivTask& dt, SelTask& t, int64_t lo, int64_t hi, int64_t budget, A
   dt.cand_bad = static_cast<int32_t*>(alloc(sizeof(int32_t)));
   dt.pre_key = static_cast<uint32_t*>(alloc(sizeof(uint32_t)));
   dt.samp_hist = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * kSampBins));
+  dt.hist = static_cast<DivHistory*>(alloc(sizeof(DivHistory)));
   // ~8 sampled chunks (65k elements) per block: ~650 expected top-L samples
   // at 1% density whatever the block size
   dt.sample_every = std::max(1, nch / 8);
@@ -64,6 +65,8 @@ void div_plan(DivTask& dt, SelTask& t, int64_t lo, int64_t hi, int64_t budget, A
   t.dn = static_cast<int32_t>(nb);
   t.cand_total = dt.cand_total;
   t.cand_bad = dt.cand_bad;
+  t.div_hist = dt.use_cand ? dt.hist : nullptr;
+  t.pre_key_dev = dt.pre_key;
   t.budget = budget;
   t.weight = 1.f;
 }

@@ -999,6 +999,7 @@ void Engine::reset_state() {
     CK(cudaMemset(ledger_total_[static_cast<size_t>(i)], 0, sizeof(int64_t)));
   }
   std::fill(rounds_.begin(), rounds_.end(), 0);
+  for (const auto& dt : div_tasks_) CK(cudaMemset(dt.hist, 0, sizeof(sdl::DivHistory)));
   if (cfg_.sag == SPARDL_SAG_BSAG) {
     std::vector<sdl::HCtl> c(static_cast<size_t>(wloc_));
     std::vector<int64_t> b(static_cast<size_t>(wloc_));
@@ -1132,6 +1133,14 @@ void Engine::div_diag(int task, int64_t* out) {
   out[3] = cnt;
   out[4] = pre;
   out[5] = dt.cap;
+  sdl::DivHistory h{};
+  CK(mcpy(&h, dt.hist, sizeof(h), cudaMemcpyDeviceToHost));
+  uint32_t T = 0;
+  CK(mcpy(&T, &div_scr_[static_cast<size_t>(li)][static_cast<size_t>(b)]->prefix, sizeof(T),
+          cudaMemcpyDeviceToHost));
+  out[6] = T;
+  out[7] = h.valid ? static_cast<int64_t>(h.next_pre) : -1;
+  out[8] = h.delta;
 }
 
 void Engine::select_timestamps(int step, int task, int64_t* out12) {

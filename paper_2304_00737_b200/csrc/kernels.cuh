@@ -25,7 +25,10 @@ namespace sdl {
 constexpr int kThreads = 256;
 constexpr int kBins = 2048;            // radix digit width of passes 0 and 1 (11 bits)
 constexpr int kMaxR = 16;              // max lists folded by one merge task
-constexpr int kChunk = 8192;           // dividing chunk (elements per CTA)
+#ifndef SPARDL_DIV_CHUNK
+#define SPARDL_DIV_CHUNK 8192
+#endif
+constexpr int kChunk = SPARDL_DIV_CHUNK;   // dividing chunk (elements per CTA)
 constexpr int kMaxSamples = 8000;      // merge splitter samples per task (< kMaxSegPerTask)
 constexpr int kTile = 256;             // select work item (entries per warp task)
 constexpr int kCl = 16;                // CTAs per select cluster (one cluster per task)
@@ -100,7 +103,8 @@ struct SelTask {
   // candidate-path verdict (dividing)
   const int64_t* cand_total;
   const int32_t* cand_bad;
-  uint32_t* cand_hist;   // nullable: pass-0 histogram built by the candidate pass
+  struct DivHistory* div_hist;   // nullable: dividing select -> next pre-threshold
+  const uint32_t* pre_key_dev;   // the pre-threshold of this run (dividing select)
   // budget
   int64_t budget;
   const int64_t* budget_dev;
@@ -148,6 +152,24 @@ struct MergeTask {
 // ---------------------------------------------------------------------------
 // Dividing
 // ---------------------------------------------------------------------------
+// Pre-threshold carried between iterations: after a successful candidate
+// run the dividing select stores next_pre = key(T' ) - delta (T: the exact
+// L-th key it found; T' = T extrapolated linearly in magnitude from the
+// previous run's threshold, for residuals that keep growing) and the next
+// iteration skips the sample.  delta is re-fitted every run from the two
+// points it observed -- (pre-threshold, candidates) and (T, L) -- so that
+// the next candidate count is ~1.5 L (a secant step in log-count over key
+// space).  A fallback to the dense path clears `valid`: the next iteration
+// samples again.  Only the amount of work depends on it, never the result.
+struct DivHistory {
+  uint32_t next_pre;
+  uint32_t delta;
+  int32_t valid;
+  uint32_t last_T;       // threshold of the previous run (valid when has_T)
+  int32_t has_T;
+  int32_t pad_;
+};
+
 struct DivTask {
   const float* const* g_tab;  // gradient pointer table (updated per call)
   int32_t g_id;            // this worker's entry in g_tab
@@ -170,7 +192,7 @@ struct DivTask {
   int32_t* cand_bad;       // bit 0: candidate path off for this run, bit 1: overflow
   uint32_t* pre_key;       // candidate threshold (key >= pre_key)
   uint32_t* samp_hist;     // [kSampBins]
-  uint32_t* cand_hist;     // [kBins] pass-0 histogram of the candidates (for the select)
+  struct DivHistory* hist;  // threshold carried over from the previous iteration
   int32_t sample_every;    // sample one chunk in `sample_every`
   int32_t use_cand;        // 0: candidate path disabled (dense select)
   int32_t* err;            // NaN flag

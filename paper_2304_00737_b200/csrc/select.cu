@@ -24,6 +24,7 @@
 //      explicitly rounded multiply (no FMA contraction, inc/residual.hpp:119).
 #include <cooperative_groups.h>
 
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -38,7 +39,10 @@ namespace {
 
 constexpr int kSelThreads = 512;   // 16 warps per CTA
 constexpr int kWarps = kSelThreads / 32;
-constexpr int kIlp = 8;   // 32-entry groups loaded per warp step (memory-level parallelism)
+#ifndef SPARDL_SEL_ILP
+#define SPARDL_SEL_ILP 8
+#endif
+constexpr int kIlp = SPARDL_SEL_ILP;   // 32-entry groups loaded per warp step (memory-level parallelism)
 constexpr int kChunkE = 32 * kIlp;   // flat entries per work chunk (one warp step)
 
 __device__ __forceinline__ int resolve_mode(const SelTask& t) {
@@ -90,6 +94,44 @@ struct RadixState {     // lives in CTA 0, read by the cluster through DSMEM
 struct CtaTotals {      // per-CTA counters exchanged through DSMEM
   long long cnt, gt, eq;
 };
+
+// Dividing select epilogue: the pre-threshold of the next iteration.
+__device__ void update_history(DivHistory* h, int mode, int all, uint32_t T, uint32_t pre,
+                               long long cand, long long budget) {
+  constexpr uint32_t kMinDelta = 1u << 12, kMaxDelta = 1u << 26;
+  constexpr double kTarget = 1.5;    // wanted candidates / L
+  if (mode != 0 || all != 0 || budget <= 0) {   // dense fallback (or trivial): sample again
+    if (h->valid) h->delta = h->delta < kMaxDelta / 2 ? h->delta * 2 : kMaxDelta;
+    h->valid = 0;
+    h->has_T = all == 0 && budget > 0;
+    h->last_T = T;
+    return;
+  }
+  // secant in (key, log count): count(pre) = cand, count(T) = budget
+  const double span = (double)(T - pre);
+  const double ratio = (double)cand / (double)budget;
+  double d;
+  if (ratio > 1.02 && span > 0) d = span * log(kTarget) / log(ratio);
+  else d = 2.0 * (span > 0 ? span : (double)kMinDelta);
+  if (h->valid) {   // at most x2 / x0.5 per run
+    const double old = (double)h->delta;
+    d = d > 2 * old ? 2 * old : (d < old / 2 ? old / 2 : d);
+  }
+  d = d < kMinDelta ? kMinDelta : (d > kMaxDelta ? kMaxDelta : d);
+  // a threshold that grows from run to run (residual accumulation) is
+  // extrapolated linearly in magnitude
+  const float tv = __uint_as_float(T), tp = __uint_as_float(h->last_T);
+  const float grown = h->has_T && tv > tp ? tv + (tv - tp) : tv;
+  const uint32_t Tn = grown < 3.0e38f ? __float_as_uint(grown) : T;
+  long long next = (long long)Tn - (long long)d;
+  h->delta = (uint32_t)d;
+  h->next_pre = next < 0 ? 0u : (uint32_t)next;
+  // the first threshold after a (re)start only seeds the trend: trust the
+  // carried pre-threshold from the second sampled run on
+  h->valid = h->has_T;
+  h->last_T = T;
+  h->has_T = 1;
+}
 
 // CTA 0: locate the digit holding the rank-th largest key in agg[0..nb).
 __device__ void find_digit(uint32_t* agg, int nb, int shift, RadixState* st, long long* suf) {
@@ -494,6 +536,14 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     sc->all = all;
     sc->mode = mode;
     sc->total = my.total;
+    if (all == 1 && mode == 0 && t.mode_from_cand) {
+      // exactly L candidates, all kept: the selection is {key >= pre-threshold},
+      // not the whole block
+      sc->all = 0;
+      sc->prefix = *t.pre_key_dev;
+      sc->cut_idx = INT_MAX;
+    }
+    if (t.div_hist) update_history(t.div_hist, mode, all, T, *t.pre_key_dev, total, budget);
   }
   stamp(11);
   cluster.sync();   // keep CTA 0's shared memory alive until every reader is done

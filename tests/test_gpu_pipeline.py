@@ -35,7 +35,7 @@ def configs():
     return out
 
 
-def _run(env, P, d, sag, residual, timing, kind, N, k, iters, seed, graph=True):
+def _run(env, P, d, sag, residual, timing, kind, N, k, iters, seed, graph=True, scales=None):
     sd, orc, torch = env
     from pyoracle import make_config
     cfg = sd.ClusterConfig(workers=P, dimension=N, k=k, teams=d, sag=sag, residual=residual,
@@ -45,6 +45,8 @@ def _run(env, P, d, sag, residual, timing, kind, N, k, iters, seed, graph=True):
     rng = np.random.default_rng(seed)
     for it in range(iters):
         g = gen(kind, (P, N), rng)
+        if scales is not None:
+            g = (g * np.float32(scales[it])).astype(np.float32)
         dev = [torch.from_numpy(g[w]).cuda() for w in range(P)]
         ctx.all_reduce(dev)
         info = ctx.run_info()
@@ -100,6 +102,14 @@ def test_pipeline_modes(env, residual, timing, P, d, sag):
 def test_pipeline_medium(env, P, d, sag, N, dens):
     k = P * max(1, int(N * dens) // P)
     _run(env, P, d, sag, "gres", "optimized", "gauss", N, k, iters=3, seed=5)
+
+
+def test_pipeline_distribution_shift(env):
+    """The dividing pre-threshold carried between iterations (DivHistory) is
+    only a work estimate: abrupt scale changes must still give exact results
+    (through the dense fallback when the carried threshold is off)."""
+    _run(env, 8, 1, "none", "gres", "optimized", "gauss", 1_000_000, 10_000, iters=6, seed=9,
+         scales=[1.0, 1e3, 1e-3, 1.0, 1e-6, 1e6])
 
 
 def test_pipeline_no_graph(env):
