@@ -310,7 +310,7 @@ EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* c
       mt.in_cnt[q] = cnts + q;
     }
     int64_t T = std::max<int64_t>(2048 / r, (capsum + sdl::kMaxSamples - 1) / sdl::kMaxSamples);
-    T = std::max<int64_t>(T, 32);
+    T = (std::max<int64_t>(T, 32) + 3) & ~int64_t(3);
     if (static_cast<int64_t>(r) * T > 12800)
       sdlh::fail(SPARDL_E_UNSUPPORTED, "merge of this size exceeds the shared-memory envelope");
     mt.T = static_cast<int32_t>(T);

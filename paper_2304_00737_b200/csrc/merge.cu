@@ -24,6 +24,12 @@ namespace sdl {
 
 namespace {
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const size_t ga = __cvta_generic_to_global(gmem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(ga) : "memory");
+}
+
 // Rank all samples of a task; write the sorted splitters and, for each
 // splitter, the window of every list that can hold its partition.
 __global__ void __launch_bounds__(kThreads) k_merge_rank(const MergeTask* __restrict__ tasks) {
@@ -120,14 +126,25 @@ __global__ void __launch_bounds__(kThreads) k_merge_part(const MergeTask* __rest
     }
   }
   __syncthreads();
+  // stage the windows with asynchronous 16-byte copies: every thread issues
+  // all of its copies before waiting once (16-byte aligned windows: block
+  // buffers are, and T % 4 == 0); the < 4-entry tail and unaligned lists
+  // (component API inputs) are copied with plain loads
   for (int l = 0; l < r; ++l) {
     const int32_t* gi = t.in_idx[l] + wstart[l];
     const float* gv = t.in_val[l] + wstart[l];
-    for (int j = threadIdx.x; j < wlen[l]; j += blockDim.x) {
+    const bool al = ((reinterpret_cast<uintptr_t>(gi) | reinterpret_cast<uintptr_t>(gv)) & 15) == 0;
+    const int n4 = al ? (wlen[l] >> 2) : 0;
+    for (int j = threadIdx.x; j < n4; j += blockDim.x) {
+      cp_async16(w_idx + l * T + 4 * j, gi + 4 * j);
+      cp_async16(w_val + l * T + 4 * j, gv + 4 * j);
+    }
+    for (int j = 4 * n4 + threadIdx.x; j < wlen[l]; j += blockDim.x) {
       w_idx[l * T + j] = gi[j];
       w_val[l * T + j] = gv[j];
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (threadIdx.x < r) {
     const int l = threadIdx.x;
