@@ -99,6 +99,9 @@ __device__ __forceinline__ int warp_bound(const int32_t* a, int n, int32_t x, bo
 constexpr int kFinChunk = 1024;              // global entries per CTA
 constexpr int kFinPer = kFinChunk / kThreads;
 
+constexpr int kXiBatch = 4;                  // discard entries per thread per batch
+constexpr int kMaxXiLists = kThreads / 64;   // bound searches in parallel (2 warps each)
+
 __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __restrict__ tasks) {
   const FinalizeTask& t = tasks[blockIdx.z];
   if (t.mode == 2) return;   // lres ignores the global gradient
@@ -109,69 +112,108 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __res
   if (c0 >= gn) return;
   const int nloc = min(kFinChunk, gn - c0);
   const int tid = threadIdx.x;
+  float* __restrict__ carry = t.carry;
   if (t.mode == 1) {   // pres: zero at the global indices
-    for (int e = tid; e < nloc; e += kThreads) t.carry[G.idx[c0 + e]] = 0.f;
+    for (int e = tid; e < nloc; e += kThreads) carry[G.idx[c0 + e]] = 0.f;
     return;
   }
   __shared__ int32_t gi[kFinChunk];
   __shared__ float sv[kFinChunk];
   __shared__ unsigned char sf[kFinChunk];
-  __shared__ int range[2];
+  __shared__ int range[2 * kMaxXiLists];
+  // dividing-select state, read once
   const SelScratch* dsc = t.div_sc[b];
+  const int d_all = dsc->all;
+  const uint32_t d_pre = dsc->prefix;
+  const int32_t d_cut = dsc->cut_idx;
+  auto div_member = [&](uint32_t key, int32_t j) {
+    if (d_all == 1) return true;
+    if (d_all == 2) return false;
+    return key > d_pre || (key == d_pre && j <= d_cut);
+  };
+  // global indices of the chunk, then the combined values (two rounds of
+  // independent loads)
+  int32_t jj[kFinPer];
+  float x[kFinPer];
+#pragma unroll
+  for (int q = 0; q < kFinPer; ++q) {
+    const int e = tid + q * kThreads;
+    jj[q] = e < nloc ? G.idx[c0 + e] : INT_MAX;
+  }
+#pragma unroll
+  for (int q = 0; q < kFinPer; ++q) x[q] = jj[q] != INT_MAX ? carry[jj[q]] : 0.f;
   float acc[kFinPer];
   bool present[kFinPer];
 #pragma unroll
   for (int q = 0; q < kFinPer; ++q) {
-    const int e = tid + q * kThreads;
-    const bool valid = e < nloc;
-    const int32_t j = valid ? G.idx[c0 + e] : INT_MAX;
-    gi[e] = j;
-    acc[q] = 0.f;
-    present[q] = false;
-    if (valid) {
-      const float x = t.carry[j];   // combined == g_copy, in place
-      present[q] = !sel_member(dsc, mag_key(x), j);
-      acc[q] = present[q] ? x : 0.f;
-    }
+    gi[tid + q * kThreads] = jj[q];
+    present[q] = jj[q] != INT_MAX && !div_member(mag_key(x[q]), jj[q]);
+    acc[q] = present[q] ? x[q] : 0.f;
   }
   __syncthreads();
   const int32_t jlo = gi[0], jhi = gi[nloc - 1];
-  for (int xq = t.xi_off[b]; xq < t.xi_off[b + 1]; ++xq) {
-    const XiList X = t.xi[xq];
-    const int xn = *X.cnt;
-    if (tid < 32) {
-      const int r = warp_bound(X.idx, xn, jlo, false);
-      if (tid == 0) range[0] = r;
-    } else if (tid < 64) {
-      const int r = warp_bound(X.idx, xn, jhi, true);
-      if (tid == 32) range[1] = r;
+  const int x0 = t.xi_off[b], x1 = t.xi_off[b + 1];
+  for (int xb = x0; xb < x1; xb += kMaxXiLists) {
+    const int nx = min(kMaxXiLists, x1 - xb);
+    // the sub-range of each discard list inside [jlo, jhi], in parallel
+    {
+      const int warp = tid >> 5, li = warp >> 1;
+      if (li < nx) {
+        const XiList X = t.xi[xb + li];
+        const int xn = *X.cnt;
+        const bool upper = warp & 1;
+        const int r = warp_bound(X.idx, xn, upper ? jhi : jlo, upper);
+        if ((tid & 31) == 0) range[warp] = r;
+      }
     }
 #pragma unroll
     for (int q = 0; q < kFinPer; ++q) sf[tid + q * kThreads] = 0;
     __syncthreads();
-    for (int p = range[0] + tid; p < range[1]; p += kThreads) {
-      const int32_t xi = X.idx[p];
-      const int pos = lower_bound_i32(gi, nloc, xi);
-      if (pos < nloc && gi[pos] == xi) {
-        sv[pos] = X.val[p];
-        sf[pos] = 1;
-      }
-    }
-    __syncthreads();
+    for (int li = 0; li < nx; ++li) {   // fold in recording order
+      const XiList X = t.xi[xb + li];
+      const int r0 = range[2 * li], r1 = range[2 * li + 1];
+      for (int p0 = r0; p0 < r1; p0 += kThreads * kXiBatch) {
+        int32_t xi[kXiBatch];
+        int pos[kXiBatch];
 #pragma unroll
-    for (int q = 0; q < kFinPer; ++q) {
-      const int e = tid + q * kThreads;
-      if (e < nloc && sf[e]) {
-        acc[q] = present[q] ? __fadd_rn(acc[q], sv[e]) : sv[e];
-        present[q] = true;
+        for (int u = 0; u < kXiBatch; ++u) {
+          const int p = p0 + u * kThreads + tid;
+          xi[u] = p < r1 ? X.idx[p] : INT_MIN;
+        }
+        float xv[kXiBatch];
+#pragma unroll
+        for (int u = 0; u < kXiBatch; ++u) {
+          pos[u] = -1;
+          if (xi[u] != INT_MIN) {
+            const int ps = lower_bound_i32(gi, nloc, xi[u]);
+            if (ps < nloc && gi[ps] == xi[u]) pos[u] = ps;
+          }
+          xv[u] = pos[u] >= 0 ? X.val[p0 + u * kThreads + tid] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < kXiBatch; ++u)
+          if (pos[u] >= 0) {
+            sv[pos[u]] = xv[u];
+            sf[pos[u]] = 1;
+          }
       }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kFinPer; ++q) {
+        const int e = tid + q * kThreads;
+        if (e < nloc && sf[e]) {
+          acc[q] = present[q] ? __fadd_rn(acc[q], sv[e]) : sv[e];
+          present[q] = true;
+          sf[e] = 0;
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int q = 0; q < kFinPer; ++q) {
     const int e = tid + q * kThreads;
-    if (e < nloc) t.carry[gi[e]] = present[q] ? acc[q] : 0.f;
+    if (e < nloc) carry[gi[e]] = present[q] ? acc[q] : 0.f;
   }
 }
 
