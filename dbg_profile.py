@@ -11,7 +11,7 @@ for i in range(P):
     grads.append(torch.randn(N, device='cuda', generator=gen))
 for it in range(5):
     ctx.all_reduce(grads); ctx.sync()
-out = (C.c_int64 * 44)()
+out = (C.c_int64 * 52)()
 names = ['p1','p0h','p0s','p0f','p1h','p1s','p1f','p2h','p2s','p2f','cnt+scan','write']
 for step in (-1, 0, 1, 2, 3):
     for task in (0,):
@@ -42,3 +42,9 @@ for step in (-1, 1, 2, 3):
     starts = [round((x - t0) / 1000, 1) for x in ts[12:28] if x]
     ends = [round((x - t0) / 1000, 1) for x in ts[28:44] if x]
     print('step', step, 'cta starts', starts, 'hist0 ends', ends)
+
+for step in (1, 2, 3):
+    rc = lib().spardl_debug_select_timestamps(ctx._h, step, 0, out)
+    if rc: continue
+    ts = list(out); t0 = ts[0]
+    print('step', step, 'prologue', [round((x - t0) / 1000, 1) for x in ts[44:51]])

@@ -79,12 +79,13 @@ void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf) {
     sdlh::fail(SPARDL_E_UNSUPPORTED, "selection larger than the device work-item bound");
   t.scr = buf.get<sdl::SelScratch>(1);
   const int nck = std::max(1, sdl::sel_chunk_capacity(t));
-  int32_t* segs = buf.get<int32_t>(5 * static_cast<size_t>(nck));
+  int32_t* segs = buf.get<int32_t>(6 * static_cast<size_t>(nck));
   t.seg_gt = segs;
   t.seg_eq = segs + nck;
   t.seg_sel_off = segs + 2 * nck;
   t.seg_dis_off = segs + 3 * nck;
   t.seg_take = segs + 4 * nck;
+  t.seg_valid = segs + 5 * nck;
   sdl::SelTask* td = buf.get<sdl::SelTask>(1);
   CK(cudaMemcpyAsync(td, &t, sizeof(t), cudaMemcpyHostToDevice, s));
   sdl::launch_select(td, 1, std::max(1, sdl::sel_scratch_segments(t)), s);

@@ -241,12 +241,13 @@ void Engine::add_select(Stage& st, const sdl::SelTask& t0) {
     sdlh::fail(SPARDL_E_UNSUPPORTED, "selection larger than the device work-item bound");
   t.scr = static_cast<sdl::SelScratch*>(arena_.alloc(sizeof(sdl::SelScratch)));
   const int nck = std::max(1, sdl::sel_chunk_capacity(t));
-  int32_t* segs = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * 5 * nck));
+  int32_t* segs = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * 6 * nck));
   t.seg_gt = segs;
   t.seg_eq = segs + nck;
   t.seg_sel_off = segs + 2 * nck;
   t.seg_dis_off = segs + 3 * nck;
   t.seg_take = segs + 4 * nck;
+  t.seg_valid = segs + 5 * nck;
   // the select's per-CTA segment table is sized for a whole task's segments
   st.max_nseg = std::max(st.max_nseg, sdl::sel_scratch_segments(t));
   st.sels.push_back(t);
@@ -295,6 +296,7 @@ sdl::SelTask Engine::select_from_merge(Stage& st, const std::vector<int>& pieces
   mt.seg_off = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * parts));
   mt.seg_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * parts));
   st.merges.push_back(mt);
+  st.merge_cap.push_back(capsum);
   st.max_parts = std::max<int>(st.max_parts, static_cast<int>(parts));
   st.max_rT = std::max<int>(st.max_rT, static_cast<int>(r * T));
 
@@ -307,6 +309,7 @@ sdl::SelTask Engine::select_from_merge(Stage& st, const std::vector<int>& pieces
   t.nseg = static_cast<int32_t>(parts);
   t.stride = static_cast<int32_t>(r * T);   // longest partition (offsets come from seg_off)
   t.weight = 1.f;
+  t.merge_slot = static_cast<int32_t>(st.merges.size());
   return t;
 }
 
@@ -373,14 +376,52 @@ void Engine::transfer(std::vector<Xfer>& xs, int uid, int src, int dst, int phas
   }
 }
 
+// Fused merge+select for a stage: the widest cluster whose per-CTA window
+// fits shared memory and whose clusters are all resident at once.
+void Engine::plan_fused(Stage& st) {
+  // opt-in: on B200 the separate merge kernels (every SM busy) beat the
+  // fused prologue (one cluster per task) -- see DESIGN.md
+  const char* env = std::getenv("SPARDL_FUSED_MERGE");
+  if (dry_ || st.merges.empty() || !env || std::strcmp(env, "1") != 0) return;
+  int64_t capmax = 0;
+  int rmax = 0, tab = 1;
+  for (size_t i = 0; i < st.merges.size(); ++i) {
+    capmax = std::max(capmax, st.merge_cap[i]);
+    rmax = std::max(rmax, static_cast<int>(st.merges[i].r));
+  }
+  for (const auto& t : st.sels)
+    if (!t.merge_slot) tab = std::max(tab, sdl::sel_scratch_segments(t));
+  const int64_t Ts = (std::max<int64_t>(32, (capmax + sdl::kMergeSamples - 1) / sdl::kMergeSamples) + 3) & ~int64_t(3);
+  const int maxwin = sdl::select_max_window();
+  const int ntask = static_cast<int>(st.sels.size());
+  for (int cl : {16, 8, 4, 2}) {
+    const int64_t win = (capmax + cl - 1) / cl + (2 * rmax + 2) * Ts;
+    if (win > maxwin) continue;
+    if (sdl::select_resident_clusters(cl, tab, static_cast<int>(win)) < ntask) continue;
+    st.fused = true;
+    st.cl = cl;
+    st.win_cap = static_cast<int>(win);
+    st.max_nseg = tab;
+    for (auto& mt : st.merges) mt.T = static_cast<int32_t>(Ts);
+    return;
+  }
+}
+
 void Engine::finish_stage(Stage& st) {
+  plan_fused(st);
   if (!st.merges.empty()) {
     st.merges_dev = static_cast<sdl::MergeTask*>(
         arena_.alloc(sizeof(sdl::MergeTask) * st.merges.size()));
     CK(mcpy(st.merges_dev, st.merges.data(), sizeof(sdl::MergeTask) * st.merges.size(),
                   cudaMemcpyHostToDevice));
-    launches_ += 2;
+    if (!st.fused) launches_ += 2;
   }
+  if (st.fused)
+    for (auto& t : st.sels)
+      if (t.merge_slot) {
+        t.merge = st.merges_dev + (t.merge_slot - 1);
+        t.nseg = 1;
+      }
   if (!st.sels.empty()) {
     st.sels_dev =
         static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));
@@ -837,11 +878,12 @@ void Engine::plan_peer() {
 // execution
 int Engine::exec_stage(const Stage& st) {
   int n = 0;
-  if (!st.merges.empty())
+  if (!st.merges.empty() && !st.fused)
     n += sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts,
                            st.max_rT, stream_);
   if (!st.sels.empty())
-    n += sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_);
+    n += sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_,
+                            st.fused ? st.cl : 0, st.fused ? st.win_cap : 0);
   return n;
 }
 
@@ -1147,7 +1189,7 @@ void Engine::select_timestamps(int step, int task, int64_t* out12) {
   sync();
   const Stage& st = step < 0 ? div_stage_ : steps_.at(static_cast<size_t>(step)).stage;
   const sdl::SelScratch* sc = st.sels.at(static_cast<size_t>(task)).scr;
-  CK(mcpy(out12, sc->tstamp, sizeof(long long) * 44, cudaMemcpyDeviceToHost));
+  CK(mcpy(out12, sc->tstamp, sizeof(long long) * 52, cudaMemcpyDeviceToHost));
 }
 
 int64_t Engine::dense_fallbacks() {

@@ -69,6 +69,10 @@ struct Stage {           // one batch of merge + select tasks
   int max_rT = 0;
   int max_nseg = 0;
   std::set<int> produced;    // uids written by this stage (dependency guard)
+  std::vector<int64_t> merge_cap;   // input capacity of each merge task
+  bool fused = false;        // merges run inside the select kernel (no merge launches)
+  int cl = 0;                // fused: cluster width
+  int win_cap = 0;           // fused: window entries per CTA
 };
 
 struct Step {            // a stage followed by a transport round
@@ -140,6 +144,7 @@ class Engine {
   sdl::SelTask select_from_slot(const Slot& in);
   sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);
   void finish_stage(Stage& st);
+  void plan_fused(Stage& st);
   void transfer(std::vector<Xfer>& xs, int uid, int src_worker, int dst_worker, int phase,
                 std::vector<std::vector<int>>* recv_into = nullptr);
   void plan();

@@ -64,6 +64,7 @@ struct SelScratch {
   int32_t pad_;
   long long tstamp[12];  // phase timestamps (globaltimer ns) of the last run, CTA 0
   long long cta_ts[2][16];   // per CTA: start, end of the pass-0 histogram
+  long long pro_ts[8];       // CTA 0: fused-merge prologue phase ends
 };
 
 // Membership in a finished selection without searching its output:
@@ -125,7 +126,20 @@ struct SelTask {
   int32_t* seg_sel_off;
   int32_t* seg_dis_off;
   int32_t* seg_take;
+  int32_t* seg_valid;    // entries per work item that are not merge holes
+  // fused merge (nullable): the select first merges the r lists of *merge
+  // itself, each cluster CTA one index range, into merge->out_* (idx/val
+  // above), leaving a hole (kHoleKey) where equal indices were folded
+  const struct MergeTask* merge;
+  int32_t merge_slot;    // host bookkeeping: 1 + index of the stage's merge task, 0 none
+  int32_t pad3_;
 };
+
+// value bits of a merge hole: its magnitude key is kHoleKey, never a real
+// entry's (a NaN with every mantissa bit set)
+constexpr uint32_t kHoleBits = 0xffffffffu;
+constexpr uint32_t kHoleKey = 0x7fffffffu;
+constexpr int kMergeSamples = 2048;   // fused merge: splitter samples per task
 
 // ---------------------------------------------------------------------------
 // Merge
@@ -202,7 +216,12 @@ struct DivTask {
 // Launchers (stream-ordered; no host synchronisation inside)
 // ---------------------------------------------------------------------------
 // tasks_dev: device copy of the task array; ntask; max_nseg: grid extent.
-int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s);
+int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s,
+                  int cluster = 0, int win_cap = 0);
+// fused merge+select: smem window capacity (entries) available per CTA, and
+// the clusters of width cl resident at once for a launch with that window
+int select_max_window();
+int select_resident_clusters(int cl, int tab_cap, int win_cap);
 int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T,
                   cudaStream_t s);
 // part: 0 = whole pass, 1 = sample + pre-threshold only, 2 = candidate pass only

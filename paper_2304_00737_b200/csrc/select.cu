@@ -24,6 +24,7 @@
 //      explicitly rounded multiply (no FMA contraction, inc/residual.hpp:119).
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -168,12 +169,238 @@ __device__ void find_digit(uint32_t* agg, int nb, int shift, RadixState* st, lon
   for (int q = 0; q < bpt; ++q) agg[threadIdx.x * bpt + q] = 0;   // ready for the next pass
 }
 
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const size_t ga = __cvta_generic_to_global(gmem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(ga) : "memory");
+}
+
+__device__ __forceinline__ int32_t lds_i32(unsigned addr) {
+  int32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// list holding position p of a concatenation with list starts base[0..r]
+__device__ __forceinline__ int list_of(const int* base, int r, int p) {
+  int l = 0;
+  while (l + 1 < r && p >= base[l + 1]) ++l;
+  return l;
+}
+
+// Fused merge (inc/sparse.hpp:182-208 folded left over the lists, as in
+// merge.cu) of one cluster CTA's index range.  The task's lists are cut at
+// union splitter samples (every Ts-th entry of every list): CTA cr takes the
+// index range between the samples of union rank S*cr/CL and S*(cr+1)/CL, so
+// equal indices never straddle two CTAs and each CTA holds at most
+// sum/CL + (2r + 2) Ts entries.  Its windows are staged in shared memory and
+// every entry is written at its stable merged rank inside the CTA's output
+// range [sum of window starts, + window size): the first entry of an index
+// (lowest list) carries the fold in list order, later copies become holes.
+// Builds the CTA's work items and returns the task's merged total.
+template <int CL>
+__device__ long long merge_prologue(const MergeTask& mt, int cr, int32_t* w_idx, float* w_val,
+                                    int32_t* samp, int win_cap, int32_t* iof, int32_t* ilen,
+                                    int tab_cap, int& s_F, int& s_before, int& s_nit,
+                                    long long* lscr, CtaTotals* tot,
+                                    cg::cluster_group& cluster, SelScratch* sc) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto pstamp = [&](int i) {
+    if (cr == 0 && tid == 0) {
+      long long ts;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+      sc->pro_ts[i] = ts;
+    }
+  };
+  const int r = mt.r, Ts = mt.T;
+  __shared__ int ncnt[kMaxR], sb[kMaxR + 1], lo_q[kMaxR], hi_q[kMaxR], wb[kMaxR + 1];
+  __shared__ int32_t vb[2];
+  __shared__ int s_base, s_nin;
+  if (tid < r) ncnt[tid] = *mt.in_cnt[tid];
+  if (tid == 0) {
+    vb[0] = INT_MIN;
+    vb[1] = INT_MAX;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int S = 0;
+    for (int q = 0; q < r; ++q) {
+      sb[q] = S;
+      S += (ncnt[q] + Ts - 1) / Ts;
+    }
+    sb[r] = S;
+  }
+  __syncthreads();
+  const int S = sb[r];
+  pstamp(0);
+  // samples: every Ts-th index of every list
+  for (int i = tid; i < S; i += kSelThreads) {
+    const int q = list_of(sb, r, i);
+    samp[i] = mt.in_idx[q][(size_t)(i - sb[q]) * Ts];
+  }
+  __syncthreads();
+  pstamp(1);
+  // the two splitters of this CTA: samples of union rank S*cr/CL, S*(cr+1)/CL
+  // (ties ordered by list, as the merge orders equal indices)
+  const int rlo = (int)((long long)S * cr / CL), rhi = (int)((long long)S * (cr + 1) / CL);
+  for (int i = tid; i < S; i += kSelThreads) {
+    const int q = list_of(sb, r, i);
+    const int32_t v = samp[i];
+    int rank = i - sb[q];
+    for (int u = 0; u < r; ++u) {
+      if (u == q) continue;
+      const int n = sb[u + 1] - sb[u];
+      rank += u < q ? upper_bound_i32(samp + sb[u], n, v) : lower_bound_i32(samp + sb[u], n, v);
+    }
+    if (cr > 0 && rank == rlo) vb[0] = v;
+    if (rank == rhi) vb[1] = v;   // rhi == S (last CTA) matches no sample: stays +inf
+  }
+  __syncthreads();
+  pstamp(2);
+  // window bounds: lower_bound of each splitter in each list, bracketed by
+  // the list's own samples to < Ts entries (one warp per bound)
+  for (int p = warp; p < 2 * r; p += kWarps) {
+    const int q = p >> 1;
+    const int32_t v = vb[p & 1];
+    const int n = ncnt[q];
+    int pos;
+    if (v == INT_MIN) {
+      pos = 0;
+    } else if (v == INT_MAX) {
+      pos = n;
+    } else {
+      const int c = lower_bound_i32(samp + sb[q], sb[q + 1] - sb[q], v);   // samples < v
+      const int lo = c == 0 ? 0 : (c - 1) * Ts + 1;
+      const int hi = min(c * Ts, n);
+      int cnt = 0;
+      for (int j = lo + lane; j < hi; j += 32) cnt += mt.in_idx[q][j] < v;
+      pos = lo + __reduce_add_sync(0xffffffffu, cnt);
+    }
+    if (lane == 0) (p & 1 ? hi_q : lo_q)[q] = pos;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int w = 0, base = 0;
+    for (int q = 0; q < r; ++q) {
+      wb[q] = w;
+      w += max(0, hi_q[q] - lo_q[q]);
+      base += lo_q[q];
+    }
+    wb[r] = w;
+    s_base = base;
+    s_nin = min(w, win_cap);   // the planner sizes win_cap so this never clips
+  }
+  __syncthreads();
+  const int nin = s_nin, base = s_base;
+  pstamp(3);
+  // stage the windows (asynchronous copies, one wait)
+  for (int e = tid; e < nin; e += kSelThreads) {
+    const int q = list_of(wb, r, e);
+    const int j = lo_q[q] + (e - wb[q]);
+    cp_async4(w_idx + e, mt.in_idx[q] + j);
+    cp_async4(w_val + e, mt.in_val[q] + j);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  pstamp(4);
+  // stable merged rank of every entry; the head of an index (its copy in the
+  // lowest list) folds the later copies in list order.  Batches of kMB
+  // entries per thread share every binary-search step (independent loads).
+  constexpr int kMB = 8;
+  int heads = 0;
+  for (int e0 = 0; e0 < nin; e0 += kSelThreads * kMB) {
+    int32_t x[kMB];
+    int q[kMB], rank[kMB];
+    float acc[kMB];
+    bool head[kMB];
+#pragma unroll
+    for (int b = 0; b < kMB; ++b) {
+      const int e = e0 + b * kSelThreads + tid;
+      q[b] = -1;
+      x[b] = 0;
+      rank[b] = 0;
+      acc[b] = 0.f;
+      head[b] = false;
+      if (e < nin) {
+        q[b] = list_of(wb, r, e);
+        x[b] = w_idx[e];
+        acc[b] = w_val[e];
+        rank[b] = e - wb[q[b]];
+        head[b] = true;
+      }
+    }
+    for (int u = 0; u < r; ++u) {   // ascending: the fold follows list order
+      const int32_t* a = w_idx + wb[u];
+      const unsigned a_s = static_cast<unsigned>(__cvta_generic_to_shared(a));
+      const int n = wb[u + 1] - wb[u];
+      int step = 1;
+      while (step * 2 <= n) step *= 2;
+      int32_t tgt[kMB];
+      int pos[kMB];
+#pragma unroll
+      for (int b = 0; b < kMB; ++b) {
+        tgt[b] = q[b] >= 0 && u < q[b] ? x[b] + 1 : x[b];   // upper_bound == lower_bound(x + 1)
+        pos[b] = 0;
+      }
+      // branch-free steps: the kMB probes of a step are independent loads
+      for (; n > 0 && step > 0; step >>= 1) {
+        int32_t av[kMB];
+#pragma unroll
+        for (int b = 0; b < kMB; ++b) av[b] = lds_i32(a_s + 4u * (min(pos[b] + step, n) - 1));
+#pragma unroll
+        for (int b = 0; b < kMB; ++b) {
+          const int p = pos[b] + step;
+          pos[b] = (p <= n && av[b] < tgt[b]) ? p : pos[b];
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < kMB; ++b) {
+        if (q[b] < 0 || u == q[b]) continue;
+        if (u < q[b]) {
+          rank[b] += pos[b];
+          if (pos[b] > 0 && a[pos[b] - 1] == x[b]) head[b] = false;
+        } else {
+          rank[b] += pos[b];
+          if (pos[b] < n && a[pos[b]] == x[b]) acc[b] = __fadd_rn(acc[b], w_val[wb[u] + pos[b]]);
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kMB; ++b) {
+      if (q[b] < 0) continue;
+      heads += head[b];
+      mt.out_idx[base + rank[b]] = x[b];
+      mt.out_val[base + rank[b]] = head[b] ? acc[b] : __uint_as_float(kHoleBits);
+    }
+  }
+  const long long my_heads = block_sum_ll(heads, lscr);   // (syncs: outputs visible in-CTA)
+  pstamp(5);
+  // the CTA's work items: pieces of its output range
+  const int nit = min((nin + kChunkE - 1) / kChunkE, tab_cap);
+  const int plen = nit > 0 ? ((nin + nit - 1) / nit + 31) & ~31 : kChunkE;
+  for (int k = tid; k < nit; k += kSelThreads) {
+    iof[k] = base + k * plen;
+    ilen[k] = max(0, min(plen, nin - k * plen));
+  }
+  if (tid == 0) {
+    s_F = nin;
+    s_before = base / kChunkE + cr;
+    s_nit = nit;
+    cluster.map_shared_rank(tot, 0)[cr].cnt = my_heads;
+  }
+  cluster.sync();
+  pstamp(6);
+  long long total = 0;
+  for (int q = 0; q < CL; ++q) total += cluster.map_shared_rank(tot, 0)[q].cnt;
+  return total;
+}
+
 #ifndef SPARDL_SEL_MINB
 #define SPARDL_SEL_MINB 1
 #endif
-template <int CL>
+template <int CL, bool FUSED>
 __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
-    k_select(const SelTask* __restrict__ tasks, int tab_cap) {
+    k_select(const SelTask* __restrict__ tasks, int tab_cap, int win_cap) {
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank();
   const SelTask t = tasks[blockIdx.y];   // by value: fields live in registers, not re-read
@@ -194,6 +421,10 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   extern __shared__ int32_t dyn[];
   int32_t* iof = dyn;
   int32_t* ilen = dyn + tab_cap;
+  // fused merge: the CTA's input windows and the task's splitter samples
+  int32_t* w_idx = dyn + 2 * tab_cap;
+  float* w_val = reinterpret_cast<float*>(w_idx + win_cap);
+  int32_t* samp = reinterpret_cast<int32_t*>(w_val + win_cap);
 
   RadixState* st0 = cluster.map_shared_rank(&st, 0);
   uint32_t* agg0 = cluster.map_shared_rank(agg, 0);
@@ -218,11 +449,16 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     }
   };
   cta_stamp(0);
+  __shared__ int s_lo, s_hi, s_F, s_before;
+  __shared__ int s_nit, s_plen;
+  long long total = 0;
+  if (FUSED && t.merge) {
+    total = merge_prologue<CL>(*t.merge, cr, w_idx, w_val, samp, win_cap, iof, ilen, tab_cap,
+                               s_F, s_before, s_nit, lscr, tot, cluster, sc);
+  } else {
   // ---- 1. totals and an entry-balanced split of the segments over the
   // cluster: every CTA scans all segment lengths (cheap: <= 8192 counts) and
   // owns the segments whose first entry falls in its 1/CL of the entries.
-  __shared__ int s_lo, s_hi, s_F, s_before;
-  long long total = 0;
   {
     // pass A: the total
     long long part = 0;
@@ -258,7 +494,6 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   const int nloc = s1 - s0;
   // ---- 1b. the work items of this CTA; its per-item scratch starts at
   // s0 + (entries before it) / kChunkE + cr (disjoint across the cluster)
-  __shared__ int s_nit, s_plen;
   {
     long long before = 0, here = 0;
     for (int s = threadIdx.x; s < s1; s += kSelThreads) {
@@ -293,6 +528,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       s_before = s0 + (int)(before / kChunkE) + cr;
     }
   }
+  }
   for (int b = threadIdx.x; b < kBins; b += kSelThreads) agg[b] = 0;
   const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
   if (cr == 0 && threadIdx.x == 0) {
@@ -323,6 +559,12 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   int* c_dis = t.seg_dis_off + s_before;
   const float* __restrict__ vbase = mode == 1 ? t.dval : t.val;
   const int32_t* __restrict__ ibase = mode == 1 ? nullptr : t.idx;
+  int* c_val = t.seg_valid + s_before;
+  // merged inputs were written by this kernel: read them through L2 (the
+  // read-only path is only for data that is constant during the kernel)
+  const bool merged = FUSED && t.merge != nullptr;
+  auto ldv = [&](const float* p) { return FUSED ? __ldcg(p) : __ldg(p); };
+  auto ldi = [&](const int32_t* p) { return FUSED ? __ldcg(p) : __ldg(p); };
 
   // ---- 2. radix passes: warp w histograms chunks w, w + kWarps, ...
   if (my.all == 0) {
@@ -341,12 +583,12 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
 #pragma unroll
           for (int u = 0; u < kIlp; ++u) {   // all loads in flight first
             const int j = j0 + u * 32 + lane;
-            key[u] = j < c ? mag_key(__ldg(vp + j)) : 0u;
+            key[u] = j < c ? mag_key(ldv(vp + j)) : kHoleKey;
           }
 #pragma unroll
           for (int u = 0; u < kIlp; ++u) {
-            const int j = j0 + u * 32 + lane;
-            hist_add(hist, (key[u] >> shift) & (nb - 1), j < c && (key[u] & pmask) == prefix);
+            hist_add(hist, (key[u] >> shift) & (nb - 1),
+                     key[u] != kHoleKey && (key[u] & pmask) == prefix);
           }
         }
       }
@@ -378,42 +620,53 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   const uint32_t T = my.prefix;
   const int64_t need_eq = all == 0 ? my.rank : 0;
 
-  // ---- 3. per-chunk counts, offsets
-  long long g_loc = 0, e_loc = 0;
+  // ---- 3. per-item counts (entries above T, equal to T, not holes), offsets
+  long long g_loc = 0, e_loc = 0, v_loc = 0;
   for (int k = warp; k < nit; k += kWarps) {
     const int c = ilen[k];
-    int gt = 0, eq = 0;
-    if (all == 1) {
-      gt = c;
-    } else if (all == 0) {
+    int gt = 0, eq = 0, nv = c;
+    if (all == 0 || merged) {
       const float* __restrict__ vp = vbase + iof[k];
+      nv = 0;
       for (int j0 = 0; j0 < c; j0 += kChunkE) {
         uint32_t key[kIlp];
 #pragma unroll
         for (int u = 0; u < kIlp; ++u) {
           const int j = j0 + u * 32 + lane;
-          key[u] = j < c ? mag_key(__ldg(vp + j)) : 0u;
+          key[u] = j < c ? mag_key(ldv(vp + j)) : kHoleKey;
         }
 #pragma unroll
         for (int u = 0; u < kIlp; ++u) {
-          const bool in = j0 + u * 32 + lane < c;
+          const bool in = key[u] != kHoleKey;
+          nv += in;
           gt += in && key[u] > T;
           eq += in && key[u] == T;
         }
       }
+      nv = __reduce_add_sync(0xffffffffu, nv);
       gt = __reduce_add_sync(0xffffffffu, gt);
       eq = __reduce_add_sync(0xffffffffu, eq);
+    }
+    if (all == 1) {
+      gt = nv;
+      eq = 0;
+    } else if (all == 2) {
+      gt = 0;
+      eq = 0;
     }
     if (lane == 0) {
       c_gt[k] = gt;
       c_eq[k] = eq;
+      c_val[k] = nv;
       g_loc += gt;
       e_loc += eq;
+      v_loc += nv;
     }
   }
   g_loc = block_sum_ll(g_loc, lscr);
   e_loc = block_sum_ll(e_loc, lscr);
-  if (threadIdx.x == 0) tot0[cr] = {(long long)s_F, g_loc, e_loc};
+  v_loc = block_sum_ll(v_loc, lscr);
+  if (threadIdx.x == 0) tot0[cr] = {v_loc, g_loc, e_loc};
   cluster.sync();
   __shared__ long long base_eq, base_sel, base_cnt, all_sel, all_cnt;
   if (threadIdx.x == 0) {
@@ -446,7 +699,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       if (k < nit) {
         gt = c_gt[k];
         eq = c_eq[k];
-        c = ilen[k];
+        c = c_val[k];
       }
       int teq, tsel, tcnt;
       const int eq_before = eq_carry + block_exscan(eq, scratch, &teq);
@@ -476,7 +729,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   for (int k = warp; k < nit; k += kWarps) {
     const int c = ilen[k], e0 = iof[k];
     const int sel_base = c_sel[k], dis_base = c_dis[k], take = c_take[k];
-    int eq_seen = 0, sel_seen = 0;
+    int eq_seen = 0, sel_seen = 0, val_seen = 0;
     const float* __restrict__ vp = vbase + e0;
     const int32_t* __restrict__ ip = ibase ? ibase + e0 : nullptr;
     const int32_t ib = t.dbase + e0;
@@ -486,16 +739,15 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
 #pragma unroll
       for (int u = 0; u < kIlp; ++u) {   // all loads in flight first
         const int j = j00 + u * 32 + lane;
-        vv[u] = j < c ? __ldg(vp + j) : 0.f;
-        iv[u] = j < c ? (ip ? __ldg(ip + j) : ib + j) : 0;
+        vv[u] = j < c ? ldv(vp + j) : __uint_as_float(kHoleBits);
+        iv[u] = j < c ? (ip ? ldi(ip + j) : ib + j) : 0;
       }
 #pragma unroll
       for (int u = 0; u < kIlp; ++u) {
-        const int j = j00 + u * 32 + lane;
-        const bool valid = j < c;
         const float v = vv[u];
         const int32_t ix = iv[u];
         const uint32_t key = mag_key(v);
+        const bool valid = key != kHoleKey;
         bool is_sel;
         if (all == 1) {
           is_sel = valid;
@@ -510,13 +762,16 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
           if (is_sel && is_eq) cut = max(cut, ix);
         }
         const uint32_t bs = __ballot_sync(0xffffffffu, is_sel);
+        const uint32_t bv = __ballot_sync(0xffffffffu, valid);
         const int sel_rank = sel_seen + __popc(bs & lt);
+        const int val_rank = val_seen + __popc(bv & lt);
         sel_seen += __popc(bs);
+        val_seen += __popc(bv);
         if (is_sel) {
           t.sel_idx[sel_base + sel_rank] = ix;
           t.sel_val[sel_base + sel_rank] = v;
         } else if (valid && want_dis) {
-          const int p = dis_base + (j - sel_rank);
+          const int p = dis_base + (val_rank - sel_rank);
           t.dis_idx[p] = ix;
           t.dis_val[p] = __fmul_rn(v, w);
         }
@@ -587,45 +842,93 @@ cudaLaunchConfig_t cl_config(int ntask, size_t smem, cudaStream_t s, cudaLaunchA
   return lc;
 }
 
-size_t table_bytes(int tab_cap) { return sizeof(int32_t) * 2 * static_cast<size_t>(tab_cap); }
+size_t dyn_bytes(int tab_cap, int win_cap) {
+  size_t b = sizeof(int32_t) * 2 * static_cast<size_t>(tab_cap);
+  if (win_cap > 0) b += 8 * static_cast<size_t>(win_cap) + sizeof(int32_t) * (kMergeSamples + kMaxR);
+  return b;
+}
+
+int optin_smem() {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return optin;
+}
+
+template <int CL, bool F>
+int configure() {   // returns the dynamic shared memory this instantiation may use
+  static int maxdyn = -1;
+  if (maxdyn < 0) {   // 16 is a non-portable cluster size on sm_100
+    cudaFuncSetAttribute(k_select<CL, F>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_select<CL, F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_select<CL, F>);
+    maxdyn = optin_smem() - (int)fa.sharedSizeBytes;
+    if (cudaFuncSetAttribute(k_select<CL, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             maxdyn) != cudaSuccess) {
+      cudaGetLastError();
+      maxdyn = 48 * 1024 - (int)fa.sharedSizeBytes;
+    }
+  }
+  return maxdyn;
+}
+
+// dynamic shared memory every instantiation may use
+int max_dyn_smem() {
+  const int a = std::min(configure<16, true>(), configure<8, true>());
+  const int b = std::min(configure<4, true>(), configure<2, true>());
+  const int c = std::min(configure<16, false>(), configure<8, false>());
+  const int d = std::min(configure<4, false>(), configure<2, false>());
+  return std::min(std::min(a, b), std::min(c, d));
+}
 
 // clusters of width CL that can be resident at once on this device (a
 // cluster must fit in one GPC, so wide clusters leave SMs unused)
-template <int CL>
+template <int CL, bool F>
 int max_clusters(size_t smem) {
-  static bool configured = false;
+  configure<CL, F>();
   static size_t last_smem = ~size_t(0);
   static int n = 0;
-  if (!configured) {   // 16 is a non-portable cluster size on sm_100
-    cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(k_select<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)table_bytes(kMaxSegPerTask));
-    configured = true;
-  }
   if (smem != last_smem) {
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t lc = cl_config<CL>(1, smem, nullptr, attr);
     int c = 0;
-    if (cudaOccupancyMaxActiveClusters(&c, k_select<CL>, &lc) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&c, k_select<CL, F>, &lc) != cudaSuccess) {
       cudaGetLastError();
       c = 0;
     }
     n = c;
     last_smem = smem;
     if (getenv("SPARDL_DEBUG"))
-      fprintf(stderr, "k_select<%d>: %d resident clusters (%zu B tables)\n", CL, n, smem);
+      fprintf(stderr, "k_select<%d,%d>: %d resident clusters (%zu B dynamic smem)\n", CL, (int)F,
+              n, smem);
   }
   return n;
 }
 
-template <int CL>
-void launch_cl(const SelTask* tasks_dev, int ntask, int tab_cap, cudaStream_t s) {
-  const size_t smem = table_bytes(tab_cap);
-  max_clusters<CL>(smem);
+template <bool F>
+int clusters_for(int cl, size_t smem) {
+  if (cl >= 16) return max_clusters<16, F>(smem);
+  if (cl >= 8) return max_clusters<8, F>(smem);
+  if (cl >= 4) return max_clusters<4, F>(smem);
+  return max_clusters<2, F>(smem);
+}
+
+template <int CL, bool F>
+void launch_cl(const SelTask* tasks_dev, int ntask, int tab_cap, int win_cap, cudaStream_t s) {
+  const size_t smem = dyn_bytes(tab_cap, win_cap);
+  configure<CL, F>();
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t lc = cl_config<CL>(ntask, smem, s, attr);
-  cudaLaunchKernelEx(&lc, k_select<CL>, tasks_dev, tab_cap);
+  cudaLaunchKernelEx(&lc, k_select<CL, F>, tasks_dev, tab_cap, win_cap);
+}
+
+template <bool F>
+void launch_w(int cl, const SelTask* tasks_dev, int ntask, int tab_cap, int win_cap, cudaStream_t s) {
+  if (cl >= 16) launch_cl<16, F>(tasks_dev, ntask, tab_cap, win_cap, s);
+  else if (cl >= 8) launch_cl<8, F>(tasks_dev, ntask, tab_cap, win_cap, s);
+  else if (cl >= 4) launch_cl<4, F>(tasks_dev, ntask, tab_cap, win_cap, s);
+  else launch_cl<2, F>(tasks_dev, ntask, tab_cap, win_cap, s);
 }
 
 int forced_cl() {
@@ -636,6 +939,8 @@ int forced_cl() {
   }
   return f;
 }
+
+int table_cap(int max_nseg) { return max_nseg < 2048 ? 2048 : max_nseg; }
 }  // namespace
 
 int sel_chunk_capacity(const SelTask& t) {
@@ -645,29 +950,38 @@ int sel_chunk_capacity(const SelTask& t) {
   return ns + (int)((mx + kChunkE - 1) / kChunkE) + kCl + 2;
 }
 
-int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s) {
+int select_max_window() {
+  const int avail = max_dyn_smem() - (int)dyn_bytes(table_cap(1), 0) -
+                    (int)(sizeof(int32_t) * (kMergeSamples + kMaxR)) - 1024;
+  return avail > 0 ? avail / 8 : 0;
+}
+
+int select_resident_clusters(int cl, int tab_cap, int win_cap) {
+  return clusters_for<true>(cl, dyn_bytes(table_cap(tab_cap), win_cap));
+}
+
+int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s, int cluster,
+                  int win_cap) {
   if (ntask <= 0) return 0;
   // item table: at least 2048 entries so long inputs split into short pieces
-  const int tab_cap = max_nseg < 2048 ? 2048 : max_nseg;
-  const size_t smem = table_bytes(tab_cap);
+  const int tab_cap = table_cap(max_nseg);
+  const size_t smem = dyn_bytes(tab_cap, win_cap);
   // the widest cluster for which every task's cluster is resident in one
   // wave (a second wave would double the latency of the whole batch)
-  int cl = forced_cl();
+  int cl = cluster > 0 ? cluster : forced_cl();
   if (cl == 0) {
-    if (max_clusters<16>(smem) >= ntask) cl = 16;
-    else if (max_clusters<8>(smem) >= ntask) cl = 8;
-    else if (max_clusters<4>(smem) >= ntask) cl = 4;
+    if (clusters_for<false>(16, smem) >= ntask) cl = 16;
+    else if (clusters_for<false>(8, smem) >= ntask) cl = 8;
+    else if (clusters_for<false>(4, smem) >= ntask) cl = 4;
     else cl = 2;
   }
   static int dbg = 0;
   if (dbg < 8 && getenv("SPARDL_DEBUG")) {
     ++dbg;
-    fprintf(stderr, "select batch: %d tasks -> cluster %d\n", ntask, cl);
+    fprintf(stderr, "select batch: %d tasks -> cluster %d (window %d)\n", ntask, cl, win_cap);
   }
-  if (cl >= 16) launch_cl<16>(tasks_dev, ntask, tab_cap, s);
-  else if (cl >= 8) launch_cl<8>(tasks_dev, ntask, tab_cap, s);
-  else if (cl >= 4) launch_cl<4>(tasks_dev, ntask, tab_cap, s);
-  else launch_cl<2>(tasks_dev, ntask, tab_cap, s);
+  if (win_cap > 0) launch_w<true>(cl, tasks_dev, ntask, tab_cap, win_cap, s);
+  else launch_w<false>(cl, tasks_dev, ntask, tab_cap, win_cap, s);
   return 1;
 }
 

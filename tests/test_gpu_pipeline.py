@@ -166,3 +166,12 @@ def test_pipeline_golden_fixture(env, path):
             assert np.array_equal(ctx.carry(w).cpu().numpy().astype(np.float64), z[f"carry{it}_{w}"])
         assert [info["max_rounds"], info["max_scalars"]] == z[f"ledger{it}"].tolist()
     ctx.close()
+
+
+@pytest.mark.parametrize("P,d,sag", [(8, 1, "none"), (6, 3, "bsag"), (8, 2, "rsag")])
+def test_pipeline_fused_merge(env, P, d, sag, monkeypatch):
+    """The opt-in fused merge+select path (SPARDL_FUSED_MERGE=1, read when a
+    context is planned) gives the same bits as the two-kernel path."""
+    monkeypatch.setenv("SPARDL_FUSED_MERGE", "1")
+    _run(env, P, d, sag, "gres", "optimized", "gauss", 300_000, P * 1500, iters=3, seed=21)
+    _run(env, P, d, sag, "gres", "optimized", "int", 60_000 + P, P * 300, iters=2, seed=22)
