@@ -296,12 +296,30 @@ class SparDL:
         check(lib().spardl_ctx_stream(self._h, C.byref(s)))
         return s.value or 0
 
-    def all_reduce(self, grads) -> None:
+    def all_reduce(self, grads, order_with_torch: bool = True) -> None:
         """Enqueue one synchronisation; grads[i] is local worker i's float32
-        CUDA tensor of N elements."""
+        CUDA tensor of N elements.  With `order_with_torch` the context's
+        stream first waits for torch's current stream (the producer of the
+        gradients) and torch's current stream then waits for the
+        synchronisation, so the results can be used by the next torch op."""
         assert len(grads) == self.local_workers
         ptrs = (C.c_void_p * self.local_workers)(*[g.data_ptr() for g in grads])
-        check(lib().spardl_allreduce(self._h, ptrs))
+        if order_with_torch:
+            torch = _torch()
+            cur = torch.cuda.current_stream(self.device)
+            ext = self._ext_stream()
+            ext.wait_stream(cur)
+            check(lib().spardl_allreduce(self._h, ptrs))
+            cur.wait_stream(ext)
+        else:
+            check(lib().spardl_allreduce(self._h, ptrs))
+
+    def _ext_stream(self):
+        if getattr(self, "_ext", None) is None:
+            torch = _torch()
+            self._ext = torch.cuda.ExternalStream(self.stream_handle(),
+                                                  device=torch.device("cuda", self.device))
+        return self._ext
 
     def all_reduce_host(self, grads_host):
         """Host-buffer entry (numpy float32 arrays): H2D copies, the device
