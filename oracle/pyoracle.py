@@ -214,6 +214,23 @@ class Oracle:
                                                  C.byref(r), C.byref(lo), C.byref(hi)))
         return r.value, lo.value, hi.value
 
+    def topka(self, grads, k):
+        """inc/collectives.hpp:185-216: (idx, val) of the merged union (every
+        worker's), per-worker (rounds, scalars)."""
+        g = np.ascontiguousarray(grads, dtype=self.dtype)
+        p, n = g.shape
+        ptrs = (C.c_void_p * p)(*[g[w].ctypes.data for w in range(p)])
+        oi = np.empty(max(1, p * k), np.int64)
+        ov = np.empty(max(1, p * k), self.dtype)
+        no = C.c_int64()
+        rr = np.empty(p, np.int64)
+        rs = np.empty(p, np.int64)
+        self._check(self.lib.orc_topka(C.c_int(p), C.c_int64(n), C.c_int64(k), ptrs,
+                                       oi.ctypes.data_as(C.c_void_p), ov.ctypes.data_as(C.c_void_p),
+                                       C.byref(no), rr.ctypes.data_as(C.c_void_p),
+                                       rs.ctypes.data_as(C.c_void_p)))
+        return oi[: no.value], ov[: no.value], rr, rs
+
     def topka_cost(self, P, k):
         r, lo, hi = C.c_int64(), C.c_int64(), C.c_int64()
         self._check(self.lib.orc_topka_cost(C.c_int64(P), C.c_int64(k), C.byref(r), C.byref(lo), C.byref(hi)))

@@ -264,6 +264,31 @@ EXPORT int orc_top_k_select_slice(const double* g, int64_t lo, int64_t hi, int64
   });
 }
 
+// inc/collectives.hpp:185-216, unmodified, on a fresh Fabric
+EXPORT int orc_topka(int p, int64_t n, int64_t k, const double* const* grads, int64_t* out_idx,
+                     double* out_val, int64_t* n_out, int64_t* rounds, int64_t* scalars) {
+  return guarded([&] {
+    std::vector<spardl::GradientVector> g;
+    for (int w = 0; w < p; ++w) g.emplace_back(std::vector<double>(grads[w], grads[w] + n));
+    spardl::Fabric fabric(p);
+    auto res = spardl::topka_baseline(fabric, g, k);
+    const auto& e = res[0].entries;
+    for (size_t i = 0; i < e.size(); ++i) {
+      out_idx[i] = e[i].index;
+      out_val[i] = e[i].value;
+    }
+    *n_out = static_cast<int64_t>(e.size());
+    for (int w = 1; w < p; ++w)
+      if (!(res[static_cast<size_t>(w)] == res[0]))
+        throw spardl::consistency_error("topka: workers disagree");
+    const auto& l = fabric.ledger();
+    for (size_t w = 0; w < l.size(); ++w) {
+      rounds[w] = l[w].rounds;
+      scalars[w] = l[w].scalars_received;
+    }
+  });
+}
+
 EXPORT int orc_merge_add(int a_id, const int64_t* a_idx, const double* a_val, int64_t na,
                          int b_id, const int64_t* b_idx, const double* b_val, int64_t nb,
                          int64_t* out_idx, double* out_val, int64_t* n_out) {

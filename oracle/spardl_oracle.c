@@ -1182,6 +1182,38 @@ EXPORT int orc_merge_add(int a_id, const int64_t *a_idx, const real *a_val, int6
   API_END
 }
 
+/* inc/collectives.hpp:185-216 -- Top-k All-Gather baseline: every worker's
+ * top_k_select_slice over the whole vector, a Bruck all-gather of the P
+ * selections, and at every worker a left fold of merge_add over the gathered
+ * blocks in source order starting from an empty block.  Returns worker 0's
+ * union (all workers hold the same) and the per-worker ledger. */
+EXPORT int orc_topka(int p, int64_t n, int64_t k, const real *const *grads, int64_t *out_idx,
+                     real *out_val, int64_t *n_out, int64_t *rounds, int64_t *scalars) {
+  API_BEGIN
+  if (p < 1) throw_err(E_CONFIG, "topka: gradient count != worker count");
+  if (k > n) throw_err(E_CONFIG, "topka: k must satisfy k <= N");
+  fabric_t f;
+  f.p = p;
+  f.cost = (wcost *)amalloc(sizeof(wcost) * (size_t)p);
+  memset(f.cost, 0, sizeof(wcost) * (size_t)p);
+  int *workers = (int *)amalloc(sizeof(int) * (size_t)p);
+  blk *locals = (blk *)amalloc(sizeof(blk) * (size_t)p);
+  for (int w = 0; w < p; ++w) {
+    blk disc;
+    workers[w] = w;
+    top_k_slice(grads[w], 0, 0, n, k, &locals[w], &disc);
+  }
+  group_gather g = {p, workers, locals};
+  blk **out = bruck_multi(&f, &g, 1);
+  blk acc = blk_new(0, 0, n, 0);
+  for (int s = 0; s < p; ++s) acc = merge_add(&acc, &out[0][s]);   /* worker 0's view */
+  memcpy(out_idx, acc.idx, sizeof(int64_t) * (size_t)acc.n);
+  memcpy(out_val, acc.val, sizeof(real) * (size_t)acc.n);
+  *n_out = acc.n;
+  for (int w = 0; w < p; ++w) { rounds[w] = f.cost[w].rounds; scalars[w] = f.cost[w].scalars; }
+  API_END
+}
+
 EXPORT int orc_partition(int64_t n, int count, int64_t *lo, int64_t *hi) {
   API_BEGIN
   partition_t p = make_partition(n, count);

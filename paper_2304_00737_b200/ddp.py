@@ -12,8 +12,6 @@ which is exactly DDP's averaged-gradient convention (w -= lr * grad).
     state = SparDLHookState(density=0.01)
     ddp_model.register_comm_hook(state, spardl_hook)
 """
-from __future__ import annotations
-
 import torch
 import torch.distributed as dist
 
@@ -33,7 +31,7 @@ class SparDLHookState:
         self.pg = process_group
         self.contexts: dict = {}
 
-    def context(self, bucket) -> SparDL:
+    def context(self, bucket) -> "SparDL":
         buf = bucket.buffer()
         key = (bucket.index(), buf.numel())
         ctx = self.contexts.get(key)
@@ -54,7 +52,7 @@ class SparDLHookState:
         self.contexts.clear()
 
 
-def spardl_hook(state: SparDLHookState, bucket) -> torch.futures.Future:
+def spardl_hook(state: SparDLHookState, bucket) -> torch.futures.Future[torch.Tensor]:
     """DDP comm hook: SparDL sparse all-reduce of the bucket, densified and
     averaged over the ranks."""
     buf = bucket.buffer()

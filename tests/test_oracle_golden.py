@@ -305,3 +305,20 @@ def test_golden_fixture(o, path):
         for w in range(P):
             assert np.array_equal(p.carry(w).astype(np.float64), z[f"carry{it}_{w}"])
         assert [info["max_rounds"], info["max_scalars"]] == z[f"ledger{it}"].tolist()
+
+
+@pytest.mark.parametrize("P,N,k", [(1, 100, 10), (2, 300, 30), (3, 777, 77), (4, 1000, 50),
+                                   (6, 5000, 600), (8, 5000, 300), (5, 64, 64)])
+def test_topka_restatement_matches_reference(P, N, k):
+    """orc_topka (C restatement of inc/collectives.hpp:185-216) == the
+    reference's topka_baseline on a Fabric, union and ledger."""
+    if not os.path.exists(LIBS["ref"]):
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(P * 1000 + N)
+    g = np.round(rng.standard_normal((P, N)) * 256) / 256
+    a = Oracle("f64").topka(g, k)
+    b = Oracle("ref").topka(g, k)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    rounds, low, high = Oracle("f64").topka_cost(P, k)
+    assert a[2].max() == rounds and low <= a[3].max() <= high
