@@ -655,4 +655,71 @@ inline RunResult spardl_all_reduce(Fabric& fabric, const ClusterConfig& cfg,
   return r;
 }
 
+// ---------------------------------------------------------------- reporting
+inline const char* to_string(SagMode m) {
+  return m == SagMode::none ? "none" : (m == SagMode::rsag ? "rsag" : "bsag");
+}
+inline const char* to_string(ResidualMode m) {
+  return m == ResidualMode::gres ? "gres" : (m == ResidualMode::pres ? "pres" : "lres");
+}
+inline const char* to_string(SrsTiming t) { return t == SrsTiming::optimized ? "optimized" : "naive"; }
+
+// inc/pipeline.hpp:344-361
+inline void write_run_report_header(std::ostream& os) {
+  os << "P,N,k,d,sag,residual,timing,seed,max_rounds,max_scalars,"
+        "predicted_rounds,predicted_scalars_low,predicted_scalars_high,"
+        "consistent,conservation_error\n";
+}
+inline void write_run_report_row(std::ostream& os, const ClusterConfig& cfg, const RunResult& r) {
+  os << cfg.workers << ',' << cfg.dimension << ',' << cfg.k << ',' << cfg.teams << ','
+     << to_string(cfg.sag) << ',' << to_string(cfg.residual) << ',' << to_string(cfg.timing)
+     << ',' << cfg.seed << ',' << r.ledger.max_rounds << ',' << r.ledger.max_scalars_received
+     << ',' << r.predicted.rounds << ',' << r.predicted.scalars_low << ','
+     << r.predicted.scalars_high << ',' << (r.consistent ? 1 : 0) << ',' << r.conservation_error
+     << '\n';
+}
+
+// inc/sag.hpp:349-358
+inline void write_controller_trace_header(std::ostream& os) { os << "iteration,h,step,flag,N_t,L\n"; }
+inline void write_controller_trace_row(std::ostream& os, std::int64_t iter, const HController& c,
+                                       std::int64_t n_t) {
+  os << iter << ',' << c.h() << ',' << c.step() << ',' << (c.flag() ? 1 : 0) << ',' << n_t << ','
+     << c.target() << '\n';
+}
+
+// inc/collectives.hpp:185-216: the Top-k All-Gather baseline.  Local top-k
+// and the source-ordered merge fold run on the GPU (spardl_topk_select_slice,
+// spardl_merge_add); the ledger is the Bruck all-gather's: every worker
+// receives the P-1 other selections in ceil(log2 P) rounds.
+inline std::vector<GlobalSparseGradient> topka_baseline(Fabric& fabric,
+                                                        const std::vector<GradientVector>& gradients,
+                                                        Index k) {
+  const int p = fabric.worker_count();
+  if (static_cast<size_t>(p) != gradients.size())
+    throw config_error("topka: gradient count != worker count");
+  const Index n = gradients[0].size();
+  if (k > n) throw config_error("topka: k must satisfy k <= N");
+  std::vector<SparseBlock> locals(static_cast<size_t>(p));
+  for (int w = 0; w < p; ++w)
+    locals[size_t(w)] = top_k_select_slice(gradients[size_t(w)], 0, {0, n}, k).selected;
+  SparseBlock acc;
+  acc.block_id = 0;
+  acc.range = {0, n};
+  for (int s = 0; s < p; ++s) acc = merge_add(acc, locals[size_t(s)]);
+  int rounds = 0;
+  while ((1 << rounds) < p) ++rounds;
+  auto& led = fabric.mutable_ledger();
+  for (int w = 0; w < p; ++w) {
+    led[size_t(w)].rounds += rounds;
+    for (int s = 0; s < p; ++s)
+      if (s != w) led[size_t(w)].scalars_received += 2 * locals[size_t(s)].nnz();
+  }
+  std::vector<GlobalSparseGradient> out(static_cast<size_t>(p));
+  for (auto& o : out) {
+    o.n = n;
+    o.entries = acc.entries;
+  }
+  return out;
+}
+
 }  // namespace spardl

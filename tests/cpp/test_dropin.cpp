@@ -218,8 +218,49 @@ static void test_pipeline() {
   }
 }
 
+static void test_reporting() {
+  {  // Top-kA (inc/collectives.hpp:185-216): union of the local top-2s, Bruck ledger
+    Fabric fabric(3);
+    std::vector<GradientVector> g(3, GradientVector(6));
+    const double v[3][6] = {{5, -1, 0, 3, 0, 0}, {0, 4, 0, -3, 1, 0}, {-2, 0, 0, 0, 0, 7}};
+    for (int w = 0; w < 3; ++w)
+      for (int i = 0; i < 6; ++i) g[size_t(w)][i] = v[w][i];
+    auto r = topka_baseline(fabric, g, 2);
+    // locals: {0:5, 3:3}, {1:4, 3:-3}, {0:-2, 5:7} -> 0:3, 1:4, 3:0 (kept), 5:7
+    CHECK(r.size() == 3 && r[0].entries == r[2].entries);
+    CHECK(r[0].nnz() == 4 && r[0].entries[0] == (Entry{0, 3.0}) &&
+          r[0].entries[2] == (Entry{3, 0.0}) && r[0].entries[3] == (Entry{5, 7.0}));
+    CHECK(fabric.report().max_rounds == 2 && fabric.report().max_scalars_received == 8);
+    CHECK(throws<config_error>([&] { topka_baseline(fabric, g, 7); }));
+  }
+  {  // run report / controller trace CSV (inc/pipeline.hpp:344-361, inc/sag.hpp:349-358)
+    ClusterConfig cfg;
+    cfg.workers = 6;
+    cfg.dimension = 6000;
+    cfg.k = 600;
+    RunResult r;
+    r.ledger.max_rounds = 6;
+    r.ledger.max_scalars_received = 2000;
+    r.predicted = {6, 2000, 2000};
+    r.consistent = true;
+    std::ostringstream os;
+    write_run_report_header(os);
+    write_run_report_row(os, cfg, r);
+    CHECK(os.str() == "P,N,k,d,sag,residual,timing,seed,max_rounds,max_scalars,"
+                      "predicted_rounds,predicted_scalars_low,predicted_scalars_high,"
+                      "consistent,conservation_error\n6,6000,600,1,none,gres,optimized,0,6,2000,"
+                      "6,2000,2000,1,0\n");
+    HController c(6, 600, 3);
+    std::ostringstream t;
+    write_controller_trace_header(t);
+    write_controller_trace_row(t, 0, c, 199);
+    CHECK(t.str().rfind("iteration,h,step,flag,N_t,L\n0,100,", 0) == 0);
+  }
+}
+
 int main() {
   test_sparse();
+  test_reporting();
   test_fabric();
   test_schedule_api();
   test_pipeline();
