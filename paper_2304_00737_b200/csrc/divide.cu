@@ -37,6 +37,7 @@ __device__ __forceinline__ int64_t chunk_origin(const DivTask& t) { return (int6
 
 __global__ void __launch_bounds__(kThreads) k_div_sample(const DivTask* __restrict__ tasks,
                                                          int apply_residual) {
+  pdl_enter();
   const DivTask& t = tasks[blockIdx.y];
   if (!t.use_cand || t.hist->valid) return;   // no sample needed: carried threshold
   const int c = blockIdx.x * t.sample_every;
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(kThreads) k_div_sample(const DivTask* __restri
 }
 
 __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restrict__ tasks) {
+  pdl_enter();
   const DivTask& t = tasks[blockIdx.x];
   constexpr int BPT = kSampBins / kThreads;
   __shared__ long long suf[kThreads];
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
 
 template <int APPLY>
 __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const DivTask* __restrict__ tasks) {
+  pdl_enter();
   const DivTask& t = tasks[blockIdx.y];
   const int c = blockIdx.x;
   if (c >= t.nchunks) return;
@@ -282,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const Di
 // segment cut into tiles of <= kTile candidates, in chunk (= index) order --
 // and the candidate total.  Unused tile slots get count 0.
 __global__ void __launch_bounds__(1024) k_div_tiles(const DivTask* __restrict__ tasks) {
+  pdl_enter();
   const DivTask& t = tasks[blockIdx.x];
   __shared__ int scratch[40];
   if (*t.cand_bad & 1) return;
@@ -327,16 +331,16 @@ int launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sampl
       cudaFuncSetAttribute(k_div_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       configured = true;
     }
-    k_div_sample<<<dim3(sx, ntask), kThreads, smem, s>>>(tasks_dev, apply_residual);
-    k_div_prethr<<<ntask, kThreads, 0, s>>>(tasks_dev);
+    launch_pdl(k_div_sample, dim3(sx, ntask), dim3(kThreads), smem, s, tasks_dev, apply_residual);
+    launch_pdl(k_div_prethr, dim3(ntask), dim3(kThreads), 0, s, tasks_dev);
     n += 2;
   }
   if (part != 1) {
     if (apply_residual)
-      k_div_cand<1><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
+      launch_pdl(k_div_cand<1>, dim3(max_chunks, ntask), dim3(kThreads), 0, s, tasks_dev);
     else
-      k_div_cand<0><<<dim3(max_chunks, ntask), kThreads, 0, s>>>(tasks_dev);
-    k_div_tiles<<<ntask, 1024, 0, s>>>(tasks_dev);
+      launch_pdl(k_div_cand<0>, dim3(max_chunks, ntask), dim3(kThreads), 0, s, tasks_dev);
+    launch_pdl(k_div_tiles, dim3(ntask), dim3(1024), 0, s, tasks_dev);
     n += 2;
   }
   return n;

@@ -14,6 +14,7 @@ namespace {
 // blocks in position order (inc/pipeline.hpp:279-291); blocks cover
 // increasing index ranges, so the result is index-sorted.
 __global__ void __launch_bounds__(kThreads) k_assemble(const AssembleTask* __restrict__ tasks) {
+  pdl_enter();
   const AssembleTask& t = tasks[blockIdx.y];
   __shared__ int off[65];
   if (threadIdx.x == 0) {
@@ -103,6 +104,7 @@ constexpr int kXiBatch = 4;                  // discard entries per thread per b
 constexpr int kMaxXiLists = kThreads / 64;   // bound searches in parallel (2 warps each)
 
 __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __restrict__ tasks) {
+  pdl_enter();
   const FinalizeTask& t = tasks[blockIdx.z];
   if (t.mode == 2) return;   // lres ignores the global gradient
   const int b = blockIdx.y;
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __res
 }
 
 __global__ void __launch_bounds__(kThreads) k_finalize_lres(const FinalizeTask* __restrict__ tasks) {
+  pdl_enter();
   const FinalizeTask& t = tasks[blockIdx.y];
   if (t.mode != 2) return;
   for (int b = 0; b < t.m; ++b) {
@@ -230,6 +233,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize_lres(const FinalizeTask* 
 
 // ---------------------------------------------------------------------------
 __global__ void k_ledger(const LedgerAdd* __restrict__ adds, int n) {
+  pdl_enter();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const long long v = 2ll * (long long)(*adds[i].cnt);
     if (v) atomicAdd(reinterpret_cast<unsigned long long*>(adds[i].dst), (unsigned long long)v);
@@ -240,6 +244,7 @@ __global__ void k_ledger(const LedgerAdd* __restrict__ adds, int n) {
 // Algorithm 2 (inc/sag.hpp:61-81) in double precision, llround semantics
 // (round half away from zero) via CUDA's llround.
 __global__ void k_controller(const CtlTask* __restrict__ tasks, int n, int observe) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   HCtl c = *tasks[i].ctl;
@@ -276,7 +281,7 @@ int launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t
   if (ntask <= 0) return 0;
   int gx = (int)((max_k + kThreads - 1) / kThreads);
   gx = gx < 1 ? 1 : (gx > 1184 ? 1184 : gx);
-  k_assemble<<<dim3(gx, ntask), kThreads, 0, s>>>(tasks_dev);
+  launch_pdl(k_assemble, dim3(gx, ntask), dim3(kThreads), 0, s, tasks_dev);
   return 1;
 }
 
@@ -285,11 +290,11 @@ int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_blk, i
   if (ntask <= 0) return 0;
   int gx = (int)((max_blk + kFinChunk - 1) / kFinChunk);
   gx = gx < 1 ? 1 : gx;
-  k_finalize<<<dim3(gx, m, ntask), kThreads, 0, s>>>(tasks_dev);
+  launch_pdl(k_finalize, dim3(gx, m, ntask), dim3(kThreads), 0, s, tasks_dev);
   if (max_div > 0) {
     int lx = (max_div + kThreads - 1) / kThreads;
     lx = lx < 1 ? 1 : (lx > 1184 ? 1184 : lx);
-    k_finalize_lres<<<dim3(lx, ntask), kThreads, 0, s>>>(tasks_dev);
+    launch_pdl(k_finalize_lres, dim3(lx, ntask), dim3(kThreads), 0, s, tasks_dev);
     return 2;
   }
   return 1;
@@ -298,13 +303,13 @@ int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_blk, i
 int launch_ledger(const LedgerAdd* adds_dev, int nadd, cudaStream_t s) {
   if (nadd <= 0) return 0;
   const int gx = (nadd + kThreads - 1) / kThreads;
-  k_ledger<<<gx, kThreads, 0, s>>>(adds_dev, nadd);
+  launch_pdl(k_ledger, dim3(gx), dim3(kThreads), 0, s, adds_dev, nadd);
   return 1;
 }
 
 int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStream_t s) {
   if (ntask <= 0) return 0;
-  k_controller<<<(ntask + 127) / 128, 128, 0, s>>>(tasks_dev, ntask, observe);
+  launch_pdl(k_controller, dim3((ntask + 127) / 128), dim3(128), 0, s, tasks_dev, ntask, observe);
   return 1;
 }
 

@@ -33,6 +33,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // Rank all samples of a task; write the sorted splitters and, for each
 // splitter, the window of every list that can hold its partition.
 __global__ void __launch_bounds__(kThreads) k_merge_rank(const MergeTask* __restrict__ tasks) {
+  pdl_enter();
   const MergeTask& t = tasks[blockIdx.y];
   const int r = t.r, T = t.T;
   __shared__ int32_t samp[kMaxSamples];
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(kThreads) k_merge_rank(const MergeTask* __rest
 }
 
 __global__ void __launch_bounds__(kThreads) k_merge_part(const MergeTask* __restrict__ tasks) {
+  pdl_enter();
   const MergeTask& t = tasks[blockIdx.y];
   const int q = blockIdx.x;
   const int S = *t.nparts;
@@ -209,7 +211,7 @@ int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r
                  cudaStream_t s) {
   if (ntask <= 0 || max_parts <= 0) return 0;
   const int rx = (max_parts + kThreads - 1) / kThreads;
-  k_merge_rank<<<dim3(rx, ntask), kThreads, 0, s>>>(tasks_dev);
+  launch_pdl(k_merge_rank, dim3(rx, ntask), dim3(kThreads), 0, s, tasks_dev);
   const size_t smem = (size_t)max_r_T * 16;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
@@ -217,7 +219,7 @@ int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r
                          (int)smem);
     configured = smem;
   }
-  k_merge_part<<<dim3(max_parts, ntask), kThreads, smem, s>>>(tasks_dev);
+  launch_pdl(k_merge_part, dim3(max_parts, ntask), dim3(kThreads), smem, s, tasks_dev);
   return 2;
 }
 

@@ -401,6 +401,7 @@ __device__ long long merge_prologue(const MergeTask& mt, int cr, int32_t* w_idx,
 template <int CL, bool FUSED>
 __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     k_select(const SelTask* __restrict__ tasks, int tab_cap, int win_cap) {
+  pdl_enter();
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank();
   const SelTask t = tasks[blockIdx.y];   // by value: fields live in registers, not re-read
@@ -837,8 +838,10 @@ cudaLaunchConfig_t cl_config(int ntask, size_t smem, cudaStream_t s, cudaLaunchA
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = pdl_enabled() && s ? 2 : 1;
   return lc;
 }
 
@@ -890,7 +893,7 @@ int max_clusters(size_t smem) {
   static size_t last_smem = ~size_t(0);
   static int n = 0;
   if (smem != last_smem) {
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t lc = cl_config<CL>(1, smem, nullptr, attr);
     int c = 0;
     if (cudaOccupancyMaxActiveClusters(&c, k_select<CL, F>, &lc) != cudaSuccess) {
@@ -918,7 +921,7 @@ template <int CL, bool F>
 void launch_cl(const SelTask* tasks_dev, int ntask, int tab_cap, int win_cap, cudaStream_t s) {
   const size_t smem = dyn_bytes(tab_cap, win_cap);
   configure<CL, F>();
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   cudaLaunchConfig_t lc = cl_config<CL>(ntask, smem, s, attr);
   cudaLaunchKernelEx(&lc, k_select<CL, F>, tasks_dev, tab_cap, win_cap);
 }

@@ -17,6 +17,7 @@
 //              every peer's done[rank] flag
 // Waits are bounded (~10 s): a peer that never arrives sets *err and the next
 // sync() reports it instead of hanging the device.
+#include "common.cuh"
 #include "kernels.cuh"
 
 namespace sdl {
@@ -56,6 +57,7 @@ __device__ void spin_until(const long long* flag, long long target, int32_t* err
 }
 
 __global__ void k_begin(long long* epoch, const long long* const* done, int n, int32_t* err) {
+  pdl_enter();
   __shared__ long long e;
   if (threadIdx.x == 0) {
     e = *epoch + 1;
@@ -66,6 +68,7 @@ __global__ void k_begin(long long* epoch, const long long* const* done, int n, i
 }
 
 __global__ void k_publish(long long* const* targets, int n, const long long* epoch) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const long long e = *epoch;
@@ -74,6 +77,7 @@ __global__ void k_publish(long long* const* targets, int n, const long long* epo
 }
 
 __global__ void k_wait(const long long* const* flags, int n, const long long* epoch, int32_t* err) {
+  pdl_enter();
   const long long e = *epoch;
   for (int i = threadIdx.x; i < n; i += blockDim.x) spin_until(flags[i], e, err);
 }
@@ -82,20 +86,20 @@ __global__ void k_wait(const long long* const* flags, int n, const long long* ep
 
 int launch_begin(long long* epoch, const long long* const* done, int n, int32_t* err,
                  cudaStream_t s) {
-  k_begin<<<1, 32, 0, s>>>(epoch, done, n, err);
+  launch_pdl(k_begin, dim3(1), dim3(32), 0, s, epoch, done, n, err);
   return 1;
 }
 
 int launch_publish(long long* const* targets, int n, const long long* epoch, cudaStream_t s) {
   if (n <= 0) return 0;
-  k_publish<<<(n + 127) / 128, 128, 0, s>>>(targets, n, epoch);
+  launch_pdl(k_publish, dim3((n + 127) / 128), dim3(128), 0, s, targets, n, epoch);
   return 1;
 }
 
 int launch_wait(const long long* const* flags, int n, const long long* epoch, int32_t* err,
                 cudaStream_t s) {
   if (n <= 0) return 0;
-  k_wait<<<1, 128, 0, s>>>(flags, n, epoch, err);
+  launch_pdl(k_wait, dim3(1), dim3(128), 0, s, flags, n, epoch, err);
   return 1;
 }
 
