@@ -748,7 +748,10 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
         const float v = vv[u];
         const int32_t ix = iv[u];
         const uint32_t key = mag_key(v);
-        const bool valid = key != kHoleKey;
+        // holes exist only in fused-merge inputs; otherwise validity is the
+        // position (lanes past the item hold hole bits)
+        const int j = j00 + u * 32 + lane;
+        const bool valid = FUSED ? key != kHoleKey : j < c;
         bool is_sel;
         if (all == 1) {
           is_sel = valid;
@@ -763,11 +766,14 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
           if (is_sel && is_eq) cut = max(cut, ix);
         }
         const uint32_t bs = __ballot_sync(0xffffffffu, is_sel);
-        const uint32_t bv = __ballot_sync(0xffffffffu, valid);
         const int sel_rank = sel_seen + __popc(bs & lt);
-        const int val_rank = val_seen + __popc(bv & lt);
         sel_seen += __popc(bs);
-        val_seen += __popc(bv);
+        int val_rank = j;   // entries of the item before this one
+        if (FUSED) {
+          const uint32_t bv = __ballot_sync(0xffffffffu, valid);
+          val_rank = val_seen + __popc(bv & lt);
+          val_seen += __popc(bv);
+        }
         if (is_sel) {
           t.sel_idx[sel_base + sel_rank] = ix;
           t.sel_val[sel_base + sel_rank] = v;
