@@ -23,7 +23,7 @@
 #include "kernels.cuh"
 
 #ifndef SPARDL_DIV_MINB
-#define SPARDL_DIV_MINB 2
+#define SPARDL_DIV_MINB 3
 #endif
 
 namespace sdl {
@@ -161,7 +161,9 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const Di
   const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int ITER = kChunk / (kThreads * 4);   // float4 groups per lane
-  float v[ITER][4];
+  // the combined values wait here for the compaction (registers are the
+  // occupancy limit: the loads in flight need them)
+  __shared__ __align__(16) float s_comb[kChunk];
   uint32_t mask = 0;
   bool nan = false;
   const int64_t lo = t.lo, hi = t.hi;
@@ -195,10 +197,11 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const Di
       } else {
         o = cc;
       }
-      v[it][0] = o.x; v[it][1] = o.y; v[it][2] = o.z; v[it][3] = o.w;
+      reinterpret_cast<float4*>(s_comb)[warp * (32 * ITER) + it * 32 + lane] = o;
+      const float ov[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const uint32_t k = mag_key(v[it][e]);
+        const uint32_t k = mag_key(ov[e]);
         nan |= k > 0x7f800000u;
         if (k >= pre) mask |= 1u << (it * 4 + e);
       }
@@ -206,14 +209,14 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const Di
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int64_t i = i0 + e;
-        v[it][e] = 0.f;
+        s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e] = 0.f;
         if (i >= lo && i < hi) {
           float x = carry[i];
           if (APPLY) {
             x = __fadd_rn(g[i], x);
             carry[i] = x;
           }
-          v[it][e] = x;
+          s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e] = x;
           const uint32_t k = mag_key(x);
           nan |= k > 0x7f800000u;
           if (k >= pre) mask |= 1u << (it * 4 + e);
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const Di
     for (int e = 0; e < 4; ++e) {
       if (mask & (1u << (it * 4 + e))) {
         ci[p] = (int32_t)(i0 + e);
-        cv[p] = v[it][e];
+        cv[p] = s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e];
         ++p;
       }
     }
