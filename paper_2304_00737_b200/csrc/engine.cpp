@@ -280,7 +280,11 @@ sdl::SelTask Engine::select_from_merge(Stage& st, const std::vector<int>& pieces
     mt.in_cnt[q] = s.cnt;
     capsum += s.cap;
   }
-  int64_t T = std::max<int64_t>(2048 / r, (capsum + sdl::kMaxSamples - 1) / sdl::kMaxSamples);
+  static const int64_t tnum = [] {
+    const char* e = std::getenv("SPARDL_MERGE_TNUM");   // tuning experiments only
+    return static_cast<int64_t>(e ? std::atoi(e) : 2048);
+  }();
+  int64_t T = std::max<int64_t>(tnum / r, (capsum + sdl::kMaxSamples - 1) / sdl::kMaxSamples);
   T = (std::max<int64_t>(T, 32) + 3) & ~int64_t(3);   // windows start 16-byte aligned
   if (static_cast<int64_t>(r) * T > kMergeSmemEntries)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "merge of this size exceeds the shared-memory envelope");
