@@ -135,22 +135,33 @@ __device__ void update_history(DivHistory* h, int mode, int all, uint32_t T, uin
 }
 
 // CTA 0: locate the digit holding the rank-th largest key in agg[0..nb).
+// Suffix sums over the threads' bin groups by warp shuffles (two barriers).
 __device__ void find_digit(uint32_t* agg, int nb, int shift, RadixState* st, long long* suf) {
   const int bpt = nb / kSelThreads;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   long long mine = 0;
   for (int q = 0; q < bpt; ++q) mine += agg[threadIdx.x * bpt + q];
-  const int r = kSelThreads - 1 - threadIdx.x;     // bins ascend with tid; scan from the top
-  suf[r] = mine;
-  __syncthreads();
-  for (int o = 1; o < kSelThreads; o <<= 1) {
-    const long long add = threadIdx.x >= (unsigned)o ? suf[threadIdx.x - o] : 0;
-    __syncthreads();
-    suf[threadIdx.x] += add;
-    __syncthreads();
+  long long x = mine;   // inclusive suffix inside the warp (this lane and above)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_down_sync(0xffffffffu, x, o);
+    if (lane + o < 32) x += y;
   }
-  const long long above = r > 0 ? suf[r - 1] : 0;
-  const int64_t rank = st->rank;
+  if (lane == 0) suf[warp] = x;   // warp total
   __syncthreads();
+  if (threadIdx.x < 32) {   // suffix over the warps above
+    long long w = threadIdx.x < kWarps ? suf[threadIdx.x] : 0;
+    const long long own = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_down_sync(0xffffffffu, w, o);
+      if (threadIdx.x + o < 32) w += y;
+    }
+    if (threadIdx.x < kWarps) suf[kWarps + threadIdx.x] = w - own;   // strictly above
+  }
+  __syncthreads();
+  const long long above = (x - mine) + suf[kWarps + warp];
+  const int64_t rank = st->rank;
   if (above < rank && rank <= above + mine) {
     long long cum = above;
     for (int q = bpt - 1; q >= 0; --q) {
