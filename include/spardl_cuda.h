@@ -73,7 +73,7 @@ typedef struct spardl_config {
 typedef struct spardl_run_info {
   int32_t consistent;
   int32_t conservation_applicable;
-  double conservation_error;   /* computed only when audit is enabled, else -1 */
+  double conservation_error;   /* when the audit is enabled (gres, pres), else -1 */
   int64_t max_rounds, max_scalars;            /* LedgerReport, fabric.hpp:41-45 */
   int64_t srs_rounds, srs_scalars;            /* srs_phase */
   int64_t sag_rounds, sag_scalars;            /* sag_phase */
@@ -185,7 +185,9 @@ int spardl_ctx_local_workers(const spardl_ctx* ctx, int32_t* first, int32_t* cou
 int spardl_ctx_transport(const spardl_ctx* ctx, int32_t* peer);
 /* enable (1) / disable (0) CUDA-graph replay of the whole iteration */
 int spardl_ctx_set_graph(spardl_ctx* ctx, int32_t enable);
-/* enable the sparse conservation audit (inc/pipeline.hpp:305-334) */
+/* enable the conservation audit (inc/pipeline.hpp:305-334), computed exactly
+ * on the k global positions (off them both sides are the same values); the
+ * next spardl_get_run_info reports it (collective). */
 int spardl_ctx_set_audit(spardl_ctx* ctx, int32_t enable);
 
 /* One synchronisation: grads[i] is local worker i's dense fp32 gradient

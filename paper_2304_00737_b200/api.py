@@ -346,6 +346,11 @@ class SparDL:
     def sync(self):
         check(lib().spardl_sync(self._h))
 
+    def set_audit(self, enable: bool = True):
+        """Compute the reference's conservation audit (inc/pipeline.hpp:304-332)
+        for run_info(): exactly, on the k global positions (gres, pres)."""
+        check(lib().spardl_ctx_set_audit(self._h, C.c_int32(1 if enable else 0)))
+
     def run_info(self) -> dict:
         ri = RunInfo()
         check(lib().spardl_get_run_info(self._h, C.byref(ri)))

@@ -754,6 +754,75 @@ void Engine::plan() {
 }
 
 // ---------------------------------------------------------------------------
+// sparse conservation audit
+void Engine::set_audit(bool on) {
+  audit_ = on;
+  if (dry_) return;
+  CK(cudaSetDevice(device_));
+  sync();
+  const size_t k = static_cast<size_t>(std::max<int64_t>(1, cfg_.k));
+  if (on && aud_comb_.empty()) {
+    for (int li = 0; li < wloc_; ++li) {
+      aud_comb_.push_back(static_cast<float*>(arena_.alloc(sizeof(float) * k)));
+      aud_carry_.push_back(static_cast<float*>(arena_.alloc(sizeof(float) * k)));
+    }
+    if (world_ > 1)
+      aud_gather_ = static_cast<float*>(
+          arena_.alloc(sizeof(float) * k * 2 * static_cast<size_t>(wloc_) * (world_ + 1)));
+  }
+  for (int li = 0; li < wloc_; ++li) {
+    fin_tasks_[static_cast<size_t>(li)].aud_comb = on ? aud_comb_[static_cast<size_t>(li)] : nullptr;
+    fin_tasks_[static_cast<size_t>(li)].aud_carry = on ? aud_carry_[static_cast<size_t>(li)] : nullptr;
+  }
+  CK(mcpy(fin_dev_, fin_tasks_.data(), sizeof(sdl::FinalizeTask) * fin_tasks_.size(),
+          cudaMemcpyHostToDevice));
+}
+
+// max over the global positions of |sum_w combined_w - (global + sum_w carry_w)|
+// / max(1, |sum_w combined_w|), sums in double in worker order (collective)
+double Engine::conservation_audit() {
+  const size_t k = static_cast<size_t>(std::max<int64_t>(1, cfg_.k));
+  const Slot& gs = global_[static_cast<size_t>(team_of_local_global_[0])];
+  int32_t n = 0;
+  CK(mcpy(&n, gs.cnt, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  std::vector<float> gval(static_cast<size_t>(n));
+  if (n) CK(mcpy(gval.data(), gs.val, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  // all workers' (combined, carry) at the global positions, worker order
+  std::vector<float> all(k * 2 * static_cast<size_t>(P_));
+  if (world_ > 1) {
+    float* send = aud_gather_;
+    for (int li = 0; li < wloc_; ++li) {
+      CK(cudaMemcpy(send + k * 2 * li, aud_comb_[static_cast<size_t>(li)], sizeof(float) * k,
+                    cudaMemcpyDeviceToDevice));
+      CK(cudaMemcpy(send + k * (2 * li + 1), aud_carry_[static_cast<size_t>(li)],
+                    sizeof(float) * k, cudaMemcpyDeviceToDevice));
+    }
+    float* recv = send + k * 2 * wloc_;
+    NK(ncclAllGather(send, recv, k * 2 * wloc_, ncclFloat, comm_, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    CK(cudaMemcpy(all.data(), recv, sizeof(float) * all.size(), cudaMemcpyDeviceToHost));
+  } else {
+    for (int li = 0; li < wloc_; ++li) {
+      CK(cudaMemcpy(all.data() + k * 2 * li, aud_comb_[static_cast<size_t>(li)],
+                    sizeof(float) * k, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(all.data() + k * (2 * li + 1), aud_carry_[static_cast<size_t>(li)],
+                    sizeof(float) * k, cudaMemcpyDeviceToHost));
+    }
+  }
+  double worst = 0.0;
+  for (int32_t p = 0; p < n; ++p) {
+    double lhs = 0.0, rhs = 0.0;
+    for (int w = 0; w < P_; ++w) lhs += all[k * 2 * w + static_cast<size_t>(p)];
+    rhs += gval[static_cast<size_t>(p)];
+    for (int w = 0; w < P_; ++w) rhs += all[k * (2 * w + 1) + static_cast<size_t>(p)];
+    const double den = std::max(1.0, lhs < 0 ? -lhs : lhs);
+    const double d = lhs - rhs;
+    worst = std::max(worst, (d < 0 ? -d : d) / den);
+  }
+  return worst;
+}
+
+// ---------------------------------------------------------------------------
 // peer-memory transport setup
 void Engine::setup_peer() {
   if (world_ == 1) return;
@@ -1156,6 +1225,8 @@ spardl_run_info Engine::run_info() {
   }
   ri.conservation_applicable = cfg_.residual == SPARDL_RES_GRES ? 1 : 0;
   ri.conservation_error = -1.0;
+  if (audit_ && !aud_comb_.empty() && cfg_.residual != SPARDL_RES_LRES)
+    ri.conservation_error = conservation_audit();
   ri.n_union = cfg_.sag == SPARDL_SAG_BSAG ? m_ : 0;
   return ri;
 }

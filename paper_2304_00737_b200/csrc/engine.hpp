@@ -126,7 +126,10 @@ class Engine {
     use_graph_ = on;
     drop_graph();
   }
-  void set_audit(bool on) { audit_ = on; }
+  // the sparse conservation audit of inc/pipeline.hpp:304-332 (gres, pres):
+  // off the global gradient both sides are the same values, so only the k
+  // global positions are compared; reported by run_info()
+  void set_audit(bool on);
 
  private:
   // --- planning
@@ -145,6 +148,9 @@ class Engine {
   sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);
   void finish_stage(Stage& st);
   void plan_fused(Stage& st);
+  double conservation_audit();
+  std::vector<float*> aud_comb_, aud_carry_;   // per local worker, k entries each
+  float* aud_gather_ = nullptr;                 // all workers' pairs (world > 1)
   void transfer(std::vector<Xfer>& xs, int uid, int src_worker, int dst_worker, int phase,
                 std::vector<std::vector<int>>* recv_into = nullptr);
   void plan();

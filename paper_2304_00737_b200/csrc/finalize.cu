@@ -115,8 +115,25 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __res
   const int nloc = min(kFinChunk, gn - c0);
   const int tid = threadIdx.x;
   float* __restrict__ carry = t.carry;
+  // audit: this block's place in the assembled global gradient
+  __shared__ int s_off;
+  if (t.aud_comb) {
+    if (tid == 0) {
+      int o = 0;
+      for (int q = 0; q < b; ++q) o += *t.gblk[q].cnt;
+      s_off = o;
+    }
+    __syncthreads();
+  }
   if (t.mode == 1) {   // pres: zero at the global indices
-    for (int e = tid; e < nloc; e += kThreads) carry[G.idx[c0 + e]] = 0.f;
+    for (int e = tid; e < nloc; e += kThreads) {
+      const int32_t j = G.idx[c0 + e];
+      if (t.aud_comb) {
+        t.aud_comb[s_off + c0 + e] = carry[j];
+        t.aud_carry[s_off + c0 + e] = 0.f;
+      }
+      carry[j] = 0.f;
+    }
     return;
   }
   __shared__ int32_t gi[kFinChunk];
@@ -215,7 +232,14 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __res
 #pragma unroll
   for (int q = 0; q < kFinPer; ++q) {
     const int e = tid + q * kThreads;
-    if (e < nloc) carry[gi[e]] = present[q] ? acc[q] : 0.f;
+    if (e < nloc) {
+      const float r = present[q] ? acc[q] : 0.f;
+      carry[gi[e]] = r;
+      if (t.aud_comb) {
+        t.aud_comb[s_off + c0 + e] = x[q];
+        t.aud_carry[s_off + c0 + e] = r;
+      }
+    }
   }
 }
 

@@ -264,6 +264,10 @@ struct FinalizeTask {
   const GatherSrc* div;       // [m]
   const int32_t* xi_off;      // [m+1] offsets into xi
   const XiList* xi;           // lists
+  // conservation audit (nullable): per position of the assembled global
+  // gradient, this worker's combined value and final residual
+  float* aud_comb;
+  float* aud_carry;
 };
 int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_blk, int m,
                     int max_div, cudaStream_t s);

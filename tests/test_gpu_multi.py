@@ -56,6 +56,8 @@ def _worker(rank, world, port, q, transport):
             cfg = sd.ClusterConfig(workers=P, dimension=N, k=k, teams=d, sag=sag,
                                    residual=residual, timing=timing)
             ctx = sd.SparDL.from_process_group(cfg, device=rank)
+            if residual != "lres":
+                ctx.set_audit(True)
             if ctx.transport != transport:
                 errors.append(f"rank{rank} transport {ctx.transport} != {transport}")
             ref = orc.pipeline(make_config(P, N, k, d, sag, residual, timing))
@@ -82,8 +84,11 @@ def _worker(rank, world, port, q, transport):
                 rr, rs = ref.ledger()
                 if list(lr) != list(rr) or list(ls) != list(rs):
                     errors.append(tag + " ledger")
-                for key in ("max_rounds", "max_scalars", "srs_scalars", "sag_scalars",
-                            "gather_scalars", "consistent"):
+                keys = ["max_rounds", "max_scalars", "srs_scalars", "sag_scalars",
+                        "gather_scalars", "consistent"]
+                if residual != "lres":
+                    keys.append("conservation_error")
+                for key in keys:
                     if info[key] != rinfo[key]:
                         errors.append(tag + f" {key} {info[key]} != {rinfo[key]}")
                 if sag == "bsag" and ctx.union_sizes() != list(ref.union_sizes()):

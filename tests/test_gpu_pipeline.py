@@ -42,6 +42,8 @@ def _run(env, P, d, sag, residual, timing, kind, N, k, iters, seed, graph=True, 
     cfg = sd.ClusterConfig(workers=P, dimension=N, k=k, teams=d, sag=sag, residual=residual,
                            timing=timing)
     ctx = sd.SparDL(cfg, device=0, graph=graph)
+    if residual != "lres":
+        ctx.set_audit(True)
     ref = orc.pipeline(make_config(P, N, k, d, sag, residual, timing))
     rng = np.random.default_rng(seed)
     for it in range(iters):
@@ -56,6 +58,9 @@ def _run(env, P, d, sag, residual, timing, kind, N, k, iters, seed, graph=True, 
         gi, gv = ctx.global_gradient(0)
         ri, rv = ref.global_gradient()
         assert info["consistent"] == 1, tag
+        if residual != "lres":   # the audit, bit for bit
+            assert info["conservation_error"] == rinfo["conservation_error"], \
+                (tag, info["conservation_error"], rinfo["conservation_error"])
         assert np.array_equal(gi.cpu().numpy().astype(np.int64), ri), tag
         assert np.array_equal(gv.cpu().numpy().view(np.uint32), rv.view(np.uint32)), tag
         if carry_every or it == iters - 1:   # otherwise the finalize stays deferred
