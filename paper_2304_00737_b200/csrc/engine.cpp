@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <set>
@@ -1001,17 +1002,24 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   n += exec_stage(div_stage_);
   if (peer_) n += sdl::launch_publish(div_peer_.pub, div_peer_.npub, epoch_, stream_);
   mark(3);
+  // optional per-step events (profiling diagnostics, SPARDL_STEP_EVENTS=1)
+  auto step_mark = [&](size_t i, int what) {
+    if (ev && !step_ev_.empty()) CK(cudaEventRecord(step_ev_[3 * i + what], stream_));
+  };
   for (size_t i = 0; i < steps_.size(); ++i) {
     const Step& s = steps_[i];
     n += exec_stage(s.stage);
+    step_mark(i, 0);
     if (peer_) n += sdl::launch_publish(step_peer_[i].pub, step_peer_[i].npub, epoch_, stream_);
     if (s.controller_after)
       n += sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1,
                                   stream_);
+    step_mark(i, 1);
     if (i + 1 == steps_.size()) mark(4);
     if (peer_)
       n += sdl::launch_wait(step_peer_[i].wait, step_peer_[i].nwait, epoch_, peer_err_, stream_);
     exec_round(s.xfers);
+    step_mark(i, 2);
   }
   if (steps_.empty()) mark(4);
   n += sdl::launch_assemble(asm_dev_, static_cast<int>(asm_tasks_.size()), m_, cfg_.k, stream_);
@@ -1028,6 +1036,12 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
 void Engine::profile(const float* const* grads, int iters, double* phase_ms) {
   CK(cudaSetDevice(device_));
   run(grads);   // refresh pointer table + warm
+  const char* se = std::getenv("SPARDL_STEP_EVENTS");
+  if (se && se[0] == '1' && step_ev_.empty()) {
+    step_ev_.resize(3 * steps_.size());
+    for (auto& e : step_ev_) CK(cudaEventCreate(&e));
+  }
+  std::vector<double> step_acc(3 * steps_.size(), 0.0);
   cudaEvent_t ev[6];
   for (auto& e : ev) CK(cudaEventCreate(&e));
   double acc[5] = {0, 0, 0, 0, 0};
@@ -1043,6 +1057,17 @@ void Engine::profile(const float* const* grads, int iters, double* phase_ms) {
       CK(cudaEventElapsedTime(&ms, ev[p], ev[p + 1]));
       acc[p] += ms;
     }
+    for (size_t q = 0; q < step_ev_.size(); ++q) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, q == 0 ? ev[3] : step_ev_[q - 1], step_ev_[q]));
+      step_acc[q] += ms;
+    }
+  }
+  if (!step_ev_.empty()) {   // stage / publish / wait of every step, us
+    std::fprintf(stderr, "rank %d steps:", rank_);
+    for (size_t q = 0; q < step_acc.size(); ++q)
+      std::fprintf(stderr, "%s%.1f", q % 3 == 0 ? " | " : " ", 1e3 * step_acc[q] / std::max(iters, 1));
+    std::fprintf(stderr, "\n");
   }
   for (auto& e : ev) cudaEventDestroy(e);
   for (int p = 0; p < 5; ++p) phase_ms[p] = acc[p] / std::max(iters, 1);

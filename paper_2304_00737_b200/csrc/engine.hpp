@@ -177,6 +177,7 @@ class Engine {
   bool use_graph_ = true;
   bool audit_ = false;
   cudaGraphExec_t graph_ = nullptr;
+  std::vector<cudaEvent_t> step_ev_;   // profiling diagnostics (SPARDL_STEP_EVENTS)
   int64_t launches_ = 0;
 
   Arena arena_;

@@ -83,7 +83,12 @@ __global__ void __launch_bounds__(kThreads) k_merge_rank(const MergeTask* __rest
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_merge_part(const MergeTask* __restrict__ tasks) {
+#ifndef SPARDL_MERGE_THREADS
+#define SPARDL_MERGE_THREADS 256
+#endif
+constexpr int kMergeThreads = SPARDL_MERGE_THREADS;   // threads per partition CTA
+
+__global__ void __launch_bounds__(kMergeThreads) k_merge_part(const MergeTask* __restrict__ tasks) {
   pdl_enter();
   const MergeTask& t = tasks[blockIdx.y];
   const int q = blockIdx.x;
@@ -219,7 +224,7 @@ int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r
                          (int)smem);
     configured = smem;
   }
-  launch_pdl(k_merge_part, dim3(max_parts, ntask), dim3(kThreads), smem, s, tasks_dev);
+  launch_pdl(k_merge_part, dim3(max_parts, ntask), dim3(kMergeThreads), smem, s, tasks_dev);
   return 2;
 }
 
