@@ -101,6 +101,7 @@ constexpr int kFinChunk = 1024;              // global entries per CTA
 constexpr int kFinPer = kFinChunk / kThreads;
 
 constexpr int kXiBatch = 4;                  // discard entries per thread per batch
+constexpr int kFinLists = 4;                 // discard lists joined before the carry is read
 constexpr int kMaxXiLists = kThreads / 64;   // bound searches in parallel (2 warps each)
 
 __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __restrict__ tasks) {
@@ -150,28 +151,31 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __res
     if (d_all == 2) return false;
     return key > d_pre || (key == d_pre && j <= d_cut);
   };
-  // global indices of the chunk, then the combined values (two rounds of
-  // independent loads)
   int32_t jj[kFinPer];
-  float x[kFinPer];
 #pragma unroll
   for (int q = 0; q < kFinPer; ++q) {
     const int e = tid + q * kThreads;
     jj[q] = e < nloc ? G.idx[c0 + e] : INT_MAX;
+    gi[e] = jj[q];
   }
-#pragma unroll
-  for (int q = 0; q < kFinPer; ++q) x[q] = jj[q] != INT_MAX ? carry[jj[q]] : 0.f;
-  float acc[kFinPer];
+  const int x0 = t.xi_off[b], x1 = t.xi_off[b + 1];
+  // With <= kFinLists discard lists the join runs first and the carry is
+  // read and written back in one go (its sector is still in L2 for the
+  // write); otherwise the carry is read first and folded list by list.
+  const bool late = x1 - x0 <= kFinLists;
+  float x[kFinPer], acc[kFinPer];
   bool present[kFinPer];
+  int nd[kFinPer];
 #pragma unroll
   for (int q = 0; q < kFinPer; ++q) {
-    gi[tid + q * kThreads] = jj[q];
-    present[q] = jj[q] != INT_MAX && !div_member(mag_key(x[q]), jj[q]);
+    x[q] = (!late && jj[q] != INT_MAX) ? carry[jj[q]] : 0.f;
+    present[q] = !late && jj[q] != INT_MAX && !div_member(mag_key(x[q]), jj[q]);
     acc[q] = present[q] ? x[q] : 0.f;
+    nd[q] = 0;
   }
+  __shared__ float svl[kFinLists][kFinChunk];   // late mode: list li's value per entry
   __syncthreads();
   const int32_t jlo = gi[0], jhi = gi[nloc - 1];
-  const int x0 = t.xi_off[b], x1 = t.xi_off[b + 1];
   for (int xb = x0; xb < x1; xb += kMaxXiLists) {
     const int nx = min(kMaxXiLists, x1 - xb);
     // the sub-range of each discard list inside [jlo, jhi], in parallel
@@ -191,6 +195,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __res
     for (int li = 0; li < nx; ++li) {   // fold in recording order
       const XiList X = t.xi[xb + li];
       const int r0 = range[2 * li], r1 = range[2 * li + 1];
+      float* dst = late ? svl[xb - x0 + li] : sv;
       for (int p0 = r0; p0 < r1; p0 += kThreads * kXiBatch) {
         int32_t xi[kXiBatch];
         int pos[kXiBatch];
@@ -212,21 +217,46 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __res
 #pragma unroll
         for (int u = 0; u < kXiBatch; ++u)
           if (pos[u] >= 0) {
-            sv[pos[u]] = xv[u];
-            sf[pos[u]] = 1;
+            dst[pos[u]] = xv[u];
+            sf[pos[u]] = (unsigned char)(sf[pos[u]] | (1u << li));
           }
       }
+      if (late) {
+        __syncthreads();   // sf[e] is or-ed by list; one list at a time
+      } else {
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kFinPer; ++q) {
+          const int e = tid + q * kThreads;
+          if (e < nloc && sf[e]) {
+            acc[q] = present[q] ? __fadd_rn(acc[q], sv[e]) : sv[e];
+            present[q] = true;
+            sf[e] = 0;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (late) {   // bit li of sf[e]: list li holds entry e (all lists of this batch)
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < kFinPer; ++q) {
-        const int e = tid + q * kThreads;
-        if (e < nloc && sf[e]) {
-          acc[q] = present[q] ? __fadd_rn(acc[q], sv[e]) : sv[e];
+      for (int q = 0; q < kFinPer; ++q) nd[q] = sf[tid + q * kThreads];
+    }
+  }
+  if (late) {   // read, fold and write back each entry's carry together
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) x[q] = jj[q] != INT_MAX ? carry[jj[q]] : 0.f;
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) {
+      const int e = tid + q * kThreads;
+      present[q] = jj[q] != INT_MAX && !div_member(mag_key(x[q]), jj[q]);
+      acc[q] = present[q] ? x[q] : 0.f;
+      for (int li = 0; li < x1 - x0; ++li)
+        if ((nd[q] >> li) & 1) {
+          const float v = svl[li][e];
+          acc[q] = present[q] ? __fadd_rn(acc[q], v) : v;
           present[q] = true;
-          sf[e] = 0;
         }
-      }
-      __syncthreads();
     }
   }
 #pragma unroll
