@@ -104,7 +104,10 @@ constexpr int kXiBatch = 4;                  // discard entries per thread per b
 constexpr int kFinLists = 4;                 // discard lists joined before the carry is read
 constexpr int kMaxXiLists = kThreads / 64;   // bound searches in parallel (2 warps each)
 
-__global__ void __launch_bounds__(kThreads) k_finalize(const FinalizeTask* __restrict__ tasks) {
+#ifndef SPARDL_FIN_MINB
+#define SPARDL_FIN_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB) k_finalize(const FinalizeTask* __restrict__ tasks) {
   pdl_enter();
   const FinalizeTask& t = tasks[blockIdx.z];
   if (t.mode == 2) return;   // lres ignores the global gradient
