@@ -121,6 +121,10 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
     CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     own_stream_ = true;
   }
+  // a side stream for the work that may run beside the residual finalize
+  CK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   if (world_ > 1) {
     if (!nccl_id) sdlh::fail(SPARDL_E_ARG, "world_size > 1 needs an NCCL unique id");
     ncclUniqueId id;
@@ -165,6 +169,9 @@ Engine::~Engine() {
   if (comm_) ncclCommDestroy(comm_);
   for (float* c : carry_) cudaFree(c);
   if (gtab_host_) cudaFreeHost(gtab_host_);
+  if (side_) cudaStreamDestroy(side_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
   if (own_stream_) cudaStreamDestroy(stream_);
 }
 
@@ -1022,10 +1029,16 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
     step_mark(i, 2);
   }
   if (steps_.empty()) mark(4);
-  n += sdl::launch_assemble(asm_dev_, static_cast<int>(asm_tasks_.size()), m_, cfg_.k, stream_);
+  // the assembled global gradient and the ledger only read the gathered
+  // blocks: they run on a side stream beside the residual finalize
+  CK(cudaEventRecord(ev_fork_, stream_));
+  CK(cudaStreamWaitEvent(side_, ev_fork_, 0));
+  n += sdl::launch_assemble(asm_dev_, static_cast<int>(asm_tasks_.size()), m_, cfg_.k, side_);
+  n += sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), side_);
   n += sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), Lcap_, m_,
                             static_cast<int>(fin_max_div_), stream_);
-  n += sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), stream_);
+  CK(cudaEventRecord(ev_join_, side_));
+  CK(cudaStreamWaitEvent(stream_, ev_join_, 0));
   // last remote read of the iteration done: peers may overwrite their buffers
   if (peer_) n += sdl::launch_publish(done_dev_, npeer_, epoch_, stream_);
   mark(5);

@@ -172,6 +172,8 @@ class Engine {
   sdlh::Partition part_;
   int device_ = 0, world_ = 1, rank_ = 0, wloc_ = 1, first_ = 0;
   cudaStream_t stream_ = nullptr;
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   bool own_stream_ = false;
   ncclComm_t comm_ = nullptr;
   bool use_graph_ = true;
