@@ -89,7 +89,7 @@ struct RadixState {     // lives in CTA 0, read by the cluster through DSMEM
   int64_t total;
   int64_t budget;
   int32_t all;          // 1: everything kept, 2: nothing kept, 0: threshold
-  int32_t pad_;
+  int32_t hit;          // the guessed top digit held the rank
 };
 
 struct CtaTotals {      // per-CTA counters exchanged through DSMEM
@@ -444,6 +444,9 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
 
   const int mode = resolve_mode(t);
   const int nseg = nseg_of(t, mode);
+  // the previous run's threshold: its top digit is this run's first guess
+  const uint32_t prev_T = sc->prefix;
+  const bool have_prev = sc->all == 0 && prev_T != 0;
 
   auto stamp = [&](int i) {
     if (cr == 0 && threadIdx.x == 0) {
@@ -550,6 +553,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     st.pmask = 0;
     st.rank = budget;
     st.all = total <= budget ? 1 : (budget <= 0 ? 2 : 0);   // identity case, sparse.hpp:143-146
+    st.hit = 0;
     sc->cut_idx = -1;
   }
   if (threadIdx.x == 0) {
@@ -559,6 +563,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     my.pmask = 0;
     my.rank = budget;
     my.all = total <= budget ? 1 : (budget <= 0 ? 2 : 0);
+    my.hit = 0;
   }
   cluster.sync();   // CTA 0's aggregation histogram is zeroed; tables are visible
   stamp(1);
@@ -579,9 +584,81 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   auto ldi = [&](const int32_t* p) { return FUSED ? __ldcg(p) : __ldg(p); };
 
   // ---- 2. radix passes: warp w histograms chunks w, w + kWarps, ...
+  int first_pass = 0;
+  if (my.all == 0 && have_prev) {
+    // One pass with the previous threshold's top digit d0 as a guess: the
+    // histogram of the next 11 bits of the entries in d0, and the counts
+    // above and inside d0.  If d0 holds the rank, pass 0 is skipped.
+    const uint32_t d0 = prev_T >> 20;
+    for (int b = threadIdx.x; b < kBins; b += kSelThreads) hist[b] = 0;
+    __syncthreads();
+    long long above = 0, inside = 0;
+    for (int k = warp; k < nit; k += kWarps) {
+      const int c = ilen[k];
+      const float* __restrict__ vp = vbase + iof[k];
+      for (int j0 = 0; j0 < c; j0 += kChunkE) {
+        uint32_t key[kIlp];
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+          const int j = j0 + u * 32 + lane;
+          key[u] = j < c ? mag_key(ldv(vp + j)) : kHoleKey;
+        }
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+          const bool valid = key[u] != kHoleKey;
+          const uint32_t top = key[u] >> 20;
+          above += valid && top > d0;
+          inside += valid && top == d0;
+          hist_add(hist, (key[u] >> 9) & (kBins - 1), valid && top == d0);
+        }
+      }
+    }
+    above = block_sum_ll(above, lscr);
+    inside = block_sum_ll(inside, lscr);
+    if (threadIdx.x == 0) tot0[cr] = {0, above, inside};
+    cluster.sync();
+    {
+      const int per = kBins / CL;
+      for (int b = cr * per + threadIdx.x; b < (cr + 1) * per; b += kSelThreads) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < CL; ++q) sum += cluster.map_shared_rank(hist, q)[b];
+        agg0[b] = sum;
+      }
+    }
+    cluster.sync();
+    if (cr == 0) {
+      __shared__ int s_hit;
+      if (threadIdx.x == 0) {
+        long long a = 0, in = 0;
+        for (int q = 0; q < CL; ++q) {
+          a += tot[q].gt;
+          in += tot[q].eq;
+        }
+        const int hit = a < st.rank && st.rank <= a + in;
+        s_hit = hit;
+        st.hit = hit;
+        if (hit) {
+          st.prefix = d0 << 20;
+          st.pmask = (uint32_t)(kBins - 1) << 20;
+          st.rank -= a;
+        }
+      }
+      __syncthreads();
+      if (s_hit) {
+        find_digit(agg, kBins, 9, &st, suf);
+      } else {
+        for (int b = threadIdx.x; b < kBins; b += kSelThreads) agg[b] = 0;
+      }
+    }
+    cluster.sync();
+    if (threadIdx.x == 0) my = *st0;
+    __syncthreads();
+    if (my.hit) first_pass = 2;
+  }
   if (my.all == 0) {
 #pragma unroll 1
-    for (int pass = 0; pass < 3; ++pass) {
+    for (int pass = first_pass; pass < 3; ++pass) {
       const int shift = pass == 0 ? 20 : (pass == 1 ? 9 : 0);
       const int nb = pass == 2 ? 512 : kBins;
       for (int b = threadIdx.x; b < nb; b += kSelThreads) hist[b] = 0;
