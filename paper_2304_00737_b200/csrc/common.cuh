@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "kernels.cuh"
+
 namespace sdl {
 
 // Magnitude key: |v| ordering == unsigned ordering of the low 31 bits for
@@ -159,6 +161,59 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   lc.attrs = at;
   lc.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&lc, kernel, static_cast<KArgs>(args)...);
+}
+
+
+// ---------------------------------------------------------------------------
+// Peer-transport flags (transport.cu): system-scope acquire/release on
+// per-block readiness flags; bounded spins report through *err.
+constexpr unsigned long long kTimeoutNs = 10ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(long long* p, long long v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ inline void spin_until(const long long* flag, long long target, int32_t* err) {
+  if (ld_acquire_sys(flag) >= target) return;
+  const unsigned long long t0 = gtime();
+  unsigned ns = 32;
+  while (ld_acquire_sys(flag) < target) {
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+    if (gtime() - t0 > kTimeoutNs) {
+      atomicExch(err, 1);
+      return;
+    }
+  }
+}
+
+
+// a whole CTA: wait until the task's remote inputs are published
+__device__ inline void peer_wait(const PeerSync& ps) {
+  if (ps.nwait <= 0) return;   // uniform per task
+  const long long e = *ps.epoch;
+  for (int i = threadIdx.x; i < ps.nwait; i += blockDim.x) spin_until(ps.wait[i], e, ps.err);
+  __syncthreads();
+}
+
+// one thread, after the task's output is complete: publish it to its consumers
+__device__ inline void peer_publish(const PeerSync& ps) {
+  if (ps.npub <= 0) return;
+  const long long e = *ps.epoch;
+  __threadfence_system();
+  for (int i = 0; i < ps.npub; ++i) st_release_sys(ps.pub[i], e);
 }
 
 }  // namespace sdl

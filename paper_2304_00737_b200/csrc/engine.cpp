@@ -241,7 +241,9 @@ Slot Engine::make_slot(int uid) {
   return s;
 }
 
-void Engine::add_select(Stage& st, const sdl::SelTask& t0) {
+void Engine::add_select(Stage& st, const sdl::SelTask& t0, int out_uid, int in_uid) {
+  st.sel_uid.push_back(out_uid);
+  st.sel_in.push_back(in_uid);
   sdl::SelTask t = t0;
   // t.stride carries the longest possible input segment (see callers)
   sdl::sel_prepare(t, t.stride);
@@ -309,6 +311,7 @@ sdl::SelTask Engine::select_from_merge(Stage& st, const std::vector<int>& pieces
   mt.seg_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * parts));
   st.merges.push_back(mt);
   st.merge_cap.push_back(capsum);
+  st.merge_in.push_back(pieces);
   st.max_parts = std::max<int>(st.max_parts, static_cast<int>(parts));
   st.max_rT = std::max<int>(st.max_rT, static_cast<int>(r * T));
 
@@ -358,7 +361,7 @@ int Engine::materialize(int w, int pos, std::vector<int> pieces, int64_t budget,
   t.dis_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
   xi_[static_cast<size_t>(li)][static_cast<size_t>(xi_block)].push_back(
       {t.dis_idx, t.dis_val, t.dis_cnt});
-  add_select(st, t);
+  add_select(st, t, uid, pieces.size() == 1 ? pieces[0] : -1);
   return uid;
 }
 
@@ -482,7 +485,7 @@ void Engine::plan() {
       t.sel_idx = out.idx;
       t.sel_val = out.val;
       t.sel_cnt = out.cnt;
-      add_select(div_stage_, t);
+      add_select(div_stage_, t, uid, -1);
       div_scr_[static_cast<size_t>(li)][static_cast<size_t>(b)] = div_stage_.sels.back().scr;
     }
   }
@@ -686,6 +689,7 @@ void Engine::plan() {
     at.out_cnt = gs.cnt;
     at.out_hash = hash_dev_ + t;
     asm_tasks_.push_back(at);
+    asm_in_.push_back(team_blocks[static_cast<size_t>(t)]);
     for (int j = 0; j < m_; ++j)
       if (is_local(t * m_ + j))
         team_of_local_global_[static_cast<size_t>(t * m_ + j - first_)] =
@@ -909,40 +913,67 @@ void Engine::plan_peer() {
     if (!v.empty()) CK(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
     return d;
   };
-  std::set<std::pair<int, int>> seen;
-  std::vector<long long*> div_pub;
-  std::vector<std::vector<long long*>> pub(steps_.size());
+  // every block delivered to another rank must come out of a planned stage
   for (const auto& dl : deliveries_) {
-    const int uid = dl.first, dst = dl.second;
-    if (rank_of(uid_owner_[static_cast<size_t>(uid)]) != rank_ || dst == rank_) continue;
-    if (!seen.insert(dl).second) continue;
-    if (div_stage_.produced.count(uid)) {
-      div_pub.push_back(flag_at(dst, uid));
-      continue;
-    }
-    bool found = false;
-    for (size_t i = 0; i < steps_.size() && !found; ++i)
-      if (steps_[i].stage.produced.count(uid)) {
-        pub[i].push_back(flag_at(dst, uid));
-        found = true;
-      }
+    const int uid = dl.first;
+    if (rank_of(uid_owner_[static_cast<size_t>(uid)]) != rank_ || dl.second == rank_) continue;
+    bool found = div_stage_.produced.count(uid) != 0;
+    for (size_t i = 0; i < steps_.size() && !found; ++i) found = steps_[i].stage.produced.count(uid) != 0;
     if (!found) sdlh::fail(SPARDL_E_ERROR, "internal: delivered block has no producing stage");
   }
-  div_peer_.pub = upload(div_pub);
-  div_peer_.npub = static_cast<int>(div_pub.size());
-  step_peer_.assign(steps_.size(), PeerLists{});
-  for (size_t i = 0; i < steps_.size(); ++i) {
-    std::vector<const long long*> w;
-    std::set<int> uids;
-    for (const Xfer& x : steps_[i].xfers)
-      if (x.dst_rank == rank_ && rank_of(uid_owner_[static_cast<size_t>(x.uid)]) != rank_ &&
-          uids.insert(x.uid).second)
-        w.push_back(flag_at(rank_, x.uid));
-    step_peer_[i].pub = upload(pub[i]);
-    step_peer_[i].npub = static_cast<int>(pub[i].size());
-    step_peer_[i].wait = upload(w);
-    step_peer_[i].nwait = static_cast<int>(w.size());
-  }
+  // per-task synchronisation: a select publishes its block as soon as it is
+  // complete; a merge, a single-block select and an assembly wait for their
+  // own remote inputs (no stage-wide publish / wait kernels)
+  std::map<int, std::set<int>> dsts;   // uid -> ranks it is delivered to
+  for (const auto& dl : deliveries_)
+    if (dl.second != rank_ && rank_of(uid_owner_[static_cast<size_t>(dl.first)]) == rank_)
+      dsts[dl.first].insert(dl.second);
+  auto pubs_of = [&](int uid) {
+    std::vector<long long*> v;
+    auto it = dsts.find(uid);
+    if (it != dsts.end())
+      for (int d : it->second) v.push_back(flag_at(d, uid));
+    return v;
+  };
+  auto waits_of = [&](const std::vector<int>& uids) {
+    std::vector<const long long*> v;
+    for (int u : uids)
+      if (u >= 0 && rank_of(uid_owner_[static_cast<size_t>(u)]) != rank_) v.push_back(flag_at(rank_, u));
+    return v;
+  };
+  auto sync_of = [&](const std::vector<const long long*>& w, const std::vector<long long*>& p) {
+    sdl::PeerSync ps{};
+    ps.wait = w.empty() ? nullptr : upload(w);
+    ps.nwait = static_cast<int32_t>(w.size());
+    ps.pub = p.empty() ? nullptr : upload(p);
+    ps.npub = static_cast<int32_t>(p.size());
+    ps.epoch = epoch_;
+    ps.err = peer_err_;
+    return ps;
+  };
+  auto wire_stage = [&](Stage& st) {
+    for (size_t j = 0; j < st.merges.size(); ++j) st.merges[j].ps = sync_of(waits_of(st.merge_in[j]), {});
+    for (size_t i = 0; i < st.sels.size(); ++i) {
+      sdl::SelTask& t = st.sels[i];
+      std::vector<int> in;
+      if (st.sel_in[i] >= 0) in.push_back(st.sel_in[i]);
+      if (st.fused && t.merge_slot) in = st.merge_in[static_cast<size_t>(t.merge_slot - 1)];
+      t.ps = sync_of(waits_of(in), pubs_of(st.sel_uid[i]));
+    }
+    if (!st.merges.empty())
+      CK(cudaMemcpy(st.merges_dev, st.merges.data(), sizeof(sdl::MergeTask) * st.merges.size(),
+                    cudaMemcpyHostToDevice));
+    if (!st.sels.empty())
+      CK(cudaMemcpy(st.sels_dev, st.sels.data(), sizeof(sdl::SelTask) * st.sels.size(),
+                    cudaMemcpyHostToDevice));
+  };
+  wire_stage(div_stage_);
+  for (Step& stp : steps_) wire_stage(stp.stage);
+  for (size_t q = 0; q < asm_tasks_.size(); ++q) asm_tasks_[q].ps = sync_of(waits_of(asm_in_[q]), {});
+  if (!asm_tasks_.empty())
+    CK(cudaMemcpy(asm_dev_, asm_tasks_.data(), sizeof(sdl::AssembleTask) * asm_tasks_.size(),
+                  cudaMemcpyHostToDevice));
+
   std::vector<const long long*> begin;
   std::vector<long long*> done;
   for (int q = 0; q < world_; ++q) {
@@ -1006,8 +1037,7 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   n += sdl::launch_divide(div_dev_, static_cast<int>(div_tasks_.size()), div_max_chunks_,
                           div_sample_every_, 1, stream_, 2);
   mark(2);
-  n += exec_stage(div_stage_);
-  if (peer_) n += sdl::launch_publish(div_peer_.pub, div_peer_.npub, epoch_, stream_);
+  n += exec_stage(div_stage_);   // (peer transport: each select publishes its block)
   mark(3);
   // optional per-step events (profiling diagnostics, SPARDL_STEP_EVENTS=1)
   auto step_mark = [&](size_t i, int what) {
@@ -1017,15 +1047,12 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
     const Step& s = steps_[i];
     n += exec_stage(s.stage);
     step_mark(i, 0);
-    if (peer_) n += sdl::launch_publish(step_peer_[i].pub, step_peer_[i].npub, epoch_, stream_);
     if (s.controller_after)
       n += sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1,
                                   stream_);
     step_mark(i, 1);
     if (i + 1 == steps_.size()) mark(4);
-    if (peer_)
-      n += sdl::launch_wait(step_peer_[i].wait, step_peer_[i].nwait, epoch_, peer_err_, stream_);
-    exec_round(s.xfers);
+    exec_round(s.xfers);   // NCCL transport only: peers wait per task
     step_mark(i, 2);
   }
   if (steps_.empty()) mark(4);

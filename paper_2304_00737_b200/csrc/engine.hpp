@@ -70,6 +70,9 @@ struct Stage {           // one batch of merge + select tasks
   int max_nseg = 0;
   std::set<int> produced;    // uids written by this stage (dependency guard)
   std::vector<int64_t> merge_cap;   // input capacity of each merge task
+  std::vector<std::vector<int>> merge_in;   // input block uids of each merge task
+  std::vector<int> sel_uid;         // output block uid of each select task
+  std::vector<int> sel_in;          // input block uid of a single-block select, else -1
   bool fused = false;        // merges run inside the select kernel (no merge launches)
   int cl = 0;                // fused: cluster width
   int win_cap = 0;           // fused: window entries per CTA
@@ -143,7 +146,7 @@ class Engine {
   Slot sym_slot(int uid) const;   // uid's buffer in its owner's symmetric region
   int materialize(int w, int pos, std::vector<int> pieces, int64_t budget, float weight,
                   const int64_t* budget_dev, int64_t* total_out, Stage& st, int xi_block);
-  void add_select(Stage& st, const sdl::SelTask& t);
+  void add_select(Stage& st, const sdl::SelTask& t, int out_uid, int in_uid);
   sdl::SelTask select_from_slot(const Slot& in);
   sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);
   void finish_stage(Stage& st);
@@ -210,6 +213,7 @@ class Engine {
   std::vector<sdl::LedgerAdd> ledger_adds_;
   sdl::LedgerAdd* ledger_dev_ = nullptr;
   std::vector<sdl::AssembleTask> asm_tasks_;
+  std::vector<std::vector<int>> asm_in_;     // source block uids of each assembly
   sdl::AssembleTask* asm_dev_ = nullptr;
   std::vector<sdl::FinalizeTask> fin_tasks_;
   sdl::FinalizeTask* fin_dev_ = nullptr;
@@ -228,12 +232,6 @@ class Engine {
   bool ran_ = false;
 
   // --- peer-memory transport (transport.cu); NCCL send/recv when off
-  struct PeerLists {
-    long long** pub = nullptr;          // device: remote flags to publish after the stage
-    int npub = 0;
-    const long long** wait = nullptr;   // device: local flags to wait for at the round
-    int nwait = 0;
-  };
   void setup_peer();                    // before plan(): symmetric region + IPC mappings
   void plan_peer();                     // after plan(): publish / wait lists
   bool peer_ = false;
@@ -245,8 +243,6 @@ class Engine {
   std::vector<std::pair<int, int>> deliveries_;   // (uid, destination rank), whole plan
   long long* epoch_ = nullptr;
   int32_t* peer_err_ = nullptr;
-  PeerLists div_peer_;
-  std::vector<PeerLists> step_peer_;
   const long long** begin_dev_ = nullptr;
   long long** done_dev_ = nullptr;
   int npeer_ = 0;

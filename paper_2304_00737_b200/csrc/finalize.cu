@@ -16,6 +16,7 @@ namespace {
 __global__ void __launch_bounds__(kThreads) k_assemble(const AssembleTask* __restrict__ tasks) {
   pdl_enter();
   const AssembleTask& t = tasks[blockIdx.y];
+  peer_wait(t.ps);   // the gathered blocks of other GPUs are published
   __shared__ int off[65];
   if (threadIdx.x == 0) {
     int s = 0;

@@ -36,6 +36,19 @@ constexpr int kMaxSegPerTask = 8192;   // select work items per task (smem bound
 constexpr int kSampShift = 18;         // dividing sample histogram: key >> 18
 constexpr int kSampBins = 1 << (31 - kSampShift);   // 8192 bins (1/32 octave)
 
+// Peer-transport synchronisation carried by a task (empty lists: none): the
+// task first waits until the flags of its remote inputs reach the iteration
+// epoch, and its producer publishes the epoch to the consumers' flags of its
+// output as soon as the output is complete.
+struct PeerSync {
+  const long long* const* wait;   // local flags of remote inputs
+  long long* const* pub;          // consumers' flags of this task's output
+  int32_t nwait;
+  int32_t npub;
+  const long long* epoch;
+  int32_t* err;                   // timeout flag
+};
+
 struct SelTask;
 // Host helper: fills the derived work-decomposition fields of a select task
 // (tiles per input segment; dense tiles) given the largest possible length of
@@ -133,6 +146,7 @@ struct SelTask {
   const struct MergeTask* merge;
   int32_t merge_slot;    // host bookkeeping: 1 + index of the stage's merge task, 0 none
   int32_t pad3_;
+  PeerSync ps;           // waits on remote inputs, publishes the output
 };
 
 // value bits of a merge hole: its magnitude key is kHoleKey, never a real
@@ -147,6 +161,7 @@ constexpr int kMergeSamples = 2048;   // fused merge: splitter samples per task
 struct MergeTask {
   int32_t r;
   int32_t T;                        // window (sample spacing) per list
+  PeerSync ps;                      // waits on remote input lists
   const int32_t* in_idx[kMaxR];
   const float* in_val[kMaxR];
   const int32_t* in_cnt[kMaxR];
@@ -242,6 +257,7 @@ struct AssembleTask {
   float* out_val;
   int32_t* out_cnt;
   int64_t* out_hash;          // nullable: FNV-style hash for consistency checks
+  PeerSync ps;                // waits on remote source blocks
 };
 int launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t max_k,
                      cudaStream_t s);
@@ -298,7 +314,5 @@ int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStre
 int launch_begin(long long* epoch, const long long* const* done, int n, int32_t* err,
                  cudaStream_t s);
 int launch_publish(long long* const* targets, int n, const long long* epoch, cudaStream_t s);
-int launch_wait(const long long* const* flags, int n, const long long* epoch, int32_t* err,
-                cudaStream_t s);
 
 }  // namespace sdl

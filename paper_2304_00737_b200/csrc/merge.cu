@@ -35,6 +35,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __global__ void __launch_bounds__(kThreads) k_merge_rank(const MergeTask* __restrict__ tasks) {
   pdl_enter();
   const MergeTask& t = tasks[blockIdx.y];
+  peer_wait(t.ps);   // remote input lists published (k_merge_part follows in order)
   const int r = t.r, T = t.T;
   __shared__ int32_t samp[kMaxSamples];
   __shared__ int base[kMaxR + 1];

@@ -442,6 +442,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   uint32_t* agg0 = cluster.map_shared_rank(agg, 0);
   CtaTotals* tot0 = cluster.map_shared_rank(tot, 0);
 
+  peer_wait(t.ps);   // remote inputs (a slot, or the fused merge's lists)
   const int mode = resolve_mode(t);
   const int nseg = nseg_of(t, mode);
   // the previous run's threshold: its top digit is this run's first guess
@@ -897,6 +898,9 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   }
   stamp(11);
   cluster.sync();   // keep CTA 0's shared memory alive until every reader is done
+  // every CTA's output writes are ordered before this (cluster barrier):
+  // the block can go to its consumers now, not at the end of the batch
+  if (cr == 0 && threadIdx.x == 0) peer_publish(t.ps);
 }
 
 }  // namespace

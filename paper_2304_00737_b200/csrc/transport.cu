@@ -9,11 +9,13 @@
 // see fresh values):
 //   k_begin    e = ++epoch; wait until every peer finished iteration e-1
 //              (peers may still read our block buffers until then)
-//   k_publish  after the stage producing a block: fence, then store e into
-//              the consumer's flag for that block (remote store)
-//   k_wait     at the round that delivers a block: spin (acquire, system
-//              scope) until the local flag for the block reaches e
-//   k_done     after the last remote read of the iteration: store e into
+//   publish    the select producing a block, as soon as its cluster is done:
+//              fence, then store e into each consumer's flag for the block
+//              (remote store; peer_publish, common.cuh)
+//   wait       the merge, single-block select or assembly consuming a remote
+//              block: spin (acquire, system scope) until its local flag
+//              reaches e (peer_wait, common.cuh)
+//   k_publish  after the last remote read of the iteration: store e into
 //              every peer's done[rank] flag
 // Waits are bounded (~10 s): a peer that never arrives sets *err and the next
 // sync() reports it instead of hanging the device.
@@ -23,38 +25,6 @@
 namespace sdl {
 
 namespace {
-
-constexpr unsigned long long kTimeoutNs = 10ull * 1000 * 1000 * 1000;
-
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
-  long long v;
-  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release_sys(long long* p, long long v) {
-  asm volatile("st.release.sys.global.b64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
-}
-
-__device__ void spin_until(const long long* flag, long long target, int32_t* err) {
-  if (ld_acquire_sys(flag) >= target) return;
-  const unsigned long long t0 = gtime();
-  unsigned ns = 32;
-  while (ld_acquire_sys(flag) < target) {
-    __nanosleep(ns);
-    if (ns < 1024) ns <<= 1;
-    if (gtime() - t0 > kTimeoutNs) {
-      atomicExch(err, 1);
-      return;
-    }
-  }
-}
 
 __global__ void k_begin(long long* epoch, const long long* const* done, int n, int32_t* err) {
   pdl_enter();
@@ -76,11 +46,6 @@ __global__ void k_publish(long long* const* targets, int n, const long long* epo
   st_release_sys(targets[i], e);
 }
 
-__global__ void k_wait(const long long* const* flags, int n, const long long* epoch, int32_t* err) {
-  pdl_enter();
-  const long long e = *epoch;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) spin_until(flags[i], e, err);
-}
 
 }  // namespace
 
@@ -96,11 +61,5 @@ int launch_publish(long long* const* targets, int n, const long long* epoch, cud
   return 1;
 }
 
-int launch_wait(const long long* const* flags, int n, const long long* epoch, int32_t* err,
-                cudaStream_t s) {
-  if (n <= 0) return 0;
-  launch_pdl(k_wait, dim3(1), dim3(128), 0, s, flags, n, epoch, err);
-  return 1;
-}
 
 }  // namespace sdl
