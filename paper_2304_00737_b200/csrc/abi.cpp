@@ -451,6 +451,11 @@ struct spardl_ctx {
   std::unique_ptr<sdle::Engine> eng;
   std::vector<float*> staging;     // device copies of host gradients (allreduce_host)
   std::vector<const float*> staging_c;
+  cudaEvent_t ev_up = nullptr, ev_up2 = nullptr;   // upload fork / join
+  ~spardl_ctx() {
+    if (ev_up) cudaEventDestroy(ev_up);
+    if (ev_up2) cudaEventDestroy(ev_up2);
+  }
 };
 
 EXPORT int spardl_nccl_unique_id(void* out128) {
@@ -561,11 +566,22 @@ EXPORT int spardl_allreduce_host(spardl_ctx* ctx, const float* const* grads_host
       }
     }
     cudaStream_t s = e.stream();
+    // the uploads alternate between two streams (two copy engines on the
+    // link) and join before the iteration
+    cudaStream_t s2 = e.side_stream();
+    if (!ctx->ev_up) {
+      CK(cudaEventCreateWithFlags(&ctx->ev_up, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_up2, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ctx->ev_up, s));
+    CK(cudaStreamWaitEvent(s2, ctx->ev_up, 0));
     for (int i = 0; i < wl; ++i) {
       need(grads_host[i], "grads[i]");
       CK(cudaMemcpyAsync(ctx->staging[static_cast<size_t>(i)], grads_host[i], bytes,
-                         cudaMemcpyHostToDevice, s));
+                         cudaMemcpyHostToDevice, (i & 1) ? s2 : s));
     }
+    CK(cudaEventRecord(ctx->ev_up2, s2));
+    CK(cudaStreamWaitEvent(s, ctx->ev_up2, 0));
     e.run(ctx->staging_c.data());
     const int32_t* di = nullptr;
     const float* dv = nullptr;

@@ -125,6 +125,7 @@ class Engine {
   int local_workers() const { return wloc_; }
   int64_t launches_per_iter() const { return launches_; }
   cudaStream_t stream() const { return stream_; }
+  cudaStream_t side_stream() const { return side_; }
   void set_graph(bool on) {
     use_graph_ = on;
     drop_graph();
