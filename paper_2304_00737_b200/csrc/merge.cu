@@ -91,8 +91,11 @@ constexpr int kMergeThreads = SPARDL_MERGE_THREADS;   // threads per partition C
 
 __global__ void __launch_bounds__(kMergeThreads) k_merge_part(const MergeTask* __restrict__ tasks) {
   pdl_enter();
-  const MergeTask& t = tasks[blockIdx.y];
-  const int q = blockIdx.x;
+  // grid (task, partition): partitions of every task come first in launch
+  // order, so the live ones (q < nparts, usually far fewer than max_parts)
+  // all start in the first wave
+  const MergeTask& t = tasks[blockIdx.x];
+  const int q = blockIdx.y;
   const int S = *t.nparts;
   if (q >= t.max_parts) return;
   if (q >= S) {
@@ -225,7 +228,7 @@ int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r
                          (int)smem);
     configured = smem;
   }
-  launch_pdl(k_merge_part, dim3(max_parts, ntask), dim3(kMergeThreads), smem, s, tasks_dev);
+  launch_pdl(k_merge_part, dim3(ntask, max_parts), dim3(kMergeThreads), smem, s, tasks_dev);
   return 2;
 }
 

@@ -177,7 +177,6 @@ __device__ void find_digit(uint32_t* agg, int nb, int shift, RadixState* st, lon
     }
   }
   __syncthreads();
-  for (int q = 0; q < bpt; ++q) agg[threadIdx.x * bpt + q] = 0;   // ready for the next pass
 }
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
@@ -420,28 +419,31 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   __shared__ uint32_t hist[kBins];
-  __shared__ uint32_t agg[kBins];                   // meaningful in CTA 0
-  __shared__ RadixState st;                         // meaningful in CTA 0
-  __shared__ CtaTotals tot[CL];                     // meaningful in CTA 0
+  __shared__ uint32_t agg[kBins];                   // cluster-wide histogram (every CTA a copy)
+  __shared__ CtaTotals tot[CL];                     // every CTA's totals (every CTA a copy)
   __shared__ long long suf[kSelThreads];
   __shared__ int scratch[40];
   __shared__ long long lscr[32];
-  __shared__ RadixState my;                         // this CTA's copy of CTA 0's state
+  __shared__ RadixState my;                         // radix state (identical in every CTA)
   // this CTA's work items: contiguous pieces of its segments, <= plen long
   // (item i = input elements [iof[i], iof[i] + ilen[i])), so the warps share
   // long merge partitions evenly and never re-read segment bounds
   extern __shared__ int32_t dyn[];
   int32_t* iof = dyn;
   int32_t* ilen = dyn + tab_cap;
+  // per-item counters (#above, #equal, #entries -> output offsets and tie
+  // quota), kept on chip: the scan and the compaction read them without a
+  // round trip to L2
+  int32_t* c_a = dyn + 2 * tab_cap;
+  int32_t* c_b = dyn + 3 * tab_cap;
+  int32_t* c_c = dyn + 4 * tab_cap;
   // fused merge: the CTA's input windows and the task's splitter samples
-  int32_t* w_idx = dyn + 2 * tab_cap;
+  int32_t* w_idx = dyn + 5 * tab_cap;
   float* w_val = reinterpret_cast<float*>(w_idx + win_cap);
   int32_t* samp = reinterpret_cast<int32_t*>(w_val + win_cap);
 
-  RadixState* st0 = cluster.map_shared_rank(&st, 0);
-  uint32_t* agg0 = cluster.map_shared_rank(agg, 0);
-  CtaTotals* tot0 = cluster.map_shared_rank(tot, 0);
 
+  if (!FUSED) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   peer_wait(t.ps);   // remote inputs (a slot, or the fused merge's lists)
   const int mode = resolve_mode(t);
   const int nseg = nseg_of(t, mode);
@@ -508,17 +510,14 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   }
   const int s0 = s_lo, s1 = s_hi;
   const int nloc = s1 - s0;
-  // ---- 1b. the work items of this CTA; its per-item scratch starts at
-  // s0 + (entries before it) / kChunkE + cr (disjoint across the cluster)
+  // ---- 1b. the work items of this CTA
   {
-    long long before = 0, here = 0;
-    for (int s = threadIdx.x; s < s1; s += kSelThreads) {
+    long long here = 0;
+    for (int s = s0 + threadIdx.x; s < s1; s += kSelThreads) {
       int off, c;
       seg_bounds(t, mode, s, off, c);
-      if (s < s0) before += c;
-      else here += c;
+      here += c;
     }
-    before = block_sum_ll(before, lscr);
     here = block_sum_ll(here, lscr);
     // smallest piece length (kChunkE * 2^j) whose items fit the table
     long long plen = kChunkE;
@@ -541,48 +540,63 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       s_nit = min(carry, tab_cap);
       s_plen = (int)plen;
       s_F = (int)here;
-      s_before = s0 + (int)(before / kChunkE) + cr;
     }
   }
   }
-  for (int b = threadIdx.x; b < kBins; b += kSelThreads) agg[b] = 0;
   const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
-  if (cr == 0 && threadIdx.x == 0) {
-    st.total = total;
-    st.budget = budget;
-    st.prefix = 0;
-    st.pmask = 0;
-    st.rank = budget;
-    st.all = total <= budget ? 1 : (budget <= 0 ? 2 : 0);   // identity case, sparse.hpp:143-146
-    st.hit = 0;
-    sc->cut_idx = -1;
-  }
+  if (cr == 0 && threadIdx.x == 0) sc->cut_idx = -1;
   if (threadIdx.x == 0) {
     my.total = total;
     my.budget = budget;
     my.prefix = 0;
     my.pmask = 0;
     my.rank = budget;
-    my.all = total <= budget ? 1 : (budget <= 0 ? 2 : 0);
+    my.all = total <= budget ? 1 : (budget <= 0 ? 2 : 0);   // identity case, sparse.hpp:143-146
     my.hit = 0;
   }
-  cluster.sync();   // CTA 0's aggregation histogram is zeroed; tables are visible
+  // the fused prologue's totals live in CTA 0's `tot`, which the exchanges
+  // below overwrite: every CTA must have read them first
+  if (FUSED) {
+    cluster.sync();
+  } else {
+    // every CTA of the cluster has started (arrived at kernel entry): its
+    // shared memory may be accessed from here on
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    __syncthreads();
+  }
   stamp(1);
   const int nit = s_nit;
-  // per-item counters of this CTA (task scratch, L2 resident)
-  int* c_gt = t.seg_gt + s_before;
-  int* c_eq = t.seg_eq + s_before;
-  int* c_take = t.seg_take + s_before;
-  int* c_sel = t.seg_sel_off + s_before;
-  int* c_dis = t.seg_dis_off + s_before;
   const float* __restrict__ vbase = mode == 1 ? t.dval : t.val;
   const int32_t* __restrict__ ibase = mode == 1 ? nullptr : t.idx;
-  int* c_val = t.seg_valid + s_before;
   // merged inputs were written by this kernel: read them through L2 (the
   // read-only path is only for data that is constant during the kernel)
   const bool merged = FUSED && t.merge != nullptr;
   auto ldv = [&](const float* p) { return FUSED ? __ldcg(p) : __ldg(p); };
   auto ldi = [&](const int32_t* p) { return FUSED ? __ldcg(p) : __ldg(p); };
+
+  // Cluster exchange of a pass (two barriers): every CTA histograms its own
+  // entries; after barrier A, CTA r sums its 1/CL slice of the bins over all
+  // CTAs' histograms (DSMEM loads) and stores the sums into EVERY CTA's `agg`
+  // (DSMEM stores); after barrier B each CTA locates the digit itself, all on
+  // identical data, so no CTA waits for a leader and no state is broadcast.
+  // A CTA rewrites its histogram only after barrier B (all reads done), and
+  // the next pass's stores into `agg` come after the next barrier A (every
+  // CTA has finished its digit search by then).
+  auto reduce_slice = [&](int nb) {
+    const int per = (nb + CL - 1) / CL;
+    const int hi = min(nb, (cr + 1) * per);
+    for (int b = cr * per + threadIdx.x; b < hi; b += kSelThreads) {
+      uint32_t sum = 0;
+#pragma unroll
+      for (int q = 0; q < CL; ++q) sum += cluster.map_shared_rank(hist, q)[b];
+#pragma unroll
+      for (int q = 0; q < CL; ++q) cluster.map_shared_rank(agg, q)[b] = sum;
+    }
+  };
+  // CTA totals go to every CTA's `tot` (thread q stores into CTA q)
+  auto bcast_tot = [&](CtaTotals v) {
+    if (threadIdx.x < CL) cluster.map_shared_rank(tot, (int)threadIdx.x)[cr] = v;
+  };
 
   // ---- 2. radix passes: warp w histograms chunks w, w + kWarps, ...
   int first_pass = 0;
@@ -616,46 +630,31 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     }
     above = block_sum_ll(above, lscr);
     inside = block_sum_ll(inside, lscr);
-    if (threadIdx.x == 0) tot0[cr] = {0, above, inside};
-    cluster.sync();
-    {
-      const int per = kBins / CL;
-      for (int b = cr * per + threadIdx.x; b < (cr + 1) * per; b += kSelThreads) {
-        uint32_t sum = 0;
-#pragma unroll
-        for (int q = 0; q < CL; ++q) sum += cluster.map_shared_rank(hist, q)[b];
-        agg0[b] = sum;
+    bcast_tot({0, above, inside});
+    cluster.sync();   // A
+    reduce_slice(kBins);
+    cluster.sync();   // B
+    __shared__ int s_hit;
+    if (threadIdx.x == 0) {
+      long long a = 0, in = 0;
+      for (int q = 0; q < CL; ++q) {
+        a += tot[q].gt;
+        in += tot[q].eq;
+      }
+      const int hit = a < my.rank && my.rank <= a + in;
+      s_hit = hit;
+      my.hit = hit;
+      if (hit) {
+        my.prefix = d0 << 20;
+        my.pmask = (uint32_t)(kBins - 1) << 20;
+        my.rank -= a;
       }
     }
-    cluster.sync();
-    if (cr == 0) {
-      __shared__ int s_hit;
-      if (threadIdx.x == 0) {
-        long long a = 0, in = 0;
-        for (int q = 0; q < CL; ++q) {
-          a += tot[q].gt;
-          in += tot[q].eq;
-        }
-        const int hit = a < st.rank && st.rank <= a + in;
-        s_hit = hit;
-        st.hit = hit;
-        if (hit) {
-          st.prefix = d0 << 20;
-          st.pmask = (uint32_t)(kBins - 1) << 20;
-          st.rank -= a;
-        }
-      }
-      __syncthreads();
-      if (s_hit) {
-        find_digit(agg, kBins, 9, &st, suf);
-      } else {
-        for (int b = threadIdx.x; b < kBins; b += kSelThreads) agg[b] = 0;
-      }
-    }
-    cluster.sync();
-    if (threadIdx.x == 0) my = *st0;
     __syncthreads();
-    if (my.hit) first_pass = 2;
+    if (s_hit) {
+      find_digit(agg, kBins, 9, &my, suf);
+      first_pass = 2;
+    }
   }
   if (my.all == 0) {
 #pragma unroll 1
@@ -685,24 +684,11 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       __syncthreads();
       stamp(2 + 3 * pass);
       if (pass == 0) cta_stamp(1);
-      // distributed reduction: CTA r sums its 1/CL slice of the bins over
-      // all CTAs' histograms (DSMEM loads) and stores it into CTA 0's copy
-      cluster.sync();
-      {
-        const int per = nb / CL;
-        for (int b = cr * per + threadIdx.x; b < (cr + 1) * per; b += kSelThreads) {
-          uint32_t sum = 0;
-#pragma unroll
-          for (int q = 0; q < CL; ++q) sum += cluster.map_shared_rank(hist, q)[b];
-          agg0[b] = sum;
-        }
-      }
-      cluster.sync();
+      cluster.sync();   // A
+      reduce_slice(nb);
+      cluster.sync();   // B
       stamp(3 + 3 * pass);
-      if (cr == 0) find_digit(agg, nb, shift, &st, suf);
-      cluster.sync();
-      if (threadIdx.x == 0) my = *st0;
-      __syncthreads();
+      find_digit(agg, nb, shift, &my, suf);
       stamp(4 + 3 * pass);
     }
   }
@@ -745,9 +731,9 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       eq = 0;
     }
     if (lane == 0) {
-      c_gt[k] = gt;
-      c_eq[k] = eq;
-      c_val[k] = nv;
+      c_a[k] = gt;
+      c_b[k] = eq;
+      c_c[k] = nv;
       g_loc += gt;
       e_loc += eq;
       v_loc += nv;
@@ -756,13 +742,13 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   g_loc = block_sum_ll(g_loc, lscr);
   e_loc = block_sum_ll(e_loc, lscr);
   v_loc = block_sum_ll(v_loc, lscr);
-  if (threadIdx.x == 0) tot0[cr] = {v_loc, g_loc, e_loc};
+  bcast_tot({v_loc, g_loc, e_loc});
   cluster.sync();
   __shared__ long long base_eq, base_sel, base_cnt, all_sel, all_cnt;
   if (threadIdx.x == 0) {
     long long be = 0, bs = 0, bc = 0, ts = 0, tc = 0;
     for (int q = 0; q < CL; ++q) {
-      const CtaTotals x = tot0[q];
+      const CtaTotals x = tot[q];
       long long take = need_eq - be;
       take = take < 0 ? 0 : (take > x.eq ? x.eq : take);
       if (q == cr) {
@@ -779,7 +765,6 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     all_sel = ts;
     all_cnt = tc;
   }
-  cluster.sync();   // every CTA has read CTA 0's totals
   __syncthreads();
   {
     int eq_carry = (int)base_eq, sel_carry = (int)base_sel, cnt_carry = (int)base_cnt;
@@ -787,9 +772,9 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       const int k = l0 + threadIdx.x;
       int gt = 0, eq = 0, c = 0;
       if (k < nit) {
-        gt = c_gt[k];
-        eq = c_eq[k];
-        c = c_val[k];
+        gt = c_a[k];
+        eq = c_b[k];
+        c = c_c[k];
       }
       int teq, tsel, tcnt;
       const int eq_before = eq_carry + block_exscan(eq, scratch, &teq);
@@ -799,9 +784,9 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       const int sel_off = sel_carry + block_exscan(sel, scratch, &tsel);
       const int cnt_off = cnt_carry + block_exscan(c, scratch, &tcnt);
       if (k < nit) {
-        c_take[k] = take;
-        c_sel[k] = sel_off;
-        c_dis[k] = cnt_off - sel_off;
+        c_a[k] = sel_off;   // in place: item k is this thread's alone
+        c_b[k] = take;
+        c_c[k] = cnt_off - sel_off;
       }
       eq_carry += teq;
       sel_carry += tsel;
@@ -818,7 +803,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   int cut = -1;
   for (int k = warp; k < nit; k += kWarps) {
     const int c = ilen[k], e0 = iof[k];
-    const int sel_base = c_sel[k], dis_base = c_dis[k], take = c_take[k];
+    const int sel_base = c_a[k], dis_base = c_c[k], take = c_b[k];
     int eq_seen = 0, sel_seen = 0, val_seen = 0;
     const float* __restrict__ vp = vbase + e0;
     const int32_t* __restrict__ ip = ibase ? ibase + e0 : nullptr;
@@ -897,10 +882,13 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     if (t.div_hist) update_history(t.div_hist, mode, all, T, *t.pre_key_dev, total, budget);
   }
   stamp(11);
-  cluster.sync();   // keep CTA 0's shared memory alive until every reader is done
-  // every CTA's output writes are ordered before this (cluster barrier):
-  // the block can go to its consumers now, not at the end of the batch
-  if (cr == 0 && threadIdx.x == 0) peer_publish(t.ps);
+  // (no shared-memory access crosses CTAs after the totals exchange)
+  if (t.ps.npub > 0) {
+    // every CTA's output writes are ordered before this cluster barrier: the
+    // block can go to its consumers now, not at the end of the batch
+    cluster.sync();
+    if (cr == 0 && threadIdx.x == 0) peer_publish(t.ps);
+  }
 }
 
 }  // namespace
@@ -944,7 +932,7 @@ cudaLaunchConfig_t cl_config(int ntask, size_t smem, cudaStream_t s, cudaLaunchA
 }
 
 size_t dyn_bytes(int tab_cap, int win_cap) {
-  size_t b = sizeof(int32_t) * 2 * static_cast<size_t>(tab_cap);
+  size_t b = sizeof(int32_t) * 5 * static_cast<size_t>(tab_cap);
   if (win_cap > 0) b += 8 * static_cast<size_t>(win_cap) + sizeof(int32_t) * (kMergeSamples + kMaxR);
   return b;
 }
