@@ -3,23 +3,23 @@ sys.path.insert(0, '.')
 import paper_2304_00737_b200 as sd
 from paper_2304_00737_b200._lib import lib
 P, N, k = 8, 25_600_000, 256_000
-ctx = sd.SparDL(sd.ClusterConfig(workers=P, dimension=N, k=k), device=0, graph=False)
+ctx = sd.SparDL(sd.ClusterConfig(workers=P, dimension=N, k=k), device=0, graph=(len(sys.argv) > 1 and sys.argv[1] == 'graph'))
 gen = torch.Generator(device='cuda')
 grads = []
 for i in range(P):
     gen.manual_seed(1000 + i)
     grads.append(torch.randn(N, device='cuda', generator=gen))
-for it in range(5):
+for it in range(int(__import__("os").environ.get("DBG_ITERS", "210"))):
     ctx.all_reduce(grads); ctx.sync()
-out = (C.c_int64 * 52)()
+out = (C.c_int64 * 116)()
 names = ['p1','p0h','p0s','p0f','p1h','p1s','p1f','p2h','p2s','p2f','cnt+scan','write']
 for step in (-1, 0, 1, 2, 3):
     for task in (0,):
         rc = lib().spardl_debug_select_timestamps(ctx._h, step, task, out)
         if rc: print(step, 'rc', rc, lib().spardl_last_error()); continue
         ts = list(out)
-        d = [(names[i], round((ts[i+1]-ts[i])/1000, 1)) for i in range(11)]
-        print('step', step, 'total us', round((ts[11]-ts[0])/1000,1), d)
+        rel = [round((ts[i]-ts[0])/1000, 1) for i in range(12)]
+        print('step', step, 'total us', round((ts[11]-ts[0])/1000,1), 'stamps rel', rel, 'guess', ts[51], 'd0,a,in,rank', ts[47:51])
 # per-task spread of the dividing select and the SRS selects (CTA 0 of each cluster)
 for step, ntask in ((-1, 64), (0, 16), (1, 8), (2, 8)):
     rows = []
@@ -48,3 +48,12 @@ for step in (1, 2, 3):
     if rc: continue
     ts = list(out); t0 = ts[0]
     print('step', step, 'prologue', [round((x - t0) / 1000, 1) for x in ts[44:51]])
+
+# the feeding merge of each SRS select: per partition 0..3, phase stamps rel. to partition 0 start
+for step in (1, 2, 3):
+    rc = lib().spardl_debug_select_timestamps(ctx._h, step, 0, out)
+    if rc: continue
+    ts = list(out); m = ts[52:116]; t0 = m[0]
+    sel0 = ts[0]
+    for qq in range(4):
+        print('step', step, 'merge part', qq, [round((x - t0) / 1000, 1) if x else None for x in m[qq*8:qq*8+7]], 'select start', round((sel0 - t0)/1000, 1))

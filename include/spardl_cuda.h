@@ -239,10 +239,11 @@ int spardl_dense_fallbacks(spardl_ctx* ctx, int64_t* count);
 int spardl_div_diag(spardl_ctx* ctx, int32_t task, int64_t* out9);
 /* diagnostics: device timestamps (ns) of the phases of select `task` of
  * planner step `step` (-1: the dividing stage) in the last iteration:
- * out44[0..12) CTA 0's phase stamps, [12..28) each cluster CTA's start,
+ * out[0..12) CTA 0's phase stamps, [12..28) each cluster CTA's start,
  * [28..44) each CTA's end of the first histogram pass, [44..52) CTA 0's
- * fused-merge phases */
-int spardl_debug_select_timestamps(spardl_ctx* ctx, int32_t step, int32_t task, int64_t* out52);
+ * fused-merge phases (and guess diagnostics), [52..116) the feeding merge's
+ * phase stamps for its partitions 0..7 (8 each) */
+int spardl_debug_select_timestamps(spardl_ctx* ctx, int32_t step, int32_t task, int64_t* out116);
 /* number of kernels this context launches per iteration */
 int spardl_kernel_launches(const spardl_ctx* ctx, int64_t* per_iteration);
 /* the stream the context enqueues on (cudaStream_t) */

@@ -328,7 +328,7 @@ EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* c
     mt.seg_cnt = buf.get<int32_t>(parts);
     sdl::MergeTask* mtd = buf.get<sdl::MergeTask>(1);
     CK(cudaMemcpyAsync(mtd, &mt, sizeof(mt), cudaMemcpyHostToDevice, s));
-    sdl::launch_merge(mtd, 1, static_cast<int>(parts), static_cast<int>(r * T), s);
+    sdl::launch_merge(mtd, 1, static_cast<int>(parts), static_cast<int>(r * T), static_cast<int>(r), s);
     sdl::SelTask t{};
     t.mode = 0;
     t.idx = mt.out_idx;

@@ -51,6 +51,94 @@ __device__ __forceinline__ int block_rank(bool pred, int* scratch, int* total) {
   return r;
 }
 
+// CTA sums of three long longs (two barriers); scratch holds 3 * 32.
+__device__ __forceinline__ void block_sum3_ll(long long& a, long long& b, long long& c,
+                                              long long* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+    c += __shfl_down_sync(0xffffffffu, c, o);
+  }
+  if (lane == 0) {
+    scratch[3 * warp] = a;
+    scratch[3 * warp + 1] = b;
+    scratch[3 * warp + 2] = c;
+  }
+  __syncthreads();
+  a = b = c = 0;
+  for (int w = 0; w < nwarps; ++w) {
+    a += scratch[3 * w];
+    b += scratch[3 * w + 1];
+    c += scratch[3 * w + 2];
+  }
+  __syncthreads();
+}
+
+// Exclusive prefix sums of three ints over the CTA in one pass (two
+// barriers); scratch holds 3 * 33 ints.  e* = exclusive prefix, t* = total.
+__device__ __forceinline__ void block_exscan3(int a, int b, int c, int* scratch, int& ea, int& eb,
+                                              int& ec, int& ta, int& tb, int& tc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  int ia = a, ib = b, ic = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int na = __shfl_up_sync(0xffffffffu, ia, o);
+    const int nb = __shfl_up_sync(0xffffffffu, ib, o);
+    const int nc = __shfl_up_sync(0xffffffffu, ic, o);
+    if (lane >= o) {
+      ia += na;
+      ib += nb;
+      ic += nc;
+    }
+  }
+  if (lane == 31) {
+    scratch[warp] = ia;
+    scratch[33 + warp] = ib;
+    scratch[66 + warp] = ic;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const bool in = threadIdx.x < nwarps;
+    int wa = in ? scratch[threadIdx.x] : 0, wb = in ? scratch[33 + threadIdx.x] : 0,
+        wc = in ? scratch[66 + threadIdx.x] : 0;
+    int xa = wa, xb = wb, xc = wc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int na = __shfl_up_sync(0xffffffffu, xa, o);
+      const int nb = __shfl_up_sync(0xffffffffu, xb, o);
+      const int nc = __shfl_up_sync(0xffffffffu, xc, o);
+      if (lane >= o) {
+        xa += na;
+        xb += nb;
+        xc += nc;
+      }
+    }
+    __syncwarp();
+    if (in) {
+      scratch[threadIdx.x] = xa - wa;
+      scratch[33 + threadIdx.x] = xb - wb;
+      scratch[66 + threadIdx.x] = xc - wc;
+    }
+    if (threadIdx.x == 31) {
+      scratch[32] = xa;
+      scratch[65] = xb;
+      scratch[98] = xc;
+    }
+  }
+  __syncthreads();
+  ea = scratch[warp] + ia - a;
+  eb = scratch[33 + warp] + ib - b;
+  ec = scratch[66 + warp] + ic - c;
+  ta = scratch[32];
+  tb = scratch[65];
+  tc = scratch[98];
+  __syncthreads();
+}
+
 // Exclusive prefix sum of an int over the CTA.
 __device__ __forceinline__ int block_exscan(int v, int* scratch, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

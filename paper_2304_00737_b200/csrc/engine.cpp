@@ -314,6 +314,7 @@ sdl::SelTask Engine::select_from_merge(Stage& st, const std::vector<int>& pieces
   st.merge_in.push_back(pieces);
   st.max_parts = std::max<int>(st.max_parts, static_cast<int>(parts));
   st.max_rT = std::max<int>(st.max_rT, static_cast<int>(r * T));
+  st.max_r = std::max<int>(st.max_r, r);
 
   sdl::SelTask t{};
   t.mode = 0;
@@ -362,6 +363,8 @@ int Engine::materialize(int w, int pos, std::vector<int> pieces, int64_t budget,
   xi_[static_cast<size_t>(li)][static_cast<size_t>(xi_block)].push_back(
       {t.dis_idx, t.dis_val, t.dis_cnt});
   add_select(st, t, uid, pieces.size() == 1 ? pieces[0] : -1);
+  if (t.merge_slot)   // diagnostics: the merge stamps its phases into the select's scratch
+    st.merges[static_cast<size_t>(t.merge_slot - 1)].dbg = st.sels.back().scr->merge_ts;
   return uid;
 }
 
@@ -992,7 +995,7 @@ int Engine::exec_stage(const Stage& st) {
   int n = 0;
   if (!st.merges.empty() && !st.fused)
     n += sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts,
-                           st.max_rT, stream_);
+                           st.max_rT, st.max_r, stream_);
   if (!st.sels.empty())
     n += sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_,
                             st.fused ? st.cl : 0, st.fused ? st.win_cap : 0);
@@ -1329,7 +1332,7 @@ void Engine::select_timestamps(int step, int task, int64_t* out12) {
   sync();
   const Stage& st = step < 0 ? div_stage_ : steps_.at(static_cast<size_t>(step)).stage;
   const sdl::SelScratch* sc = st.sels.at(static_cast<size_t>(task)).scr;
-  CK(mcpy(out12, sc->tstamp, sizeof(long long) * 52, cudaMemcpyDeviceToHost));
+  CK(mcpy(out12, sc->tstamp, sizeof(long long) * 116, cudaMemcpyDeviceToHost));
 }
 
 int64_t Engine::dense_fallbacks() {

@@ -67,6 +67,7 @@ struct Stage {           // one batch of merge + select tasks
   sdl::SelTask* sels_dev = nullptr;
   int max_parts = 0;
   int max_rT = 0;
+  int max_r = 0;
   int max_nseg = 0;
   std::set<int> produced;    // uids written by this stage (dependency guard)
   std::vector<int64_t> merge_cap;   // input capacity of each merge task

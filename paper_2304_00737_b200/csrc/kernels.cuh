@@ -78,6 +78,7 @@ struct SelScratch {
   long long tstamp[12];  // phase timestamps (globaltimer ns) of the last run, CTA 0
   long long cta_ts[2][16];   // per CTA: start, end of the pass-0 histogram
   long long pro_ts[8];       // CTA 0: fused-merge prologue phase ends
+  long long merge_ts[64];    // the feeding merge: 8 phase stamps of its partitions 0..7
 };
 
 // Membership in a finished selection without searching its output:
@@ -176,6 +177,7 @@ struct MergeTask {
   float* out_val;
   int32_t* seg_off;                 // [max_parts]
   int32_t* seg_cnt;                 // [max_parts]
+  long long* dbg;                   // diagnostics: phase stamps of partitions 0..7, or null
 };
 
 // ---------------------------------------------------------------------------
@@ -237,8 +239,8 @@ int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_
 // the clusters of width cl resident at once for a launch with that window
 int select_max_window();
 int select_resident_clusters(int cl, int tab_cap, int win_cap);
-int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T,
-                  cudaStream_t s);
+int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T, int max_r,
+                 cudaStream_t s);
 // part: 0 = whole pass, 1 = sample + pre-threshold only, 2 = candidate pass only
 int launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sample_every,
                   int apply_residual, cudaStream_t s, int part = 0);

@@ -15,7 +15,9 @@
 // is written at the partition's position in concatenation space, so the
 // result is a segmented list (one segment per partition, gaps where indices
 // coincided) that the select kernels consume directly.
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -88,32 +90,101 @@ __global__ void __launch_bounds__(kThreads) k_merge_rank(const MergeTask* __rest
 #define SPARDL_MERGE_THREADS 256
 #endif
 constexpr int kMergeThreads = SPARDL_MERGE_THREADS;   // threads per partition CTA
+#ifndef SPARDL_MERGE_MINB
+#define SPARDL_MERGE_MINB 1
+#endif
 
-__global__ void __launch_bounds__(kMergeThreads) k_merge_part(const MergeTask* __restrict__ tasks) {
-  pdl_enter();
-  // grid (task, partition): partitions of every task come first in launch
-  // order, so the live ones (q < nparts, usually far fewer than max_parts)
-  // all start in the first wave
-  const MergeTask& t = tasks[blockIdx.x];
-  const int q = blockIdx.y;
-  const int S = *t.nparts;
-  if (q >= t.max_parts) return;
-  if (q >= S) {
-    if (threadIdx.x == 0) {
-      t.seg_off[q] = 0;
-      t.seg_cnt[q] = 0;
-    }
-    return;
+__device__ __forceinline__ void mstamp(const MergeTask& t, int q, int k) {
+  if (t.dbg && q < 8 && threadIdx.x == 0) {
+    long long ts;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+    t.dbg[q * 8 + k] = ts;
   }
-  const int32_t v_lo = t.splitters[q];
-  const int32_t v_hi = t.splitters[q + 1];
-  if (v_lo == v_hi) {
-    if (threadIdx.x == 0) {
-      t.seg_off[q] = 0;
-      t.seg_cnt[q] = 0;
-    }
-    return;
+}
+
+// Entries of one 2-way merge pass: A (the fold so far) and B (the next
+// list), both ascending in index; equal indices are folded acc + next.
+struct Run {
+  const int32_t* idx;
+  const float* val;
+  int n;
+};
+
+// One merge-path pass over the CTA: thread t owns the merged positions
+// [t*E, (t+1)*E) (ties: A first), finds its start with one binary search and
+// merges sequentially.  An index present in both A and B is one output,
+// folded by whichever thread owns its A entry (the next thread skips the B
+// entry).  Returns the output count; writes idx/val at out + rank.
+__device__ __forceinline__ int merge_pass(Run A, Run B, int32_t* out_idx, float* out_val,
+                                          int* scratch) {
+  const int n = A.n + B.n;
+  const int E = (n + kMergeThreads - 1) / kMergeThreads;
+  const int d0 = min(n, (int)threadIdx.x * E), d1 = min(n, d0 + E);
+  // co-rank: i = #A among the first d0 merged entries
+  int lo = max(0, d0 - B.n), hi = min(d0, A.n);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A.idx[mid] <= B.idx[d0 - 1 - mid]) lo = mid + 1;
+    else hi = mid;
   }
+  const int i0 = lo, j0 = d0 - lo;
+  // the first entry is B's half of a fold the previous thread owns
+  const bool skip_first = d0 < d1 && j0 < B.n && i0 > 0 && (i0 == A.n || B.idx[j0] < A.idx[i0]) &&
+                          A.idx[i0 - 1] == B.idx[j0];
+  // sweep 1: count outputs (a fold consumes two merged positions)
+  int cnt = 0;
+  {
+    int i = i0, j = j0;
+    bool first = true;
+    while (i + j < d1) {
+      const bool take_a = j >= B.n || (i < A.n && A.idx[i] <= B.idx[j]);
+      if (take_a) {
+        if (j < B.n && B.idx[j] == A.idx[i]) ++j;   // folded partner, maybe past d1
+        ++i;
+        ++cnt;
+      } else {
+        if (!(first && skip_first)) ++cnt;
+        ++j;
+      }
+      first = false;
+    }
+  }
+  int total;
+  const int base = block_exscan(cnt, scratch, &total);
+  // sweep 2: write
+  {
+    int i = i0, j = j0, o = base;
+    bool first = true;
+    while (i + j < d1) {
+      const bool take_a = j >= B.n || (i < A.n && A.idx[i] <= B.idx[j]);
+      if (take_a) {
+        const int32_t x = A.idx[i];
+        float v = A.val[i];
+        if (j < B.n && B.idx[j] == x) v = __fadd_rn(v, B.val[j++]);
+        ++i;
+        out_idx[o] = x;
+        out_val[o] = v;
+        ++o;
+      } else {
+        if (!(first && skip_first)) {
+          out_idx[o] = B.idx[j];
+          out_val[o] = B.val[j];
+          ++o;
+        }
+        ++j;
+      }
+      first = false;
+    }
+  }
+  __syncthreads();   // outputs visible before they are read as the next A
+  return total;
+}
+
+// Merge of partition q: entries with v_lo <= index < v_hi, from list l's
+// window win[l] (-1: none).
+template <bool PATH>
+__device__ __forceinline__ void merge_body(const MergeTask& t, int q, int32_t v_lo, int32_t v_hi,
+                                           const int* win) {
   const int r = t.r, T = t.T;
   extern __shared__ __align__(16) unsigned char smem[];
   int32_t* w_idx = reinterpret_cast<int32_t*>(smem);          // [r*T]
@@ -125,7 +196,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_part(const MergeTask* _
   __shared__ int scratch[40];
   if (threadIdx.x < r) {
     const int l = threadIdx.x;
-    const int w = t.windows[(size_t)q * r + l];
+    const int w = win[l];
     const int n = *t.in_cnt[l];
     if (w < 0) {
       wstart[l] = 0;
@@ -157,6 +228,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_part(const MergeTask* _
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  mstamp(t, q, 4);
   if (threadIdx.x < r) {
     const int l = threadIdx.x;
     a_[l] = lower_bound_i32(w_idx + l * T, wlen[l], v_lo);
@@ -174,6 +246,35 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_part(const MergeTask* _
     seg_base = base;
   }
   __syncthreads();
+  mstamp(t, q, 5);
+  if constexpr (PATH) {
+    // left fold ((l0 + l1) + l2) + ... as r-1 merge-path passes; the last
+    // pass writes the segment, the others ping-pong between two buffers
+    int32_t* const q_idx = reinterpret_cast<int32_t*>(m_val + r * T);   // second buffer
+    float* const q_val = reinterpret_cast<float*>(q_idx + r * T);
+    Run acc{w_idx + a_[0], w_val + a_[0], b_[0] - a_[0]};
+    int out = acc.n;
+    if (r == 1) {
+      for (int e = threadIdx.x; e < acc.n; e += blockDim.x) {
+        t.out_idx[seg_base + e] = acc.idx[e];
+        t.out_val[seg_base + e] = acc.val[e];
+      }
+    }
+    for (int u = 1; u < r; ++u) {
+      const Run B{w_idx + u * T + a_[u], w_val + u * T + a_[u], b_[u] - a_[u]};
+      const bool last = u == r - 1;
+      int32_t* oi = last ? t.out_idx + seg_base : ((u & 1) ? m_idx : q_idx);
+      float* ov = last ? t.out_val + seg_base : ((u & 1) ? m_val : q_val);
+      out = merge_pass(acc, B, oi, ov, scratch);
+      acc = Run{oi, ov, out};
+    }
+    if (threadIdx.x == 0) {
+      t.seg_off[q] = seg_base;
+      t.seg_cnt[q] = out;
+    }
+    mstamp(t, q, 6);
+    return;
+  }
   const int M = sz_pref[r];
   // stable r-way merge by (index, list): scatter every entry to its rank
   for (int e = threadIdx.x; e < M; e += blockDim.x) {
@@ -214,21 +315,168 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_part(const MergeTask* _
   }
 }
 
+template <bool PATH>
+__global__ void __launch_bounds__(kMergeThreads, SPARDL_MERGE_MINB) k_merge_part(const MergeTask* __restrict__ tasks) {
+  pdl_enter();
+  // grid (task, partition): partitions of every task come first in launch
+  // order, so the live ones (q < nparts, usually far fewer than max_parts)
+  // all start in the first wave
+  const MergeTask& t = tasks[blockIdx.x];
+  const int q = blockIdx.y;
+  const int S = *t.nparts;
+  if (q >= t.max_parts) return;
+  if (q >= S) {
+    if (threadIdx.x == 0) {
+      t.seg_off[q] = 0;
+      t.seg_cnt[q] = 0;
+    }
+    return;
+  }
+  const int32_t v_lo = t.splitters[q];
+  const int32_t v_hi = t.splitters[q + 1];
+  if (v_lo == v_hi) {
+    if (threadIdx.x == 0) {
+      t.seg_off[q] = 0;
+      t.seg_cnt[q] = 0;
+    }
+    return;
+  }
+  __shared__ int win[kMaxR];
+  if (threadIdx.x < t.r) win[threadIdx.x] = t.windows[(size_t)q * t.r + threadIdx.x];
+  __syncthreads();
+  merge_body<PATH>(t, q, v_lo, v_hi, win);
+}
+
+// One kernel per merge batch when the splitter samples are few (<= 4 per
+// thread): every partition CTA loads all samples of its task, ranks them in
+// shared memory and takes its own splitters and windows -- the ranking that
+// k_merge_rank does once, repeated per CTA, instead of a kernel boundary and
+// two more dependent global round trips.
+constexpr int kOneShotSamples = 4 * kMergeThreads;
+
+template <bool PATH>
+__global__ void __launch_bounds__(kMergeThreads, SPARDL_MERGE_MINB) k_merge_one(const MergeTask* __restrict__ tasks) {
+  pdl_enter();
+  const MergeTask& t = tasks[blockIdx.x];
+  const int q = blockIdx.y;
+  if (q >= t.max_parts) return;
+  mstamp(t, q, 0);
+  peer_wait(t.ps);   // remote input lists published
+  const int r = t.r, T = t.T;
+  __shared__ int base[kMaxR + 1];
+  __shared__ int32_t samp[kOneShotSamples];
+  __shared__ int win[kMaxR];
+  __shared__ int32_t s_lo, s_hi;
+  if (threadIdx.x < r) base[threadIdx.x + 1] = *t.in_cnt[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int b = 0;
+    base[0] = 0;
+    for (int l = 0; l < r; ++l) {
+      const int n = base[l + 1];
+      b += (n + T - 1) / T;
+      base[l + 1] = b;
+    }
+    s_lo = INT_MIN;
+    s_hi = INT_MAX;   // the last partition is open above
+  }
+  __syncthreads();
+  mstamp(t, q, 1);
+  const int S = base[r];
+  if (q >= S) {
+    if (threadIdx.x == 0) {
+      t.seg_off[q] = 0;
+      t.seg_cnt[q] = 0;
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < S; i += kMergeThreads) {
+    int l = 0;
+    while (i >= base[l + 1]) ++l;
+    samp[i] = t.in_idx[l][(i - base[l]) * T];
+  }
+  __syncthreads();
+  mstamp(t, q, 2);
+  // rank every sample (ties: list order); keep the splitters of ranks q, q+1
+  for (int i = threadIdx.x; i < S; i += kMergeThreads) {
+    int l = 0;
+    while (i >= base[l + 1]) ++l;
+    const int j = i - base[l];
+    const int32_t v = samp[i];
+    int rank = j;
+    for (int u = 0; u < r; ++u) {
+      if (u == l) continue;
+      const int32_t* a = samp + base[u];
+      const int n = base[u + 1] - base[u];
+      rank += (u < l) ? upper_bound_i32(a, n, v) : lower_bound_i32(a, n, v);
+    }
+    if (rank == q) {
+      s_lo = v;
+      for (int u = 0; u < r; ++u)
+        win[u] = u == l ? j : upper_bound_i32(samp + base[u], base[u + 1] - base[u], v) - 1;
+    } else if (rank == q + 1) {
+      s_hi = v;
+    }
+  }
+  __syncthreads();
+  mstamp(t, q, 3);
+  const int32_t v_lo = s_lo, v_hi = s_hi;
+  if (v_lo == v_hi) {
+    if (threadIdx.x == 0) {
+      t.seg_off[q] = 0;
+      t.seg_cnt[q] = 0;
+    }
+    return;
+  }
+  merge_body<PATH>(t, q, v_lo, v_hi, win);
+}
+
+bool merge_path_on() {
+  static const bool on = [] {
+    const char* e = getenv("SPARDL_MERGE_PATH");   // tuning experiments only
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool merge_one_shot() {
+  static const bool on = [] {
+    const char* e = getenv("SPARDL_MERGE_ONESHOT");   // tuning experiments only
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace
 
-int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T,
+int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r_T, int max_r,
                  cudaStream_t s) {
   if (ntask <= 0 || max_parts <= 0) return 0;
+  // merge-path folds: the windows plus one intermediate buffer for r = 3 and
+  // two for r >= 4 (8 B per window entry each; r = 2 writes straight to the
+  // output, so a CTA needs 16 KB and the whole batch fits one wave); the
+  // rank-scatter fallback 16 B per entry
+  const size_t path_bytes = (size_t)max_r_T * 8 * (1 + std::min(std::max(max_r - 2, 0), 2));
+  // (r >= 4: two intermediates cost more occupancy than the rank scatter)
+  const bool path = merge_path_on() && max_r <= 3 && path_bytes <= 200 * 1024;
+  const size_t smem = path ? path_bytes : (size_t)max_r_T * 16;
+  const bool one = max_parts <= kOneShotSamples && merge_one_shot();
+  auto part = path ? k_merge_part<true> : k_merge_part<false>;
+  auto single = path ? k_merge_one<true> : k_merge_one<false>;
+  // (dynamic + static shared memory above 48 KB needs the opt-in)
+  static size_t configured[2][2] = {{0, 0}, {0, 0}};
+  if (smem > configured[path][one]) {
+    cudaFuncSetAttribute(one ? single : part, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured[path][one] = smem;
+  }
+  if (one) {
+    launch_pdl(single, dim3(ntask, max_parts), dim3(kMergeThreads), smem, s, tasks_dev);
+    return 1;
+  }
   const int rx = (max_parts + kThreads - 1) / kThreads;
   launch_pdl(k_merge_rank, dim3(rx, ntask), dim3(kThreads), 0, s, tasks_dev);
-  const size_t smem = (size_t)max_r_T * 16;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_merge_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    configured = smem;
-  }
-  launch_pdl(k_merge_part, dim3(ntask, max_parts), dim3(kMergeThreads), smem, s, tasks_dev);
+  launch_pdl(part, dim3(ntask, max_parts), dim3(kMergeThreads), smem, s, tasks_dev);
   return 2;
 }
 

@@ -410,7 +410,7 @@ __device__ long long merge_prologue(const MergeTask& mt, int cr, int32_t* w_idx,
 #endif
 template <int CL, bool FUSED>
 __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
-    k_select(const SelTask* __restrict__ tasks, int tab_cap, int win_cap) {
+    k_select(const SelTask* __restrict__ tasks, int tab_cap, int win_cap, int vcap) {
   pdl_enter();
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank();
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   __shared__ CtaTotals tot[CL];                     // every CTA's totals (every CTA a copy)
   __shared__ long long suf[kSelThreads];
   __shared__ int scratch[40];
-  __shared__ long long lscr[32];
+  __shared__ long long lscr[3 * 32];
   __shared__ RadixState my;                         // radix state (identical in every CTA)
   // this CTA's work items: contiguous pieces of its segments, <= plen long
   // (item i = input elements [iof[i], iof[i] + ilen[i])), so the warps share
@@ -437,8 +437,14 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   int32_t* c_a = dyn + 2 * tab_cap;
   int32_t* c_b = dyn + 3 * tab_cap;
   int32_t* c_c = dyn + 4 * tab_cap;
+  // on-chip copy of the CTA's entries: item k's values at vc[coff[k]...] and
+  // indices at ic[coff[k]...], staged once (1c) so that every pass reads
+  // shared memory instead of L2 (items past vcap stay in memory)
+  int32_t* coff = dyn + 5 * tab_cap;
+  float* vc = reinterpret_cast<float*>(dyn + 6 * tab_cap);
+  int32_t* ic = dyn + 6 * tab_cap + vcap;   // the indices beside them
   // fused merge: the CTA's input windows and the task's splitter samples
-  int32_t* w_idx = dyn + 5 * tab_cap;
+  int32_t* w_idx = dyn + 6 * tab_cap;
   float* w_val = reinterpret_cast<float*>(w_idx + win_cap);
   int32_t* samp = reinterpret_cast<int32_t*>(w_val + win_cap);
 
@@ -477,25 +483,26 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   // ---- 1. totals and an entry-balanced split of the segments over the
   // cluster: every CTA scans all segment lengths (cheap: <= 8192 counts) and
   // owns the segments whose first entry falls in its 1/CL of the entries.
+  // The segment bounds are read once (all loads in flight) into the counter
+  // arrays, which are free until the counting phase.
+  for (int s = threadIdx.x; s < nseg; s += kSelThreads) {
+    int off, c;
+    seg_bounds(t, mode, s, off, c);
+    c_a[s] = off;
+    c_b[s] = c;
+  }
+  __syncthreads();
   {
     // pass A: the total
     long long part = 0;
-    for (int s = threadIdx.x; s < nseg; s += kSelThreads) {
-      int off, c;
-      seg_bounds(t, mode, s, off, c);
-      part += c;
-    }
+    for (int s = threadIdx.x; s < nseg; s += kSelThreads) part += c_b[s];
     total = block_sum_ll(part, lscr);
     const long long lo_t = total * cr / CL, hi_t = total * (cr + 1) / CL;
     // pass B: s0 = #{s : start(s) < lo_t}, s1 = #{s : start(s) < hi_t}
     int carry = 0, n_lo = 0, n_hi = 0;
     for (int b0 = 0; b0 < nseg; b0 += kSelThreads) {
       const int s = b0 + threadIdx.x;
-      int c = 0;
-      if (s < nseg) {
-        int off;
-        seg_bounds(t, mode, s, off, c);
-      }
+      const int c = s < nseg ? c_b[s] : 0;
       int tt;
       const long long start = carry + block_exscan(c, scratch, &tt);
       n_lo += __syncthreads_count(s < nseg && start < lo_t);
@@ -513,11 +520,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   // ---- 1b. the work items of this CTA
   {
     long long here = 0;
-    for (int s = s0 + threadIdx.x; s < s1; s += kSelThreads) {
-      int off, c;
-      seg_bounds(t, mode, s, off, c);
-      here += c;
-    }
+    for (int s = s0 + threadIdx.x; s < s1; s += kSelThreads) here += c_b[s];
     here = block_sum_ll(here, lscr);
     // smallest piece length (kChunkE * 2^j) whose items fit the table
     long long plen = kChunkE;
@@ -525,8 +528,8 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     int carry = 0;
     for (int b0 = 0; b0 < nloc; b0 += kSelThreads) {
       const int ls = b0 + threadIdx.x;
-      int off = 0, c = 0;
-      if (ls < nloc) seg_bounds(t, mode, s0 + ls, off, c);
+      const int off = ls < nloc ? c_a[s0 + ls] : 0;
+      const int c = ls < nloc ? c_b[s0 + ls] : 0;
       const int np = (int)((c + plen - 1) / plen);
       int tt;
       int it = carry + block_exscan(np, scratch, &tt);
@@ -540,6 +543,18 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       s_nit = min(carry, tab_cap);
       s_plen = (int)plen;
       s_F = (int)here;
+    }
+    if (vcap > 0) {
+      __syncthreads();
+      const int n = s_nit;
+      int ccar = 0;
+      for (int b0 = 0; b0 < n; b0 += kSelThreads) {
+        const int k = b0 + threadIdx.x;
+        int tt;
+        const int o = ccar + block_exscan(k < n ? ilen[k] : 0, scratch, &tt);
+        if (k < n) coff[k] = o;
+        ccar += tt;
+      }
     }
   }
   }
@@ -573,6 +588,40 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   const bool merged = FUSED && t.merge != nullptr;
   auto ldv = [&](const float* p) { return FUSED ? __ldcg(p) : __ldg(p); };
   auto ldi = [&](const int32_t* p) { return FUSED ? __ldcg(p) : __ldg(p); };
+  // ---- 1c. stage the CTA's entries on chip: every item that fits is copied
+  // with 4-byte asynchronous copies, all in flight at once (one memory
+  // round trip instead of one per chunk and pass); the passes below read
+  // shared memory, items past vcap read memory
+  if (vcap > 0) {
+    for (int k = warp; k < nit; k += kWarps) {
+      const int c = ilen[k], cb = coff[k];
+      if (cb + c > vcap) continue;
+      const float* vp = vbase + iof[k];
+      for (int j = lane; j < c; j += 32) cp_async4(vc + cb + j, vp + j);
+      if (ibase) {
+        const int32_t* ip = ibase + iof[k];
+        for (int j = lane; j < c; j += 32) cp_async4(ic + cb + j, ip + j);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+  }
+  auto staged = [&](int cb, int c) { return vcap > 0 && cb + c <= vcap; };
+  auto fetch = [&](int cb, const float* __restrict__ vp, int c, int j0, float* v) {
+    if (staged(cb, c)) {
+#pragma unroll
+      for (int u = 0; u < kIlp; ++u) {
+        const int j = j0 + u * 32 + lane;
+        v[u] = j < c ? vc[cb + j] : __uint_as_float(kHoleBits);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kIlp; ++u) {   // all loads in flight first
+        const int j = j0 + u * 32 + lane;
+        v[u] = j < c ? ldv(vp + j) : __uint_as_float(kHoleBits);
+      }
+    }
+  };
 
   // Cluster exchange of a pass (two barriers): every CTA histograms its own
   // entries; after barrier A, CTA r sums its 1/CL slice of the bins over all
@@ -610,14 +659,14 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     long long above = 0, inside = 0;
     for (int k = warp; k < nit; k += kWarps) {
       const int c = ilen[k];
+      const int cb = vcap > 0 ? coff[k] : 0;
       const float* __restrict__ vp = vbase + iof[k];
       for (int j0 = 0; j0 < c; j0 += kChunkE) {
+        float v[kIlp];
+        fetch(cb, vp, c, j0, v);
         uint32_t key[kIlp];
 #pragma unroll
-        for (int u = 0; u < kIlp; ++u) {
-          const int j = j0 + u * 32 + lane;
-          key[u] = j < c ? mag_key(ldv(vp + j)) : kHoleKey;
-        }
+        for (int u = 0; u < kIlp; ++u) key[u] = mag_key(v[u]);
 #pragma unroll
         for (int u = 0; u < kIlp; ++u) {
           const bool valid = key[u] != kHoleKey;
@@ -628,12 +677,16 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
         }
       }
     }
-    above = block_sum_ll(above, lscr);
-    inside = block_sum_ll(inside, lscr);
+    {
+      long long unused = 0;
+      block_sum3_ll(above, inside, unused, lscr);
+    }
+    stamp(2);
     bcast_tot({0, above, inside});
     cluster.sync();   // A
     reduce_slice(kBins);
     cluster.sync();   // B
+    stamp(3);
     __shared__ int s_hit;
     if (threadIdx.x == 0) {
       long long a = 0, in = 0;
@@ -642,6 +695,12 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
         in += tot[q].eq;
       }
       const int hit = a < my.rank && my.rank <= a + in;
+      if (cr == 0) {   // diagnostics: guess inputs
+        sc->pro_ts[3] = d0;
+        sc->pro_ts[4] = a;
+        sc->pro_ts[5] = in;
+        sc->pro_ts[6] = my.rank;
+      }
       s_hit = hit;
       my.hit = hit;
       if (hit) {
@@ -655,6 +714,8 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       find_digit(agg, kBins, 9, &my, suf);
       first_pass = 2;
     }
+    stamp(4);
+    if (cr == 0 && threadIdx.x == 0) sc->pro_ts[7] = 100 + s_hit;   // diagnostics: guess outcome
   }
   if (my.all == 0) {
 #pragma unroll 1
@@ -666,18 +727,16 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       const uint32_t prefix = my.prefix, pmask = my.pmask;
       for (int k = warp; k < nit; k += kWarps) {
         const int c = ilen[k];
+        const int cb = vcap > 0 ? coff[k] : 0;
         const float* __restrict__ vp = vbase + iof[k];
         for (int j0 = 0; j0 < c; j0 += kChunkE) {
-          uint32_t key[kIlp];
-#pragma unroll
-          for (int u = 0; u < kIlp; ++u) {   // all loads in flight first
-            const int j = j0 + u * 32 + lane;
-            key[u] = j < c ? mag_key(ldv(vp + j)) : kHoleKey;
-          }
+          float v[kIlp];
+          fetch(cb, vp, c, j0, v);
 #pragma unroll
           for (int u = 0; u < kIlp; ++u) {
-            hist_add(hist, (key[u] >> shift) & (nb - 1),
-                     key[u] != kHoleKey && (key[u] & pmask) == prefix);
+            const uint32_t key = mag_key(v[u]);
+            hist_add(hist, (key >> shift) & (nb - 1),
+                     key != kHoleKey && (key & pmask) == prefix);
           }
         }
       }
@@ -703,14 +762,14 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     int gt = 0, eq = 0, nv = c;
     if (all == 0 || merged) {
       const float* __restrict__ vp = vbase + iof[k];
+      const int cb = vcap > 0 ? coff[k] : 0;
       nv = 0;
       for (int j0 = 0; j0 < c; j0 += kChunkE) {
+        float v[kIlp];
+        fetch(cb, vp, c, j0, v);
         uint32_t key[kIlp];
 #pragma unroll
-        for (int u = 0; u < kIlp; ++u) {
-          const int j = j0 + u * 32 + lane;
-          key[u] = j < c ? mag_key(ldv(vp + j)) : kHoleKey;
-        }
+        for (int u = 0; u < kIlp; ++u) key[u] = mag_key(v[u]);
 #pragma unroll
         for (int u = 0; u < kIlp; ++u) {
           const bool in = key[u] != kHoleKey;
@@ -739,35 +798,33 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       v_loc += nv;
     }
   }
-  g_loc = block_sum_ll(g_loc, lscr);
-  e_loc = block_sum_ll(e_loc, lscr);
-  v_loc = block_sum_ll(v_loc, lscr);
+  block_sum3_ll(g_loc, e_loc, v_loc, lscr);
   bcast_tot({v_loc, g_loc, e_loc});
   cluster.sync();
-  __shared__ long long base_eq, base_sel, base_cnt, all_sel, all_cnt;
+  // Offsets in cluster order.  The tie quota is filled by the equal-key
+  // entries in index order, so the entries selected before a position are
+  // #{key > T before it} + min(#{key == T before it}, need_eq).
+  __shared__ long long base_eq, base_gt, base_cnt, all_sel, all_cnt;
   if (threadIdx.x == 0) {
-    long long be = 0, bs = 0, bc = 0, ts = 0, tc = 0;
+    long long be = 0, bg = 0, bc = 0;
     for (int q = 0; q < CL; ++q) {
       const CtaTotals x = tot[q];
-      long long take = need_eq - be;
-      take = take < 0 ? 0 : (take > x.eq ? x.eq : take);
       if (q == cr) {
         base_eq = be;
-        base_sel = bs;
+        base_gt = bg;
         base_cnt = bc;
       }
       be += x.eq;
-      bs += x.gt + take;
+      bg += x.gt;
       bc += x.cnt;
-      ts += x.gt + take;
-      tc += x.cnt;
     }
-    all_sel = ts;
-    all_cnt = tc;
+    all_sel = bg + (be < need_eq ? be : need_eq);
+    all_cnt = bc;
   }
   __syncthreads();
   {
-    int eq_carry = (int)base_eq, sel_carry = (int)base_sel, cnt_carry = (int)base_cnt;
+    __shared__ int scr3[3 * 33];
+    int g_carry = (int)base_gt, e_carry = (int)base_eq, c_carry = (int)base_cnt;
     for (int l0 = 0; l0 < nit; l0 += kSelThreads) {
       const int k = l0 + threadIdx.x;
       int gt = 0, eq = 0, c = 0;
@@ -776,21 +833,22 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
         eq = c_b[k];
         c = c_c[k];
       }
-      int teq, tsel, tcnt;
-      const int eq_before = eq_carry + block_exscan(eq, scratch, &teq);
-      const long long q = need_eq - eq_before;
+      int gb, eb, cb, tg, te, tc;
+      block_exscan3(gt, eq, c, scr3, gb, eb, cb, tg, te, tc);
+      gb += g_carry;
+      eb += e_carry;
+      cb += c_carry;
+      const long long q = need_eq - eb;
       const int take = q <= 0 ? 0 : (q >= eq ? eq : (int)q);
-      const int sel = gt + take;
-      const int sel_off = sel_carry + block_exscan(sel, scratch, &tsel);
-      const int cnt_off = cnt_carry + block_exscan(c, scratch, &tcnt);
+      const int sel_off = gb + (int)(eb < need_eq ? (long long)eb : need_eq);
       if (k < nit) {
         c_a[k] = sel_off;   // in place: item k is this thread's alone
         c_b[k] = take;
-        c_c[k] = cnt_off - sel_off;
+        c_c[k] = cb - sel_off;
       }
-      eq_carry += teq;
-      sel_carry += tsel;
-      cnt_carry += tcnt;
+      g_carry += tg;
+      e_carry += te;
+      c_carry += tc;
     }
   }
   __syncthreads();
@@ -808,15 +866,24 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     const float* __restrict__ vp = vbase + e0;
     const int32_t* __restrict__ ip = ibase ? ibase + e0 : nullptr;
     const int32_t ib = t.dbase + e0;
+    const int cb = vcap > 0 ? coff[k] : 0;
     for (int j00 = 0; j00 < c; j00 += kChunkE) {
       float vv[kIlp];
       int32_t iv[kIlp];
+      if (staged(cb, c)) {
 #pragma unroll
-      for (int u = 0; u < kIlp; ++u) {   // all loads in flight first
-        const int j = j00 + u * 32 + lane;
-        vv[u] = j < c ? ldv(vp + j) : __uint_as_float(kHoleBits);
-        iv[u] = j < c ? (ip ? ldi(ip + j) : ib + j) : 0;
+        for (int u = 0; u < kIlp; ++u) {
+          const int j = j00 + u * 32 + lane;
+          iv[u] = j < c ? (ip ? ic[cb + j] : ib + j) : 0;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {   // index loads first, then the values
+          const int j = j00 + u * 32 + lane;
+          iv[u] = j < c ? (ip ? ldi(ip + j) : ib + j) : 0;
+        }
       }
+      fetch(cb, vp, c, j00, vv);
 #pragma unroll
       for (int u = 0; u < kIlp; ++u) {
         const float v = vv[u];
@@ -931,9 +998,27 @@ cudaLaunchConfig_t cl_config(int ntask, size_t smem, cudaStream_t s, cudaLaunchA
   return lc;
 }
 
+// item table: iof, ilen, three counters, cache offset
+size_t table_bytes(int tab_cap) { return sizeof(int32_t) * 6 * static_cast<size_t>(tab_cap); }
+
+int max_dyn_smem();
+
+// entries of the on-chip value copy: whatever shared memory the table
+// leaves (one CTA per SM either way: 512 threads at > 64 registers)
+int value_cache_cap(int tab_cap) {
+  static const bool off = [] {
+    const char* e = getenv("SPARDL_SEL_VCACHE");   // tuning experiments only
+    return e && e[0] == '0';
+  }();
+  if (off) return 0;
+  const long long avail = (long long)max_dyn_smem() - (long long)table_bytes(tab_cap);
+  return avail >= 8 * 1024 ? (int)((avail / 8) & ~31ll) : 0;
+}
+
 size_t dyn_bytes(int tab_cap, int win_cap) {
-  size_t b = sizeof(int32_t) * 5 * static_cast<size_t>(tab_cap);
+  size_t b = table_bytes(tab_cap);
   if (win_cap > 0) b += 8 * static_cast<size_t>(win_cap) + sizeof(int32_t) * (kMergeSamples + kMaxR);
+  else b += 8 * static_cast<size_t>(value_cache_cap(tab_cap));   // value + index
   return b;
 }
 
@@ -966,8 +1051,10 @@ int configure() {   // returns the dynamic shared memory this instantiation may 
 int max_dyn_smem() {
   const int a = std::min(configure<16, true>(), configure<8, true>());
   const int b = std::min(configure<4, true>(), configure<2, true>());
-  const int c = std::min(configure<16, false>(), configure<8, false>());
-  const int d = std::min(configure<4, false>(), configure<2, false>());
+  const int c = std::min(std::min(configure<16, false>(), configure<10, false>()),
+                         configure<8, false>());
+  const int d = std::min(std::min(configure<6, false>(), configure<4, false>()),
+                         configure<2, false>());
   return std::min(std::min(a, b), std::min(c, d));
 }
 
@@ -998,7 +1085,13 @@ int max_clusters(size_t smem) {
 template <bool F>
 int clusters_for(int cl, size_t smem) {
   if (cl >= 16) return max_clusters<16, F>(smem);
+  if constexpr (!F) {
+    if (cl >= 10) return max_clusters<10, F>(smem);
+  }
   if (cl >= 8) return max_clusters<8, F>(smem);
+  if constexpr (!F) {
+    if (cl >= 6) return max_clusters<6, F>(smem);
+  }
   if (cl >= 4) return max_clusters<4, F>(smem);
   return max_clusters<2, F>(smem);
 }
@@ -1006,14 +1099,19 @@ int clusters_for(int cl, size_t smem) {
 template <int CL, bool F>
 void launch_cl(const SelTask* tasks_dev, int ntask, int tab_cap, int win_cap, cudaStream_t s) {
   const size_t smem = dyn_bytes(tab_cap, win_cap);
+  const int vcap = win_cap > 0 ? 0 : value_cache_cap(tab_cap);
   configure<CL, F>();
   cudaLaunchAttribute attr[2];
   cudaLaunchConfig_t lc = cl_config<CL>(ntask, smem, s, attr);
-  cudaLaunchKernelEx(&lc, k_select<CL, F>, tasks_dev, tab_cap, win_cap);
+  cudaLaunchKernelEx(&lc, k_select<CL, F>, tasks_dev, tab_cap, win_cap, vcap);
 }
 
 template <bool F>
 void launch_w(int cl, const SelTask* tasks_dev, int ntask, int tab_cap, int win_cap, cudaStream_t s) {
+  if constexpr (!F) {   // widths that are not powers of two: plain selects only
+    if (cl >= 10 && cl < 16) return launch_cl<10, F>(tasks_dev, ntask, tab_cap, win_cap, s);
+    if (cl >= 6 && cl < 8) return launch_cl<6, F>(tasks_dev, ntask, tab_cap, win_cap, s);
+  }
   if (cl >= 16) launch_cl<16, F>(tasks_dev, ntask, tab_cap, win_cap, s);
   else if (cl >= 8) launch_cl<8, F>(tasks_dev, ntask, tab_cap, win_cap, s);
   else if (cl >= 4) launch_cl<4, F>(tasks_dev, ntask, tab_cap, win_cap, s);
@@ -1040,7 +1138,7 @@ int sel_chunk_capacity(const SelTask& t) {
 }
 
 int select_max_window() {
-  const int avail = max_dyn_smem() - (int)dyn_bytes(table_cap(1), 0) -
+  const int avail = max_dyn_smem() - (int)table_bytes(table_cap(1)) -
                     (int)(sizeof(int32_t) * (kMergeSamples + kMaxR)) - 1024;
   return avail > 0 ? avail / 8 : 0;
 }
@@ -1059,10 +1157,14 @@ int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_
   // wave (a second wave would double the latency of the whole batch)
   int cl = cluster > 0 ? cluster : forced_cl();
   if (cl == 0) {
-    if (clusters_for<false>(16, smem) >= ntask) cl = 16;
-    else if (clusters_for<false>(8, smem) >= ntask) cl = 8;
-    else if (clusters_for<false>(4, smem) >= ntask) cl = 4;
-    else cl = 2;
+    // widths 10 and 6 fill the GPCs better than 8 and 4 (B200: 11 and 22
+    // resident clusters against 15 and 33, i.e. 80/96 CTAs for 8/16 tasks)
+    cl = 2;
+    for (int w : {16, 10, 8, 6, 4})
+      if (clusters_for<false>(w, smem) >= ntask) {
+        cl = w;
+        break;
+      }
   }
   static int dbg = 0;
   if (dbg < 8 && getenv("SPARDL_DEBUG")) {
