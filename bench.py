@@ -60,7 +60,10 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self):
+    def __init__(self, gpus=None):
+        # physical indices of the GPUs this job runs on: idle GPUs of a larger
+        # box would otherwise pull the median down to their idle clock
+        self.gpus = None if gpus is None else {str(g) for g in gpus}
         self.rows = []
         self.proc = None
         self.recording = False
@@ -80,7 +83,9 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             if self.recording:
-                self.rows.append([x.strip() for x in line.split(",")])
+                row = [x.strip() for x in line.split(",")]
+                if self.gpus is None or (row and row[0] in self.gpus):
+                    self.rows.append(row)
 
     def stop(self):
         if self.proc:
@@ -259,7 +264,9 @@ def main():
             ctx.all_reduce(grads)
         ctx.sync()
         out = {"P": P, "N": N, "k": k, "wloc": wloc}
-        sampler = ClockSampler() if (extras and local_rank == 0) else None
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        phys = [v.strip() for v in vis.split(",")] if vis else [str(i) for i in range(world)]
+        sampler = ClockSampler(phys[:world]) if (extras and local_rank == 0) else None
         if sampler:
             sampler.start()
             time.sleep(0.3)

@@ -63,7 +63,11 @@ def test_topk_select_slice(env, kind, lo, hi, budget):
 @pytest.mark.parametrize("kind", ["gauss", "int", "mixed"])
 @pytest.mark.parametrize("r,nnz,span", [(2, 10, 30), (2, 5000, 20000), (3, 40000, 60000),
                                         (4, 100000, 300000), (5, 1000, 1000), (8, 20000, 50000),
-                                        (2, 0, 10), (3, 50000, 50000)])
+                                        (2, 0, 10), (3, 50000, 50000),
+                                        # > 1024 splitters: the rank + partition kernel pair
+                                        # (merge-path folds for r <= 3, rank scatter above)
+                                        (2, 700000, 3000000), (3, 400000, 2000000),
+                                        (4, 200000, 1000000)])
 def test_merge_add(env, kind, r, nnz, span):
     sd, orc, torch = env
     rng = np.random.default_rng(r * 1000 + nnz)
