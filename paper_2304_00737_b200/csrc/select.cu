@@ -39,6 +39,9 @@ namespace sdl {
 namespace {
 
 constexpr int kSelThreads = 512;   // 16 warps per CTA
+#ifndef SPARDL_SEL_MINB
+#define SPARDL_SEL_MINB 1
+#endif
 constexpr int kWarps = kSelThreads / 32;
 #ifndef SPARDL_SEL_ILP
 #define SPARDL_SEL_ILP 8
@@ -405,9 +408,6 @@ __device__ long long merge_prologue(const MergeTask& mt, int cr, int32_t* w_idx,
   return total;
 }
 
-#ifndef SPARDL_SEL_MINB
-#define SPARDL_SEL_MINB 1
-#endif
 template <int CL, bool FUSED>
 __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     k_select(const SelTask* __restrict__ tasks, int tab_cap, int win_cap, int vcap) {
@@ -1011,7 +1011,11 @@ int value_cache_cap(int tab_cap) {
     return e && e[0] == '0';
   }();
   if (off) return 0;
-  const long long avail = (long long)max_dyn_smem() - (long long)table_bytes(tab_cap);
+  // (SPARDL_SEL_MINB CTAs share an SM's 228 KB; ~24 KB of static shared
+  // memory and reserve per CTA)
+  const long long budget = SPARDL_SEL_MINB > 1 ? 233472ll / SPARDL_SEL_MINB - 24 * 1024
+                                               : (long long)max_dyn_smem();
+  const long long avail = budget - (long long)table_bytes(tab_cap);
   return avail >= 8 * 1024 ? (int)((avail / 8) & ~31ll) : 0;
 }
 

@@ -1,3 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_components.py -x -q -m gpu -k merge > gpurun_out/gt.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_components.py -x -q -m gpu > gpurun_out/gt.log 2>&1
 tail -2 gpurun_out/gt.log
+bash run_ab.sh "|SPARDL_STEP_EVENTS=1" "|SPARDL_STEP_EVENTS=1 SPARDL_MERGE_PATH=0" > gpurun_out/ab.log 2>&1
+cat gpurun_out/ab.log | grep -v resident; for i in 0 1; do grep -h "steps:" gpurun_out/ab_$i.log; done
+python dbg_profile.py graph 2>&1 | tail -12
