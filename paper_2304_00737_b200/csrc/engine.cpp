@@ -203,7 +203,10 @@ void Engine::drop_graph() {
 int Engine::new_uid(int owner) {
   uid_owner_.push_back(owner);
   if (rank_slots_.size() != static_cast<size_t>(world_)) rank_slots_.assign(static_cast<size_t>(world_), 0);
-  uid_slot_.push_back(rank_slots_[static_cast<size_t>(rank_of(owner))]++);
+  // every uid has its own buffer index on every rank (peer transport: a
+  // producer may write a block straight into its consumer's copy)
+  rank_slots_[static_cast<size_t>(rank_of(owner))]++;
+  uid_slot_.push_back(next_uid_);
   return next_uid_++;
 }
 
@@ -223,6 +226,29 @@ Slot Engine::sym_slot(int uid) const {
   s.idx = reinterpret_cast<int32_t*>(s.base + 16);
   s.val = reinterpret_cast<float*>(s.base + 16 + 4 * static_cast<size_t>(Lcap_));
   return s;
+}
+
+Slot Engine::own_slot(int uid) const {
+  Slot s = sym_slot(uid);
+  const size_t off = slot_stride_ * static_cast<size_t>(uid_slot_[static_cast<size_t>(uid)]);
+  s.base = peer_base_[static_cast<size_t>(rank_)] + off;
+  s.cnt = reinterpret_cast<int32_t*>(s.base);
+  s.idx = reinterpret_cast<int32_t*>(s.base + 16);
+  s.val = reinterpret_cast<float*>(s.base + 16 + 4 * static_cast<size_t>(Lcap_));
+  return s;
+}
+
+// A block with exactly one remote consumer rank: its producing select also
+// writes the selection into the consumer's copy (same place in its region).
+void Engine::wire_push(sdl::SelTask& t, int uid) const {
+  if (!peer_) return;
+  auto pd = push_dst_.find(uid);
+  if (pd == push_dst_.end()) return;
+  unsigned char* base = peer_base_[static_cast<size_t>(pd->second)] +
+                        slot_stride_ * static_cast<size_t>(uid_slot_[static_cast<size_t>(uid)]);
+  t.sel_cnt2 = reinterpret_cast<int32_t*>(base);
+  t.sel_idx2 = reinterpret_cast<int32_t*>(base + 16);
+  t.sel_val2 = reinterpret_cast<float*>(base + 16 + 4 * static_cast<size_t>(Lcap_));
 }
 
 // A block buffer.  Peer transport: the buffer lives at a fixed place of its
@@ -355,6 +381,7 @@ int Engine::materialize(int w, int pos, std::vector<int> pieces, int64_t budget,
   t.sel_idx = out.idx;
   t.sel_val = out.val;
   t.sel_cnt = out.cnt;
+  wire_push(t, uid);
   int64_t capsum = 0;
   for (int u : pieces) capsum += local_slot(u).cap;
   t.dis_idx = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * capsum));
@@ -379,7 +406,8 @@ void Engine::transfer(std::vector<Xfer>& xs, int uid, int src, int dst, int phas
   deliveries_.push_back({uid, dr});
   if (dr == rank_) {
     if (!has_local(uid)) {
-      slots_[uid] = make_slot(uid);
+      // a pushed block arrives in this rank's own copy of the buffer
+      slots_[uid] = peer_ && push_dst_.count(uid) ? own_slot(uid) : make_slot(uid);
       xs.push_back({uid, src, sr, dr});
     }
     const int li = dst - first_;
@@ -488,6 +516,7 @@ void Engine::plan() {
       t.sel_idx = out.idx;
       t.sel_val = out.val;
       t.sel_cnt = out.cnt;
+      wire_push(t, uid);
       add_select(div_stage_, t, uid, -1);
       div_scr_[static_cast<size_t>(li)][static_cast<size_t>(b)] = div_stage_.sels.back().scr;
     }
@@ -848,8 +877,21 @@ void Engine::setup_peer() {
   int max_slots = 0, nuid = 0;
   {
     Engine dry(cfg_, 0, world_, rank_, nullptr, nullptr, true);
-    for (int c : dry.rank_slots_) max_slots = std::max(max_slots, c);
     nuid = dry.next_uid_;
+    max_slots = nuid;   // global buffer numbering
+    // blocks delivered to exactly one other rank are pushed by their
+    // producing select into the consumer's copy (consumers then read local
+    // memory); blocks with several remote consumers are read remotely
+    const char* pe = std::getenv("SPARDL_PUSH");
+    if (!(pe && pe[0] == '0')) {
+      std::map<int, std::set<int>> dst;
+      for (const auto& dl : dry.deliveries_) {
+        const int o = rank_of(dry.uid_owner_[static_cast<size_t>(dl.first)]);
+        if (dl.second != o) dst[dl.first].insert(dl.second);
+      }
+      for (const auto& kv : dst)
+        if (kv.second.size() == 1) push_dst_[kv.first] = *kv.second.begin();
+    }
   }
   auto align = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
   slot_stride_ = align(16 + 8 * static_cast<size_t>(Lcap_));

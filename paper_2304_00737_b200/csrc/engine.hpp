@@ -240,7 +240,10 @@ class Engine {
   unsigned char* sym_ = nullptr;
   std::vector<unsigned char*> peer_base_;   // per rank; own entry is sym_
   size_t slot_stride_ = 0, flags_off_ = 0, done_off_ = 0;
-  std::vector<int> uid_slot_;               // owner-rank-local buffer index of each uid
+  std::vector<int> uid_slot_;               // buffer index of each uid (peer transport: global)
+  std::map<int, int> push_dst_;             // uid -> the one remote rank its producer writes into
+  Slot own_slot(int uid) const;             // this rank's copy of a pushed block
+  void wire_push(sdl::SelTask& t, int uid) const;
   std::vector<int> rank_slots_;             // buffers numbered so far, per rank
   std::vector<std::pair<int, int>> deliveries_;   // (uid, destination rank), whole plan
   long long* epoch_ = nullptr;

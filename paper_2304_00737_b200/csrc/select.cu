@@ -857,6 +857,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   // ---- 4. ordered compaction, chunk by chunk
   const float w = t.weight;
   const bool want_dis = t.dis_idx != nullptr;
+  const bool push = t.sel_idx2 != nullptr;
   const uint32_t lt = lanemask_lt();
   int cut = -1;
   for (int k = warp; k < nit; k += kWarps) {
@@ -918,6 +919,10 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
         if (is_sel) {
           t.sel_idx[sel_base + sel_rank] = ix;
           t.sel_val[sel_base + sel_rank] = v;
+          if (push) {
+            t.sel_idx2[sel_base + sel_rank] = ix;
+            t.sel_val2[sel_base + sel_rank] = v;
+          }
         } else if (valid && want_dis) {
           const int p = dis_base + (val_rank - sel_rank);
           t.dis_idx[p] = ix;
@@ -932,6 +937,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   }
   if (cr == 0 && threadIdx.x == 0) {
     *t.sel_cnt = (int32_t)all_sel;
+    if (push) *t.sel_cnt2 = (int32_t)all_sel;
     if (t.dis_cnt) *t.dis_cnt = (int32_t)(all_cnt - all_sel);
     if (t.total_out) *t.total_out = my.total;
     // the finished selection, for membership tests (sel_member)
@@ -952,7 +958,9 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   // (no shared-memory access crosses CTAs after the totals exchange)
   if (t.ps.npub > 0) {
     // every CTA's output writes are ordered before this cluster barrier: the
-    // block can go to its consumers now, not at the end of the batch
+    // block can go to its consumers now, not at the end of the batch (the
+    // copy pushed into a peer's memory is fenced at system scope first)
+    if (push) __threadfence_system();
     cluster.sync();
     if (cr == 0 && threadIdx.x == 0) peer_publish(t.ps);
   }
