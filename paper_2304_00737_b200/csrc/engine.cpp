@@ -238,17 +238,21 @@ Slot Engine::own_slot(int uid) const {
   return s;
 }
 
-// A block with exactly one remote consumer rank: its producing select also
-// writes the selection into the consumer's copy (same place in its region).
-void Engine::wire_push(sdl::SelTask& t, int uid) const {
+// A block with remote consumer ranks: its producing select also writes the
+// selection into each consumer's copy (the same place in its region).
+void Engine::wire_push(sdl::SelTask& t, int uid) {
   if (!peer_) return;
   auto pd = push_dst_.find(uid);
   if (pd == push_dst_.end()) return;
-  unsigned char* base = peer_base_[static_cast<size_t>(pd->second)] +
-                        slot_stride_ * static_cast<size_t>(uid_slot_[static_cast<size_t>(uid)]);
-  t.sel_cnt2 = reinterpret_cast<int32_t*>(base);
-  t.sel_idx2 = reinterpret_cast<int32_t*>(base + 16);
-  t.sel_val2 = reinterpret_cast<float*>(base + 16 + 4 * static_cast<size_t>(Lcap_));
+  std::vector<unsigned char*> bases;
+  for (int r : pd->second)
+    bases.push_back(peer_base_[static_cast<size_t>(r)] +
+                    slot_stride_ * static_cast<size_t>(uid_slot_[static_cast<size_t>(uid)]));
+  auto* d = static_cast<unsigned char**>(arena_.alloc(sizeof(unsigned char*) * bases.size()));
+  CK(mcpy(d, bases.data(), sizeof(unsigned char*) * bases.size(), cudaMemcpyHostToDevice));
+  t.push_base = d;
+  t.npush = static_cast<int32_t>(bases.size());
+  t.push_cap = static_cast<int32_t>(Lcap_);
 }
 
 // A block buffer.  Peer transport: the buffer lives at a fixed place of its
@@ -879,9 +883,8 @@ void Engine::setup_peer() {
     Engine dry(cfg_, 0, world_, rank_, nullptr, nullptr, true);
     nuid = dry.next_uid_;
     max_slots = nuid;   // global buffer numbering
-    // blocks delivered to exactly one other rank are pushed by their
-    // producing select into the consumer's copy (consumers then read local
-    // memory); blocks with several remote consumers are read remotely
+    // blocks delivered to other ranks are pushed by their producing select
+    // into every consumer rank's copy (consumers then read local memory)
     const char* pe = std::getenv("SPARDL_PUSH");
     if (!(pe && pe[0] == '0')) {
       std::map<int, std::set<int>> dst;
@@ -890,7 +893,8 @@ void Engine::setup_peer() {
         if (dl.second != o) dst[dl.first].insert(dl.second);
       }
       for (const auto& kv : dst)
-        if (kv.second.size() == 1) push_dst_[kv.first] = *kv.second.begin();
+        if (kv.second.size() <= static_cast<size_t>(sdl::kMaxPush))
+          push_dst_[kv.first] = std::vector<int>(kv.second.begin(), kv.second.end());
     }
   }
   auto align = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };

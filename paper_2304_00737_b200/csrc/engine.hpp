@@ -241,9 +241,9 @@ class Engine {
   std::vector<unsigned char*> peer_base_;   // per rank; own entry is sym_
   size_t slot_stride_ = 0, flags_off_ = 0, done_off_ = 0;
   std::vector<int> uid_slot_;               // buffer index of each uid (peer transport: global)
-  std::map<int, int> push_dst_;             // uid -> the one remote rank its producer writes into
+  std::map<int, std::vector<int>> push_dst_;   // uid -> remote ranks its producer writes into
   Slot own_slot(int uid) const;             // this rank's copy of a pushed block
-  void wire_push(sdl::SelTask& t, int uid) const;
+  void wire_push(sdl::SelTask& t, int uid);
   std::vector<int> rank_slots_;             // buffers numbered so far, per rank
   std::vector<std::pair<int, int>> deliveries_;   // (uid, destination rank), whole plan
   long long* epoch_ = nullptr;

@@ -148,12 +148,14 @@ struct SelTask {
   int32_t merge_slot;    // host bookkeeping: 1 + index of the stage's merge task, 0 none
   int32_t pad3_;
   PeerSync ps;           // waits on remote inputs, publishes the output
-  // peer transport, block with one remote consumer: a second copy of the
-  // selection written straight into the consumer's buffer (null: none)
-  int32_t* sel_idx2;
-  float* sel_val2;
-  int32_t* sel_cnt2;
+  // peer transport: copies of the selection written straight into the
+  // buffers of the consumer ranks (slot layout: count, idx[push_cap],
+  // val[push_cap]); npush = 0: none
+  unsigned char* const* push_base;
+  int32_t npush;
+  int32_t push_cap;
 };
+constexpr int kMaxPush = 8;   // remote consumer ranks a select writes into
 
 // value bits of a merge hole: its magnitude key is kHoleKey, never a real
 // entry's (a NaN with every mantissa bit set)

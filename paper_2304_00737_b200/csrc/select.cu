@@ -857,7 +857,16 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   // ---- 4. ordered compaction, chunk by chunk
   const float w = t.weight;
   const bool want_dis = t.dis_idx != nullptr;
-  const bool push = t.sel_idx2 != nullptr;
+  // consumer ranks' copies (peer transport): bases held in registers
+  const int npush = t.npush;
+  int32_t* pidx[kMaxPush];
+  float* pval[kMaxPush];
+#pragma unroll
+  for (int p = 0; p < kMaxPush; ++p) {
+    unsigned char* b = p < npush ? t.push_base[p] : nullptr;
+    pidx[p] = reinterpret_cast<int32_t*>(b + 16);
+    pval[p] = reinterpret_cast<float*>(b + 16 + 4 * (size_t)t.push_cap);
+  }
   const uint32_t lt = lanemask_lt();
   int cut = -1;
   for (int k = warp; k < nit; k += kWarps) {
@@ -919,10 +928,12 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
         if (is_sel) {
           t.sel_idx[sel_base + sel_rank] = ix;
           t.sel_val[sel_base + sel_rank] = v;
-          if (push) {
-            t.sel_idx2[sel_base + sel_rank] = ix;
-            t.sel_val2[sel_base + sel_rank] = v;
-          }
+#pragma unroll
+          for (int p = 0; p < kMaxPush; ++p)
+            if (p < npush) {
+              pidx[p][sel_base + sel_rank] = ix;
+              pval[p][sel_base + sel_rank] = v;
+            }
         } else if (valid && want_dis) {
           const int p = dis_base + (val_rank - sel_rank);
           t.dis_idx[p] = ix;
@@ -937,7 +948,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   }
   if (cr == 0 && threadIdx.x == 0) {
     *t.sel_cnt = (int32_t)all_sel;
-    if (push) *t.sel_cnt2 = (int32_t)all_sel;
+    for (int p = 0; p < npush; ++p) *reinterpret_cast<int32_t*>(t.push_base[p]) = (int32_t)all_sel;
     if (t.dis_cnt) *t.dis_cnt = (int32_t)(all_cnt - all_sel);
     if (t.total_out) *t.total_out = my.total;
     // the finished selection, for membership tests (sel_member)
@@ -960,7 +971,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     // every CTA's output writes are ordered before this cluster barrier: the
     // block can go to its consumers now, not at the end of the batch (the
     // copy pushed into a peer's memory is fenced at system scope first)
-    if (push) __threadfence_system();
+    if (npush > 0) __threadfence_system();
     cluster.sync();
     if (cr == 0 && threadIdx.x == 0) peer_publish(t.ps);
   }
