@@ -44,7 +44,7 @@ constexpr int kSelThreads = 512;   // 16 warps per CTA
 #endif
 constexpr int kWarps = kSelThreads / 32;
 #ifndef SPARDL_SEL_ILP
-#define SPARDL_SEL_ILP 8
+#define SPARDL_SEL_ILP 4
 #endif
 constexpr int kIlp = SPARDL_SEL_ILP;   // 32-entry groups loaded per warp step (memory-level parallelism)
 constexpr int kChunkE = 32 * kIlp;   // flat entries per work chunk (one warp step)
