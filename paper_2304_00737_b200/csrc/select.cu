@@ -606,6 +606,18 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
   }
+  // the staged items are a prefix (coff is their running sum): items < kst,
+  // entries vc[0, nst) -- the histogram passes sweep them flat, whatever
+  // the item boundaries (short candidate segments would leave lanes idle)
+  __shared__ int s_kst;
+  if (threadIdx.x == 0) s_kst = nit;
+  __syncthreads();
+  if (vcap > 0)
+    for (int k = threadIdx.x; k < nit; k += kSelThreads)
+      if (coff[k] + ilen[k] > vcap) atomicMin(&s_kst, k);
+  __syncthreads();
+  const int kst = vcap > 0 ? s_kst : 0;
+  const int nst = kst > 0 ? coff[kst - 1] + ilen[kst - 1] : 0;
   auto staged = [&](int cb, int c) { return vcap > 0 && cb + c <= vcap; };
   auto fetch = [&](int cb, const float* __restrict__ vp, int c, int j0, float* v) {
     if (staged(cb, c)) {
@@ -657,7 +669,23 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     for (int b = threadIdx.x; b < kBins; b += kSelThreads) hist[b] = 0;
     __syncthreads();
     long long above = 0, inside = 0;
-    for (int k = warp; k < nit; k += kWarps) {
+    for (int e0 = threadIdx.x; e0 < nst; e0 += kSelThreads * kIlp) {
+      uint32_t key[kIlp];
+#pragma unroll
+      for (int u = 0; u < kIlp; ++u) {
+        const int e = e0 + u * kSelThreads;
+        key[u] = e < nst ? mag_key(vc[e]) : kHoleKey;
+      }
+#pragma unroll
+      for (int u = 0; u < kIlp; ++u) {
+        const bool valid = key[u] != kHoleKey;
+        const uint32_t top = key[u] >> 20;
+        above += valid && top > d0;
+        inside += valid && top == d0;
+        hist_add(hist, (key[u] >> 9) & (kBins - 1), valid && top == d0);
+      }
+    }
+    for (int k = kst + warp; k < nit; k += kWarps) {
       const int c = ilen[k];
       const int cb = vcap > 0 ? coff[k] : 0;
       const float* __restrict__ vp = vbase + iof[k];
@@ -725,7 +753,19 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       for (int b = threadIdx.x; b < nb; b += kSelThreads) hist[b] = 0;
       __syncthreads();
       const uint32_t prefix = my.prefix, pmask = my.pmask;
-      for (int k = warp; k < nit; k += kWarps) {
+      for (int e0 = threadIdx.x; e0 < nst; e0 += kSelThreads * kIlp) {
+        uint32_t key[kIlp];
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+          const int e = e0 + u * kSelThreads;
+          key[u] = e < nst ? mag_key(vc[e]) : kHoleKey;
+        }
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u)
+          hist_add(hist, (key[u] >> shift) & (nb - 1),
+                   key[u] != kHoleKey && (key[u] & pmask) == prefix);
+      }
+      for (int k = kst + warp; k < nit; k += kWarps) {
         const int c = ilen[k];
         const int cb = vcap > 0 ? coff[k] : 0;
         const float* __restrict__ vp = vbase + iof[k];
