@@ -375,6 +375,11 @@ def main():
     cand_bytes = 12 * N * wloc                      # read g, read carry, write carry
     achieved = cand_bytes / (ph[1] * 1e-3) / 1e9
     t_roof_ms = 12 * N * wloc / (peak * 1e9) * 1e3  # HBM bound of the whole step
+    # fabric bytes: the ledger's scalars received per worker per iteration x 4 B
+    # (SURVEY 8d B_NVL, closed form of inc/sag.hpp:295-340); t_roof = max of both
+    _, _, nvl_scalars = sd.expected_cost_sag(P, r["k"], 1, "none")   # C2/C4: d = 1
+    b_nvl = 4 * nvl_scalars
+    t_nvl_ms = b_nvl / 900e9 * 1e3
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_div_cand.json")
     if os.path.exists(prof):
@@ -407,8 +412,10 @@ def main():
                      "frac": round(achieved / peak, 4), "peak_source": peak_kind,
                      "traffic": traffic, "algorithmic_bytes_per_launch": cand_bytes,
                      "kernel_ms": round(ph[1], 4),
-                     "step_t_roof_ms": round(t_roof_ms, 4),
-                     "step_frac_of_roof": round(t_roof_ms / ms, 4)},
+                     "step_t_roof_ms": round(max(t_roof_ms, t_nvl_ms), 4),
+                     "step_frac_of_roof": round(max(t_roof_ms, t_nvl_ms) / ms, 4),
+                     "nvlink_bytes_per_worker_step": b_nvl,
+                     "t_nvl_ms": round(t_nvl_ms, 4)},
         "phases_ms": {"sample_prethr": round(ph[0], 4), "cand_pass": round(ph[1], 4),
                       "divide_select": round(ph[2], 4), "srs_sag": round(ph[3], 4),
                       "gather_finalize": round(ph[4], 4)},
