@@ -901,11 +901,13 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   const int npush = t.npush;
   int32_t* pidx[kMaxPush];
   float* pval[kMaxPush];
+  if (npush > 0) {
 #pragma unroll
-  for (int p = 0; p < kMaxPush; ++p) {
-    unsigned char* b = p < npush ? t.push_base[p] : nullptr;
-    pidx[p] = reinterpret_cast<int32_t*>(b + 16);
-    pval[p] = reinterpret_cast<float*>(b + 16 + 4 * (size_t)t.push_cap);
+    for (int p = 0; p < kMaxPush; ++p) {
+      unsigned char* b = p < npush ? t.push_base[p] : nullptr;
+      pidx[p] = reinterpret_cast<int32_t*>(b + 16);
+      pval[p] = reinterpret_cast<float*>(b + 16 + 4 * (size_t)t.push_cap);
+    }
   }
   const uint32_t lt = lanemask_lt();
   int cut = -1;
@@ -968,12 +970,14 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
         if (is_sel) {
           t.sel_idx[sel_base + sel_rank] = ix;
           t.sel_val[sel_base + sel_rank] = v;
+          if (npush > 0) {
 #pragma unroll
-          for (int p = 0; p < kMaxPush; ++p)
-            if (p < npush) {
-              pidx[p][sel_base + sel_rank] = ix;
-              pval[p][sel_base + sel_rank] = v;
-            }
+            for (int p = 0; p < kMaxPush; ++p)
+              if (p < npush) {
+                pidx[p][sel_base + sel_rank] = ix;
+                pval[p][sel_base + sel_rank] = v;
+              }
+          }
         } else if (valid && want_dis) {
           const int p = dis_base + (val_rank - sel_rank);
           t.dis_idx[p] = ix;
