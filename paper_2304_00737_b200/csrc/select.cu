@@ -10,12 +10,15 @@
 //   1. counts: CTA totals exchanged through DSMEM -> total, identity case.
 //   2. radix select on the 31-bit magnitude key, digits 11/11/9 bits: each
 //      CTA histograms its entries matching the current prefix in shared
-//      memory, adds the non-zero bins into CTA 0's histogram through DSMEM,
-//      CTA 0 locates the digit holding the rank-th largest key and the other
-//      CTAs read the new prefix from CTA 0 -- two cluster barriers per pass,
-//      no global atomics, no kernel boundaries.  After the three passes the
-//      threshold key T is exact, and need_eq = L - #{key > T} entries of key
-//      T are kept: the lowest-index ones (the reference's tie rule).
+//      memory and sums them into 32-bin super-bins; after ONE cluster barrier
+//      every CTA reads the CL super-bin histograms through DSMEM, finds the
+//      super-bin holding the rank-th largest key, reads the CL copies of its
+//      32 bins and finds the digit itself (identical data, no leader, no
+//      global atomics, no kernel boundaries; histograms double-buffered
+//      across passes).  The previous run's top digit is tried first.  After
+//      the passes the threshold key T is exact, and need_eq = L - #{key > T}
+//      entries of key T are kept: the lowest-index ones (the reference's tie
+//      rule).
 //   3. per segment (one warp each) #{key > T}, #{key == T}; CTA totals go
 //      through DSMEM so every CTA knows the tie quota and the output offsets
 //      of the CTAs before it; a CTA-wide scan places each segment.
@@ -135,51 +138,6 @@ __device__ void update_history(DivHistory* h, int mode, int all, uint32_t T, uin
   h->valid = h->has_T;
   h->last_T = T;
   h->has_T = 1;
-}
-
-// CTA 0: locate the digit holding the rank-th largest key in agg[0..nb).
-// Suffix sums over the threads' bin groups by warp shuffles (two barriers).
-__device__ void find_digit(uint32_t* agg, int nb, int shift, RadixState* st, long long* suf) {
-  const int bpt = nb / kSelThreads;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  long long mine = 0;
-  for (int q = 0; q < bpt; ++q) mine += agg[threadIdx.x * bpt + q];
-  long long x = mine;   // inclusive suffix inside the warp (this lane and above)
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const long long y = __shfl_down_sync(0xffffffffu, x, o);
-    if (lane + o < 32) x += y;
-  }
-  if (lane == 0) suf[warp] = x;   // warp total
-  __syncthreads();
-  if (threadIdx.x < 32) {   // suffix over the warps above
-    long long w = threadIdx.x < kWarps ? suf[threadIdx.x] : 0;
-    const long long own = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_down_sync(0xffffffffu, w, o);
-      if (threadIdx.x + o < 32) w += y;
-    }
-    if (threadIdx.x < kWarps) suf[kWarps + threadIdx.x] = w - own;   // strictly above
-  }
-  __syncthreads();
-  const long long above = (x - mine) + suf[kWarps + warp];
-  const int64_t rank = st->rank;
-  if (above < rank && rank <= above + mine) {
-    long long cum = above;
-    for (int q = bpt - 1; q >= 0; --q) {
-      const uint32_t c = agg[threadIdx.x * bpt + q];
-      if (cum + (long long)c >= rank) {
-        const uint32_t digit = threadIdx.x * bpt + q;
-        st->prefix |= digit << shift;
-        st->pmask |= (uint32_t)(nb - 1) << shift;
-        st->rank = rank - cum;
-        break;
-      }
-      cum += c;
-    }
-  }
-  __syncthreads();
 }
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
@@ -418,10 +376,13 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   SelScratch* sc = t.scr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  __shared__ uint32_t hist[kBins];
-  __shared__ uint32_t agg[kBins];                   // cluster-wide histogram (every CTA a copy)
+  // this CTA's histograms, double-buffered across exchanges (peers read
+  // exchange e's buffer until they reach the barrier of exchange e + 1), and
+  // their 32-bin super-bin sums
+  __shared__ uint32_t histb[2][kBins];
+  __shared__ uint32_t coarse[2][kBins / 32];
+  uint32_t* hist = histb[0];
   __shared__ CtaTotals tot[CL];                     // every CTA's totals (every CTA a copy)
-  __shared__ long long suf[kSelThreads];
   __shared__ int scratch[40];
   __shared__ long long lscr[3 * 32];
   __shared__ RadixState my;                         // radix state (identical in every CTA)
@@ -635,24 +596,72 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     }
   };
 
-  // Cluster exchange of a pass (two barriers): every CTA histograms its own
-  // entries; after barrier A, CTA r sums its 1/CL slice of the bins over all
-  // CTAs' histograms (DSMEM loads) and stores the sums into EVERY CTA's `agg`
-  // (DSMEM stores); after barrier B each CTA locates the digit itself, all on
-  // identical data, so no CTA waits for a leader and no state is broadcast.
-  // A CTA rewrites its histogram only after barrier B (all reads done), and
-  // the next pass's stores into `agg` come after the next barrier A (every
-  // CTA has finished its digit search by then).
-  auto reduce_slice = [&](int nb) {
-    const int per = (nb + CL - 1) / CL;
-    const int hi = min(nb, (cr + 1) * per);
-    for (int b = cr * per + threadIdx.x; b < hi; b += kSelThreads) {
-      uint32_t sum = 0;
-#pragma unroll
-      for (int q = 0; q < CL; ++q) sum += cluster.map_shared_rank(hist, q)[b];
-#pragma unroll
-      for (int q = 0; q < CL; ++q) cluster.map_shared_rank(agg, q)[b] = sum;
+  // Cluster exchange of a pass (one barrier): every CTA histograms its own
+  // entries into histb[x] and sums them into 32-bin super-bins; after the
+  // cluster barrier every CTA reads the CL super-bin histograms (DSMEM),
+  // finds the super-bin holding the rank, reads the CL copies of its 32 bins
+  // and finds the digit -- all CTAs on identical data, no leader, no
+  // broadcast, no second barrier.
+  int xb = 0;   // exchange buffer
+  auto make_coarse = [&](int nb) {   // after the histogram is complete
+    __syncthreads();
+    for (int c = warp; c < nb / 32; c += kWarps) {
+      const uint32_t v = __reduce_add_sync(0xffffffffu, hist[c * 32 + lane]);
+      if (lane == 0) coarse[xb][c] = v;
     }
+  };
+  __shared__ int s_sb;
+  __shared__ long long s_above;
+  auto find_digit_x = [&](int nb, int shift) {   // after the cluster barrier
+    const int nc = nb / 32;            // 64 or 16 super-bins
+    const int spl = nc >= 32 ? nc / 32 : 1;
+    if (warp == 0) {
+      long long part[2] = {0, 0};
+      for (int q = 0; q < CL; ++q) {
+        const uint32_t* cq = cluster.map_shared_rank(coarse[xb], q);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          if (i < spl && lane * spl + i < nc) part[i] += cq[lane * spl + i];
+      }
+      const long long mine = part[0] + part[1];
+      long long x = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_down_sync(0xffffffffu, x, o);
+        if (lane + o < 32) x += y;
+      }
+      const long long above = x - mine;
+      const int64_t rank = my.rank;
+      if (above < rank && rank <= above + mine) {
+        long long cum = above;
+        for (int i = spl - 1; i >= 0; --i) {
+          if (cum + part[i] >= rank) {
+            s_sb = lane * spl + i;
+            s_above = cum;
+            break;
+          }
+          cum += part[i];
+        }
+      }
+      __syncwarp();
+      const int sb = s_sb;
+      const int bin = sb * 32 + lane;
+      long long f = 0;
+      for (int q = 0; q < CL; ++q) f += cluster.map_shared_rank(histb[xb], q)[bin];
+      long long y = f;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long z = __shfl_down_sync(0xffffffffu, y, o);
+        if (lane + o < 32) y += z;
+      }
+      const long long ab = s_above + (y - f);
+      if (ab < rank && rank <= ab + f) {
+        my.prefix |= (uint32_t)bin << shift;
+        my.pmask |= (uint32_t)(nb - 1) << shift;
+        my.rank = rank - ab;
+      }
+    }
+    __syncthreads();
   };
   // CTA totals go to every CTA's `tot` (thread q stores into CTA q)
   auto bcast_tot = [&](CtaTotals v) {
@@ -666,6 +675,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     // histogram of the next 11 bits of the entries in d0, and the counts
     // above and inside d0.  If d0 holds the rank, pass 0 is skipped.
     const uint32_t d0 = prev_T >> 20;
+    hist = histb[xb];
     for (int b = threadIdx.x; b < kBins; b += kSelThreads) hist[b] = 0;
     __syncthreads();
     long long above = 0, inside = 0;
@@ -711,9 +721,8 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     }
     stamp(2);
     bcast_tot({0, above, inside});
-    cluster.sync();   // A
-    reduce_slice(kBins);
-    cluster.sync();   // B
+    make_coarse(kBins);
+    cluster.sync();   // histograms, super-bins and totals of every CTA final
     stamp(3);
     __shared__ int s_hit;
     if (threadIdx.x == 0) {
@@ -739,9 +748,10 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     }
     __syncthreads();
     if (s_hit) {
-      find_digit(agg, kBins, 9, &my, suf);
+      find_digit_x(kBins, 9);
       first_pass = 2;
     }
+    xb ^= 1;
     stamp(4);
     if (cr == 0 && threadIdx.x == 0) sc->pro_ts[7] = 100 + s_hit;   // diagnostics: guess outcome
   }
@@ -750,6 +760,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     for (int pass = first_pass; pass < 3; ++pass) {
       const int shift = pass == 0 ? 20 : (pass == 1 ? 9 : 0);
       const int nb = pass == 2 ? 512 : kBins;
+      hist = histb[xb];
       for (int b = threadIdx.x; b < nb; b += kSelThreads) hist[b] = 0;
       __syncthreads();
       const uint32_t prefix = my.prefix, pmask = my.pmask;
@@ -783,11 +794,11 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       __syncthreads();
       stamp(2 + 3 * pass);
       if (pass == 0) cta_stamp(1);
-      cluster.sync();   // A
-      reduce_slice(nb);
-      cluster.sync();   // B
+      make_coarse(nb);
+      cluster.sync();   // every CTA's histogram and super-bins final
       stamp(3 + 3 * pass);
-      find_digit(agg, nb, shift, &my, suf);
+      find_digit_x(nb, shift);
+      xb ^= 1;
       stamp(4 + 3 * pass);
     }
   }
