@@ -93,6 +93,9 @@ constexpr int kMergeThreads = SPARDL_MERGE_THREADS;   // threads per partition C
 #ifndef SPARDL_MERGE_MINB
 #define SPARDL_MERGE_MINB 1
 #endif
+#ifndef SPARDL_MERGE_PATH_MINB   // merge-path variant (8: one wave for r = 2, but spills)
+#define SPARDL_MERGE_PATH_MINB 1
+#endif
 
 __device__ __forceinline__ void mstamp(const MergeTask& t, int q, int k) {
   if (t.dbg && q < 8 && threadIdx.x == 0) {
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(kMergeThreads, SPARDL_MERGE_MINB) k_merge_part
 constexpr int kOneShotSamples = 4 * kMergeThreads;
 
 template <bool PATH>
-__global__ void __launch_bounds__(kMergeThreads, SPARDL_MERGE_MINB) k_merge_one(const MergeTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(kMergeThreads, PATH ? SPARDL_MERGE_PATH_MINB : SPARDL_MERGE_MINB) k_merge_one(const MergeTask* __restrict__ tasks) {
   pdl_enter();
   const MergeTask& t = tasks[blockIdx.x];
   const int q = blockIdx.y;
