@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kThreads) k_merge_rank(const MergeTask* __rest
 #endif
 constexpr int kMergeThreads = SPARDL_MERGE_THREADS;   // threads per partition CTA
 #ifndef SPARDL_MERGE_MINB
-#define SPARDL_MERGE_MINB 1
+#define SPARDL_MERGE_MINB 6   // 6 CTAs per SM (<= 42 registers): fewer waves for r >= 4
 #endif
 #ifndef SPARDL_MERGE_PATH_MINB   // merge-path variant (8: one wave for r = 2, but spills)
 #define SPARDL_MERGE_PATH_MINB 1
@@ -319,7 +319,7 @@ __device__ __forceinline__ void merge_body(const MergeTask& t, int q, int32_t v_
 }
 
 template <bool PATH>
-__global__ void __launch_bounds__(kMergeThreads, SPARDL_MERGE_MINB) k_merge_part(const MergeTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(kMergeThreads, PATH ? SPARDL_MERGE_PATH_MINB : SPARDL_MERGE_MINB) k_merge_part(const MergeTask* __restrict__ tasks) {
   pdl_enter();
   // grid (task, partition): partitions of every task come first in launch
   // order, so the live ones (q < nparts, usually far fewer than max_parts)

@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-bash run_ab.sh "|SPARDL_STEP_EVENTS=1" "-DSPARDL_MERGE_PATH_MINB=1|SPARDL_STEP_EVENTS=1" "|SPARDL_STEP_EVENTS=1" > gpurun_out/ab.log 2>&1
-cat gpurun_out/ab.log | grep -v resident; for i in 0 1 2; do grep -h "steps:" gpurun_out/ab_$i.log; done
+timeout 900 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_components.py tests/test_gpu_multi.py -q -m gpu > gpurun_out/gt.log 2>&1
+tail -2 gpurun_out/gt.log
+python bench.py --no-cpu --no-north-star --no-e2e > gpurun_out/b1.log 2>&1; grep '^{' gpurun_out/b1.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['n_gpus'], d['ms_per_step'], d['phases_ms'], d['clocks'])"
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29591 bench.py --gpus 2 --no-e2e --no-cpu --no-north-star > gpurun_out/b2.log 2>&1; grep '^{' gpurun_out/b2.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['n_gpus'], d['ms_per_step'], d['phases_ms'], d['clocks'])"
