@@ -457,7 +457,11 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     // pass A: the total
     long long part = 0;
     for (int s = threadIdx.x; s < nseg; s += kSelThreads) part += c_b[s];
-    total = block_sum_ll(part, lscr);
+    {
+      long long u0 = 0, u1 = 0;
+      block_sum3_ll(part, u0, u1, lscr);
+      total = part;
+    }
     const long long lo_t = total * cr / CL, hi_t = total * (cr + 1) / CL;
     // pass B: s0 = #{s : start(s) < lo_t}, s1 = #{s : start(s) < hi_t}
     int carry = 0, n_lo = 0, n_hi = 0;
@@ -482,7 +486,10 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   {
     long long here = 0;
     for (int s = s0 + threadIdx.x; s < s1; s += kSelThreads) here += c_b[s];
-    here = block_sum_ll(here, lscr);
+    {
+      long long u0 = 0, u1 = 0;
+      block_sum3_ll(here, u0, u1, lscr);
+    }
     // smallest piece length (kChunkE * 2^j) whose items fit the table
     long long plen = kChunkE;
     while (nloc + (here + plen - 1) / plen > tab_cap && plen < (1ll << 30)) plen <<= 1;
