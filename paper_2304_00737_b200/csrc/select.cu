@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       const int sel_off = gb + (int)(eb < need_eq ? (long long)eb : need_eq);
       if (k < nit) {
         c_a[k] = sel_off;   // in place: item k is this thread's alone
-        c_b[k] = take;
+        c_b[k] = take == eq ? -1 : take;   // -1: every tie of the item is kept
         c_c[k] = cb - sel_off;
       }
       g_carry += tg;
@@ -968,6 +968,9 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
           is_sel = valid;
         } else if (all == 2) {
           is_sel = false;
+        } else if (take < 0) {   // all ties of this item kept: no tie ranking
+          is_sel = valid && key >= T;
+          if (is_sel && key == T) cut = max(cut, ix);
         } else {
           const bool is_eq = valid && key == T;
           const uint32_t be = __ballot_sync(0xffffffffu, is_eq);
