@@ -125,6 +125,14 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   CK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  {
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CK(cudaStreamCreateWithPriority(&hi_, cudaStreamNonBlocking, greatest));
+    for (auto& e : ev_div_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const char* e = std::getenv("SPARDL_DIV_SPLIT");
+    if (e) div_split_ = std::max(1, std::atoi(e));
+  }
   if (world_ > 1) {
     if (!nccl_id) sdlh::fail(SPARDL_E_ARG, "world_size > 1 needs an NCCL unique id");
     ncclUniqueId id;
@@ -172,6 +180,9 @@ Engine::~Engine() {
   if (side_) cudaStreamDestroy(side_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  if (hi_) cudaStreamDestroy(hi_);
+  for (auto& e : ev_div_)
+    if (e) cudaEventDestroy(e);
   if (own_stream_) cudaStreamDestroy(stream_);
 }
 
@@ -1083,10 +1094,34 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   n += sdl::launch_divide(div_dev_, static_cast<int>(div_tasks_.size()), div_max_chunks_,
                           div_sample_every_, 1, stream_, 1);
   mark(1);
-  n += sdl::launch_divide(div_dev_, static_cast<int>(div_tasks_.size()), div_max_chunks_,
-                          div_sample_every_, 1, stream_, 2);
-  mark(2);
-  n += exec_stage(div_stage_);   // (peer transport: each select publishes its block)
+  // Tasks are worker-major (m_ blocks per local worker).  With a split the
+  // candidate passes of the worker groups run back to back on stream_ and
+  // each group's select runs on the high-priority stream as soon as its own
+  // pass is done, beside the next group's pass.
+  const int ndt = static_cast<int>(div_tasks_.size());
+  const int G = std::min(div_split_, wloc_);
+  if (G <= 1 || div_stage_.sels.size() != div_tasks_.size()) {
+    n += sdl::launch_divide(div_dev_, ndt, div_max_chunks_, div_sample_every_, 1, stream_, 2);
+    mark(2);
+    n += exec_stage(div_stage_);   // (peer transport: each select publishes its block)
+  } else {
+    for (int g = 0; g < G; ++g) {
+      const int t0 = (g * wloc_ / G) * m_, t1 = ((g + 1) * wloc_ / G) * m_;
+      n += sdl::launch_divide(div_dev_ + t0, t1 - t0, div_max_chunks_, div_sample_every_, 1,
+                              stream_, 2);
+      const bool last = g + 1 == G;
+      cudaStream_t ss = last ? stream_ : hi_;
+      if (!last) {
+        CK(cudaEventRecord(ev_div_[0], stream_));
+        CK(cudaStreamWaitEvent(hi_, ev_div_[0], 0));
+      } else {
+        mark(2);
+      }
+      n += sdl::launch_select(div_stage_.sels_dev + t0, t1 - t0, div_stage_.max_nseg, ss);
+    }
+    CK(cudaEventRecord(ev_div_[1], hi_));
+    CK(cudaStreamWaitEvent(stream_, ev_div_[1], 0));
+  }
   mark(3);
   // optional per-step events (profiling diagnostics, SPARDL_STEP_EVENTS=1)
   auto step_mark = [&](size_t i, int what) {
@@ -1192,7 +1227,7 @@ void Engine::run(const float* const* grads) {
         throw;
       }
       CK(cudaStreamEndCapture(stream_, &g));
-      CK(cudaGraphInstantiate(&graph_, g, 0));
+      CK(cudaGraphInstantiate(&graph_, g, cudaGraphInstantiateFlagUseNodePriority));
       cudaGraphDestroy(g);
     }
     CK(cudaGraphLaunch(graph_, stream_));

@@ -179,6 +179,11 @@ class Engine {
   cudaStream_t stream_ = nullptr;
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  // dividing pass split into worker groups: group g's select (high-priority
+  // stream hi_) overlaps the candidate pass of group g+1 (SPARDL_DIV_SPLIT)
+  cudaStream_t hi_ = nullptr;
+  cudaEvent_t ev_div_[2] = {nullptr, nullptr};
+  int div_split_ = 1;
   bool own_stream_ = false;
   ncclComm_t comm_ = nullptr;
   bool use_graph_ = true;

@@ -1189,8 +1189,16 @@ void launch_cl(const SelTask* tasks_dev, int ntask, int tab_cap, int win_cap, cu
   const size_t smem = dyn_bytes(tab_cap, win_cap);
   const int vcap = win_cap > 0 ? 0 : value_cache_cap(tab_cap);
   configure<CL, F>();
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   cudaLaunchConfig_t lc = cl_config<CL>(ntask, smem, s, attr);
+  // a select on a high-priority stream (overlapping a streaming pass) keeps
+  // its priority inside a captured graph as a node attribute
+  int prio = 0;
+  if (s && cudaStreamGetPriority(s, &prio) == cudaSuccess && prio != 0) {
+    attr[lc.numAttrs].id = cudaLaunchAttributePriority;
+    attr[lc.numAttrs].val.priority = prio;
+    ++lc.numAttrs;
+  }
   cudaLaunchKernelEx(&lc, k_select<CL, F>, tasks_dev, tab_cap, win_cap, vcap);
 }
 

@@ -185,6 +185,18 @@ def test_pipeline_fused_merge(env, P, d, sag, monkeypatch):
     _run(env, P, d, sag, "gres", "optimized", "int", 60_000 + P, P * 300, iters=2, seed=22)
 
 
+@pytest.mark.parametrize("split", [1, 2, 3, 4])
+@pytest.mark.parametrize("P,d,sag", [(8, 1, "none"), (6, 3, "bsag"), (7, 1, "none")])
+def test_pipeline_div_split(env, split, P, d, sag, monkeypatch):
+    """The dividing pass split into worker groups (SPARDL_DIV_SPLIT: group g's
+    select on the high-priority stream beside group g+1's candidate pass),
+    with and without the CUDA graph, gives the same bits."""
+    monkeypatch.setenv("SPARDL_DIV_SPLIT", str(split))
+    _run(env, P, d, sag, "gres", "optimized", "gauss", 300_000, P * 1500, iters=3, seed=23)
+    _run(env, P, d, sag, "gres", "optimized", "int", 60_000 + P, P * 300, iters=2, seed=24,
+         graph=False)
+
+
 @pytest.mark.parametrize("residual", ["gres", "pres", "lres"])
 @pytest.mark.parametrize("P,d,sag,N,kind", [(8, 1, "none", 1_000_000, "gauss"),
                                             (6, 3, "bsag", 300_007, "gauss"),
