@@ -102,11 +102,14 @@ struct CtaTotals {      // per-CTA counters exchanged through DSMEM
   long long cnt, gt, eq;
 };
 
+#ifndef SPARDL_DIV_TARGET
+#define SPARDL_DIV_TARGET 1.3
+#endif
 // Dividing select epilogue: the pre-threshold of the next iteration.
 __device__ void update_history(DivHistory* h, int mode, int all, uint32_t T, uint32_t pre,
                                long long cand, long long budget) {
   constexpr uint32_t kMinDelta = 1u << 12, kMaxDelta = 1u << 26;
-  constexpr double kTarget = 1.5;    // wanted candidates / L
+  constexpr double kTarget = SPARDL_DIV_TARGET;   // wanted candidates / L
   if (mode != 0 || all != 0 || budget <= 0) {   // dense fallback (or trivial): sample again
     if (h->valid) h->delta = h->delta < kMaxDelta / 2 ? h->delta * 2 : kMaxDelta;
     h->valid = 0;
