@@ -98,7 +98,10 @@ __device__ __forceinline__ int warp_bound(const int32_t* a, int n, int32_t x, bo
 // The dividing-selection membership comes from the dividing select's
 // threshold (no search); each in-procedure discard list is joined with the
 // chunk through a shared-memory binary search over the chunk's indices.
-constexpr int kFinChunk = 1024;              // global entries per CTA
+#ifndef SPARDL_FIN_CHUNK
+#define SPARDL_FIN_CHUNK 1024
+#endif
+constexpr int kFinChunk = SPARDL_FIN_CHUNK;  // global entries per CTA
 constexpr int kFinPer = kFinChunk / kThreads;
 
 constexpr int kXiBatch = 4;                  // discard entries per thread per batch

@@ -1,0 +1,10 @@
+#!/bin/bash
+# round-end check: GPU tests, smoke, default bench, launch list
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -8 > gpurun_out/final_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final_smoke.log 2>&1
+timeout 600 python bench.py > gpurun_out/final_bench.log 2>&1
+timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/final_ref.log 2>&1
+SPARDL_DIV_SPLIT=1 python bench.py --profile-only --steps 3 --warmup 3 > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches.csv \
+    python bench.py --profile-only --steps 3 --warmup 3 > gpurun_out/ncu.log 2>&1
