@@ -1,4 +1,5 @@
 import sys, ctypes as C, torch
+# (needs a build with device stamps: make -C paper_2304_00737_b200/csrc -B EXTRA=-DSPARDL_STAMPS=1)
 sys.path.insert(0, '.')
 import paper_2304_00737_b200 as sd
 from paper_2304_00737_b200._lib import lib

@@ -16,6 +16,9 @@
 //   divide  -- the dividing pass (inc/pipeline.hpp:162-184): residual add fused
 //              with candidate compaction above a sampled pre-threshold.
 #pragma once
+#ifndef SPARDL_STAMPS
+#define SPARDL_STAMPS 0   // device phase timestamps (diagnostics; make EXTRA=-DSPARDL_STAMPS=1)
+#endif
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -75,6 +78,7 @@ struct SelScratch {
   int32_t mode;          // resolved input mode for this run
   int32_t cut_idx;       // largest selected index among entries with key == T
   int32_t pad_;
+  // (phase stamps are compiled in only with -DSPARDL_STAMPS=1; zero otherwise)
   long long tstamp[12];  // phase timestamps (globaltimer ns) of the last run, CTA 0
   long long cta_ts[2][16];   // per CTA: start, end of the pass-0 histogram
   long long pro_ts[8];       // CTA 0: fused-merge prologue phase ends

@@ -98,7 +98,7 @@ constexpr int kMergeThreads = SPARDL_MERGE_THREADS;   // threads per partition C
 #endif
 
 __device__ __forceinline__ void mstamp(const MergeTask& t, int q, int k) {
-  if (t.dbg && q < 8 && threadIdx.x == 0) {
+  if (SPARDL_STAMPS && t.dbg && q < 8 && threadIdx.x == 0) {
     long long ts;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
     t.dbg[q * 8 + k] = ts;

@@ -180,7 +180,7 @@ __device__ long long merge_prologue(const MergeTask& mt, int cr, int32_t* w_idx,
                                     cg::cluster_group& cluster, SelScratch* sc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   auto pstamp = [&](int i) {
-    if (cr == 0 && tid == 0) {
+    if (SPARDL_STAMPS && cr == 0 && tid == 0) {
       long long ts;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
       sc->pro_ts[i] = ts;
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   const bool have_prev = sc->all == 0 && prev_T != 0;
 
   auto stamp = [&](int i) {
-    if (cr == 0 && threadIdx.x == 0) {
+    if (SPARDL_STAMPS && cr == 0 && threadIdx.x == 0) {
       long long ts;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
       sc->tstamp[i] = ts;
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   };
   stamp(0);
   auto cta_stamp = [&](int k) {
-    if (threadIdx.x == 0 && cr < 16) {
+    if (SPARDL_STAMPS && threadIdx.x == 0 && cr < 16) {
       long long ts;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
       sc->cta_ts[k][cr] = ts;
