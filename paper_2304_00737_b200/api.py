@@ -269,16 +269,26 @@ class SparDL:
         check(lib().spardl_nccl_unique_id(buf))
         return buf.raw
 
-    @classmethod
-    def from_process_group(cls, cfg: ClusterConfig, device: int, **kw):
-        """One context per rank of the default torch.distributed group (the
-        plumbing only carries the 128-byte NCCL id)."""
+    @staticmethod
+    def rendezvous(group=None):
+        """(world, rank, nccl_id) of this process in `group` (default: the
+        default group): the group's first rank creates the NCCL id and
+        broadcasts it over the group -- the torch.distributed plumbing only
+        carries these 128 bytes."""
         import torch.distributed as dist
-        world, rank = dist.get_world_size(), dist.get_rank()
-        obj = [cls.nccl_unique_id() if rank == 0 else None]
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        obj = [SparDL.nccl_unique_id() if rank == 0 else None]
         if world > 1:
-            dist.broadcast_object_list(obj, src=0)
-        return cls(cfg, device=device, world_size=world, rank=rank, nccl_id=obj[0], **kw)
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+        return world, rank, obj[0]
+
+    @classmethod
+    def from_process_group(cls, cfg: ClusterConfig, device: int, group=None, **kw):
+        """One context per rank of `group` (default: the default group); the
+        rank inside the group is the SparDL worker rank."""
+        world, rank, nid = cls.rendezvous(group)
+        return cls(cfg, device=device, world_size=world, rank=rank, nccl_id=nid, **kw)
 
     def close(self):
         if self._h:

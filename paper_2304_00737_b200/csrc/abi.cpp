@@ -50,8 +50,12 @@ void need(const void* p, const char* what) {
   if (!p) sdlh::fail(SPARDL_E_ARG, std::string("null argument: ") + what);
 }
 
-// scoped device allocations for the one-shot component entry points
+// scoped device allocations for the one-shot component entry points; the
+// zero fill is ordered on the caller's stream (a torch side stream is
+// non-blocking: a legacy-stream memset would race the uploads on it)
 struct DevBuf {
+  explicit DevBuf(cudaStream_t st) : s(st) {}
+  cudaStream_t s;
   std::vector<void*> ptrs;
   ~DevBuf() {
     for (void* p : ptrs) cudaFree(p);
@@ -60,9 +64,30 @@ struct DevBuf {
   T* get(size_t n) {
     void* p = nullptr;
     CK(cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)));
-    CK(cudaMemset(p, 0, std::max<size_t>(n * sizeof(T), 16)));
+    CK(cudaMemsetAsync(p, 0, std::max<size_t>(n * sizeof(T), 16), s));
     ptrs.push_back(p);
     return static_cast<T*>(p);
+  }
+};
+
+// The component entry points run on the device that owns their inputs
+// (restored on return), so a caller on cuda:1 needs no cudaSetDevice.
+struct DeviceOf {
+  int prev = -1;
+  explicit DeviceOf(const void* p) {
+    cudaPointerAttributes a{};
+    if (p && cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      if (cur != a.device) {
+        prev = cur;
+        CK(cudaSetDevice(a.device));
+      }
+    }
+    cudaGetLastError();
+  }
+  ~DeviceOf() {
+    if (prev >= 0) cudaSetDevice(prev);
   }
 };
 
@@ -215,8 +240,9 @@ EXPORT int spardl_topk_select(const int32_t* idx, const float* val, int64_t n, i
     require_device();
     if (budget < 0) sdlh::fail(SPARDL_E_ERROR, "top_k_select: negative budget");
     if (n < 0 || n >= (int64_t(1) << 31)) sdlh::fail(SPARDL_E_ARG, "n out of range");
+    DeviceOf on(val);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    DevBuf buf;
+    DevBuf buf(s);
     int32_t* cnt = buf.get<int32_t>(3);
     const int32_t n32 = static_cast<int32_t>(n);
     CK(cudaMemcpyAsync(cnt, &n32, sizeof(n32), cudaMemcpyHostToDevice, s));
@@ -255,13 +281,14 @@ EXPORT int spardl_topk_select_slice(const float* g, int64_t lo, int64_t hi, int6
     if (lo < 0 || hi < lo || hi >= (int64_t(1) << 31)) sdlh::fail(SPARDL_E_ARG, "bad range");
     if (reinterpret_cast<uintptr_t>(g) % 16 != 0)
       sdlh::fail(SPARDL_E_ARG, "slice base must be 16-byte aligned");
+    DeviceOf on(g);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t nb = hi - lo;
     if (nb == 0) {
       *n_sel = 0;
       return;
     }
-    DevBuf buf;
+    DevBuf buf(s);
     sdl::DivTask dt{};
     sdl::SelTask t{};
     sdl::div_plan(dt, t, lo, hi, budget,
@@ -292,8 +319,9 @@ EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* c
   return guarded([&] {   // inc/sparse.hpp:182-208 folded left over r lists
     require_device();
     if (r < 1 || r > sdl::kMaxR) sdlh::fail(SPARDL_E_ARG, "merge_add: 1 <= r <= 16 lists");
+    DeviceOf on(out_idx);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    DevBuf buf;
+    DevBuf buf(s);
     int32_t* cnts = buf.get<int32_t>(static_cast<size_t>(r) + 1);
     std::vector<int32_t> hc(static_cast<size_t>(r));
     int64_t capsum = 0, capmax = 1;
@@ -372,7 +400,7 @@ EXPORT int spardl_topk_select_hostbuf(const int32_t* idx, const float* val, int6
   int rc = SPARDL_OK;
   const int outer = guarded([&] {
     require_device();
-    DevBuf buf;
+    DevBuf buf(nullptr);
     const size_t un = static_cast<size_t>(n < 0 ? 0 : n);
     int32_t* di = to_dev(buf, idx, un);
     float* dv = to_dev(buf, val, un);
@@ -402,7 +430,7 @@ EXPORT int spardl_topk_select_slice_hostbuf(const float* g, int64_t lo, int64_t 
   const int outer = guarded([&] {
     require_device();
     if (hi < lo || lo < 0) sdlh::fail(SPARDL_E_ARG, "bad range");
-    DevBuf buf;
+    DevBuf buf(nullptr);
     float* dg = to_dev(buf, g, static_cast<size_t>(hi));
     const size_t cap = static_cast<size_t>(hi - lo) + 1;
     int32_t* si = buf.get<int32_t>(cap);
@@ -424,7 +452,7 @@ EXPORT int spardl_merge_add_hostbuf(int32_t r, const int32_t* const* idx, const 
   const int outer = guarded([&] {
     require_device();
     if (r < 1 || r > sdl::kMaxR) sdlh::fail(SPARDL_E_ARG, "merge_add: 1 <= r <= 16 lists");
-    DevBuf buf;
+    DevBuf buf(nullptr);
     std::vector<const int32_t*> di(static_cast<size_t>(r));
     std::vector<const float*> dv(static_cast<size_t>(r));
     size_t total = 0;

@@ -235,6 +235,15 @@ inline bool pdl_enabled() {
   return on == 1;
 }
 
+// Kernel attributes (dynamic shared memory opt-in, cluster permissions) are
+// per device: the launchers cache them per current device.
+constexpr int kMaxDevices = 64;
+inline int cur_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+  return d < 0 ? 0 : (d >= kMaxDevices ? kMaxDevices - 1 : d);
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t s, Args... args) {
@@ -248,14 +257,15 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&lc, kernel, static_cast<KArgs>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&lc, kernel, static_cast<KArgs>(args)...);
+  note_launch(e);
+  return e;
 }
 
 
 // ---------------------------------------------------------------------------
 // Peer-transport flags (transport.cu): system-scope acquire/release on
 // per-block readiness flags; bounded spins report through *err.
-constexpr unsigned long long kTimeoutNs = 10ull * 1000 * 1000 * 1000;
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -273,26 +283,38 @@ __device__ __forceinline__ void st_release_sys(long long* p, long long v) {
   asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ inline void spin_until(const long long* flag, long long target, int32_t* err) {
-  if (ld_acquire_sys(flag) >= target) return;
+// Spins until *flag >= target.  Gives up after `timeout_ns`, or as soon as
+// another waiter of this GPU has given up (*err set): the iteration then
+// drains quickly on stale (but in-bounds: every count ever stored is within
+// its buffer's capacity) data, the writers of persistent state skip their
+// stores (err_set), and the host poisons the context at the next sync().
+__device__ __forceinline__ bool err_set(const int32_t* err) {
+  return err && *reinterpret_cast<const volatile int32_t*>(err) != 0;
+}
+
+__device__ inline bool spin_until(const long long* flag, long long target, int32_t* err,
+                                  unsigned long long timeout_ns) {
+  if (ld_acquire_sys(flag) >= target) return true;
   const unsigned long long t0 = gtime();
   unsigned ns = 32;
   while (ld_acquire_sys(flag) < target) {
     __nanosleep(ns);
     if (ns < 1024) ns <<= 1;
-    if (gtime() - t0 > kTimeoutNs) {
+    if (err_set(err)) return false;
+    if (gtime() - t0 > timeout_ns) {
       atomicExch(err, 1);
-      return;
+      return false;
     }
   }
+  return true;
 }
-
 
 // a whole CTA: wait until the task's remote inputs are published
 __device__ inline void peer_wait(const PeerSync& ps) {
   if (ps.nwait <= 0) return;   // uniform per task
   const long long e = *ps.epoch;
-  for (int i = threadIdx.x; i < ps.nwait; i += blockDim.x) spin_until(ps.wait[i], e, ps.err);
+  for (int i = threadIdx.x; i < ps.nwait; i += blockDim.x)
+    spin_until(ps.wait[i], e, ps.err, ps.timeout_ns);
   __syncthreads();
 }
 

@@ -329,10 +329,11 @@ int launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sampl
     // sample_every is uniform across a batch (set by the planner)
     const int sx = (max_chunks + sample_every - 1) / sample_every;
     const int smem = kSampBins * (int)sizeof(uint32_t);
-    static bool configured = false;
-    if (!configured) {
+    static bool configured[kMaxDevices] = {};   // per device (benign race: idempotent)
+    const int dev = cur_device();
+    if (!configured[dev]) {
       cudaFuncSetAttribute(k_div_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      configured = true;
+      configured[dev] = true;
     }
     launch_pdl(k_div_sample, dim3(sx, ntask), dim3(kThreads), smem, s, tasks_dev, apply_residual);
     launch_pdl(k_div_prethr, dim3(ntask), dim3(kThreads), 0, s, tasks_dev);

@@ -163,6 +163,8 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   phase_rounds_.assign(static_cast<size_t>(P_), {0, 0, 0});
   epoch_ = static_cast<long long*>(arena_.alloc(sizeof(long long)));
   peer_err_ = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+  if (const char* to = std::getenv("SPARDL_PEER_TIMEOUT_MS"))
+    timeout_ns_ = static_cast<unsigned long long>(std::max(1, std::atoi(to))) * 1000000ull;
   setup_peer();
   plan();
   plan_peer();
@@ -1009,6 +1011,7 @@ void Engine::plan_peer() {
     ps.npub = static_cast<int32_t>(p.size());
     ps.epoch = epoch_;
     ps.err = peer_err_;
+    ps.timeout_ns = timeout_ns_;
     return ps;
   };
   auto wire_stage = [&](Stage& st) {
@@ -1086,10 +1089,11 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   auto mark = [&](int i) {
     if (ev) CK(cudaEventRecord(ev[i], stream_));
   };
+  const int32_t* abort = peer_ ? peer_err_ : nullptr;   // peer timeout: state untouched
   CK(cudaMemsetAsync(ledger_phase_, 0, sizeof(int64_t) * 3 * wloc_, stream_));
   CK(cudaMemsetAsync(hash_dev_, 0, sizeof(int64_t) * d_, stream_));
   // peers may read our block buffers until they finish the previous iteration
-  if (peer_) n += sdl::launch_begin(epoch_, begin_dev_, npeer_, peer_err_, stream_);
+  if (peer_) n += sdl::launch_begin(epoch_, begin_dev_, npeer_, peer_err_, timeout_ns_, stream_);
   mark(0);
   n += sdl::launch_divide(div_dev_, static_cast<int>(div_tasks_.size()), div_max_chunks_,
                           div_sample_every_, 1, stream_, 1);
@@ -1132,7 +1136,7 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
     n += exec_stage(s.stage);
     step_mark(i, 0);
     if (s.controller_after)
-      n += sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1,
+      n += sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1, abort,
                                   stream_);
     step_mark(i, 1);
     if (i + 1 == steps_.size()) mark(4);
@@ -1145,14 +1149,15 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   CK(cudaEventRecord(ev_fork_, stream_));
   CK(cudaStreamWaitEvent(side_, ev_fork_, 0));
   n += sdl::launch_assemble(asm_dev_, static_cast<int>(asm_tasks_.size()), m_, cfg_.k, side_);
-  n += sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), side_);
+  n += sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), abort, side_);
   n += sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), Lcap_, m_,
-                            static_cast<int>(fin_max_div_), stream_);
+                            static_cast<int>(fin_max_div_), abort, stream_);
   CK(cudaEventRecord(ev_join_, side_));
   CK(cudaStreamWaitEvent(stream_, ev_join_, 0));
   // last remote read of the iteration done: peers may overwrite their buffers
   if (peer_) n += sdl::launch_publish(done_dev_, npeer_, epoch_, stream_);
   mark(5);
+  CK(sdl::take_launch_error());
   CK(cudaGetLastError());
   launches_ = n;
 }
@@ -1199,6 +1204,9 @@ void Engine::profile(const float* const* grads, int iters, double* phase_ms) {
 
 void Engine::run(const float* const* grads) {
   CK(cudaSetDevice(device_));
+  if (poisoned_)
+    sdlh::fail(SPARDL_E_STATE, "peer transport: an earlier iteration timed out waiting for a "
+                               "peer; the residual state is void until reset_state()");
   bool changed = false;
   for (int i = 0; i < wloc_; ++i) {
     if (!grads[i]) sdlh::fail(SPARDL_E_ARG, "null gradient pointer");
@@ -1244,8 +1252,9 @@ void Engine::sync() {
   if (peer_) {
     CK(cudaMemcpy(&err, peer_err_, sizeof(err), cudaMemcpyDeviceToHost));
     if (err) {
-      CK(cudaMemset(peer_err_, 0, sizeof(int32_t)));
-      sdlh::fail(SPARDL_E_CUDA, "peer transport: a peer did not arrive within 10 s");
+      poisoned_ = true;   // carry / controller / ledger of that iteration are void
+      sdlh::fail(SPARDL_E_CUDA, "peer transport: a peer did not arrive within the timeout (" +
+                                    std::to_string(timeout_ns_ / 1000000) + " ms)");
     }
   }
   CK(mcpy(&err, err_dev_, sizeof(err), cudaMemcpyDeviceToHost));
@@ -1258,6 +1267,8 @@ void Engine::sync() {
 void Engine::reset_state() {
   CK(cudaSetDevice(device_));
   CK(cudaStreamSynchronize(stream_));
+  if (peer_) CK(cudaMemset(peer_err_, 0, sizeof(int32_t)));
+  poisoned_ = false;
   for (int i = 0; i < wloc_; ++i) {
     CK(cudaMemset(carry_[static_cast<size_t>(i)], 0, sizeof(float) * cfg_.dimension));
     CK(cudaMemset(ledger_total_[static_cast<size_t>(i)], 0, sizeof(int64_t)));

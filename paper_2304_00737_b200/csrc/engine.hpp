@@ -253,6 +253,8 @@ class Engine {
   std::vector<std::pair<int, int>> deliveries_;   // (uid, destination rank), whole plan
   long long* epoch_ = nullptr;
   int32_t* peer_err_ = nullptr;
+  unsigned long long timeout_ns_ = 10ull * 1000 * 1000 * 1000;   // one peer wait
+  bool poisoned_ = false;   // a peer wait timed out: state void until reset_state()
   const long long** begin_dev_ = nullptr;
   long long** done_dev_ = nullptr;
   int npeer_ = 0;

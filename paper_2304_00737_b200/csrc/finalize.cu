@@ -13,26 +13,33 @@ namespace {
 // Assembly: the global gradient is the concatenation of the m reserved
 // blocks in position order (inc/pipeline.hpp:279-291); blocks cover
 // increasing index ranges, so the result is index-sorted.
+// off[] holds m + 1 ints of dynamic shared memory (any team size).
 __global__ void __launch_bounds__(kThreads) k_assemble(const AssembleTask* __restrict__ tasks) {
   pdl_enter();
   const AssembleTask& t = tasks[blockIdx.y];
   peer_wait(t.ps);   // the gathered blocks of other GPUs are published
-  __shared__ int off[65];
-  if (threadIdx.x == 0) {
-    int s = 0;
-    for (int b = 0; b < t.m; ++b) {
-      off[b] = s;
-      s += *t.src[b].cnt;
+  extern __shared__ int off[];
+  __shared__ int s_part[kThreads / 32];
+  {   // block offsets: CTA-wide exclusive scan of the m counts
+    int run = 0;
+    for (int b0 = 0; b0 < t.m; b0 += kThreads) {
+      const int b = b0 + threadIdx.x;
+      const int c = b < t.m ? *t.src[b].cnt : 0;
+      int tot = 0;
+      const int ex = block_exscan(c, s_part, &tot);
+      if (b < t.m) off[b] = run + ex;
+      run += tot;
     }
-    off[t.m] = s;
-    if (blockIdx.x == 0) *t.out_cnt = s;
+    if (threadIdx.x == 0) {
+      off[t.m] = run;
+      if (blockIdx.x == 0) *t.out_cnt = run;
+    }
   }
   __syncthreads();
   const int total = off[t.m];
   unsigned long long h = 0;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < total; p += gridDim.x * blockDim.x) {
-    int b = 0;
-    while (p >= off[b + 1]) ++b;
+    const int b = upper_bound_i32(off, t.m + 1, p) - 1;   // off[b] <= p < off[b + 1]
     const int j = p - off[b];
     const int32_t ix = t.src[b].idx[j];
     const float v = t.src[b].val[j];
@@ -111,8 +118,10 @@ constexpr int kMaxXiLists = kThreads / 64;   // bound searches in parallel (2 wa
 #ifndef SPARDL_FIN_MINB
 #define SPARDL_FIN_MINB 4
 #endif
-__global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB) k_finalize(const FinalizeTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB)
+    k_finalize(const FinalizeTask* __restrict__ tasks, const int32_t* abort) {
   pdl_enter();
+  if (err_set(abort)) return;   // void iteration (peer timeout): carry untouched
   const FinalizeTask& t = tasks[blockIdx.z];
   if (t.mode == 2) return;   // lres ignores the global gradient
   const int b = blockIdx.y;
@@ -280,8 +289,10 @@ __global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB) k_finalize(const Fi
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_finalize_lres(const FinalizeTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(kThreads)
+    k_finalize_lres(const FinalizeTask* __restrict__ tasks, const int32_t* abort) {
   pdl_enter();
+  if (err_set(abort)) return;
   const FinalizeTask& t = tasks[blockIdx.y];
   if (t.mode != 2) return;
   for (int b = 0; b < t.m; ++b) {
@@ -293,8 +304,9 @@ __global__ void __launch_bounds__(kThreads) k_finalize_lres(const FinalizeTask* 
 }
 
 // ---------------------------------------------------------------------------
-__global__ void k_ledger(const LedgerAdd* __restrict__ adds, int n) {
+__global__ void k_ledger(const LedgerAdd* __restrict__ adds, int n, const int32_t* abort) {
   pdl_enter();
+  if (err_set(abort)) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const long long v = 2ll * (long long)(*adds[i].cnt);
     if (v) atomicAdd(reinterpret_cast<unsigned long long*>(adds[i].dst), (unsigned long long)v);
@@ -304,8 +316,10 @@ __global__ void k_ledger(const LedgerAdd* __restrict__ adds, int n) {
 // ---------------------------------------------------------------------------
 // Algorithm 2 (inc/sag.hpp:61-81) in double precision, llround semantics
 // (round half away from zero) via CUDA's llround.
-__global__ void k_controller(const CtlTask* __restrict__ tasks, int n, int observe) {
+__global__ void k_controller(const CtlTask* __restrict__ tasks, int n, int observe,
+                             const int32_t* abort) {
   pdl_enter();
+  if (err_set(abort)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   HCtl c = *tasks[i].ctl;
@@ -338,39 +352,49 @@ __global__ void k_controller(const CtlTask* __restrict__ tasks, int n, int obser
 
 int launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t max_k,
                     cudaStream_t s) {
-  (void)max_m;
   if (ntask <= 0) return 0;
   int gx = (int)((max_k + kThreads - 1) / kThreads);
   gx = gx < 1 ? 1 : (gx > 1184 ? 1184 : gx);
-  launch_pdl(k_assemble, dim3(gx, ntask), dim3(kThreads), 0, s, tasks_dev);
+  const size_t smem = sizeof(int) * (static_cast<size_t>(max_m) + 1);
+  if (smem > 48 * 1024) {
+    static bool configured[kMaxDevices] = {};
+    const int dev = cur_device();
+    if (!configured[dev]) {
+      cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      configured[dev] = true;
+    }
+  }
+  launch_pdl(k_assemble, dim3(gx, ntask), dim3(kThreads), smem, s, tasks_dev);
   return 1;
 }
 
 int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_blk, int m,
-                    int max_div, cudaStream_t s) {
+                    int max_div, const int32_t* abort, cudaStream_t s) {
   if (ntask <= 0) return 0;
   int gx = (int)((max_blk + kFinChunk - 1) / kFinChunk);
   gx = gx < 1 ? 1 : gx;
-  launch_pdl(k_finalize, dim3(gx, m, ntask), dim3(kThreads), 0, s, tasks_dev);
+  launch_pdl(k_finalize, dim3(gx, m, ntask), dim3(kThreads), 0, s, tasks_dev, abort);
   if (max_div > 0) {
     int lx = (max_div + kThreads - 1) / kThreads;
     lx = lx < 1 ? 1 : (lx > 1184 ? 1184 : lx);
-    launch_pdl(k_finalize_lres, dim3(lx, ntask), dim3(kThreads), 0, s, tasks_dev);
+    launch_pdl(k_finalize_lres, dim3(lx, ntask), dim3(kThreads), 0, s, tasks_dev, abort);
     return 2;
   }
   return 1;
 }
 
-int launch_ledger(const LedgerAdd* adds_dev, int nadd, cudaStream_t s) {
+int launch_ledger(const LedgerAdd* adds_dev, int nadd, const int32_t* abort, cudaStream_t s) {
   if (nadd <= 0) return 0;
   const int gx = (nadd + kThreads - 1) / kThreads;
-  launch_pdl(k_ledger, dim3(gx), dim3(kThreads), 0, s, adds_dev, nadd);
+  launch_pdl(k_ledger, dim3(gx), dim3(kThreads), 0, s, adds_dev, nadd, abort);
   return 1;
 }
 
-int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStream_t s) {
+int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, const int32_t* abort,
+                      cudaStream_t s) {
   if (ntask <= 0) return 0;
-  launch_pdl(k_controller, dim3((ntask + 127) / 128), dim3(128), 0, s, tasks_dev, ntask, observe);
+  launch_pdl(k_controller, dim3((ntask + 127) / 128), dim3(128), 0, s, tasks_dev, ntask, observe,
+             abort);
   return 1;
 }
 

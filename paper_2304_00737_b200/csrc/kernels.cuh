@@ -49,7 +49,8 @@ struct PeerSync {
   int32_t nwait;
   int32_t npub;
   const long long* epoch;
-  int32_t* err;                   // timeout flag
+  int32_t* err;                   // timeout flag (this GPU's; set: the iteration is void)
+  unsigned long long timeout_ns;  // bound of one wait (SPARDL_PEER_TIMEOUT_MS, default 10 s)
 };
 
 struct SelTask;
@@ -242,6 +243,11 @@ struct DivTask {
 
 // ---------------------------------------------------------------------------
 // Launchers (stream-ordered; no host synchronisation inside)
+// They return the number of kernels launched; a failed launch is recorded
+// per host thread (note_launch) and reported by take_launch_error(), which
+// the engine checks after enqueueing an iteration.
+void note_launch(cudaError_t e);
+cudaError_t take_launch_error();
 // ---------------------------------------------------------------------------
 // tasks_dev: device copy of the task array; ntask; max_nseg: grid extent.
 int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s,
@@ -273,7 +279,7 @@ struct AssembleTask {
   PeerSync ps;                // waits on remote source blocks
 };
 int launch_assemble(const AssembleTask* tasks_dev, int ntask, int max_m, int64_t max_k,
-                     cudaStream_t s);
+                    cudaStream_t s);
 
 constexpr int kMaxXi = 24;
 struct XiList {               // one in-procedure discard list (already weight-scaled)
@@ -298,15 +304,17 @@ struct FinalizeTask {
   float* aud_comb;
   float* aud_carry;
 };
+// abort (nullable): the peer-timeout flag; when set the persistent-state
+// writers (finalize, ledger, controller) leave their state untouched
 int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_blk, int m,
-                    int max_div, cudaStream_t s);
+                    int max_div, const int32_t* abort, cudaStream_t s);
 
 // ledger: scalars += 2 * count for each (worker slot, count pointer)
 struct LedgerAdd {
   int64_t* dst;
   const int32_t* cnt;
 };
-int launch_ledger(const LedgerAdd* adds_dev, int nadd, cudaStream_t s);
+int launch_ledger(const LedgerAdd* adds_dev, int nadd, const int32_t* abort, cudaStream_t s);
 
 // B-SAG controller (Algorithm 2, inc/sag.hpp:37-90) on the device
 struct HCtl {
@@ -321,11 +329,12 @@ struct CtlTask {
   const int64_t* n_t;         // its group's union size
   int64_t* budget;            // pre-selection budget for the next run
 };
-int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, cudaStream_t s);
+int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, const int32_t* abort,
+                      cudaStream_t s);
 
 // peer-memory transport (transport.cu): iteration epoch, readiness flags
 int launch_begin(long long* epoch, const long long* const* done, int n, int32_t* err,
-                 cudaStream_t s);
+                 unsigned long long timeout_ns, cudaStream_t s);
 int launch_publish(long long* const* targets, int n, const long long* epoch, cudaStream_t s);
 
 }  // namespace sdl

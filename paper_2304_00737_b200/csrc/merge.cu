@@ -19,6 +19,8 @@
 #include <climits>
 #include <cstdlib>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -467,11 +469,16 @@ int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r
   auto part = path ? k_merge_part<true> : k_merge_part<false>;
   auto single = path ? k_merge_one<true> : k_merge_one<false>;
   // (dynamic + static shared memory above 48 KB needs the opt-in)
-  static size_t configured[2][2] = {{0, 0}, {0, 0}};
-  if (smem > configured[path][one]) {
-    cudaFuncSetAttribute(one ? single : part, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    configured[path][one] = smem;
+  static std::mutex mu;
+  static size_t configured[kMaxDevices][2][2] = {};   // per device
+  {
+    const int dev = cur_device();
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem > configured[dev][path][one]) {
+      cudaFuncSetAttribute(one ? single : part, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      configured[dev][path][one] = smem;
+    }
   }
   if (one) {
     launch_pdl(single, dim3(ntask, max_parts), dim3(kMergeThreads), smem, s, tasks_dev);

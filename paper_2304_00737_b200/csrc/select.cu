@@ -32,6 +32,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -1122,20 +1124,24 @@ int optin_smem() {
 
 template <int CL, bool F>
 int configure() {   // returns the dynamic shared memory this instantiation may use
-  static int maxdyn = -1;
-  if (maxdyn < 0) {   // 16 is a non-portable cluster size on sm_100
+  static std::mutex mu;
+  static int maxdyn[kMaxDevices] = {};   // 0: not configured on that device
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lock(mu);
+  if (maxdyn[dev] <= 0) {   // 16 is a non-portable cluster size on sm_100
     cudaFuncSetAttribute(k_select<CL, F>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(k_select<CL, F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, k_select<CL, F>);
-    maxdyn = optin_smem() - (int)fa.sharedSizeBytes;
-    if (cudaFuncSetAttribute(k_select<CL, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             maxdyn) != cudaSuccess) {
+    int md = optin_smem() - (int)fa.sharedSizeBytes;
+    if (cudaFuncSetAttribute(k_select<CL, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, md) !=
+        cudaSuccess) {
       cudaGetLastError();
-      maxdyn = 48 * 1024 - (int)fa.sharedSizeBytes;
+      md = 48 * 1024 - (int)fa.sharedSizeBytes;
     }
+    maxdyn[dev] = md;
   }
-  return maxdyn;
+  return maxdyn[dev];
 }
 
 // dynamic shared memory every instantiation may use
@@ -1154,9 +1160,17 @@ int max_dyn_smem() {
 template <int CL, bool F>
 int max_clusters(size_t smem) {
   configure<CL, F>();
-  static size_t last_smem = ~size_t(0);
-  static int n = 0;
-  if (smem != last_smem) {
+  static std::mutex mu;
+  static size_t last_smem[kMaxDevices];
+  static int n[kMaxDevices] = {};
+  static bool init = [] {
+    for (auto& x : last_smem) x = ~size_t(0);
+    return true;
+  }();
+  (void)init;
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lock(mu);
+  if (smem != last_smem[dev]) {
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t lc = cl_config<CL>(1, smem, nullptr, attr);
     int c = 0;
@@ -1164,13 +1178,13 @@ int max_clusters(size_t smem) {
       cudaGetLastError();
       c = 0;
     }
-    n = c;
-    last_smem = smem;
+    n[dev] = c;
+    last_smem[dev] = smem;
     if (getenv("SPARDL_DEBUG"))
       fprintf(stderr, "k_select<%d,%d>: %d resident clusters (%zu B dynamic smem)\n", CL, (int)F,
-              n, smem);
+              c, smem);
   }
-  return n;
+  return n[dev];
 }
 
 template <bool F>
@@ -1202,7 +1216,7 @@ void launch_cl(const SelTask* tasks_dev, int ntask, int tab_cap, int win_cap, cu
     attr[lc.numAttrs].val.priority = prio;
     ++lc.numAttrs;
   }
-  cudaLaunchKernelEx(&lc, k_select<CL, F>, tasks_dev, tab_cap, win_cap, vcap);
+  note_launch(cudaLaunchKernelEx(&lc, k_select<CL, F>, tasks_dev, tab_cap, win_cap, vcap));
 }
 
 template <bool F>

@@ -17,8 +17,11 @@
 //              reaches e (peer_wait, common.cuh)
 //   k_publish  after the last remote read of the iteration: store e into
 //              every peer's done[rank] flag
-// Waits are bounded (~10 s): a peer that never arrives sets *err and the next
-// sync() reports it instead of hanging the device.
+// Waits are bounded (10 s, SPARDL_PEER_TIMEOUT_MS): a peer that never arrives
+// sets *err, every later wait of the iteration returns at once, the writers
+// of persistent state (residual finalize, ledger, controller) skip their
+// stores, and the next sync() reports the error and poisons the context
+// until reset_state().
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -26,7 +29,8 @@ namespace sdl {
 
 namespace {
 
-__global__ void k_begin(long long* epoch, const long long* const* done, int n, int32_t* err) {
+__global__ void k_begin(long long* epoch, const long long* const* done, int n, int32_t* err,
+                        unsigned long long timeout_ns) {
   pdl_enter();
   __shared__ long long e;
   if (threadIdx.x == 0) {
@@ -34,7 +38,7 @@ __global__ void k_begin(long long* epoch, const long long* const* done, int n, i
     *epoch = e;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) spin_until(done[i], e - 1, err);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) spin_until(done[i], e - 1, err, timeout_ns);
 }
 
 __global__ void k_publish(long long* const* targets, int n, const long long* epoch) {
@@ -49,9 +53,21 @@ __global__ void k_publish(long long* const* targets, int n, const long long* epo
 
 }  // namespace
 
+namespace {
+thread_local cudaError_t g_launch_error = cudaSuccess;
+}
+void note_launch(cudaError_t e) {
+  if (e != cudaSuccess && g_launch_error == cudaSuccess) g_launch_error = e;
+}
+cudaError_t take_launch_error() {
+  const cudaError_t e = g_launch_error;
+  g_launch_error = cudaSuccess;
+  return e;
+}
+
 int launch_begin(long long* epoch, const long long* const* done, int n, int32_t* err,
-                 cudaStream_t s) {
-  launch_pdl(k_begin, dim3(1), dim3(32), 0, s, epoch, done, n, err);
+                 unsigned long long timeout_ns, cudaStream_t s) {
+  launch_pdl(k_begin, dim3(1), dim3(32), 0, s, epoch, done, n, err, timeout_ns);
   return 1;
 }
 

@@ -42,7 +42,7 @@ class SparDLHookState:
             cfg = ClusterConfig(workers=world, dimension=n, k=min(k, n // world * world),
                                 teams=self.teams, sag=self.sag, residual=self.residual,
                                 timing=self.timing)
-            ctx = SparDL.from_process_group(cfg, device=buf.device.index)
+            ctx = SparDL.from_process_group(cfg, device=buf.device.index, group=self.pg)
             self.contexts[key] = ctx
         return ctx
 

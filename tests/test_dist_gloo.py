@@ -51,10 +51,23 @@ def _worker(rank, world, port, cfgs, q):
                         s = [(o[0], o[3], o[4]) for o in allops[a] if o[1] == b and o[2] == 1]
                         r = [(o[0], o[3], o[4]) for o in allops[b] if o[1] == a and o[2] == 0]
                         ok &= s == r and len(s) > 0
-        # NCCL-id rendezvous as done by SparDL.from_process_group
-        obj = [bytes(range(128)) if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ok &= obj[0] == bytes(range(128))
+        # NCCL-id rendezvous of SparDL.from_process_group: default group and a
+        # subgroup whose first rank is not global rank 0 (DDP hook with a
+        # process_group): every member gets the subgroup leader's id
+        from paper_2304_00737_b200.api import SparDL
+        w, r, nid = SparDL.rendezvous()
+        ids = [None] * world
+        dist.all_gather_object(ids, nid)
+        ok &= (w, r) == (world, rank) and len(nid) == 128 and ids[0] == ids[1]
+        sub = dist.new_group([1])   # a one-rank subgroup led by global rank 1
+        if rank == 1:
+            w, r, nid2 = SparDL.rendezvous(sub)
+            ok &= (w, r) == (1, 0) and len(nid2) == 128
+        pair = dist.new_group([1, 0])
+        w, r, nid3 = SparDL.rendezvous(pair)
+        ids = [None] * world
+        dist.all_gather_object(ids, nid3)
+        ok &= w == 2 and r == rank and ids[0] == ids[1]
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
