@@ -233,6 +233,13 @@ int spardl_get_controller(spardl_ctx* ctx, int32_t local_worker, spardl_hctrl* o
 /* diagnostics: dividing selections of the last call that could not use the
  * candidate fast path and selected from the dense slice (synchronises) */
 int spardl_dense_fallbacks(spardl_ctx* ctx, int64_t* count);
+/* diagnostics: dividing selections that took the dense path, summed over every
+ * call since creation / reset_state (synchronises) */
+int spardl_dense_fallbacks_total(spardl_ctx* ctx, int64_t* count);
+/* diagnostics: selections the wide (whole-GPU) select handed back to the
+ * cluster select (threshold outside the dividing window, massive key ties),
+ * summed since creation / reset_state (synchronises) */
+int spardl_wide_handed_back(spardl_ctx* ctx, int64_t* count);
 /* diagnostics of local dividing task i (= local_worker * m + block):
  * [resolved mode, candidate flags, candidate total, list length, pre-key, capacity,
  *  selection threshold key, carried next pre-key (-1: none), carried margin] */

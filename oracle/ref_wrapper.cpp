@@ -396,6 +396,56 @@ EXPORT int orc_parallel_allreduce_f32(const orc_config* c, const float* const* g
   });
 }
 
+// The reference on all host cores: `threads` independent unmodified
+// reference instances (spardl_all_reduce is single-threaded by design,
+// inc/fabric.hpp:47-53), instance t on slice [t*N, (t+1)*N) of every worker's
+// gradient (N = c->dimension), run in lockstep: step_seconds[it] is the wall
+// time until every instance has finished iteration it.
+EXPORT int orc_parallel_slices_f32(const orc_config* c, const float* const* grads, int threads,
+                                   int iters, double* step_seconds) {
+  return guarded([&] {
+    const auto cfg = to_cluster(c);
+    const size_t n = static_cast<size_t>(cfg.dimension);
+    std::vector<std::vector<spardl::GradientVector>> inputs(static_cast<size_t>(threads));
+    std::vector<std::vector<spardl::WorkerState>> states(static_cast<size_t>(threads));
+    std::vector<std::unique_ptr<spardl::Fabric>> fabrics(static_cast<size_t>(threads));
+    {
+      std::vector<std::thread> prep;
+      for (int t = 0; t < threads; ++t)
+        prep.emplace_back([&, t] {
+          for (int64_t w = 0; w < cfg.workers; ++w) {
+            const float* src = grads[w] + static_cast<size_t>(t) * n;
+            inputs[static_cast<size_t>(t)].emplace_back(std::vector<double>(src, src + n));
+          }
+          states[static_cast<size_t>(t)] = spardl::make_worker_states(cfg);
+          fabrics[static_cast<size_t>(t)] =
+              std::make_unique<spardl::Fabric>(static_cast<int>(cfg.workers));
+        });
+      for (auto& th : prep) th.join();
+    }
+    std::vector<int> bad(static_cast<size_t>(threads), 0);
+    for (int it = 0; it < iters; ++it) {
+      std::vector<std::thread> pool;
+      auto t0 = std::chrono::steady_clock::now();
+      for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+          try {
+            auto r = spardl::spardl_all_reduce(*fabrics[static_cast<size_t>(t)], cfg,
+                                               inputs[static_cast<size_t>(t)],
+                                               states[static_cast<size_t>(t)]);
+            if (!r.consistent) bad[static_cast<size_t>(t)] = 1;
+          } catch (...) {
+            bad[static_cast<size_t>(t)] = 1;
+          }
+        });
+      for (auto& th : pool) th.join();
+      step_seconds[it] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    for (int b : bad)
+      if (b) throw spardl::consistency_error("reference run failed or was inconsistent");
+  });
+}
+
 EXPORT int orc_bsag_phase_cost(int64_t P, int64_t k, int64_t d, int64_t* rounds, int64_t* low,
                                int64_t* high) {
   return guarded([&] {

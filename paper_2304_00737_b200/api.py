@@ -411,6 +411,20 @@ class SparDL:
         check(lib().spardl_dense_fallbacks(self._h, C.byref(n)))
         return n.value
 
+    def dense_fallbacks_total(self) -> int:
+        """Dividing selects that took the dense path, summed since creation /
+        reset_state()."""
+        n = C.c_int64()
+        check(lib().spardl_dense_fallbacks_total(self._h, C.byref(n)))
+        return n.value
+
+    def wide_handed_back(self) -> int:
+        """Selections the whole-GPU select handed back to the cluster select
+        (window miss, massive ties), summed since creation / reset_state()."""
+        n = C.c_int64()
+        check(lib().spardl_wide_handed_back(self._h, C.byref(n)))
+        return n.value
+
     def kernel_launches(self) -> int:
         n = C.c_int64()
         check(lib().spardl_kernel_launches(self._h, C.byref(n)))

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -97,8 +98,48 @@ void require_device() {
     sdlh::fail(SPARDL_E_CUDA, "no CUDA device: the SparDL device path has no CPU fallback");
 }
 
-// One select over prepared inputs, with its scratch.
-void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf) {
+bool wide_enabled() {
+  const char* e = std::getenv("SPARDL_WSEL");
+  return !(e && e[0] == '0');
+}
+
+// The wide-select scratch of a one-shot select (the same layout the engine
+// plans, wselect.cu); t.ws points at its device copy.
+sdl::WScratch* attach_wide(sdl::SelTask& t, DevBuf& buf, cudaStream_t s, const int32_t* idx,
+                           const float* val, const int32_t* seg_off, const int32_t* seg_cnt,
+                           const int32_t* count, int stride, int nseg, int group, int mode,
+                           int is_div, int64_t bin_cap) {
+  sdl::WScratch w{};
+  w.idx = idx;
+  w.val = val;
+  w.seg_off = seg_off;
+  w.seg_cnt = seg_cnt;
+  w.count = count;
+  w.stride = stride;
+  w.nseg = nseg;
+  w.group = std::max(1, std::min(group, 64));
+  w.max_tiles = (nseg + w.group - 1) / w.group;
+  w.mode = mode;
+  w.is_div = is_div;
+  w.bin_cap = static_cast<int32_t>(std::max<int64_t>(1, bin_cap));
+  w.bin_c = buf.get<unsigned long long>(static_cast<size_t>(w.bin_cap));
+  w.bin_tile = buf.get<int32_t>(static_cast<size_t>(w.bin_cap));
+  const size_t nt = static_cast<size_t>(std::max(1, w.max_tiles));
+  w.tile_n = buf.get<int32_t>(nt);
+  w.tile_sel = buf.get<int32_t>(nt);
+  w.tile_sel_off = buf.get<int32_t>(nt);
+  w.tile_dis_off = buf.get<int32_t>(nt);
+  sdl::WScratch* d = buf.get<sdl::WScratch>(1);
+  CK(cudaMemcpyAsync(d, &w, sizeof(w), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));   // (w is a host temporary)
+  t.ws = d;
+  return d;
+}
+
+// One select over prepared inputs, with its scratch: the wide path (when
+// t.ws is set), then the cluster select for a task it hands back.
+void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf, int max_tiles = 0,
+                bool dividing = false) {
   sdl::sel_prepare(t, t.stride);
   if (t.nseg > sdl::kMaxSegPerTask || t.dnseg > sdl::kMaxSegPerTask)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "selection larger than the device work-item bound");
@@ -113,8 +154,11 @@ void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf) {
   t.seg_valid = segs + 5 * nck;
   sdl::SelTask* td = buf.get<sdl::SelTask>(1);
   CK(cudaMemcpyAsync(td, &t, sizeof(t), cudaMemcpyHostToDevice, s));
+  if (t.ws) sdl::launch_wselect(td, 1, max_tiles, !dividing, s);
   sdl::launch_select(td, 1, std::max(1, sdl::sel_scratch_segments(t)), s);
+  CK(sdl::take_launch_error());
   CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));   // (t is a host temporary)
 }
 
 }  // namespace
@@ -263,7 +307,15 @@ EXPORT int spardl_topk_select(const int32_t* idx, const float* val, int64_t n, i
     t.dis_val = dis_val;
     t.dis_cnt = dis_idx ? cnt + 2 : nullptr;
     t.weight = 1.f;
-    if (n > 0) run_select(t, s, buf);
+    int tiles = 0;
+    if (n > 0 && wide_enabled()) {
+      constexpr int kStride = 4096;
+      const int ns = static_cast<int>((n + kStride - 1) / kStride);
+      attach_wide(t, buf, s, idx, val, nullptr, nullptr, cnt, kStride, ns, 1, sdl::kWFull, 0,
+                  std::max<int64_t>(16384, n / 8));
+      tiles = ns;
+    }
+    if (n > 0) run_select(t, s, buf, tiles);
     int32_t out[3] = {0, 0, 0};
     CK(cudaMemcpyAsync(out, cnt, sizeof(out), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -295,6 +347,13 @@ EXPORT int spardl_topk_select_slice(const float* g, int64_t lo, int64_t hi, int6
                   [&](size_t n) { return static_cast<void*>(buf.get<unsigned char>(n)); });
     dt.carry = const_cast<float*>(g);   // read only when apply_residual == 0
     dt.err = buf.get<int32_t>(1);
+    int tiles = 0;
+    if (dt.use_cand && wide_enabled()) {
+      dt.ws = attach_wide(t, buf, s, dt.cand_idx, dt.cand_val, nullptr, dt.cand_cnt, nullptr,
+                          dt.cap, dt.nchunks, 16, sdl::kWWindow, 1,
+                          std::max<int64_t>(16384, budget / 8));
+      tiles = (dt.nchunks + 15) / 16;
+    }
     sdl::DivTask* dtd = buf.get<sdl::DivTask>(1);
     CK(cudaMemcpyAsync(dtd, &dt, sizeof(dt), cudaMemcpyHostToDevice, s));
     sdl::launch_divide(dtd, 1, dt.nchunks, dt.sample_every, 0, s);
@@ -303,7 +362,7 @@ EXPORT int spardl_topk_select_slice(const float* g, int64_t lo, int64_t hi, int6
     t.sel_idx = sel_idx;
     t.sel_val = sel_val;
     t.sel_cnt = cnt;
-    run_select(t, s, buf);
+    run_select(t, s, buf, tiles, true);
     int32_t out = 0, err = 0;
     CK(cudaMemcpyAsync(&out, cnt, sizeof(out), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&err, dt.err, sizeof(err), cudaMemcpyDeviceToHost, s));
@@ -370,7 +429,14 @@ EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* c
     t.sel_val = out_val;
     t.sel_cnt = cnts + r;
     t.weight = 1.f;
-    run_select(t, s, buf);
+    int tiles = 0;
+    if (wide_enabled()) {
+      const int grp = std::max(1, 4096 / static_cast<int>(T));
+      attach_wide(t, buf, s, mt.out_idx, mt.out_val, mt.seg_off, mt.seg_cnt, nullptr,
+                  static_cast<int>(r * T), static_cast<int>(parts), grp, sdl::kWFull, 0, 16384);
+      tiles = static_cast<int>((parts + grp - 1) / grp);
+    }
+    run_select(t, s, buf, tiles);
     int32_t out = 0;
     CK(cudaMemcpyAsync(&out, cnts + r, sizeof(out), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -736,6 +802,22 @@ EXPORT int spardl_dense_fallbacks(spardl_ctx* ctx, int64_t* count) {
   return guarded([&] {
     need(ctx, "ctx");
     *count = ctx->eng->dense_fallbacks();
+  });
+}
+
+EXPORT int spardl_dense_fallbacks_total(spardl_ctx* ctx, int64_t* count) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(count, "count");
+    *count = ctx->eng->dense_fallbacks_total();
+  });
+}
+
+EXPORT int spardl_wide_handed_back(spardl_ctx* ctx, int64_t* count) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(count, "count");
+    *count = ctx->eng->wide_handed_back();
   });
 }
 

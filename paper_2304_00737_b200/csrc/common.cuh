@@ -187,6 +187,54 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* scratc
   return t;
 }
 
+#ifndef SPARDL_DIV_EXTRAP
+#define SPARDL_DIV_EXTRAP 0.5
+#endif
+#ifndef SPARDL_DIV_TARGET
+#define SPARDL_DIV_TARGET 1.3
+#endif
+// Dividing select epilogue: the pre-threshold of the next iteration.
+__device__ inline void update_history(DivHistory* h, int mode, int all, uint32_t T, uint32_t pre,
+                               long long cand, long long budget) {
+  constexpr uint32_t kMinDelta = 1u << 12, kMaxDelta = 1u << 26;
+  constexpr double kTarget = SPARDL_DIV_TARGET;   // wanted candidates / L
+  if (mode != 0 || all != 0 || budget <= 0) {   // dense fallback (or trivial): sample again
+    if (h->valid) h->delta = h->delta < kMaxDelta / 2 ? h->delta * 2 : kMaxDelta;
+    h->valid = 0;
+    h->has_T = all == 0 && budget > 0;
+    h->last_T = T;
+    return;
+  }
+  // secant in (key, log count): count(pre) = cand, count(T) = budget
+  const double span = (double)(T - pre);
+  const double ratio = (double)cand / (double)budget;
+  double d;
+  if (ratio > 1.02 && span > 0) d = span * log(kTarget) / log(ratio);
+  else d = 2.0 * (span > 0 ? span : (double)kMinDelta);
+  if (h->valid) {   // at most x2 / x0.5 per run
+    const double old = (double)h->delta;
+    d = d > 2 * old ? 2 * old : (d < old / 2 ? old / 2 : d);
+  }
+  d = d < kMinDelta ? kMinDelta : (d > kMaxDelta ? kMaxDelta : d);
+  // a threshold that grows from run to run (residual accumulation) is
+  // extrapolated in magnitude, by a fraction of the last growth: with fresh
+  // gradients every run T also fluctuates, and a full linear step would
+  // overshoot after every upward fluctuation (fewer than L candidates: the
+  // dense fallback)
+  const float tv = __uint_as_float(T), tp = __uint_as_float(h->last_T);
+  const float grown = h->has_T && tv > tp ? tv + (float)SPARDL_DIV_EXTRAP * (tv - tp) : tv;
+  const uint32_t Tn = grown < 3.0e38f ? __float_as_uint(grown) : T;
+  long long next = (long long)Tn - (long long)d;
+  h->delta = (uint32_t)d;
+  h->next_pre = next < 0 ? 0u : (uint32_t)next;
+  // the first threshold after a (re)start only seeds the trend: trust the
+  // carried pre-threshold from the second sampled run on
+  h->valid = h->has_T;
+  h->last_T = T;
+  h->has_T = 1;
+}
+
+
 // lower_bound over a sorted int array [a, a+n)
 __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t x) {
   int lo = 0, hi = n;

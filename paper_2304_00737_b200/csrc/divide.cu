@@ -98,11 +98,22 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
   for (int q = 0; q < BPT; ++q) mine += hist[q];
   const long long ns = block_sum_ll(mine, lscr);
   const int64_t nb = (int64_t)t.hi - t.lo;
+  // the wide select's histogram window (wselect.cu): 2048 bins from the
+  // pre-threshold up, together ~4x the expected distance to the threshold
+  auto set_window = [&](uint32_t pre, uint32_t w) {
+    if (t.ws) {
+      uint32_t s = 0;
+      while (s < 31 && ((unsigned long long)kWBins << s) < 4ull * w) ++s;
+      t.ws->base = pre;
+      t.ws->shift = s;
+    }
+  };
   if (t.use_cand && t.hist->valid) {   // threshold carried from the last iteration
     if (threadIdx.x == 0) {
       *t.cand_total = 0;
       *t.cand_bad = 0;
       *t.pre_key = t.hist->next_pre;
+      set_window(t.hist->next_pre, t.hist->delta);
     }
     return;   // the sample histogram was not touched: still zero
   }
@@ -140,6 +151,7 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
       const uint32_t cq = hist[q];
       if (cum + (long long)cq >= target) {
         *t.pre_key = (uint32_t)(threadIdx.x * BPT + q) << kSampShift;
+        set_window((uint32_t)(threadIdx.x * BPT + q) << kSampShift, 8u << kSampShift);
         break;
       }
       cum += cq;
@@ -268,6 +280,10 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const Di
   const int wbase = wtot[warp];
   int32_t* ci = t.cand_idx + (size_t)c * t.cap;
   float* cv = t.cand_val + (size_t)c * t.cap;
+  // the wide select's level-1 histogram of the candidates (window above the
+  // pre-threshold; fire-and-forget reductions)
+  WScratch* ws = t.ws;
+  const uint32_t wb = ws ? ws->base : 0u, wsh = ws ? ws->shift : 0u;
 #pragma unroll
   for (int it = 0; it < ITER; ++it) {
     int p = wbase + lane_excl[it];
@@ -275,9 +291,14 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const Di
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (mask & (1u << (it * 4 + e))) {
+        const float x = s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e];
         ci[p] = (int32_t)(i0 + e);
-        cv[p] = s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e];
+        cv[p] = x;
         ++p;
+        if (ws) {
+          const uint32_t d = (mag_key(x) - wb) >> wsh;
+          atomicAdd(d < (uint32_t)kWBins ? &ws->hist[d] : &ws->above, 1u);
+        }
       }
     }
   }

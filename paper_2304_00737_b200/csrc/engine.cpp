@@ -14,6 +14,7 @@
 #include "divplan.hpp"
 
 #include <algorithm>
+#include <cstddef>
 #include <array>
 #include <cstdio>
 #include <cstdlib>
@@ -83,6 +84,7 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
     sdlh::fail(SPARDL_E_UNSUPPORTED, "device path supports N < 2^31 - 1");
   if (world < 1 || rank < 0 || rank >= world || P_ % world != 0)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "P must be a positive multiple of the process count");
+  if (const char* we = std::getenv("SPARDL_WSEL")) wide_on_ = we[0] != '0';
   if (cfg.sag == SPARDL_SAG_BSAG && d_ > sdl::kMaxR)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "bsag on the device supports d <= 16");
   wloc_ = P_ / world;
@@ -153,9 +155,13 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   budget_dev_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * wloc_));
   ctl_dev_ = static_cast<sdl::HCtl*>(arena_.alloc(sizeof(sdl::HCtl) * wloc_));
   gtab_dev_ = static_cast<const float**>(arena_.alloc(sizeof(float*) * wloc_));
-  CK(cudaMallocHost(reinterpret_cast<void**>(&gtab_host_), sizeof(float*) * wloc_));
-  std::memset(gtab_host_, 0, sizeof(float*) * wloc_);
+  CK(cudaMallocHost(reinterpret_cast<void**>(&gtab_host_), sizeof(float*) * wloc_ * kTabRing));
+  std::memset(gtab_host_, 0, sizeof(float*) * wloc_ * kTabRing);
+  gtab_cur_.assign(static_cast<size_t>(wloc_), nullptr);
+  for (auto& e : tab_ev_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   err_dev_ = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+  fallbacks_dev_ = static_cast<unsigned long long*>(arena_.alloc(sizeof(unsigned long long)));
+  wide_back_dev_ = static_cast<unsigned long long*>(arena_.alloc(sizeof(unsigned long long)));
   hash_dev_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * d_));
   rb_dev_ = static_cast<int64_t*>(
       arena_.alloc(sizeof(int64_t) * (static_cast<size_t>(P_ + wloc_) + static_cast<size_t>(d_) * (world_ + 1))));
@@ -179,6 +185,8 @@ Engine::~Engine() {
   if (comm_) ncclCommDestroy(comm_);
   for (float* c : carry_) cudaFree(c);
   if (gtab_host_) cudaFreeHost(gtab_host_);
+  for (auto& e : tab_ev_)
+    if (e) cudaEventDestroy(e);
   if (side_) cudaStreamDestroy(side_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
@@ -306,6 +314,40 @@ void Engine::add_select(Stage& st, const sdl::SelTask& t0, int out_uid, int in_u
   st.sels.push_back(t);
 }
 
+sdl::WScratch* Engine::make_wide(Stage& st, sdl::SelTask& t, const int32_t* idx, const float* val,
+                                  const int32_t* seg_off, const int32_t* seg_cnt,
+                                  const int32_t* count, int stride, int nseg, int group, int mode,
+                                  int is_div, int64_t bin_cap) {
+  sdl::WScratch w{};
+  w.idx = idx;
+  w.val = val;
+  w.seg_off = seg_off;
+  w.seg_cnt = seg_cnt;
+  w.count = count;
+  w.stride = stride;
+  w.nseg = nseg;
+  w.group = std::max(1, std::min(group, 64));
+  w.max_tiles = (nseg + w.group - 1) / w.group;
+  w.mode = mode;
+  w.is_div = is_div;
+  w.handed_back = wide_back_dev_;
+  bin_cap = std::max<int64_t>(1, std::min<int64_t>(bin_cap, int64_t(1) << 30));
+  w.bin_cap = static_cast<int32_t>(bin_cap);
+  w.bin_c = static_cast<unsigned long long*>(arena_.alloc(sizeof(unsigned long long) * bin_cap));
+  w.bin_tile = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * bin_cap));
+  const size_t nt = static_cast<size_t>(std::max(1, w.max_tiles));
+  w.tile_n = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * nt));
+  w.tile_sel = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * nt));
+  w.tile_sel_off = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * nt));
+  w.tile_dis_off = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * nt));
+  auto* d = static_cast<sdl::WScratch*>(arena_.alloc(sizeof(sdl::WScratch)));
+  CK(mcpy(d, &w, sizeof(w), cudaMemcpyHostToDevice));
+  t.ws = d;
+  st.w_max_tiles = std::max(st.w_max_tiles, w.max_tiles);
+  st.ws.push_back(d);
+  return d;
+}
+
 sdl::SelTask Engine::select_from_slot(const Slot& in) {
   sdl::SelTask t{};
   t.mode = 0;
@@ -406,6 +448,20 @@ int Engine::materialize(int w, int pos, std::vector<int> pieces, int64_t budget,
   t.dis_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
   xi_[static_cast<size_t>(li)][static_cast<size_t>(xi_block)].push_back(
       {t.dis_idx, t.dis_val, t.dis_cnt});
+  if (wide_on_) {
+    if (pieces.size() == 1) {   // a single block buffer: one compact list
+      const Slot& in = local_slot(pieces[0]);
+      constexpr int kStride = 4096;
+      make_wide(st, t, in.idx, in.val, nullptr, nullptr, in.cnt, kStride,
+                static_cast<int>((in.cap + kStride - 1) / kStride), 1, sdl::kWFull, 0,
+                std::max<int64_t>(16384, in.cap / 8));
+    } else {                    // the merge's partitions
+      const sdl::MergeTask& mt = st.merges.back();
+      make_wide(st, t, mt.out_idx, mt.out_val, mt.seg_off, mt.seg_cnt, nullptr, t.stride, t.nseg,
+                std::max(1, 4096 / std::max(1, static_cast<int>(mt.T))), sdl::kWFull, 0,
+                std::max<int64_t>(16384, capsum / 8));
+    }
+  }
   add_select(st, t, uid, pieces.size() == 1 ? pieces[0] : -1);
   if (t.merge_slot)   // diagnostics: the merge stamps its phases into the select's scratch
     st.merges[static_cast<size_t>(t.merge_slot - 1)].dbg = st.sels.back().scr->merge_ts;
@@ -472,6 +528,9 @@ void Engine::plan_fused(Stage& st) {
 
 void Engine::finish_stage(Stage& st) {
   plan_fused(st);
+  st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size();
+  if (!st.wide)
+    for (auto& t : st.sels) t.ws = nullptr;   // (cluster selects only)
   if (!st.merges.empty()) {
     st.merges_dev = static_cast<sdl::MergeTask*>(
         arena_.alloc(sizeof(sdl::MergeTask) * st.merges.size()));
@@ -491,6 +550,15 @@ void Engine::finish_stage(Stage& st) {
     CK(mcpy(st.sels_dev, st.sels.data(), sizeof(sdl::SelTask) * st.sels.size(),
                   cudaMemcpyHostToDevice));
     launches_ += 9;
+  }
+}
+
+// the wide scratch of every task of a stage back to its idle state
+void Engine::reset_wide(const Stage& st) {
+  for (sdl::WScratch* w : st.ws) {
+    // hist .. ntiles (the run state); the input descriptor and buffers stay
+    const size_t a = offsetof(sdl::WScratch, hist), b = offsetof(sdl::WScratch, total);
+    CK(cudaMemset(reinterpret_cast<unsigned char*>(w) + a, 0, b - a));
   }
 }
 
@@ -530,6 +598,11 @@ void Engine::plan() {
       div_tasks_.push_back(dt);
       max_chunks = std::max(max_chunks, dt.nchunks);
       t.dval = dt.carry + lo;
+      t.fallbacks = fallbacks_dev_;
+      if (wide_on_ && dt.use_cand && div_split_ <= 1)
+        dt.ws = make_wide(div_stage_, t, dt.cand_idx, dt.cand_val, nullptr, dt.cand_cnt, nullptr,
+                          dt.cap, dt.nchunks, 16, sdl::kWWindow, 1,
+                          std::max<int64_t>(16384, L_ / 8));
       t.sel_idx = out.idx;
       t.sel_val = out.val;
       t.sel_cnt = out.cnt;
@@ -1051,11 +1124,16 @@ void Engine::plan_peer() {
 
 // ---------------------------------------------------------------------------
 // execution
-int Engine::exec_stage(const Stage& st) {
+int Engine::exec_stage(const Stage& st, bool dividing) {
   int n = 0;
   if (!st.merges.empty() && !st.fused)
     n += sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts,
                            st.max_rT, st.max_r, stream_);
+  // wide path first (the dividing histogram is filled by the candidate
+  // pass); the cluster select then runs only the tasks handed back
+  if (st.wide)
+    n += sdl::launch_wselect(st.sels_dev, static_cast<int>(st.sels.size()), st.w_max_tiles,
+                             !dividing, stream_);
   if (!st.sels.empty())
     n += sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_,
                             st.fused ? st.cl : 0, st.fused ? st.win_cap : 0);
@@ -1107,7 +1185,7 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   if (G <= 1 || div_stage_.sels.size() != div_tasks_.size()) {
     n += sdl::launch_divide(div_dev_, ndt, div_max_chunks_, div_sample_every_, 1, stream_, 2);
     mark(2);
-    n += exec_stage(div_stage_);   // (peer transport: each select publishes its block)
+    n += exec_stage(div_stage_, true);   // (peer transport: each select publishes its block)
   } else {
     for (int g = 0; g < G; ++g) {
       const int t0 = (g * wloc_ / G) * m_, t1 = ((g + 1) * wloc_ / G) * m_;
@@ -1133,7 +1211,7 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   };
   for (size_t i = 0; i < steps_.size(); ++i) {
     const Step& s = steps_[i];
-    n += exec_stage(s.stage);
+    n += exec_stage(s.stage, false);
     step_mark(i, 0);
     if (s.controller_after)
       n += sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1, abort,
@@ -1212,13 +1290,22 @@ void Engine::run(const float* const* grads) {
     if (!grads[i]) sdlh::fail(SPARDL_E_ARG, "null gradient pointer");
     if (reinterpret_cast<uintptr_t>(grads[i]) % 16 != 0)
       sdlh::fail(SPARDL_E_ARG, "gradient pointers must be 16-byte aligned");
-    changed |= gtab_host_[i] != grads[i];
+    changed |= gtab_cur_[static_cast<size_t>(i)] != grads[i];
   }
   if (changed) {
-    CK(cudaStreamSynchronize(stream_));
-    for (int i = 0; i < wloc_; ++i) gtab_host_[i] = grads[i];
-    CK(cudaMemcpyAsync(gtab_dev_, gtab_host_, sizeof(float*) * wloc_, cudaMemcpyHostToDevice,
-                       stream_));
+    // the graph reads the pointer table from device memory: a new table is
+    // uploaded in stream order from a ring of pinned host slots (no host
+    // synchronisation; a slot is reused only after its upload has run)
+    float const** slot = gtab_host_ + static_cast<size_t>(tab_next_) * wloc_;
+    if (tab_used_[tab_next_]) CK(cudaEventSynchronize(tab_ev_[tab_next_]));
+    for (int i = 0; i < wloc_; ++i) {
+      slot[i] = grads[i];
+      gtab_cur_[static_cast<size_t>(i)] = grads[i];
+    }
+    CK(cudaMemcpyAsync(gtab_dev_, slot, sizeof(float*) * wloc_, cudaMemcpyHostToDevice, stream_));
+    CK(cudaEventRecord(tab_ev_[tab_next_], stream_));
+    tab_used_[tab_next_] = true;
+    tab_next_ = (tab_next_ + 1) % kTabRing;
   }
   for (int w = 0; w < P_; ++w)
     for (int p = 0; p < 3; ++p)
@@ -1274,6 +1361,10 @@ void Engine::reset_state() {
     CK(cudaMemset(ledger_total_[static_cast<size_t>(i)], 0, sizeof(int64_t)));
   }
   std::fill(rounds_.begin(), rounds_.end(), 0);
+  CK(cudaMemset(fallbacks_dev_, 0, sizeof(unsigned long long)));
+  CK(cudaMemset(wide_back_dev_, 0, sizeof(unsigned long long)));
+  reset_wide(div_stage_);
+  for (const Step& stp : steps_) reset_wide(stp.stage);
   for (const auto& dt : div_tasks_) CK(cudaMemset(dt.hist, 0, sizeof(sdl::DivHistory)));
   if (cfg_.sag == SPARDL_SAG_BSAG) {
     std::vector<sdl::HCtl> c(static_cast<size_t>(wloc_));
@@ -1425,6 +1516,20 @@ void Engine::select_timestamps(int step, int task, int64_t* out12) {
   const Stage& st = step < 0 ? div_stage_ : steps_.at(static_cast<size_t>(step)).stage;
   const sdl::SelScratch* sc = st.sels.at(static_cast<size_t>(task)).scr;
   CK(mcpy(out12, sc->tstamp, sizeof(long long) * 116, cudaMemcpyDeviceToHost));
+}
+
+int64_t Engine::wide_handed_back() {
+  sync();
+  unsigned long long n = 0;
+  if (wide_back_dev_) CK(mcpy(&n, wide_back_dev_, sizeof(n), cudaMemcpyDeviceToHost));
+  return static_cast<int64_t>(n);
+}
+
+int64_t Engine::dense_fallbacks_total() {
+  sync();
+  unsigned long long n = 0;
+  CK(mcpy(&n, fallbacks_dev_, sizeof(n), cudaMemcpyDeviceToHost));
+  return static_cast<int64_t>(n);
 }
 
 int64_t Engine::dense_fallbacks() {

@@ -77,6 +77,9 @@ struct Stage {           // one batch of merge + select tasks
   bool fused = false;        // merges run inside the select kernel (no merge launches)
   int cl = 0;                // fused: cluster width
   int win_cap = 0;           // fused: window entries per CTA
+  bool wide = false;         // every select runs the wide path first (wselect.cu)
+  int w_max_tiles = 0;       // wide: largest tile count of a task
+  std::vector<sdl::WScratch*> ws;   // wide: per select task
 };
 
 struct Step {            // a stage followed by a transport round
@@ -113,6 +116,10 @@ class Engine {
   void union_sizes(int64_t* out);
   // dividing selects of the last iteration that fell back to the dense path
   int64_t dense_fallbacks();
+  // dividing selects that fell back to the dense path since reset_state()
+  int64_t dense_fallbacks_total();
+  // wide-path selects handed back to the cluster select since reset_state()
+  int64_t wide_handed_back();
   // device timestamps (ns) of the phases of one select of the last run
   void select_timestamps(int step, int task, int64_t* out12);
   // [mode, cand_bad, cand_total, cand_count, pre_key, cap] of dividing task i
@@ -149,6 +156,11 @@ class Engine {
   int materialize(int w, int pos, std::vector<int> pieces, int64_t budget, float weight,
                   const int64_t* budget_dev, int64_t* total_out, Stage& st, int xi_block);
   void add_select(Stage& st, const sdl::SelTask& t, int out_uid, int in_uid);
+  // wide-select scratch of a task over the given input segments
+  sdl::WScratch* make_wide(Stage& st, sdl::SelTask& t, const int32_t* idx, const float* val,
+                           const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* count,
+                           int stride, int nseg, int group, int mode, int is_div, int64_t bin_cap);
+  bool wide_on_ = true;      // SPARDL_WSEL=0: cluster selects only
   sdl::SelTask select_from_slot(const Slot& in);
   sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);
   void finish_stage(Stage& st);
@@ -162,7 +174,8 @@ class Engine {
   bool is_local(int w) const { return w >= first_ && w < first_ + wloc_; }
   int rank_of(int w) const { return w / wloc_; }
   void exec_round(const std::vector<Xfer>& xs);
-  int exec_stage(const Stage& st);
+  int exec_stage(const Stage& st, bool dividing);
+  void reset_wide(const Stage& st);
   cudaError_t mcpy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
     return dry_ ? cudaSuccess : cudaMemcpy(dst, src, bytes, kind);
   }
@@ -201,8 +214,15 @@ class Engine {
   int64_t* budget_dev_ = nullptr;        // device [wloc] B-SAG pre-selection budgets
   sdl::HCtl* ctl_dev_ = nullptr;         // device [wloc]
   const float** gtab_dev_ = nullptr;     // device [wloc] gradient pointers
-  const float** gtab_host_ = nullptr;    // pinned mirror
+  const float** gtab_host_ = nullptr;    // pinned ring of kTabRing tables
+  static constexpr int kTabRing = 32;
+  std::vector<const float*> gtab_cur_;   // the table the device holds (last upload)
+  cudaEvent_t tab_ev_[kTabRing] = {};
+  bool tab_used_[kTabRing] = {};
+  int tab_next_ = 0;
   int32_t* err_dev_ = nullptr;           // NaN flag
+  unsigned long long* fallbacks_dev_ = nullptr;   // dense fallbacks since reset_state()
+  unsigned long long* wide_back_dev_ = nullptr;   // wide selects handed back since reset_state()
   int64_t* hash_dev_ = nullptr;          // [d] consistency hashes
   int64_t* rb_dev_ = nullptr;            // readback scratch
   std::vector<int64_t> rounds_;          // host, per global worker (cumulative)

@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(kThreads) k_assemble(const AssembleTask* __res
   const AssembleTask& t = tasks[blockIdx.y];
   peer_wait(t.ps);   // the gathered blocks of other GPUs are published
   extern __shared__ int off[];
-  __shared__ int s_part[kThreads / 32];
+  __shared__ int s_part[40];   // block_exscan scratch (>= 33 ints)
   {   // block offsets: CTA-wide exclusive scan of the m counts
     int run = 0;
     for (int b0 = 0; b0 < t.m; b0 += kThreads) {

@@ -54,6 +54,7 @@ struct PeerSync {
 };
 
 struct SelTask;
+struct WScratch;
 // Host helper: fills the derived work-decomposition fields of a select task
 // (tiles per input segment; dense tiles) given the largest possible length of
 // one input segment.  Returns the number of work segments of the task.
@@ -124,6 +125,7 @@ struct SelTask {
   const int64_t* cand_total;
   const int32_t* cand_bad;
   struct DivHistory* div_hist;   // nullable: dividing select -> next pre-threshold
+  unsigned long long* fallbacks; // nullable: += 1 per run that took the dense path
   const uint32_t* pre_key_dev;   // the pre-threshold of this run (dividing select)
   // budget
   int64_t budget;
@@ -153,6 +155,9 @@ struct SelTask {
   int32_t merge_slot;    // host bookkeeping: 1 + index of the stage's merge task, 0 none
   int32_t pad3_;
   PeerSync ps;           // waits on remote inputs, publishes the output
+  // wide path (wselect.cu; nullable): the select spread over the whole GPU;
+  // this kernel then only runs the tasks the wide path hands back
+  WScratch* ws;
   // peer transport: copies of the selection written straight into the
   // buffers of the consumer ranks (slot layout: count, idx[push_cap],
   // val[push_cap]); npush = 0: none
@@ -161,6 +166,64 @@ struct SelTask {
   int32_t push_cap;
 };
 constexpr int kMaxPush = 8;   // remote consumer ranks a select writes into
+
+// ---------------------------------------------------------------------------
+// Wide select (wselect.cu): one select task spread over the whole GPU.
+// The task's input is cut into tiles (groups of `group` consecutive input
+// segments).  Level 1: a 2048-bin histogram of the magnitude keys -- the full
+// key range (bin = key >> 20) or, for the dividing select, a window above
+// its pre-threshold (bin = (key - base) >> shift, past the window: `above`).
+// The bin holding the L-th key is located by every gather CTA; the gather
+// pass collects that bin's entries (key, index, tile) and per-tile counts;
+// the last gather CTA of the task selects the exact boundary entry inside
+// the bin (radix select on key desc / index asc), fixes per-tile output
+// offsets and the selection state; the write pass compacts every tile in
+// index order.  A task the wide path cannot finish (window miss, bin buffer
+// overflow, dividing candidates incomplete) is handed to k_select (state
+// kWFallback), which also covers every input with merge holes.
+constexpr int kWBins = 2048;
+constexpr int kWFull = 0, kWWindow = 1;                    // histogram modes
+constexpr int kWOk = 0, kWAll = 1, kWNone = 2, kWFallback = 3;   // run states
+struct WScratch {
+  // input: segments of the task (conventions of SelTask mode 0)
+  const int32_t* idx;
+  const float* val;
+  const int32_t* seg_off;     // nullable: segment s starts at s * stride
+  const int32_t* seg_cnt;     // nullable: clamp(*count - off, 0, stride)
+  const int32_t* count;
+  const int32_t* nseg_dev;    // nullable: segments in use
+  int32_t stride;
+  int32_t nseg;
+  int32_t group;              // segments per tile
+  int32_t max_tiles;
+  int32_t mode;               // kWFull / kWWindow
+  int32_t is_div;             // dividing select (candidates + history)
+  // level-1 histogram (zeroed by the finisher after use)
+  uint32_t hist[kWBins];
+  uint32_t above;             // window mode: keys past the last bin
+  uint32_t base;              // window mode: lowest key of bin 0 (= pre-threshold)
+  uint32_t shift;             // window mode: log2 of the bin width in key units
+  uint32_t arrive;            // gather CTAs done (reset by the finisher)
+  uint32_t wdone;             // write CTAs done (reset by the last writer)
+  uint32_t bin_n;             // entries collected into the bin buffer
+  int32_t state;              // kWOk / kWAll / kWNone / kWFallback of this run
+  uint32_t T;                 // threshold key of this run (kWOk)
+  int32_t cut;                // largest selected index among key == T
+  int32_t ntiles;             // tiles in use this run
+  long long total, total_sel; // entries, selected entries of this run
+  // the bin buffer
+  unsigned long long* bin_c;  // (key << 32) | (0x7fffffff - index): larger = earlier
+  int32_t* bin_tile;
+  int32_t bin_cap;
+  int32_t pad_;
+  // per tile: entries, selected (gather: above the bin; finisher: + in-bin),
+  // exclusive output offsets of the selected / discarded entries
+  int32_t* tile_n;
+  int32_t* tile_sel;
+  int32_t* tile_sel_off;
+  int32_t* tile_dis_off;
+  unsigned long long* handed_back;   // nullable: += 1 per run handed to k_select
+};
 
 // value bits of a merge hole: its magnitude key is kHoleKey, never a real
 // entry's (a NaN with every mantissa bit set)
@@ -239,6 +302,7 @@ struct DivTask {
   int32_t sample_every;    // sample one chunk in `sample_every`
   int32_t use_cand;        // 0: candidate path disabled (dense select)
   int32_t* err;            // NaN flag
+  WScratch* ws;            // nullable: the wide select of this block (window histogram)
 };
 
 // ---------------------------------------------------------------------------
@@ -252,6 +316,11 @@ cudaError_t take_launch_error();
 // tasks_dev: device copy of the task array; ntask; max_nseg: grid extent.
 int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s,
                   int cluster = 0, int win_cap = 0);
+// the wide path of a batch of selects (all tasks must carry ws): level-1
+// histogram (skipped for dividing selects: k_div_cand fills it), gather +
+// finisher, write; then launch_select for the tasks handed back
+int launch_wselect(const SelTask* tasks_dev, int ntask, int max_tiles, bool histogram,
+                   cudaStream_t s);
 // fused merge+select: smem window capacity (entries) available per CTA, and
 // the clusters of width cl resident at once for a launch with that window
 int select_max_window();

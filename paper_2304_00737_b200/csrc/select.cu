@@ -104,47 +104,6 @@ struct CtaTotals {      // per-CTA counters exchanged through DSMEM
   long long cnt, gt, eq;
 };
 
-#ifndef SPARDL_DIV_TARGET
-#define SPARDL_DIV_TARGET 1.3
-#endif
-// Dividing select epilogue: the pre-threshold of the next iteration.
-__device__ void update_history(DivHistory* h, int mode, int all, uint32_t T, uint32_t pre,
-                               long long cand, long long budget) {
-  constexpr uint32_t kMinDelta = 1u << 12, kMaxDelta = 1u << 26;
-  constexpr double kTarget = SPARDL_DIV_TARGET;   // wanted candidates / L
-  if (mode != 0 || all != 0 || budget <= 0) {   // dense fallback (or trivial): sample again
-    if (h->valid) h->delta = h->delta < kMaxDelta / 2 ? h->delta * 2 : kMaxDelta;
-    h->valid = 0;
-    h->has_T = all == 0 && budget > 0;
-    h->last_T = T;
-    return;
-  }
-  // secant in (key, log count): count(pre) = cand, count(T) = budget
-  const double span = (double)(T - pre);
-  const double ratio = (double)cand / (double)budget;
-  double d;
-  if (ratio > 1.02 && span > 0) d = span * log(kTarget) / log(ratio);
-  else d = 2.0 * (span > 0 ? span : (double)kMinDelta);
-  if (h->valid) {   // at most x2 / x0.5 per run
-    const double old = (double)h->delta;
-    d = d > 2 * old ? 2 * old : (d < old / 2 ? old / 2 : d);
-  }
-  d = d < kMinDelta ? kMinDelta : (d > kMaxDelta ? kMaxDelta : d);
-  // a threshold that grows from run to run (residual accumulation) is
-  // extrapolated linearly in magnitude
-  const float tv = __uint_as_float(T), tp = __uint_as_float(h->last_T);
-  const float grown = h->has_T && tv > tp ? tv + (tv - tp) : tv;
-  const uint32_t Tn = grown < 3.0e38f ? __float_as_uint(grown) : T;
-  long long next = (long long)Tn - (long long)d;
-  h->delta = (uint32_t)d;
-  h->next_pre = next < 0 ? 0u : (uint32_t)next;
-  // the first threshold after a (re)start only seeds the trend: trust the
-  // carried pre-threshold from the second sampled run on
-  h->valid = h->has_T;
-  h->last_T = T;
-  h->has_T = 1;
-}
-
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   const size_t ga = __cvta_generic_to_global(gmem);
@@ -378,6 +337,9 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank();
   const SelTask t = tasks[blockIdx.y];   // by value: fields live in registers, not re-read
+  // the wide path (wselect.cu) selected this task already unless it handed
+  // it back (uniform per cluster: every CTA returns, no barrier is pending)
+  if (!FUSED && t.ws && t.ws->state != kWFallback) return;
   SelScratch* sc = t.scr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -1034,6 +996,7 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
       sc->cut_idx = INT_MAX;
     }
     if (t.div_hist) update_history(t.div_hist, mode, all, T, *t.pre_key_dev, total, budget);
+    if (t.fallbacks && t.mode_from_cand && mode == 1) atomicAdd(t.fallbacks, 1ull);
   }
   stamp(11);
   // (no shared-memory access crosses CTAs after the totals exchange)
