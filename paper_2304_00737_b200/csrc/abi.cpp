@@ -154,7 +154,8 @@ void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf, int max_tiles = 0,
   t.seg_valid = segs + 5 * nck;
   sdl::SelTask* td = buf.get<sdl::SelTask>(1);
   CK(cudaMemcpyAsync(td, &t, sizeof(t), cudaMemcpyHostToDevice, s));
-  if (t.ws) sdl::launch_wselect(td, 1, max_tiles, !dividing, s);
+  (void)dividing;
+  if (t.ws) sdl::launch_wselect(td, 1, max_tiles, true, s);
   sdl::launch_select(td, 1, std::max(1, sdl::sel_scratch_segments(t)), s);
   CK(sdl::take_launch_error());
   CK(cudaGetLastError());
@@ -309,9 +310,9 @@ EXPORT int spardl_topk_select(const int32_t* idx, const float* val, int64_t n, i
     t.weight = 1.f;
     int tiles = 0;
     if (n > 0 && wide_enabled()) {
-      constexpr int kStride = 4096;
+      constexpr int kStride = 8192;
       const int ns = static_cast<int>((n + kStride - 1) / kStride);
-      attach_wide(t, buf, s, idx, val, nullptr, nullptr, cnt, kStride, ns, 1, sdl::kWFull, 0,
+      attach_wide(t, buf, s, idx, val, nullptr, nullptr, cnt, kStride, ns, 1, sdl::kWAuto, 0,
                   std::max<int64_t>(16384, n / 8));
       tiles = ns;
     }
@@ -350,9 +351,9 @@ EXPORT int spardl_topk_select_slice(const float* g, int64_t lo, int64_t hi, int6
     int tiles = 0;
     if (dt.use_cand && wide_enabled()) {
       dt.ws = attach_wide(t, buf, s, dt.cand_idx, dt.cand_val, nullptr, dt.cand_cnt, nullptr,
-                          dt.cap, dt.nchunks, 16, sdl::kWWindow, 1,
+                          dt.cap, dt.nchunks, 64, sdl::kWWindow, 1,
                           std::max<int64_t>(16384, budget / 8));
-      tiles = (dt.nchunks + 15) / 16;
+      tiles = (dt.nchunks + 63) / 64;
     }
     sdl::DivTask* dtd = buf.get<sdl::DivTask>(1);
     CK(cudaMemcpyAsync(dtd, &dt, sizeof(dt), cudaMemcpyHostToDevice, s));
@@ -431,9 +432,9 @@ EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* c
     t.weight = 1.f;
     int tiles = 0;
     if (wide_enabled()) {
-      const int grp = std::max(1, 4096 / static_cast<int>(T));
+      const int grp = std::max(1, 8192 / static_cast<int>(T));
       attach_wide(t, buf, s, mt.out_idx, mt.out_val, mt.seg_off, mt.seg_cnt, nullptr,
-                  static_cast<int>(r * T), static_cast<int>(parts), grp, sdl::kWFull, 0, 16384);
+                  static_cast<int>(r * T), static_cast<int>(parts), grp, sdl::kWAuto, 0, 16384);
       tiles = static_cast<int>((parts + grp - 1) / grp);
     }
     run_select(t, s, buf, tiles);

@@ -235,6 +235,25 @@ __device__ inline void update_history(DivHistory* h, int mode, int all, uint32_t
 }
 
 
+// Residual finalize of one global index (inc/residual.hpp:128-150, gres):
+// xi(j) starts as combined[j] = x when the dividing select discarded j
+// (keep), then folds the in-procedure discards in recording order; no
+// contribution at all -> +0.  Used by k_finalize's deferred form (records
+// applied in the next candidate pass or by k_fin_apply).
+__device__ __forceinline__ float fin_fold(float x, bool keep, float v1, float v2) {
+  bool has = keep;
+  float acc = keep ? x : 0.f;
+  if (__float_as_uint(v1) != kNoRec) {
+    acc = has ? __fadd_rn(acc, v1) : v1;
+    has = true;
+  }
+  if (__float_as_uint(v2) != kNoRec) {
+    acc = has ? __fadd_rn(acc, v2) : v2;
+    has = true;
+  }
+  return has ? acc : 0.f;
+}
+
 // lower_bound over a sorted int array [a, a+n)
 __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t x) {
   int lo = 0, hi = n;

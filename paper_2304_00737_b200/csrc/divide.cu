@@ -19,6 +19,8 @@
 // candidates are complete (>= L of them, no chunk overflow); otherwise it
 // selects from the dense slice instead, so the result never depends on the
 // sample.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -160,84 +162,13 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
   for (int q = 0; q < BPT; ++q) hist[q] = 0;   // leave the histogram zeroed
 }
 
-template <int APPLY>
-__global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const DivTask* __restrict__ tasks) {
-  pdl_enter();
-  const DivTask& t = tasks[blockIdx.y];
-  const int c = blockIdx.x;
-  if (c >= t.nchunks) return;
-  // participation in the look-back is decided by the pre-threshold kernel
-  // only (bit 0), never by an overflow seen later in this kernel (bit 1)
-  const bool cand = !(*t.cand_bad & 1);
-  const uint32_t pre = *t.pre_key;
-  const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
+// The chunk's candidates (bit (it * 4 + e) of `mask`: element
+// (warp * 32 * ITER + it * 32 + lane) * 4 + e of the chunk, value in s_comb)
+// compacted in index order into the chunk's candidate segment.
+__device__ __forceinline__ void cand_compact(const DivTask& t, int c, int64_t A, uint32_t mask,
+                                             const float* s_comb) {
+  constexpr int ITER = kChunk / (kThreads * 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int ITER = kChunk / (kThreads * 4);   // float4 groups per lane
-  // the combined values wait here for the compaction (registers are the
-  // occupancy limit: the loads in flight need them)
-  __shared__ __align__(16) float s_comb[kChunk];
-  uint32_t mask = 0;
-  bool nan = false;
-  const int64_t lo = t.lo, hi = t.hi;
-  // gradient and carry never alias; telling the compiler so lets every load
-  // of the chunk issue before the first store (one memory latency per CTA
-  // instead of one per float4 group)
-  const float* __restrict__ g = APPLY ? t.g_tab[t.g_id] : nullptr;
-  float* __restrict__ carry = t.carry;
-  float4 gv[ITER], cv4[ITER];
-#pragma unroll
-  for (int it = 0; it < ITER; ++it) {
-    const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
-    if (i0 >= lo && i0 + 4 <= hi) {
-      if (APPLY) gv[it] = __ldcs(reinterpret_cast<const float4*>(g + i0));
-      cv4[it] = __ldcs(reinterpret_cast<const float4*>(carry + i0));
-    }
-  }
-#pragma unroll
-  for (int it = 0; it < ITER; ++it) {
-    const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
-    if (i0 >= lo && i0 + 4 <= hi) {
-      const float4 cc = cv4[it];
-      float4 o;
-      if (APPLY) {
-        const float4 gg = gv[it];
-        o.x = __fadd_rn(gg.x, cc.x);
-        o.y = __fadd_rn(gg.y, cc.y);
-        o.z = __fadd_rn(gg.z, cc.z);
-        o.w = __fadd_rn(gg.w, cc.w);
-        __stcs(reinterpret_cast<float4*>(carry + i0), o);
-      } else {
-        o = cc;
-      }
-      reinterpret_cast<float4*>(s_comb)[warp * (32 * ITER) + it * 32 + lane] = o;
-      const float ov[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t k = mag_key(ov[e]);
-        nan |= k > 0x7f800000u;
-        if (k >= pre) mask |= 1u << (it * 4 + e);
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t i = i0 + e;
-        s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e] = 0.f;
-        if (i >= lo && i < hi) {
-          float x = carry[i];
-          if (APPLY) {
-            x = __fadd_rn(g[i], x);
-            carry[i] = x;
-          }
-          s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e] = x;
-          const uint32_t k = mag_key(x);
-          nan |= k > 0x7f800000u;
-          if (k >= pre) mask |= 1u << (it * 4 + e);
-        }
-      }
-    }
-  }
-  if (nan) *t.err = 1;
-  if (!cand) return;
   // order: (warp, it, lane, e) == index order inside the chunk
   // per group: a lane's offset = candidates of the lower lanes, from four
   // ballots (one per float4 component)
@@ -280,10 +211,6 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const Di
   const int wbase = wtot[warp];
   int32_t* ci = t.cand_idx + (size_t)c * t.cap;
   float* cv = t.cand_val + (size_t)c * t.cap;
-  // the wide select's level-1 histogram of the candidates (window above the
-  // pre-threshold; fire-and-forget reductions)
-  WScratch* ws = t.ws;
-  const uint32_t wb = ws ? ws->base : 0u, wsh = ws ? ws->shift : 0u;
 #pragma unroll
   for (int it = 0; it < ITER; ++it) {
     int p = wbase + lane_excl[it];
@@ -291,18 +218,344 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand(const Di
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (mask & (1u << (it * 4 + e))) {
-        const float x = s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e];
         ci[p] = (int32_t)(i0 + e);
-        cv[p] = x;
+        cv[p] = s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e];
         ++p;
-        if (ws) {
-          const uint32_t d = (mag_key(x) - wb) >> wsh;
-          atomicAdd(d < (uint32_t)kWBins ? &ws->hist[d] : &ws->above, 1u);
-        }
       }
     }
   }
   if (threadIdx.x == 0) t.cand_cnt[c] = total;
+}
+
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA) form of the candidate pass.  One elected thread streams
+// the chunk's carry and gradient into shared memory with cp.async.bulk
+// (two 32 KB copies completing on one mbarrier: no registers hold the
+// chunk, so every load of the SM is in flight at once); the deferred
+// finalize records patch the staged carry; combined = g + carry is written
+// back in place in shared memory and streamed out with one bulk store; the
+// candidates are compacted from shared memory as in k_div_cand.  The
+// unaligned edge elements of a block (lo, hi not multiples of 4) go through
+// plain loads and stores.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int APPLY, int FIN>
+__global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand_bulk(const DivTask* __restrict__ tasks) {
+  pdl_enter();
+  const DivTask& t = tasks[blockIdx.y];
+  const int c = blockIdx.x;
+  if (c >= t.nchunks) return;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  float* s_c = reinterpret_cast<float*>(dsm);        // carry -> combined
+  float* s_g = s_c + kChunk;                          // gradient
+  __shared__ __align__(8) unsigned long long bar;
+  const bool cand = !(*t.cand_bad & 1);
+  const uint32_t pre = *t.pre_key;
+  const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
+  const int64_t lo = t.lo, hi = t.hi;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int ITER = kChunk / (kThreads * 4);
+  // the whole-float4 span of the chunk inside [lo, hi)
+  const int64_t v0 = max(A, (lo + 3) & ~int64_t(3));
+  const int64_t v1 = max(v0, min(A + kChunk, hi & ~int64_t(3)));
+  const uint32_t bytes = (uint32_t)((v1 - v0) * 4);
+  const float* __restrict__ g = APPLY ? t.g_tab[t.g_id] : nullptr;
+  float* __restrict__ carry = t.carry;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t tx = bytes * (APPLY ? 2u : 1u);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
+                 "r"(tx)
+                 : "memory");
+    if (bytes) {
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(smem_u32(s_c + (v0 - A))),
+          "l"(carry + v0), "r"(bytes), "r"(smem_u32(&bar))
+          : "memory");
+      if (APPLY)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(smem_u32(s_g + (v0 - A))),
+            "l"(g + v0), "r"(bytes), "r"(smem_u32(&bar))
+            : "memory");
+    }
+  }
+  // the chunk's edge elements (outside the span, inside [lo, hi)) and zeros
+  // outside the block
+  for (int k = threadIdx.x; k < kChunk; k += kThreads) {
+    const int64_t i = A + k;
+    if (i >= v0 && i < v1) continue;
+    const bool in = i >= lo && i < hi;
+    s_c[k] = in ? carry[i] : 0.f;
+    if (APPLY) s_g[k] = in ? g[i] : 0.f;
+  }
+  int r0 = 0, r1 = 0;
+  int32_t d_all = 0, d_cut = 0;
+  uint32_t d_pre = 0;
+  if (FIN && *t.fin_apply) {
+    r0 = t.chunk_off[c];
+    r1 = t.chunk_off[c + 1];
+    d_all = t.prev_sel->all;   // the previous dividing selection (membership)
+    d_pre = t.prev_sel->prefix;
+    d_cut = t.prev_sel->cut_idx;
+  }
+  int32_t rj = -1;
+  float rv1 = 0.f, rv2 = 0.f;
+  if (FIN && r0 + (int)threadIdx.x < r1) {
+    const int r = r0 + (int)threadIdx.x;
+    rj = t.rec_idx[r];
+    rv1 = t.rec_v1[r];
+    rv2 = t.rec_v2[r];
+  }
+  {   // wait for the bulk copies
+    uint32_t done = 0;
+    do {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(smem_u32(&bar))
+          : "memory");
+    } while (!done);
+  }
+  __syncthreads();   // (edge elements written by plain stores)
+  if (FIN) {   // the previous iteration's deferred finalize
+    auto member = [&](uint32_t key, int32_t j) {
+      if (d_all == 1) return true;
+      if (d_all == 2) return false;
+      return key > d_pre || (key == d_pre && j <= d_cut);
+    };
+    auto patch = [&](int32_t j, float a1, float a2) {
+      const int sp = (int)(j - A);
+      const float x = s_c[sp];
+      s_c[sp] = fin_fold(x, !member(mag_key(x), j), a1, a2);
+    };
+    if (rj >= 0) patch(rj, rv1, rv2);
+    for (int q = r0 + (int)threadIdx.x + kThreads; q < r1; q += kThreads)
+      patch(t.rec_idx[q], t.rec_v1[q], t.rec_v2[q]);
+    __syncthreads();
+  }
+  uint32_t mask = 0;
+  bool nan = false;
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int q4 = warp * (32 * ITER) + it * 32 + lane;
+    const int64_t i0 = A + (int64_t)q4 * 4;
+    float4 cc = reinterpret_cast<const float4*>(s_c)[q4];
+    if (APPLY) {
+      const float4 gg = reinterpret_cast<const float4*>(s_g)[q4];
+      cc.x = __fadd_rn(gg.x, cc.x);
+      cc.y = __fadd_rn(gg.y, cc.y);
+      cc.z = __fadd_rn(gg.z, cc.z);
+      cc.w = __fadd_rn(gg.w, cc.w);
+      reinterpret_cast<float4*>(s_c)[q4] = cc;
+      if (i0 >= v0 && i0 + 4 <= v1) __stcs(reinterpret_cast<float4*>(carry + i0), cc);
+    }
+    const float ov[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t i = i0 + e;
+      if (i >= lo && i < hi) {
+        const uint32_t k = mag_key(ov[e]);
+        nan |= k > 0x7f800000u;
+        if (k >= pre) mask |= 1u << (it * 4 + e);
+        if (APPLY && (i < v0 || i >= v1)) carry[i] = ov[e];   // edge element
+      }
+    }
+  }
+  if (nan) *t.err = 1;
+  if (cand) cand_compact(t, c, A, mask, s_c);
+}
+
+// FIN: the deferred finalize of the previous iteration (records, see
+// FinRecTask) is applied to the chunk's carry before the gradient is added
+// (when *t.fin_apply).  The records of the chunk (~1 % of its elements, index
+// order) are loaded while the chunk streams in and marked in a bitmap of the
+// chunk's positions; the carry stays in registers, and an element whose bit
+// is set takes its record (its rank among the set bits) as it is combined.
+constexpr int kFinRecMax = 1024;   // records per chunk handled in place (else: staged)
+#ifndef SPARDL_DIV_FIN_MINB
+#define SPARDL_DIV_FIN_MINB 3
+#endif
+
+template <int APPLY, int FIN>
+__global__ void __launch_bounds__(kThreads, FIN ? SPARDL_DIV_FIN_MINB : SPARDL_DIV_MINB)
+    k_div_cand(const DivTask* __restrict__ tasks) {
+  pdl_enter();
+  const DivTask& t = tasks[blockIdx.y];
+  const int c = blockIdx.x;
+  if (c >= t.nchunks) return;
+  // participation in the look-back is decided by the pre-threshold kernel
+  // only (bit 0), never by an overflow seen later in this kernel (bit 1)
+  const bool cand = !(*t.cand_bad & 1);
+  const uint32_t pre = *t.pre_key;
+  const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int ITER = kChunk / (kThreads * 4);   // float4 groups per lane
+  // the combined values wait here for the compaction (registers are the
+  // occupancy limit: the loads in flight need them)
+  __shared__ __align__(16) float s_comb[kChunk];
+  uint32_t mask = 0;
+  bool nan = false;
+  const int64_t lo = t.lo, hi = t.hi;
+  // gradient and carry never alias; telling the compiler so lets every load
+  // of the chunk issue before the first store (one memory latency per CTA
+  // instead of one per float4 group)
+  const float* __restrict__ g = APPLY ? t.g_tab[t.g_id] : nullptr;
+  float* __restrict__ carry = t.carry;
+  float4 gv[ITER], cv4[ITER];
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
+    if (i0 >= lo && i0 + 4 <= hi) {
+      if (APPLY) gv[it] = __ldcs(reinterpret_cast<const float4*>(g + i0));
+      cv4[it] = __ldcs(reinterpret_cast<const float4*>(carry + i0));
+    }
+  }
+  // (every chunk load is issued before anything below waits on memory)
+  int r0 = 0, r1 = 0;
+  if (FIN && *t.fin_apply) {
+    r0 = t.chunk_off[c];
+    r1 = t.chunk_off[c + 1];
+  }
+  // ---- the chunk's finalize records, while the chunk streams in
+  __shared__ uint32_t s_bits[kChunk / 32];     // positions with a record
+  __shared__ int s_wpre[kChunk / 32];          // records before each word
+  __shared__ float s_rv[2][kFinRecMax];
+  __shared__ int s_scr[40];
+  int32_t d_all = 0, d_cut = 0;
+  uint32_t d_pre = 0;
+  const bool fin = FIN && r1 > r0;                      // uniform per CTA
+  const int nrec = r1 - r0;
+  if (fin) {
+    d_all = t.prev_sel->all;   // the previous dividing selection (membership)
+    d_pre = t.prev_sel->prefix;
+    d_cut = t.prev_sel->cut_idx;
+    s_bits[threadIdx.x] = 0;   // (kChunk / 32 == kThreads words)
+    __syncthreads();
+    for (int q = threadIdx.x; q < min(nrec, kFinRecMax); q += kThreads) {
+      const int sp = (int)(t.rec_idx[r0 + q] - A);
+      atomicOr(&s_bits[sp >> 5], 1u << (sp & 31));
+      s_rv[0][q] = t.rec_v1[r0 + q];
+      s_rv[1][q] = t.rec_v2[r0 + q];
+    }
+    __syncthreads();
+    int tot;
+    s_wpre[threadIdx.x] = block_exscan(__popc(s_bits[threadIdx.x]), s_scr, &tot);
+    __syncthreads();
+  }
+  auto fin_value = [&](int sp, float x) {   // the carry at chunk position sp
+    const uint32_t wd = s_bits[sp >> 5];
+    if (!((wd >> (sp & 31)) & 1u)) return x;
+    const int r = s_wpre[sp >> 5] + __popc(wd & ((1u << (sp & 31)) - 1u));
+    const int32_t j = (int32_t)(A + sp);
+    const uint32_t key = mag_key(x);
+    const bool member = d_all == 1 || (d_all == 0 && (key > d_pre || (key == d_pre && j <= d_cut)));
+    return fin_fold(x, !member, s_rv[0][r], s_rv[1][r]);
+  };
+  const bool big = fin && nrec > kFinRecMax;   // rare: records past the table, patched below
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
+    const int sp0 = (warp * (32 * ITER) + it * 32 + lane) * 4;
+    if (i0 >= lo && i0 + 4 <= hi) {
+      float4 cc = cv4[it];
+      if (fin && !big && s_bits[sp0 >> 5]) {
+        cc.x = fin_value(sp0, cc.x);
+        cc.y = fin_value(sp0 + 1, cc.y);
+        cc.z = fin_value(sp0 + 2, cc.z);
+        cc.w = fin_value(sp0 + 3, cc.w);
+      }
+      cv4[it] = cc;
+    }
+  }
+  if (big) {   // every record through shared memory (a dense chunk of records)
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
+      const int sp0 = (warp * (32 * ITER) + it * 32 + lane) * 4;
+      if (i0 >= lo && i0 + 4 <= hi) {
+        reinterpret_cast<float4*>(s_comb)[sp0 >> 2] = cv4[it];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (i0 + e >= lo && i0 + e < hi) s_comb[sp0 + e] = carry[i0 + e];
+      }
+    }
+    __syncthreads();
+    for (int q = r0 + (int)threadIdx.x; q < r1; q += kThreads) {
+      const int32_t j = t.rec_idx[q];
+      const int sp = (int)(j - A);
+      const float x = s_comb[sp];
+      const uint32_t key = mag_key(x);
+      const bool member =
+          d_all == 1 || (d_all == 0 && (key > d_pre || (key == d_pre && j <= d_cut)));
+      s_comb[sp] = fin_fold(x, !member, t.rec_v1[q], t.rec_v2[q]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
+      if (i0 >= lo && i0 + 4 <= hi)
+        cv4[it] = reinterpret_cast<const float4*>(s_comb)[warp * (32 * ITER) + it * 32 + lane];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int64_t i0 = A + ((int64_t)warp * (32 * ITER) + it * 32 + lane) * 4;
+    if (i0 >= lo && i0 + 4 <= hi) {
+      const float4 cc = cv4[it];
+      float4 o;
+      if (APPLY) {
+        const float4 gg = gv[it];
+        o.x = __fadd_rn(gg.x, cc.x);
+        o.y = __fadd_rn(gg.y, cc.y);
+        o.z = __fadd_rn(gg.z, cc.z);
+        o.w = __fadd_rn(gg.w, cc.w);
+        __stcs(reinterpret_cast<float4*>(carry + i0), o);
+      } else {
+        o = cc;
+      }
+      reinterpret_cast<float4*>(s_comb)[warp * (32 * ITER) + it * 32 + lane] = o;
+      const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t k = mag_key(ov[e]);
+        nan |= k > 0x7f800000u;
+        if (k >= pre) mask |= 1u << (it * 4 + e);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t i = i0 + e;
+        const int sp = (warp * (32 * ITER) + it * 32 + lane) * 4 + e;
+        const float staged = big ? s_comb[sp] : 0.f;   // (big: patched in place)
+        s_comb[sp] = 0.f;
+        if (i >= lo && i < hi) {
+          float x = big ? staged : carry[i];
+          if (fin && !big) x = fin_value(sp, x);   // an edge element with a record
+          if (APPLY) {
+            x = __fadd_rn(g[i], x);
+            carry[i] = x;
+          }
+          s_comb[sp] = x;
+          const uint32_t k = mag_key(x);
+          nan |= k > 0x7f800000u;
+          if (k >= pre) mask |= 1u << (it * 4 + e);
+        }
+      }
+    }
+  }
+  if (nan) *t.err = 1;
+  if (!cand) return;
+  cand_compact(t, c, A, mask, s_comb);
 }
 
 // One CTA per task: the work list of the dividing select -- every chunk
@@ -361,10 +614,29 @@ int launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sampl
     n += 2;
   }
   if (part != 1) {
-    if (apply_residual)
-      launch_pdl(k_div_cand<1>, dim3(max_chunks, ntask), dim3(kThreads), 0, s, tasks_dev);
-    else
-      launch_pdl(k_div_cand<0>, dim3(max_chunks, ntask), dim3(kThreads), 0, s, tasks_dev);
+    static const bool bulk = [] {
+      const char* e = getenv("SPARDL_DIV_BULK");   // 1: the bulk-copy (TMA) form
+      return e && e[0] == '1';
+    }();
+    if (bulk) {
+      constexpr int smem = 2 * kChunk * (int)sizeof(float);
+      static bool configured[kMaxDevices][3] = {};
+      const int dev = cur_device();
+      auto k = apply_residual == 2 ? k_div_cand_bulk<1, 1>
+                                   : (apply_residual ? k_div_cand_bulk<1, 0> : k_div_cand_bulk<0, 0>);
+      const int v = apply_residual == 2 ? 2 : (apply_residual ? 1 : 0);
+      if (!configured[dev][v]) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured[dev][v] = true;
+      }
+      launch_pdl(k, dim3(max_chunks, ntask), dim3(kThreads), smem, s, tasks_dev);
+    } else if (apply_residual == 2) {   // + the previous iteration's deferred finalize
+      launch_pdl(k_div_cand<1, 1>, dim3(max_chunks, ntask), dim3(kThreads), 0, s, tasks_dev);
+    } else if (apply_residual) {
+      launch_pdl(k_div_cand<1, 0>, dim3(max_chunks, ntask), dim3(kThreads), 0, s, tasks_dev);
+    } else {
+      launch_pdl(k_div_cand<0, 0>, dim3(max_chunks, ntask), dim3(kThreads), 0, s, tasks_dev);
+    }
     launch_pdl(k_div_tiles, dim3(ntask), dim3(1024), 0, s, tasks_dev);
     n += 2;
   }

@@ -451,14 +451,14 @@ int Engine::materialize(int w, int pos, std::vector<int> pieces, int64_t budget,
   if (wide_on_) {
     if (pieces.size() == 1) {   // a single block buffer: one compact list
       const Slot& in = local_slot(pieces[0]);
-      constexpr int kStride = 4096;
+      constexpr int kStride = 8192;
       make_wide(st, t, in.idx, in.val, nullptr, nullptr, in.cnt, kStride,
-                static_cast<int>((in.cap + kStride - 1) / kStride), 1, sdl::kWFull, 0,
+                static_cast<int>((in.cap + kStride - 1) / kStride), 1, sdl::kWAuto, 0,
                 std::max<int64_t>(16384, in.cap / 8));
     } else {                    // the merge's partitions
       const sdl::MergeTask& mt = st.merges.back();
       make_wide(st, t, mt.out_idx, mt.out_val, mt.seg_off, mt.seg_cnt, nullptr, t.stride, t.nseg,
-                std::max(1, 4096 / std::max(1, static_cast<int>(mt.T))), sdl::kWFull, 0,
+                std::max(1, 8192 / std::max(1, static_cast<int>(mt.T))), sdl::kWAuto, 0,
                 std::max<int64_t>(16384, capsum / 8));
     }
   }
@@ -600,8 +600,8 @@ void Engine::plan() {
       t.dval = dt.carry + lo;
       t.fallbacks = fallbacks_dev_;
       if (wide_on_ && dt.use_cand && div_split_ <= 1)
-        dt.ws = make_wide(div_stage_, t, dt.cand_idx, dt.cand_val, nullptr, dt.cand_cnt, nullptr,
-                          dt.cap, dt.nchunks, 16, sdl::kWWindow, 1,
+        div_tasks_.back().ws = make_wide(div_stage_, t, dt.cand_idx, dt.cand_val, nullptr, dt.cand_cnt, nullptr,
+                          dt.cap, dt.nchunks, 64, sdl::kWWindow, 1,
                           std::max<int64_t>(16384, L_ / 8));
       t.sel_idx = out.idx;
       t.sel_val = out.val;
@@ -796,6 +796,7 @@ void Engine::plan() {
     }
     auto* src_dev = static_cast<sdl::GatherSrc*>(arena_.alloc(sizeof(sdl::GatherSrc) * m_));
     CK(mcpy(src_dev, src.data(), sizeof(sdl::GatherSrc) * m_, cudaMemcpyHostToDevice));
+    team_src_host_.push_back(src);
     Slot gs;
     gs.cap = cfg_.k;
     gs.bytes = 16 + 8 * static_cast<size_t>((cfg_.k + 3) & ~3);
@@ -862,6 +863,60 @@ void Engine::plan() {
     ft.xi = xl_dev;
     fin_tasks_.push_back(ft);
   }
+  // deferred finalize records (gres, <= 2 discard lists per block; the
+  // split dividing pass launches per group and keeps the plain finalize)
+  {
+    bool ok = cfg_.residual == SPARDL_RES_GRES && div_split_ <= 1 &&
+              static_cast<int>(div_tasks_.size()) == wloc_ * m_;
+    for (int li = 0; li < wloc_ && ok; ++li)
+      for (int b = 0; b < m_; ++b)
+        ok &= xi_[static_cast<size_t>(li)][static_cast<size_t>(b)].size() <= 2;
+    // SPARDL_FIN_DEFER: 1 = records applied by the next candidate pass,
+    // 2 = records applied right away by k_fin_apply (no carry access in the
+    // join), 0 (default) = k_finalize (join and carry read-modify-write)
+    const char* fe = std::getenv("SPARDL_FIN_DEFER");
+    fin_mode_ = fe ? std::atoi(fe) : 0;
+    if (fin_mode_ <= 0) ok = false;
+    fin_defer_ok_ = ok;
+    fin_apply_ = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+    if (ok) {
+      for (int li = 0; li < wloc_; ++li)
+        for (int b = 0; b < m_; ++b) {
+          sdl::DivTask& dt = div_tasks_[static_cast<size_t>(li * m_ + b)];
+          const sdl::GatherSrc& gs_ = team_src_host_[static_cast<size_t>(
+              team_of_local_global_[static_cast<size_t>(li)])][static_cast<size_t>(b)];
+          sdl::FinRecTask r{};
+          r.g_idx = gs_.idx;
+          r.g_cnt = gs_.cnt;
+          const auto& xl = xi_[static_cast<size_t>(li)][static_cast<size_t>(b)];
+          r.nxl = static_cast<int32_t>(xl.size());
+          for (size_t q = 0; q < xl.size(); ++q) r.xl[q] = xl[q];
+          r.nchunks = dt.nchunks;
+          r.origin = static_cast<int64_t>(dt.lo) & ~int64_t(3);
+          r.rec_idx = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * Lcap_));
+          r.rec_v1 = static_cast<float*>(arena_.alloc(sizeof(float) * Lcap_));
+          r.rec_v2 = static_cast<float*>(arena_.alloc(sizeof(float) * Lcap_));
+          r.chunk_off = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * (dt.nchunks + 1)));
+          r.rec_n = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
+          r.carry = carry_[static_cast<size_t>(li)];
+          r.div_sc = div_scr_[static_cast<size_t>(li)][static_cast<size_t>(b)];
+          fin_rec_.push_back(r);
+          dt.rec_idx = r.rec_idx;
+          dt.rec_v1 = r.rec_v1;
+          dt.rec_v2 = r.rec_v2;
+          dt.chunk_off = r.chunk_off;
+          dt.fin_apply = fin_apply_;
+          dt.prev_sel = r.div_sc;
+        }
+      fin_rec_dev_ = static_cast<sdl::FinRecTask*>(
+          arena_.alloc(sizeof(sdl::FinRecTask) * fin_rec_.size()));
+      CK(mcpy(fin_rec_dev_, fin_rec_.data(), sizeof(sdl::FinRecTask) * fin_rec_.size(),
+              cudaMemcpyHostToDevice));
+      CK(mcpy(div_dev_, div_tasks_.data(), sizeof(sdl::DivTask) * div_tasks_.size(),
+              cudaMemcpyHostToDevice));
+    }
+    fin_defer_ = ok;
+  }
   fin_max_div_ = cfg_.residual == SPARDL_RES_LRES ? Lcap_ : 0;
   fin_dev_ = static_cast<sdl::FinalizeTask*>(
       arena_.alloc(sizeof(sdl::FinalizeTask) * fin_tasks_.size()));
@@ -888,12 +943,34 @@ void Engine::plan() {
 }
 
 // ---------------------------------------------------------------------------
+// deferred finalize
+void Engine::flush_finalize() {
+  if (dry_ || !fin_defer_ || fin_rec_.empty()) return;
+  CK(cudaSetDevice(device_));
+  sdl::launch_fin_apply(fin_rec_dev_, static_cast<int>(fin_rec_.size()), Lcap_, fin_apply_,
+                        stream_);
+  CK(cudaMemsetAsync(fin_apply_, 0, sizeof(int32_t), stream_));
+  CK(sdl::take_launch_error());
+  CK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::set_defer(bool on) {
+  on = on && fin_defer_ok_;
+  if (on == fin_defer_) return;
+  flush_finalize();   // pending records applied before the mode changes
+  fin_defer_ = on;
+  drop_graph();
+}
+
+// ---------------------------------------------------------------------------
 // sparse conservation audit
 void Engine::set_audit(bool on) {
   audit_ = on;
   if (dry_) return;
   CK(cudaSetDevice(device_));
   sync();
+  // the audit reads the finalized carry at the global positions: plain finalize
+  set_defer(!on);
   const size_t k = static_cast<size_t>(std::max<int64_t>(1, cfg_.k));
   if (on && aud_comb_.empty()) {
     for (int li = 0; li < wloc_; ++li) {
@@ -1106,6 +1183,22 @@ void Engine::plan_peer() {
   wire_stage(div_stage_);
   for (Step& stp : steps_) wire_stage(stp.stage);
   for (size_t q = 0; q < asm_tasks_.size(); ++q) asm_tasks_[q].ps = sync_of(waits_of(asm_in_[q]), {});
+  // the residual finalize (or its records) reads the global gradient's blocks
+  for (int li = 0; li < wloc_; ++li) {
+    const size_t q = static_cast<size_t>(team_of_local_global_[static_cast<size_t>(li)]);
+    fin_tasks_[static_cast<size_t>(li)].ps = sync_of(waits_of(asm_in_[q]), {});
+  }
+  if (!fin_tasks_.empty())
+    CK(cudaMemcpy(fin_dev_, fin_tasks_.data(), sizeof(sdl::FinalizeTask) * fin_tasks_.size(),
+                  cudaMemcpyHostToDevice));
+  for (size_t i = 0; i < fin_rec_.size(); ++i) {
+    const size_t li = i / static_cast<size_t>(m_), b = i % static_cast<size_t>(m_);
+    const size_t q = static_cast<size_t>(team_of_local_global_[li]);
+    fin_rec_[i].ps = sync_of(waits_of({asm_in_[q][b]}), {});
+  }
+  if (!fin_rec_.empty())
+    CK(cudaMemcpy(fin_rec_dev_, fin_rec_.data(), sizeof(sdl::FinRecTask) * fin_rec_.size(),
+                  cudaMemcpyHostToDevice));
   if (!asm_tasks_.empty())
     CK(cudaMemcpy(asm_dev_, asm_tasks_.data(), sizeof(sdl::AssembleTask) * asm_tasks_.size(),
                   cudaMemcpyHostToDevice));
@@ -1129,11 +1222,11 @@ int Engine::exec_stage(const Stage& st, bool dividing) {
   if (!st.merges.empty() && !st.fused)
     n += sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts,
                            st.max_rT, st.max_r, stream_);
-  // wide path first (the dividing histogram is filled by the candidate
-  // pass); the cluster select then runs only the tasks handed back
+  // wide path first; the cluster select then runs only the tasks handed back
+  (void)dividing;
   if (st.wide)
     n += sdl::launch_wselect(st.sels_dev, static_cast<int>(st.sels.size()), st.w_max_tiles,
-                             !dividing, stream_);
+                             true, stream_);
   if (!st.sels.empty())
     n += sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_,
                             st.fused ? st.cl : 0, st.fused ? st.win_cap : 0);
@@ -1183,7 +1276,8 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   const int ndt = static_cast<int>(div_tasks_.size());
   const int G = std::min(div_split_, wloc_);
   if (G <= 1 || div_stage_.sels.size() != div_tasks_.size()) {
-    n += sdl::launch_divide(div_dev_, ndt, div_max_chunks_, div_sample_every_, 1, stream_, 2);
+    n += sdl::launch_divide(div_dev_, ndt, div_max_chunks_, div_sample_every_,
+                            fin_defer_ && fin_mode_ == 1 ? 2 : 1, stream_, 2);
     mark(2);
     n += exec_stage(div_stage_, true);   // (peer transport: each select publishes its block)
   } else {
@@ -1228,8 +1322,17 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   CK(cudaStreamWaitEvent(side_, ev_fork_, 0));
   n += sdl::launch_assemble(asm_dev_, static_cast<int>(asm_tasks_.size()), m_, cfg_.k, side_);
   n += sdl::launch_ledger(ledger_dev_, static_cast<int>(ledger_adds_.size()), abort, side_);
-  n += sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), Lcap_, m_,
-                            static_cast<int>(fin_max_div_), abort, stream_);
+  if (fin_defer_) {   // records for the next candidate pass (no carry access here)
+    n += sdl::launch_fin_records(fin_rec_dev_, static_cast<int>(fin_rec_.size()), Lcap_,
+                                 fin_apply_, stream_);
+    if (fin_mode_ == 2) {   // ... or applied at once
+      n += sdl::launch_fin_apply(fin_rec_dev_, static_cast<int>(fin_rec_.size()), Lcap_,
+                                 fin_apply_, stream_);
+      CK(cudaMemsetAsync(fin_apply_, 0, sizeof(int32_t), stream_));
+    }
+  } else
+    n += sdl::launch_finalize(fin_dev_, static_cast<int>(fin_tasks_.size()), Lcap_, m_,
+                              static_cast<int>(fin_max_div_), abort, stream_);
   CK(cudaEventRecord(ev_join_, side_));
   CK(cudaStreamWaitEvent(stream_, ev_join_, 0));
   // last remote read of the iteration done: peers may overwrite their buffers
@@ -1362,6 +1465,7 @@ void Engine::reset_state() {
   }
   std::fill(rounds_.begin(), rounds_.end(), 0);
   CK(cudaMemset(fallbacks_dev_, 0, sizeof(unsigned long long)));
+  if (fin_apply_) CK(cudaMemset(fin_apply_, 0, sizeof(int32_t)));
   CK(cudaMemset(wide_back_dev_, 0, sizeof(unsigned long long)));
   reset_wide(div_stage_);
   for (const Step& stp : steps_) reset_wide(stp.stage);

@@ -127,7 +127,15 @@ class Engine {
   void controller(int local, spardl_hctrl* out);
   void set_controller(int local, const spardl_hctrl& c);
   void global(int local, const int32_t** idx, const float** val, int64_t* nnz);
-  float* carry(int local) { return carry_[static_cast<size_t>(local)]; }
+  // the residual of local worker `local` (pending deferred finalize applied)
+  float* carry(int local) {
+    flush_finalize();
+    return carry_[static_cast<size_t>(local)];
+  }
+  // applies the last iteration's deferred finalize records to the carries
+  // (no-op when none are pending); synchronises
+  void flush_finalize();
+  bool finalize_deferred() const { return fin_defer_; }
   int64_t dimension() const { return cfg_.dimension; }
   int first_worker() const { return first_; }
   int local_workers() const { return wloc_; }
@@ -243,6 +251,15 @@ class Engine {
   std::vector<std::vector<int>> asm_in_;     // source block uids of each assembly
   sdl::AssembleTask* asm_dev_ = nullptr;
   std::vector<sdl::FinalizeTask> fin_tasks_;
+  // deferred finalize (gres): records written at the end of an iteration,
+  // applied by the next candidate pass (or flush_finalize)
+  bool fin_defer_ = false;
+  int fin_mode_ = 0;                     // SPARDL_FIN_DEFER (see plan())
+  bool fin_defer_ok_ = false;            // the plan allows it (audit may switch it off)
+  std::vector<sdl::FinRecTask> fin_rec_;
+  sdl::FinRecTask* fin_rec_dev_ = nullptr;
+  int32_t* fin_apply_ = nullptr;         // device flag: records pending
+  void set_defer(bool on);
   sdl::FinalizeTask* fin_dev_ = nullptr;
   int64_t fin_max_div_ = 0;
   std::vector<sdl::CtlTask> ctl_tasks_;
@@ -254,6 +271,7 @@ class Engine {
   std::vector<std::vector<int>> div_uid_;
   std::vector<std::vector<const sdl::SelScratch*>> div_scr_;
   std::vector<const sdl::GatherSrc*> team_src_;   // per global_ entry: the m reserved blocks
+  std::vector<std::vector<sdl::GatherSrc>> team_src_host_;   // (host copies)
   std::vector<std::vector<std::vector<sdl::XiList>>> xi_;
   std::vector<int> union_group_owner_;       // position group -> worker providing N_t
   bool ran_ = false;

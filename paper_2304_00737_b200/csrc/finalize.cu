@@ -1,5 +1,6 @@
 // Global-gradient assembly, residual finalize, ledger and the B-SAG
 // controller on the device.
+#include <algorithm>
 #include <climits>
 
 #include "common.cuh"
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB)
   if (err_set(abort)) return;   // void iteration (peer timeout): carry untouched
   const FinalizeTask& t = tasks[blockIdx.z];
   if (t.mode == 2) return;   // lres ignores the global gradient
+  peer_wait(t.ps);           // remote blocks of the global gradient published
   const int b = blockIdx.y;
   const GatherSrc G = t.gblk[b];
   const int gn = *G.cnt;
@@ -289,6 +291,92 @@ __global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Deferred finalize records (see FinRecTask): one CTA per (task, 1024 global
+// entries of block b).  The discard lists are joined with the CTA's indices
+// exactly as in k_finalize, but nothing touches the carry: the records and
+// the per-chunk record offsets are written in global-gradient order.
+__global__ void __launch_bounds__(kThreads) k_fin_records(const FinRecTask* __restrict__ tasks,
+                                                          int32_t* apply_flag) {
+  pdl_enter();
+  const FinRecTask& t = tasks[blockIdx.y];
+  peer_wait(t.ps);
+  const int gn = *t.g_cnt;
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *apply_flag = 1;
+  if (blockIdx.x == 0 && tid == 0) *t.rec_n = gn;
+  const int c0 = blockIdx.x * kFinChunk;
+  auto chunk_of = [&](int32_t j) { return (int)(((int64_t)j - t.origin) / kChunk); };
+  if (gn == 0) {
+    if (blockIdx.x == 0)
+      for (int c = tid; c <= t.nchunks; c += kThreads) t.chunk_off[c] = 0;
+    return;
+  }
+  if (c0 >= gn) return;
+  const int nloc = min(kFinChunk, gn - c0);
+  __shared__ int32_t gi[kFinChunk];
+  __shared__ float sv[2][kFinChunk];
+  __shared__ int range[4];
+  for (int e = tid; e < kFinChunk; e += kThreads) {
+    gi[e] = e < nloc ? t.g_idx[c0 + e] : INT_MAX;
+    sv[0][e] = __uint_as_float(kNoRec);
+    sv[1][e] = __uint_as_float(kNoRec);
+  }
+  __syncthreads();
+  const int32_t jlo = gi[0], jhi = gi[nloc - 1];
+  {   // each list's sub-range inside [jlo, jhi] (warps 0-3: lower/upper bounds)
+    const int warp = tid >> 5, li = warp >> 1;
+    if (li < t.nxl) {
+      const XiList X = t.xl[li];
+      const bool upper = warp & 1;
+      const int r = warp_bound(X.idx, *X.cnt, upper ? jhi : jlo, upper);
+      if ((tid & 31) == 0) range[warp] = r;
+    }
+  }
+  __syncthreads();
+  for (int li = 0; li < t.nxl; ++li) {
+    const XiList X = t.xl[li];
+    const int r0 = range[2 * li], r1 = range[2 * li + 1];
+    for (int p = r0 + tid; p < r1; p += kThreads) {
+      const int32_t x = X.idx[p];
+      const int ps = lower_bound_i32(gi, nloc, x);
+      if (ps < nloc && gi[ps] == x) sv[li][ps] = X.val[p];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nloc; e += kThreads) {
+    const int i = c0 + e;
+    const int32_t j = gi[e];
+    t.rec_idx[i] = j;
+    t.rec_v1[i] = sv[0][e];
+    t.rec_v2[i] = sv[1][e];
+    // chunk offsets: the chunks between the previous record's and this one's
+    const int cj = chunk_of(j);
+    const int cp = i == 0 ? -1 : chunk_of(e > 0 ? gi[e - 1] : t.g_idx[i - 1]);
+    for (int c = cp + 1; c <= cj; ++c) t.chunk_off[c] = i;
+    if (i == gn - 1)
+      for (int c = cj + 1; c <= t.nchunks; ++c) t.chunk_off[c] = gn;
+  }
+}
+
+// The pending records applied to the carry in place (a reader of the carry
+// between iterations); the caller clears the apply flag afterwards.
+__global__ void __launch_bounds__(kThreads) k_fin_apply(const FinRecTask* __restrict__ tasks,
+                                                        const int32_t* apply_flag) {
+  pdl_enter();
+  if (!*apply_flag) return;
+  const FinRecTask& t = tasks[blockIdx.y];
+  const int n = *t.rec_n;
+  const SelScratch* dsc = t.div_sc;
+  for (int i = blockIdx.x * kFinChunk + threadIdx.x; i < min(n, (int)(blockIdx.x + 1) * kFinChunk);
+       i += kThreads) {
+    const int32_t j = t.rec_idx[i];
+    const float x = t.carry[j];
+    const bool keep = !sel_member(dsc, mag_key(x), j);
+    t.carry[j] = fin_fold(x, keep, t.rec_v1[i], t.rec_v2[i]);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
     k_finalize_lres(const FinalizeTask* __restrict__ tasks, const int32_t* abort) {
   pdl_enter();
@@ -380,6 +468,23 @@ int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_blk, i
     launch_pdl(k_finalize_lres, dim3(lx, ntask), dim3(kThreads), 0, s, tasks_dev, abort);
     return 2;
   }
+  return 1;
+}
+
+int launch_fin_records(const FinRecTask* tasks_dev, int ntask, int64_t max_blk,
+                       int32_t* apply_flag, cudaStream_t s) {
+  if (ntask <= 0) return 0;
+  const int gx = (int)std::max<int64_t>(1, (max_blk + kFinChunk - 1) / kFinChunk);
+  launch_pdl(k_fin_records, dim3(gx, ntask), dim3(kThreads), 0, s, tasks_dev, apply_flag);
+  return 1;
+}
+
+int launch_fin_apply(const FinRecTask* tasks_dev, int ntask, int64_t max_blk,
+                     int32_t* apply_flag, cudaStream_t s) {
+  if (ntask <= 0) return 0;
+  const int gx = (int)std::max<int64_t>(1, (max_blk + kFinChunk - 1) / kFinChunk);
+  launch_pdl(k_fin_apply, dim3(gx, ntask), dim3(kThreads), 0, s, tasks_dev,
+             static_cast<const int32_t*>(apply_flag));
   return 1;
 }
 

@@ -171,8 +171,9 @@ constexpr int kMaxPush = 8;   // remote consumer ranks a select writes into
 // Wide select (wselect.cu): one select task spread over the whole GPU.
 // The task's input is cut into tiles (groups of `group` consecutive input
 // segments).  Level 1: a 2048-bin histogram of the magnitude keys -- the full
-// key range (bin = key >> 20) or, for the dividing select, a window above
-// its pre-threshold (bin = (key - base) >> shift, past the window: `above`).
+// key range (bin = key >> 20) or a window (bin = (key - base) >> shift, past
+// the window: `above`, under it: `below`) -- for the dividing select above
+// its pre-threshold, for the others around the previous threshold.
 // The bin holding the L-th key is located by every gather CTA; the gather
 // pass collects that bin's entries (key, index, tile) and per-tile counts;
 // the last gather CTA of the task selects the exact boundary entry inside
@@ -182,7 +183,13 @@ constexpr int kMaxPush = 8;   // remote consumer ranks a select writes into
 // overflow, dividing candidates incomplete) is handed to k_select (state
 // kWFallback), which also covers every input with merge holes.
 constexpr int kWBins = 2048;
-constexpr int kWFull = 0, kWWindow = 1;                    // histogram modes
+constexpr int kWFull = 0, kWWindow = 1, kWAuto = 2;       // histogram modes
+// kWAuto (Spar-Reduce-Scatter / SAG selects): a window of 2048 bins of
+// 2^kWAutoShift keys centred on the task's previous threshold (its
+// SelScratch prefix, whichever path selected it), the full key range when
+// there is none yet.  The merged lists concentrate in a narrow magnitude
+// range, so full-range bins (1/8 octave) would hold a large share of them.
+constexpr int kWAutoShift = 12;   // window = previous T +- 1/2 octave
 constexpr int kWOk = 0, kWAll = 1, kWNone = 2, kWFallback = 3;   // run states
 struct WScratch {
   // input: segments of the task (conventions of SelTask mode 0)
@@ -196,20 +203,29 @@ struct WScratch {
   int32_t nseg;
   int32_t group;              // segments per tile
   int32_t max_tiles;
-  int32_t mode;               // kWFull / kWWindow
+  int32_t mode;               // kWWindow (dividing: window set by k_div_prethr) / kWAuto
   int32_t is_div;             // dividing select (candidates + history)
-  // level-1 histogram (zeroed by the finisher after use)
+  // level-1 histogram (zeroed by the decider after use)
   uint32_t hist[kWBins];
   uint32_t above;             // window mode: keys past the last bin
-  uint32_t base;              // window mode: lowest key of bin 0 (= pre-threshold)
-  uint32_t shift;             // window mode: log2 of the bin width in key units
+  uint32_t below;             // window mode: keys below bin 0 (kWAuto; dividing: none)
+  uint32_t base;              // dividing: lowest key of bin 0 (= pre-threshold), set by k_div_prethr
+  uint32_t shift;             // dividing: log2 of the bin width in key units
+  uint32_t harrive;           // histogram CTAs done (reset by the decider)
   uint32_t arrive;            // gather CTAs done (reset by the finisher)
   uint32_t wdone;             // write CTAs done (reset by the last writer)
   uint32_t bin_n;             // entries collected into the bin buffer
-  int32_t state;              // kWOk / kWAll / kWNone / kWFallback of this run
-  uint32_t T;                 // threshold key of this run (kWOk)
+  int32_t state;              // kWOk / kWAll / kWNone / kWFallback of this run (decider)
+  int32_t run_mode;           // this run's histogram geometry (decider, read by the gather)
+  uint32_t run_base, run_shift;
+  int32_t bstar;              // the level-1 bin holding the L-th key
+  uint32_t bin_expect;        // its count
+  long long before;           // entries in higher bins (and above the window)
+  long long total_in;         // entries of the input this run
+  uint32_t T;                 // threshold key of this run (kWOk; finisher)
   int32_t cut;                // largest selected index among key == T
   int32_t ntiles;             // tiles in use this run
+  int32_t pad1_;
   long long total, total_sel; // entries, selected entries of this run
   // the bin buffer
   unsigned long long* bin_c;  // (key << 32) | (0x7fffffff - index): larger = earlier
@@ -303,6 +319,14 @@ struct DivTask {
   int32_t use_cand;        // 0: candidate path disabled (dense select)
   int32_t* err;            // NaN flag
   WScratch* ws;            // nullable: the wide select of this block (window histogram)
+  // deferred finalize (nullable): the previous iteration's records of this
+  // block, applied to the carry before the gradient is added when *fin_apply
+  const int32_t* rec_idx;
+  const float* rec_v1;
+  const float* rec_v2;
+  const int32_t* chunk_off;
+  const int32_t* fin_apply;
+  const SelScratch* prev_sel; // the previous iteration's dividing selection (membership)
 };
 
 // ---------------------------------------------------------------------------
@@ -372,7 +396,40 @@ struct FinalizeTask {
   // gradient, this worker's combined value and final residual
   float* aud_comb;
   float* aud_carry;
+  PeerSync ps;                // waits on the remote blocks of the global gradient
 };
+
+// Deferred residual finalize (gres): instead of a random read-modify-write
+// of the carry at the k global positions at the end of an iteration, the
+// finalize is written as records -- per global index j of block b, the
+// in-procedure discard values of j in recording order (<= 2 lists per
+// block; absent = kNoRec bits) -- and the next iteration's candidate pass,
+// which streams the carry anyway, applies them chunk by chunk before it adds
+// the gradient (inc/residual.hpp:128-150 evaluated at the next apply,
+// inc/residual.hpp:63-71; same fold, same rounding).  Reading the carry in
+// between (spardl_get_carry & co.) applies them first (k_fin_apply).
+constexpr uint32_t kNoRec = 0x7fffffffu;   // a NaN: never a discard value
+struct FinRecTask {           // one (local worker, block b)
+  const int32_t* g_idx;       // the global gradient's block b
+  const int32_t* g_cnt;
+  XiList xl[2];               // the worker's discard lists of block b, recording order
+  int32_t nxl;
+  int32_t nchunks;            // chunks of the worker's dividing task of block b
+  int64_t origin;             // its chunk origin (lo rounded down to 4)
+  int32_t* rec_idx;           // [L] records, in global-gradient order
+  float* rec_v1;
+  float* rec_v2;
+  int32_t* chunk_off;         // [nchunks + 1] first record of every chunk
+  int32_t* rec_n;             // records written
+  float* carry;               // (k_fin_apply) the worker's carry
+  const SelScratch* div_sc;   // (k_fin_apply) its dividing selection of block b
+  PeerSync ps;                // waits on remote blocks of the global gradient
+};
+int launch_fin_records(const FinRecTask* tasks_dev, int ntask, int64_t max_blk,
+                       int32_t* apply_flag, cudaStream_t s);
+// apply pending records to the carry in place (a reader between iterations)
+int launch_fin_apply(const FinRecTask* tasks_dev, int ntask, int64_t max_blk,
+                     int32_t* apply_flag, cudaStream_t s);
 // abort (nullable): the peer-timeout flag; when set the persistent-state
 // writers (finalize, ledger, controller) leave their state untouched
 int launch_finalize(const FinalizeTask* tasks_dev, int ntask, int64_t max_blk, int m,

@@ -9,9 +9,13 @@
 // the Spar-Reduce-Scatter with one worker per GPU has one or two tasks, so
 // most SMs would idle.  Here a task is cut into tiles (groups of its input
 // segments, in index order) and every kernel runs one CTA per tile:
-//   k_wsel_hist    level-1 histogram of the magnitude keys, 2048 bins of
-//                  key >> 20 (the dividing select's window histogram above
-//                  its pre-threshold is filled by k_div_cand instead)
+//   k_wsel_hist    level-1 histogram of the magnitude keys, 2048 bins over a
+//                  window: above the dividing pre-threshold, or around the
+//                  task's previous threshold (full key range, key >> 20,
+//                  when there is none); a per-CTA shared histogram over 16
+//                  tiles, flushed once (fusing it into the candidate pass
+//                  as global reductions was measured 1.5x slower: the hot
+//                  bins serialise)
 //   k_wsel_gather  every CTA locates the bin holding the L-th key (suffix
 //                  scan of the histogram, identical in every CTA), counts its
 //                  tile's entries above that bin and appends the bin's
@@ -31,6 +35,7 @@
 // ties) -- is marked kWFallback and k_select (launched right after) selects
 // it; every other task makes k_select return at once.
 #include <climits>
+#include <cstdio>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -41,7 +46,6 @@ namespace {
 
 constexpr int kWThreads = 256;
 constexpr int kWWarps = kWThreads / 32;
-constexpr int kWHistTiles = 16;    // tiles per histogram CTA
 constexpr int kWMaxGroup = 64;     // segments per tile (bound of the write pass tables)
 constexpr int kWSmemSel = 2048;    // bin entries the finisher selects in shared memory
 
@@ -67,45 +71,86 @@ __device__ __forceinline__ int w_bin(int mode, uint32_t base, uint32_t shift, ui
   return d >= (uint32_t)kWBins ? kWBins : (int)d;
 }
 
+// this run's histogram geometry of a task (identical in every CTA of the
+// histogram and gather kernels: the previous threshold is only rewritten by
+// the finisher, after every gather CTA has classified its tile)
+__device__ __forceinline__ void w_geometry(const SelTask& t, const WScratch& w, int& mode,
+                                           uint32_t& base, uint32_t& shift) {
+  if (w.mode == kWWindow) {
+    mode = kWWindow;
+    base = w.base;
+    shift = w.shift;
+    return;
+  }
+  const SelScratch* sc = t.scr;
+  const uint32_t prev = sc->prefix;
+  if (sc->all == 0 && prev != 0) {
+    mode = kWWindow;
+    shift = kWAutoShift;
+    const uint32_t half = (uint32_t)(kWBins / 2) << kWAutoShift;
+    base = prev > half ? prev - half : 0u;
+  } else {
+    mode = kWFull;
+    base = 0;
+    shift = 20;
+  }
+}
+
 __device__ __forceinline__ unsigned long long w_comp(uint32_t key, int32_t idx) {
   return ((unsigned long long)key << 32) | (unsigned long long)(0x7fffffffu - (uint32_t)idx);
 }
 
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kWThreads) k_wsel_hist(const SelTask* __restrict__ tasks) {
-  pdl_enter();
-  const SelTask& t = tasks[blockIdx.y];
-  WScratch* __restrict__ ws = t.ws;
-  if (ws->mode != kWFull) return;
-  peer_wait(t.ps);
-  const int nseg = w_nseg(*ws);
-  const int G = ws->group;
-  const int s0 = blockIdx.x * kWHistTiles * G;
-  if (s0 >= nseg) return;
-  const int s1 = min(nseg, s0 + kWHistTiles * G);
-  __shared__ uint32_t h[kWBins];
-  for (int b = threadIdx.x; b < kWBins; b += kWThreads) h[b] = 0;
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int s = s0 + warp; s < s1; s += kWWarps) {
+// A tile of a task: its segments' input offsets and the exclusive prefix of
+// their lengths, in shared memory.  Entries are addressed flat (tile order ==
+// index order): the CTA sweeps them in rounds of kWRound, warp w owning
+// flat [w * kWPer * 32, (w + 1) * kWPer * 32) of a round, lane l element
+// i * 32 + l of that -- kWPer coalesced loads in flight per thread.
+constexpr int kWPer = 16;
+constexpr int kWRound = kWThreads * kWPer;
+struct TileMap {
+  int n;
+  int nseg;
+  int off[kWMaxGroup];
+  int pre[kWMaxGroup + 1];
+};
+
+__device__ void tile_map_load(const WScratch& w, int q, int nseg_total, TileMap& tm) {
+  const int G = w.group;
+  const int s0 = q * G;
+  const int ns = max(0, min(nseg_total, s0 + G) - s0);
+  __shared__ int cnts[kWMaxGroup];
+  if ((int)threadIdx.x < ns) {
     int off, cnt;
-    w_seg(*ws, s, off, cnt);
-    const float* vp = ws->val + off;
-    for (int j0 = 0; j0 < cnt; j0 += 128) {
-      float v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = j0 + u * 32 + lane;
-        v[u] = j < cnt ? __ldcg(vp + j) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (j0 + u * 32 + lane < cnt) atomicAdd(&h[mag_key(v[u]) >> 20], 1u);
-    }
+    w_seg(w, s0 + threadIdx.x, off, cnt);
+    tm.off[threadIdx.x] = off;
+    cnts[threadIdx.x] = cnt;
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kWBins; b += kWThreads)
-    if (h[b]) atomicAdd(&ws->hist[b], h[b]);
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int i = 0; i < ns; ++i) {
+      tm.pre[i] = a;
+      a += cnts[i];
+    }
+    tm.pre[ns] = a;
+    tm.n = a;
+    tm.nseg = ns;
+  }
+  __syncthreads();
+}
+
+// input position of flat entry p (0 <= p < tm.n): the last segment starting
+// at or before p (empty segments share their successor's start)
+// Branch-free (a fixed, unrolled search) so that a thread's kWPer loads are
+// all issued before the first one is used.
+__device__ __forceinline__ int tile_src(const TileMap& tm, int p) {
+  int lo = 0;
+#pragma unroll
+  for (int step = kWMaxGroup / 2; step >= 1; step >>= 1) {
+    const int mid = lo + step;
+    lo = (mid < tm.nseg && tm.pre[mid] <= p) ? mid : lo;
+  }
+  return tm.off[lo] + (p - tm.pre[lo]);
 }
 
 // The bin holding the need-th largest key of the level-1 histogram (every
@@ -233,121 +278,210 @@ __device__ unsigned long long w_select_kth(const unsigned long long* __restrict_
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kWThreads) k_wsel_gather(const SelTask* __restrict__ tasks) {
+// Histogram pass.  Every CTA adds its tile's key counts; the last CTA of the
+// task (the decider) fixes the run state, the boundary bin and this run's
+// geometry in the scratch, then zeroes the histogram for the next run.
+__global__ void __launch_bounds__(kWThreads) k_wsel_hist(const SelTask* __restrict__ tasks) {
   pdl_enter();
   const SelTask& t = tasks[blockIdx.y];
   WScratch* __restrict__ ws = t.ws;
-  peer_wait(t.ps);
-  __shared__ int scratch[40];
-  __shared__ long long lsh[32];
-  __shared__ int s_state;
-  __shared__ unsigned int s_n, s_na;
+  const int nseg = w_nseg(*ws);
+  const int q = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int mode = ws->mode;
-  const uint32_t base = ws->base, shift = ws->shift;
+  int mode;
+  uint32_t base, shift;
+  w_geometry(t, *ws, mode, base, shift);
+  __shared__ TileMap tm;
+  __shared__ uint32_t h[kWBins];
+  __shared__ uint32_t s_ab[2];
+  __shared__ int s_last;
+  __shared__ int scratch[40];
+  __shared__ long long lsh[3 * 32];
+  if (q * ws->group < nseg) {
+    peer_wait(t.ps);
+    for (int b = tid; b < kWBins; b += kWThreads) h[b] = 0;
+    if (tid < 2) s_ab[tid] = 0;
+    tile_map_load(*ws, q, nseg, tm);
+    const float* __restrict__ val = ws->val;
+    uint32_t nbelow = 0, nabove = 0;
+    for (int r0 = 0; r0 < tm.n; r0 += kWRound) {
+      const int p0 = r0 + warp * (kWPer * 32) + lane;
+      int src[kWPer];
+#pragma unroll
+      for (int i = 0; i < kWPer; ++i) src[i] = tile_src(tm, min(p0 + i * 32, tm.n - 1));
+      float v[kWPer];
+#pragma unroll
+      for (int i = 0; i < kWPer; ++i) v[i] = __ldcg(val + src[i]);   // (clamped: in bounds)
+#pragma unroll
+      for (int i = 0; i < kWPer; ++i)
+        if (p0 + i * 32 < tm.n) {
+          const int b = w_bin(mode, base, shift, mag_key(v[i]));
+          if (b < 0) ++nbelow;
+          else if (b >= kWBins) ++nabove;
+          else atomicAdd(&h[b], 1u);
+        }
+    }
+    nbelow = __reduce_add_sync(0xffffffffu, nbelow);
+    nabove = __reduce_add_sync(0xffffffffu, nabove);
+    if (lane == 0 && (nbelow | nabove)) {
+      atomicAdd(&s_ab[0], nbelow);
+      atomicAdd(&s_ab[1], nabove);
+    }
+    __syncthreads();
+    for (int b = tid; b < kWBins; b += kWThreads)
+      if (h[b]) atomicAdd(&ws->hist[b], h[b]);
+    if (tid == 0) {
+      if (s_ab[0]) atomicAdd(&ws->below, s_ab[0]);
+      if (s_ab[1]) atomicAdd(&ws->above, s_ab[1]);
+    }
+  }
+  // ---- arrival; the decider
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = (int)(atomicAdd(&ws->harrive, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
   const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
-  const long long above = mode == kWWindow ? (long long)__ldcg(&ws->above) : 0;
-  // ---- the run state and the boundary bin (identical in every CTA)
-  long long total;
+  const long long above = __ldcg(&ws->above), below = __ldcg(&ws->below);
+  long long part = 0;
+  for (int b = tid; b < kWBins; b += kWThreads) part += __ldcg(ws->hist + b);
+  {
+    long long u0 = 0, u1 = 0;
+    block_sum3_ll(part, u0, u1, lsh);
+  }
+  long long total = part + above + below;
   bool bad = false;
   if (ws->is_div) {
     total = *t.cand_total;
     bad = *t.cand_bad != 0 || total < budget;   // incomplete: dense fallback in k_select
   }
-  int bstar = -1;
+  int state, bstar = -1;
   long long before = 0;
-  {
-    long long part = 0;
-    for (int b = tid; b < kWBins; b += kWThreads) part += __ldcg(ws->hist + b);
-    long long u0 = 0, u1 = 0;
-    block_sum3_ll(part, u0, u1, lsh);
-    if (!ws->is_div) total = part;
-  }
-  int state;
   if (bad) state = kWFallback;
   else if (total <= budget) state = kWAll;
   else if (budget <= 0) state = kWNone;
   else if (above >= budget) state = kWFallback;   // threshold above the window
   else state = w_locate(ws->hist, above, budget, &bstar, &before, scratch, lsh) ? kWOk : kWFallback;
-  // ---- this tile
+  const uint32_t expect = bstar >= 0 ? __ldcg(ws->hist + bstar) : 0u;
+  __syncthreads();
+  for (int b = tid; b < kWBins; b += kWThreads) ws->hist[b] = 0;
+  if (tid == 0) {
+    ws->state = state;
+    ws->run_mode = mode;
+    ws->run_base = base;
+    ws->run_shift = shift;
+    ws->bstar = bstar;
+    ws->before = before;
+    ws->bin_expect = expect;
+    ws->total_in = total;
+    ws->above = 0;
+    ws->below = 0;
+    ws->harrive = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Gather pass: entries above the boundary bin are counted per tile, the
+// bin's entries collected.  The last CTA of the task (the finisher) selects
+// the boundary entry, fixes the per-tile output offsets and records the
+// selection.
+__global__ void __launch_bounds__(kWThreads, 2) k_wsel_gather(const SelTask* __restrict__ tasks) {
+  pdl_enter();
+  const SelTask& t = tasks[blockIdx.y];
+  WScratch* __restrict__ ws = t.ws;
+  __shared__ int scratch[40];
+  __shared__ int s_last;
+  __shared__ unsigned int s_na;
+  __shared__ TileMap tm;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int state = ws->state;
+  const int mode = ws->run_mode;
+  const uint32_t base = ws->run_base, shift = ws->run_shift;
+  const int bstar = ws->bstar;
   const int nseg = w_nseg(*ws);
   const int G = ws->group;
   const int ntiles = (nseg + G - 1) / G;
   const int q = blockIdx.x;
-  if (tid == 0) {
-    s_n = 0;
-    s_na = 0;
-  }
-  __syncthreads();
+  if (tid == 0) s_na = 0;
   if (q < ntiles && state != kWFallback) {
-    const int s0 = q * G, s1 = min(nseg, s0 + G);
-    unsigned int n = 0, na = 0;
-    for (int s = s0 + warp; s < s1; s += kWWarps) {
-      int off, cnt;
-      w_seg(*ws, s, off, cnt);
-      n += cnt;
-      if (state != kWOk) continue;
-      const float* vp = ws->val + off;
-      const int32_t* ip = ws->idx + off;
-      for (int j0 = 0; j0 < cnt; j0 += 128) {
-        float v[4];
+    peer_wait(t.ps);
+    tile_map_load(*ws, q, nseg, tm);
+    unsigned int na = 0;
+    if (state == kWOk) {
+      const float* __restrict__ val = ws->val;
+      const int32_t* __restrict__ idx = ws->idx;
+      unsigned long long* __restrict__ bin_c = ws->bin_c;
+      int32_t* __restrict__ bin_tile = ws->bin_tile;
+      const int bin_cap = ws->bin_cap;
+      const uint32_t lt = lanemask_lt();
+      for (int r0 = 0; r0 < tm.n; r0 += kWRound) {
+        const int p0 = r0 + warp * (kWPer * 32) + lane;
+        int src[kWPer];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * 32 + lane;
-          v[u] = j < cnt ? __ldcg(vp + j) : 0.f;
-        }
+        for (int i = 0; i < kWPer; ++i) src[i] = tile_src(tm, min(p0 + i * 32, tm.n - 1));
+        float v[kWPer];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * 32 + lane;
-          const uint32_t key = mag_key(v[u]);
-          const int b = j < cnt ? w_bin(mode, base, shift, key) : -1;
+        for (int i = 0; i < kWPer; ++i) v[i] = __ldcg(val + src[i]);   // (clamped: in bounds)
+#pragma unroll
+        for (int i = 0; i < kWPer; ++i) {
+          const uint32_t key = mag_key(v[i]);
+          const int b = p0 + i * 32 < tm.n ? w_bin(mode, base, shift, key) : -1;
           na += b > bstar;
           const bool in = b == bstar;
           const uint32_t bal = __ballot_sync(0xffffffffu, in);
           if (bal) {
-            int p0 = 0;
-            if (lane == 0) p0 = (int)atomicAdd(&ws->bin_n, (unsigned)__popc(bal));
-            p0 = __shfl_sync(0xffffffffu, p0, 0);
+            int pb = 0;
+            if (lane == 0) pb = (int)atomicAdd(&ws->bin_n, (unsigned)__popc(bal));
+            pb = __shfl_sync(0xffffffffu, pb, 0);
             if (in) {
-              const int p = p0 + __popc(bal & lanemask_lt());
-              if (p < ws->bin_cap) {
-                ws->bin_c[p] = w_comp(key, __ldcg(ip + j));
-                ws->bin_tile[p] = q;
+              const int pp = pb + __popc(bal & lt);
+              if (pp < bin_cap) {
+                bin_c[pp] = w_comp(key, __ldcg(idx + src[i]));
+                bin_tile[pp] = q;
               }
             }
           }
         }
       }
     }
-    n = __reduce_add_sync(0xffffffffu, lane == 0 ? n : 0u);   // (segment counts: lane-uniform)
     na = __reduce_add_sync(0xffffffffu, na);
-    if (lane == 0) {
-      atomicAdd(&s_n, n);
-      atomicAdd(&s_na, na);
-    }
+    if (lane == 0 && na) atomicAdd(&s_na, na);
     __syncthreads();
     if (tid == 0) {
-      ws->tile_n[q] = (int)s_n;
-      ws->tile_sel[q] = state == kWOk ? (int)s_na : (state == kWAll ? (int)s_n : 0);
+      ws->tile_n[q] = tm.n;
+      ws->tile_sel[q] = state == kWOk ? (int)s_na : (state == kWAll ? tm.n : 0);
     }
   }
-  // ---- arrival; the last CTA of the task finishes the selection
-  __threadfence();
+  // ---- arrival; the finisher
   __syncthreads();
-  if (tid == 0) s_state = (int)(atomicAdd(&ws->arrive, 1u) == gridDim.x - 1);
+  if (tid == 0) {
+    __threadfence();
+    s_last = (int)(atomicAdd(&ws->arrive, 1u) == gridDim.x - 1);
+  }
   __syncthreads();
-  if (!s_state) return;
+  if (!s_last) return;
   __threadfence();
   SelScratch* sc = t.scr;
+  const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
   if (state == kWOk) {
     const long long nb = (long long)__ldcg(&ws->bin_n);
-    if (nb > ws->bin_cap || nb != (long long)__ldcg(ws->hist + bstar))
+    if (nb > ws->bin_cap || nb != (long long)ws->bin_expect)
       state = kWFallback;   // bin buffer overflow (massive key ties): k_select
   }
+#ifdef SPARDL_WSEL_DEBUG
+  if (tid == 0)
+    printf("wsel task %d div %d mode %d state %d total %lld budget %lld bstar %d before %lld "
+           "bin_n %u expect %u cap %d base %u shift %u ntiles %d\n",
+           (int)blockIdx.y, ws->is_div, mode, state, ws->total_in, (long long)budget, bstar,
+           ws->before, __ldcg(&ws->bin_n), ws->bin_expect, ws->bin_cap, base, shift, ntiles);
+#endif
   unsigned long long cstar = 0;
   if (state == kWOk) {
     const int nb = (int)__ldcg(&ws->bin_n);
-    cstar = w_select_kth(ws->bin_c, nb, budget - before, scratch);
+    cstar = w_select_kth(ws->bin_c, nb, budget - ws->before, scratch);
     for (int i = tid; i < nb; i += kWThreads)
       if (__ldcg(ws->bin_c + i) >= cstar) atomicAdd(ws->tile_sel + __ldcg(ws->bin_tile + i), 1);
     __threadfence();
@@ -373,8 +507,7 @@ __global__ void __launch_bounds__(kWThreads) k_wsel_gather(const SelTask* __rest
     tot_sel = carry_s;
     tot_all = (long long)carry_s + carry_d;
   }
-  // ---- the selection record, the dividing history; zero the histogram
-  for (int b = tid; b < kWBins; b += kWThreads) ws->hist[b] = 0;
+  // ---- the selection record and the dividing history
   if (tid == 0) {
     const uint32_t T = (uint32_t)(cstar >> 32);
     const int32_t cut = (int32_t)(0x7fffffffu - (uint32_t)(cstar & 0xffffffffull));
@@ -385,7 +518,6 @@ __global__ void __launch_bounds__(kWThreads) k_wsel_gather(const SelTask* __rest
     ws->ntiles = ntiles;
     ws->total = tot_all;
     ws->total_sel = tot_sel;
-    ws->above = 0;
     ws->bin_n = 0;
     ws->arrive = 0;
     if (state != kWFallback) {
@@ -403,15 +535,21 @@ __global__ void __launch_bounds__(kWThreads) k_wsel_gather(const SelTask* __rest
           sc->cut_idx = INT_MAX;
         }
         if (t.div_hist)
-          update_history(t.div_hist, 0, all, state == kWOk ? T : 0u, *t.pre_key_dev, total,
-                         budget);
+          update_history(t.div_hist, 0, all, state == kWOk ? T : 0u, *t.pre_key_dev,
+                         ws->total_in, budget);
       }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kWThreads) k_wsel_write(const SelTask* __restrict__ tasks) {
+// Write pass: ordered compaction of every tile (round by round: warp ballots,
+// then the warps' totals), kept entries to the output block (and the peers'
+// copies), discarded ones scaled to the discard list.
+constexpr int kWPerW = 8;   // entries per thread and round here (register budget)
+constexpr int kWRoundW = kWThreads * kWPerW;
+
+__global__ void __launch_bounds__(kWThreads, 3) k_wsel_write(const SelTask* __restrict__ tasks) {
   pdl_enter();
   const SelTask& t = tasks[blockIdx.y];
   const WScratch* __restrict__ ws = t.ws;
@@ -421,125 +559,103 @@ __global__ void __launch_bounds__(kWThreads) k_wsel_write(const SelTask* __restr
   const int q = blockIdx.x;
   const int ntiles = ws->ntiles;
   const int npush = t.npush;
-  __shared__ int segsel[kWMaxGroup], segbase[kWMaxGroup + 1];
+  __shared__ TileMap tm;
+  __shared__ int wsum[2][kWWarps];
   __shared__ int s_last;
   if (q < ntiles) {
     peer_wait(t.ps);
+    tile_map_load(*ws, q, w_nseg(*ws), tm);
     const uint32_t T = ws->T;
     const int32_t cut = ws->cut;
-    auto keep = [&](uint32_t key, int32_t ix) {
-      return state == kWAll || (state == kWOk && (key > T || (key == T && ix <= cut)));
-    };
-    const int nseg = w_nseg(*ws);
-    const int G = ws->group;
-    const int s0 = q * G, s1 = min(nseg, s0 + G);
-    const int nl = s1 - s0;
-    // pass A: kept entries per segment
-    for (int ls = warp; ls < nl; ls += kWWarps) {
-      int off, cnt;
-      w_seg(*ws, s0 + ls, off, cnt);
-      const float* vp = ws->val + off;
-      const int32_t* ip = ws->idx + off;
-      int k = 0;
-      for (int j0 = 0; j0 < cnt; j0 += 128) {
-        float v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * 32 + lane;
-          v[u] = j < cnt ? __ldcg(vp + j) : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * 32 + lane;
-          const uint32_t key = mag_key(v[u]);
-          bool kp = false;
-          if (j < cnt) kp = key == T && state == kWOk ? keep(key, __ldcg(ip + j)) : keep(key, 0);
-          k += __popc(__ballot_sync(0xffffffffu, kp));
-        }
-      }
-      if (lane == 0) segsel[ls] = k;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int a = 0;
-      for (int ls = 0; ls < nl; ++ls) {
-        segbase[ls] = a;
-        a += segsel[ls];
-      }
-      segbase[nl] = a;
-    }
-    __syncthreads();
-    // pass B: ordered writes (segment bases, then warp-ballot ranks)
-    int32_t* pidx[kMaxPush];
-    float* pval[kMaxPush];
-#pragma unroll
-    for (int p = 0; p < kMaxPush; ++p) {
-      pidx[p] = nullptr;
-      pval[p] = nullptr;
-      if (p < npush) {
-        unsigned char* b = t.push_base[p];
-        pidx[p] = reinterpret_cast<int32_t*>(b + 16);
-        pval[p] = reinterpret_cast<float*>(b + 16 + 4 * (size_t)t.push_cap);
-      }
-    }
-    const int sel0 = ws->tile_sel_off[q];
-    const int dis0 = ws->tile_dis_off[q];
-    const bool want_dis = t.dis_idx != nullptr;
+    int ks = ws->tile_sel_off[q];   // output positions of the round (CTA-uniform)
+    int kd = ws->tile_dis_off[q];
+    int32_t* __restrict__ sel_idx = t.sel_idx;
+    float* __restrict__ sel_val = t.sel_val;
+    int32_t* __restrict__ dis_idx = t.dis_idx;
+    float* __restrict__ dis_val = t.dis_val;
+    unsigned char* const* push_base = t.push_base;
+    const size_t push_voff = 16 + 4 * (size_t)t.push_cap;
     const float w = t.weight;
     const uint32_t lt = lanemask_lt();
-    int seg_entry0 = 0;   // entries of the tile before segment ls (for discard ranks)
-    for (int ls = 0; ls < nl; ++ls) {
-      int off, cnt;
-      w_seg(*ws, s0 + ls, off, cnt);
-      if (ls % kWWarps == warp) {
-        const float* vp = ws->val + off;
-        const int32_t* ip = ws->idx + off;
-        int ks = sel0 + segbase[ls];
-        int kd = dis0 + (seg_entry0 - segbase[ls]);
-        for (int j0 = 0; j0 < cnt; j0 += 128) {
-          float v[4];
-          int32_t ix[4];
+    const float* __restrict__ val = ws->val;
+    const int32_t* __restrict__ idx = ws->idx;
+    for (int r0 = 0; r0 < tm.n; r0 += kWRoundW) {
+      const int p0 = r0 + warp * (kWPerW * 32) + lane;
+      int src[kWPerW];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u * 32 + lane;
-            v[u] = j < cnt ? __ldcg(vp + j) : 0.f;
-            ix[u] = j < cnt ? __ldcg(ip + j) : 0;
-          }
+      for (int i = 0; i < kWPerW; ++i) src[i] = tile_src(tm, min(p0 + i * 32, tm.n - 1));
+      float v[kWPerW];
+      int32_t ix[kWPerW];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u * 32 + lane;
-            const bool valid = j < cnt;
-            const bool kp = valid && keep(mag_key(v[u]), ix[u]);
-            const uint32_t bk = __ballot_sync(0xffffffffu, kp);
-            const uint32_t bd = __ballot_sync(0xffffffffu, valid && !kp);
-            if (kp) {
-              const int p = ks + __popc(bk & lt);
-              t.sel_idx[p] = ix[u];
-              t.sel_val[p] = v[u];
-#pragma unroll
-              for (int pp = 0; pp < kMaxPush; ++pp)
-                if (pp < npush) {
-                  pidx[pp][p] = ix[u];
-                  pval[pp][p] = v[u];
-                }
-            } else if (valid && want_dis) {
-              const int p = kd + __popc(bd & lt);
-              t.dis_idx[p] = ix[u];
-              t.dis_val[p] = __fmul_rn(v[u], w);
-            }
-            ks += __popc(bk);
-            kd += __popc(bd);
-          }
-        }
+      for (int i = 0; i < kWPerW; ++i) {   // (clamped: in bounds; past the tile: ix = -1)
+        v[i] = __ldcg(val + src[i]);
+        ix[i] = __ldcg(idx + src[i]);
       }
-      seg_entry0 += cnt;
+#pragma unroll
+      for (int i = 0; i < kWPerW; ++i)
+        if (p0 + i * 32 >= tm.n) ix[i] = -1;
+      auto keep = [&](int i) {
+        const uint32_t key = mag_key(v[i]);
+        return ix[i] >= 0 && (state == kWAll ||
+                              (state == kWOk && (key > T || (key == T && ix[i] <= cut))));
+      };
+      int cs = 0, cd = 0;
+#pragma unroll
+      for (int i = 0; i < kWPerW; ++i) {
+        const bool kp = keep(i);
+        cs += __popc(__ballot_sync(0xffffffffu, kp));
+        cd += __popc(__ballot_sync(0xffffffffu, ix[i] >= 0 && !kp));
+      }
+      if (lane == 0) {
+        wsum[0][warp] = cs;
+        wsum[1][warp] = cd;
+      }
+      __syncthreads();
+      int bs = ks, bdd = kd, ts = 0, td = 0;
+#pragma unroll
+      for (int u = 0; u < kWWarps; ++u) {
+        const int a0 = wsum[0][u], a1 = wsum[1][u];
+        if (u < warp) {
+          bs += a0;
+          bdd += a1;
+        }
+        ts += a0;
+        td += a1;
+      }
+#pragma unroll
+      for (int i = 0; i < kWPerW; ++i) {
+        const bool kp = keep(i);
+        const uint32_t bk = __ballot_sync(0xffffffffu, kp);
+        const uint32_t bd = __ballot_sync(0xffffffffu, ix[i] >= 0 && !kp);
+        if (kp) {
+          const int p = bs + __popc(bk & lt);
+          sel_idx[p] = ix[i];
+          sel_val[p] = v[i];
+          for (int pp = 0; pp < npush; ++pp) {   // peers' copies (slot layout)
+            unsigned char* b = push_base[pp];
+            reinterpret_cast<int32_t*>(b + 16)[p] = ix[i];
+            reinterpret_cast<float*>(b + push_voff)[p] = v[i];
+          }
+        } else if (dis_idx && ix[i] >= 0) {
+          const int p = bdd + __popc(bd & lt);
+          dis_idx[p] = ix[i];
+          dis_val[p] = __fmul_rn(v[i], w);
+        }
+        bs += __popc(bk);
+        bdd += __popc(bd);
+      }
+      ks += ts;
+      kd += td;
+      __syncthreads();   // wsum is reused by the next round
     }
   }
   // ---- completion: the last CTA of the task writes the counts and publishes
-  if (npush > 0) __threadfence_system();
-  else __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (int)(atomicAdd(const_cast<uint32_t*>(&ws->wdone), 1u) == gridDim.x - 1);
+  if (tid == 0) {
+    if (npush > 0) __threadfence_system();
+    else __threadfence();
+    s_last = (int)(atomicAdd(const_cast<uint32_t*>(&ws->wdone), 1u) == gridDim.x - 1);
+  }
   __syncthreads();
   if (!s_last || tid != 0) return;
   const long long ns = ws->total_sel, nt = ws->total;
@@ -556,15 +672,11 @@ __global__ void __launch_bounds__(kWThreads) k_wsel_write(const SelTask* __restr
 int launch_wselect(const SelTask* tasks_dev, int ntask, int max_tiles, bool histogram,
                    cudaStream_t s) {
   if (ntask <= 0 || max_tiles <= 0) return 0;
-  int n = 0;
-  if (histogram) {
-    launch_pdl(k_wsel_hist, dim3((max_tiles + kWHistTiles - 1) / kWHistTiles, ntask),
-               dim3(kWThreads), 0, s, tasks_dev);
-    ++n;
-  }
+  (void)histogram;
+  launch_pdl(k_wsel_hist, dim3(max_tiles, ntask), dim3(kWThreads), 0, s, tasks_dev);
   launch_pdl(k_wsel_gather, dim3(max_tiles, ntask), dim3(kWThreads), 0, s, tasks_dev);
   launch_pdl(k_wsel_write, dim3(max_tiles, ntask), dim3(kWThreads), 0, s, tasks_dev);
-  return n + 2;
+  return 3;
 }
 
 int wsel_max_group() { return kWMaxGroup; }

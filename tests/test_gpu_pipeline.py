@@ -36,13 +36,14 @@ def configs():
 
 
 def _run(env, P, d, sag, residual, timing, kind, N, k, iters, seed, graph=True, scales=None,
-         carry_every=True):
+         carry_every=True, audit=True):
     sd, orc, torch = env
     from pyoracle import make_config
     cfg = sd.ClusterConfig(workers=P, dimension=N, k=k, teams=d, sag=sag, residual=residual,
                            timing=timing)
     ctx = sd.SparDL(cfg, device=0, graph=graph)
-    if residual != "lres":
+    audit = audit and residual != "lres"
+    if audit:
         ctx.set_audit(True)
     ref = orc.pipeline(make_config(P, N, k, d, sag, residual, timing))
     rng = np.random.default_rng(seed)
@@ -58,7 +59,7 @@ def _run(env, P, d, sag, residual, timing, kind, N, k, iters, seed, graph=True, 
         gi, gv = ctx.global_gradient(0)
         ri, rv = ref.global_gradient()
         assert info["consistent"] == 1, tag
-        if residual != "lres":   # the audit, bit for bit
+        if audit:   # the audit, bit for bit
             assert info["conservation_error"] == rinfo["conservation_error"], \
                 (tag, info["conservation_error"], rinfo["conservation_error"])
         assert np.array_equal(gi.cpu().numpy().astype(np.int64), ri), tag
@@ -208,3 +209,24 @@ def test_pipeline_residual_read_at_end(env, residual, P, d, sag, N, kind):
     residuals must match."""
     _run(env, P, d, sag, residual, "optimized", kind, N, P * (N // (P * 100)), iters=5,
          seed=31, carry_every=False)
+
+
+@pytest.mark.parametrize("mode", ["1", "2", "1|bulk"])
+@pytest.mark.parametrize("carry_every", [True, False])
+@pytest.mark.parametrize("P,d,sag,N,kind", [(8, 1, "none", 1_000_000, "gauss"),
+                                            (6, 1, "none", 300_007, "int"),
+                                            (8, 2, "rsag", 400_000, "gauss"),
+                                            (4, 1, "none", 100_003, "mixed"),
+                                            (1, 1, "none", 500_000, "gauss")])
+def test_pipeline_deferred_finalize(env, mode, carry_every, P, d, sag, N, kind, monkeypatch):
+    """The opt-in record forms of the gres finalize (SPARDL_FIN_DEFER, read
+    when a context is planned; the audit switches them off): records written
+    at the end of an iteration are applied by the next candidate pass (1, in
+    the register or the bulk-copy pass; residuals read only at the end) or by
+    the reader (residuals read every iteration, k_fin_apply), or at once (2).
+    All must give the reference's residuals bit for bit."""
+    monkeypatch.setenv("SPARDL_FIN_DEFER", mode.split("|")[0])
+    if mode.endswith("bulk"):
+        monkeypatch.setenv("SPARDL_DIV_BULK", "1")
+    _run(env, P, d, sag, "gres", "optimized", kind, N, P * (N // (P * 100)), iters=5, seed=41,
+         carry_every=carry_every, audit=False)
