@@ -155,73 +155,61 @@ inline std::int32_t idx32(Index i) {
 }  // namespace b200
 
 // Device selection; the entries returned carry the caller's own values.
+// top_k_select / merge_add run on the GPU in double (the reference's
+// semantics, spardl_topk_select_f64 / spardl_merge_add_f64); the values of
+// the outputs are the inputs' values (selection) or their a + b sums.
 inline TopKResult top_k_select(const SparseBlock& block, Index budget) {
   if (budget < 0) throw error("top_k_select: negative budget");
   TopKResult out;
   out.selected.block_id = out.discarded.block_id = block.block_id;
   out.selected.range = out.discarded.range = block.range;
   const size_t n = block.entries.size();
-  std::vector<std::int32_t> idx(n), si(n + 1), di(n + 1);
-  std::vector<float> val(n), sv(n + 1), dv(n + 1);
-  std::map<Index, double> orig;
+  std::vector<std::int64_t> idx(n);
+  std::vector<double> val(n);
   for (size_t e = 0; e < n; ++e) {
-    idx[e] = b200::idx32(block.entries[e].index);
-    val[e] = static_cast<float>(block.entries[e].value);
-    orig[block.entries[e].index] = block.entries[e].value;
+    idx[e] = block.entries[e].index;
+    val[e] = block.entries[e].value;
   }
-  std::int64_t ns = 0, nd = 0;
-  b200::check(spardl_topk_select_hostbuf(idx.data(), val.data(), static_cast<std::int64_t>(n),
-                                         budget, si.data(), sv.data(), &ns, di.data(), dv.data(),
-                                         &nd));
-  for (std::int64_t e = 0; e < ns; ++e) out.selected.entries.push_back({si[size_t(e)], orig[si[size_t(e)]]});
-  for (std::int64_t e = 0; e < nd; ++e) out.discarded.entries.push_back({di[size_t(e)], orig[di[size_t(e)]]});
+  std::vector<std::uint8_t> flag(n + 1, 0);
+  if (n > 0)
+    b200::check(spardl_topk_select_f64_hostbuf(idx.data(), val.data(),
+                                               static_cast<std::int64_t>(n), budget,
+                                               flag.data()));
+  for (size_t e = 0; e < n; ++e)
+    (flag[e] ? out.selected : out.discarded).entries.push_back(block.entries[e]);
   return out;
 }
 
+// The dense slice [lo, hi) as a block (every index an entry, zeros
+// included, inc/sparse.hpp:167-177), selected on the GPU.
 inline TopKResult top_k_select_slice(const GradientVector& g, int block_id,
                                      const IndexRange& range, Index budget) {
-  if (budget < 0) throw error("top_k_select: negative budget");
-  std::vector<float> gf(static_cast<size_t>(range.hi));
-  for (Index i = range.lo; i < range.hi; ++i) gf[size_t(i)] = static_cast<float>(g[i]);
-  const size_t n = static_cast<size_t>(range.size());
-  std::vector<std::int32_t> si(n + 1);
-  std::vector<float> sv(n + 1);
-  std::int64_t ns = 0;
-  b200::check(spardl_topk_select_slice_hostbuf(gf.data(), range.lo, range.hi, budget, si.data(),
-                                               sv.data(), &ns));
-  TopKResult out;
-  out.selected.block_id = out.discarded.block_id = block_id;
-  out.selected.range = out.discarded.range = range;
-  std::vector<char> taken(n, 0);
-  for (std::int64_t e = 0; e < ns; ++e) {
-    const Index i = si[size_t(e)];
-    out.selected.entries.push_back({i, g[i]});
-    taken[size_t(i - range.lo)] = 1;
-  }
-  for (Index i = range.lo; i < range.hi; ++i)
-    if (!taken[size_t(i - range.lo)]) out.discarded.entries.push_back({i, g[i]});
-  return out;
+  SparseBlock block;
+  block.block_id = block_id;
+  block.range = range;
+  block.entries.reserve(static_cast<size_t>(range.size()));
+  for (Index i = range.lo; i < range.hi; ++i) block.entries.push_back({i, g[i]});
+  return top_k_select(block, budget);
 }
 
-// Device merge: values summed in fp32 (exact for fp32-representable sums).
 inline SparseBlock merge_add(const SparseBlock& a, const SparseBlock& b) {
   if (a.block_id != b.block_id)
     throw block_mismatch_error("merge_add: block ids differ (" + std::to_string(a.block_id) +
                                " vs " + std::to_string(b.block_id) + ")");
-  std::vector<std::int32_t> ai, bi;
-  std::vector<float> av, bv;
-  for (const Entry& e : a.entries) ai.push_back(b200::idx32(e.index)), av.push_back(float(e.value));
-  for (const Entry& e : b.entries) bi.push_back(b200::idx32(e.index)), bv.push_back(float(e.value));
-  const std::int32_t* ip[2] = {ai.data(), bi.data()};
-  const float* vp[2] = {av.data(), bv.data()};
-  const std::int64_t ns[2] = {std::int64_t(ai.size()), std::int64_t(bi.size())};
-  std::vector<std::int32_t> oi(ai.size() + bi.size() + 1);
-  std::vector<float> ov(oi.size());
+  std::vector<std::int64_t> ai, bi;
+  std::vector<double> av, bv;
+  for (const Entry& e : a.entries) ai.push_back(e.index), av.push_back(e.value);
+  for (const Entry& e : b.entries) bi.push_back(e.index), bv.push_back(e.value);
+  std::vector<std::int64_t> oi(ai.size() + bi.size() + 1);
+  std::vector<double> ov(oi.size());
   std::int64_t no = 0;
-  b200::check(spardl_merge_add_hostbuf(2, ip, vp, ns, oi.data(), ov.data(), &no));
+  b200::check(spardl_merge_add_f64_hostbuf(ai.data(), av.data(), std::int64_t(ai.size()),
+                                           bi.data(), bv.data(), std::int64_t(bi.size()),
+                                           oi.data(), ov.data(), &no));
   SparseBlock out;
   out.block_id = a.block_id;
   out.range = a.range;
+  out.entries.reserve(static_cast<size_t>(no));
   for (std::int64_t e = 0; e < no; ++e) out.entries.push_back({oi[size_t(e)], ov[size_t(e)]});
   return out;
 }
@@ -342,6 +330,106 @@ inline void write_ledger_csv(std::ostream& os, const Fabric& fabric) {
        << '\n';
 }
 
+// ---------------------------------------------------------------- inc/collectives.hpp
+// Host-side gathers over the drop-in Fabric (the reference's alpha-beta
+// ledger).  The pipeline's own gathers run GPU to GPU (spardl_all_reduce);
+// these are the component forms its callers and tests drive.
+struct GroupGather {
+  std::vector<WorkerId> workers;
+  std::vector<SparseBlock> blocks;   // blocks[i] belongs to workers[i]
+};
+// result[i][s]: the block of group member s as held by member i
+using GatherResult = std::vector<std::vector<SparseBlock>>;
+
+namespace detail {
+// inc/collectives.hpp:46-114: Bruck all-gather of several disjoint groups
+// in shared rounds.  Member i keeps its blocks in rotated order (its own
+// first); at distance 2^t it sends its first min(2^t, m - 2^t) blocks to
+// member i - 2^t and appends what member i + 2^t sent; the final un-rotation
+// is local.
+inline std::vector<GatherResult> bruck_all_gather_multi(Fabric& fabric,
+                                                        const std::vector<GroupGather>& groups) {
+  std::vector<std::vector<std::vector<SparseBlock>>> rot(groups.size());
+  int rounds = 0;
+  for (size_t g = 0; g < groups.size(); ++g) {
+    const size_t m = groups[g].workers.size();
+    if (m == 0) throw group_size_error("all-gather on empty group");
+    if (groups[g].blocks.size() != m) throw group_size_error("group has blocks != workers");
+    for (size_t i = 0; i < m; ++i) rot[g].push_back({groups[g].blocks[i]});
+    rounds = std::max(rounds, ceil_log2(static_cast<std::int64_t>(m)));
+  }
+  for (int t = 0; t < rounds; ++t) {
+    const int dist = 1 << t;
+    Fabric::RoundPlan plan(size_t(fabric.worker_count()));
+    for (size_t g = 0; g < groups.size(); ++g) {
+      const int m = static_cast<int>(groups[g].workers.size());
+      if (dist >= m) continue;
+      const int cnt = std::min(dist, m - dist);
+      for (int i = 0; i < m; ++i) {
+        Fabric::Send snd;
+        snd.target = groups[g].workers[size_t((i - dist + m) % m)];
+        snd.payload.assign(rot[g][size_t(i)].begin(), rot[g][size_t(i)].begin() + cnt);
+        plan[size_t(groups[g].workers[size_t(i)])] = std::move(snd);
+      }
+    }
+    auto inbox = fabric.exchange(std::move(plan));
+    for (size_t g = 0; g < groups.size(); ++g) {
+      const int m = static_cast<int>(groups[g].workers.size());
+      if (dist >= m) continue;
+      for (int i = 0; i < m; ++i)
+        for (SparseBlock& b : inbox[size_t(groups[g].workers[size_t(i)])])
+          rot[g][size_t(i)].push_back(std::move(b));
+    }
+  }
+  std::vector<GatherResult> out(groups.size());
+  for (size_t g = 0; g < groups.size(); ++g) {
+    const int m = static_cast<int>(groups[g].workers.size());
+    out[g].assign(size_t(m), std::vector<SparseBlock>(size_t(m)));
+    for (int i = 0; i < m; ++i)
+      for (int q = 0; q < m; ++q)   // rotated slot q holds source (i + q) mod m
+        out[g][size_t(i)][size_t((i + q) % m)] = std::move(rot[g][size_t(i)][size_t(q)]);
+  }
+  return out;
+}
+}  // namespace detail
+
+inline GatherResult bruck_all_gather(Fabric& fabric, const std::vector<WorkerId>& workers,
+                                     const std::vector<SparseBlock>& blocks) {
+  return detail::bruck_all_gather_multi(fabric, {GroupGather{workers, blocks}})[0];
+}
+
+// inc/collectives.hpp:130-178: pairwise XOR exchange of everything held,
+// power-of-two groups only; same result as bruck_all_gather.
+inline GatherResult recursive_doubling_all_gather(Fabric& fabric,
+                                                  const std::vector<WorkerId>& workers,
+                                                  const std::vector<SparseBlock>& blocks) {
+  const int m = static_cast<int>(workers.size());
+  if (m == 0) throw group_size_error("all-gather on empty group");
+  if (!is_power_of_two(m))
+    throw group_size_error("recursive doubling requires a power-of-two group, got m=" +
+                           std::to_string(m));
+  if (blocks.size() != workers.size()) throw group_size_error("group has blocks != workers");
+  GatherResult have(static_cast<size_t>(m), std::vector<SparseBlock>(static_cast<size_t>(m)));
+  for (int i = 0; i < m; ++i) have[size_t(i)][size_t(i)] = blocks[size_t(i)];
+  for (int dist = 1; dist < m; dist <<= 1) {
+    Fabric::RoundPlan plan(size_t(fabric.worker_count()));
+    for (int i = 0; i < m; ++i) {   // i holds the aligned run of `dist` slots around i
+      Fabric::Send snd;
+      snd.target = workers[size_t(i ^ dist)];
+      const int base = i & ~(dist - 1);
+      snd.payload.assign(have[size_t(i)].begin() + base, have[size_t(i)].begin() + base + dist);
+      plan[size_t(workers[size_t(i)])] = std::move(snd);
+    }
+    auto inbox = fabric.exchange(std::move(plan));
+    for (int i = 0; i < m; ++i) {
+      const int base = (i ^ dist) & ~(dist - 1);
+      auto& got = inbox[size_t(workers[size_t(i)])];
+      for (int q = 0; q < dist; ++q) have[size_t(i)][size_t(base + q)] = std::move(got[size_t(q)]);
+    }
+  }
+  return have;
+}
+
 // ---------------------------------------------------------------- inc/reduce_scatter.hpp
 enum class SrsTiming { optimized, naive };
 
@@ -382,6 +470,120 @@ inline SrsCost expected_cost_srs(std::int64_t m, std::int64_t k) {
   SrsCost c;
   b200::check(spardl_expected_cost_srs(m, k, &c.rounds, &c.scalars));
   return c;
+}
+
+// The reduce-scatter schedule as a component (the tests and callers that
+// drive their own phases): blocks move through the host Fabric (its ledger
+// is the reference's), every merge and selection runs on the GPU (fp64
+// components).  The pipeline's own reduce-scatter is planned once and runs
+// on the device (spardl_all_reduce).
+using DiscardSink = std::function<void(WorkerId, int, const SparseBlock&, double)>;
+inline DiscardSink null_discard_sink() {
+  return [](WorkerId, int, const SparseBlock&, double) {};
+}
+
+struct SrsTeam {
+  std::vector<WorkerId> workers;                  // team rank = position here
+  std::vector<std::vector<SparseBlock>> blocks;   // blocks[i][b]: member i, position b
+};
+
+namespace b200 {
+// a held block back within the budget; the cut goes to the discard sink
+inline void srs_sparsify(std::optional<SparseBlock>& slot, Index budget, WorkerId w,
+                         const DiscardSink& sink) {
+  if (!slot || slot->nnz() <= budget) return;
+  TopKResult r = top_k_select(*slot, budget);
+  if (!r.discarded.empty()) sink(w, r.discarded.block_id, r.discarded, 1.0);
+  *slot = std::move(r.selected);
+}
+}  // namespace b200
+
+// inc/reduce_scatter.hpp:120-236 (Spar-Reduce-Scatter of every team in
+// lockstep); returns each team's preservation blocks, team-rank order.
+inline std::vector<std::vector<SparseBlock>> run_srs_teams(
+    Fabric& fabric, std::vector<SrsTeam> teams, Index budget,
+    SrsTiming timing = SrsTiming::optimized, const DiscardSink& on_discard = null_discard_sink()) {
+  if (teams.empty()) throw group_size_error("reduce-scatter with no teams");
+  const int m = static_cast<int>(teams[0].workers.size());
+  for (const SrsTeam& t : teams)
+    if (static_cast<int>(t.workers.size()) != m)
+      throw group_size_error("reduce-scatter teams must share one size");
+  const int l = ceil_log2(m);
+  // held[t][i][b]: what member i of team t holds of position b
+  std::vector<std::vector<std::vector<std::optional<SparseBlock>>>> held(teams.size());
+  std::vector<BagSchedule> bags;
+  for (int i = 0; i < m; ++i) bags.push_back(build_bags(m, i));
+  for (size_t t = 0; t < teams.size(); ++t) {
+    held[t].resize(size_t(m));
+    for (int i = 0; i < m; ++i) {
+      auto& mine = teams[t].blocks[size_t(i)];
+      if (static_cast<int>(mine.size()) != m)
+        throw config_error("reduce-scatter: member needs one block per position");
+      held[t][size_t(i)].resize(size_t(m));
+      for (int b = 0; b < m; ++b) {
+        if (mine[size_t(b)].nnz() > budget)
+          throw config_error(
+              "reduce-scatter: initial block exceeds budget; sparsify during dividing first");
+        held[t][size_t(i)][size_t(b)] = std::move(mine[size_t(b)]);
+      }
+    }
+  }
+  for (int s = 1; s <= l; ++s) {
+    const int dist = 1 << (l - s);
+    const int bag = l - s;   // index of B_{l-s+1}
+    Fabric::RoundPlan plan(size_t(fabric.worker_count()));
+    for (size_t t = 0; t < teams.size(); ++t)
+      for (int i = 0; i < m; ++i) {
+        Fabric::Send snd;
+        snd.target = teams[t].workers[size_t((i + dist) % m)];
+        for (int pos : bags[size_t(i)].sending_bags[size_t(bag)]) {
+          auto& slot = held[t][size_t(i)][size_t(pos)];
+          if (!slot) throw theorem_violation_error("sending a block already given up");
+          if (slot->nnz() > budget) throw error("budget discipline violated before send");
+          snd.payload.push_back(std::move(*slot));
+          slot.reset();
+        }
+        plan[size_t(teams[t].workers[size_t(i)])] = std::move(snd);
+      }
+    auto inbox = fabric.exchange(std::move(plan));
+    for (size_t t = 0; t < teams.size(); ++t)
+      for (int i = 0; i < m; ++i) {
+        const WorkerId self = teams[t].workers[size_t(i)];
+        auto& row = held[t][size_t(i)];
+        for (SparseBlock& got : inbox[size_t(self)]) {
+          if (got.block_id < 0 || got.block_id >= m)
+            throw theorem_violation_error("received block id out of range");
+          auto& slot = row[size_t(got.block_id)];
+          if (!slot)
+            throw theorem_violation_error("received block " + std::to_string(got.block_id) +
+                                          " not held by worker " + std::to_string(self));
+          *slot = merge_add(*slot, got);
+        }
+        if (timing == SrsTiming::naive) {
+          for (auto& slot : row) b200::srs_sparsify(slot, budget, self, on_discard);
+        } else if (s < l) {   // only the next bag must be back in budget
+          for (int pos : bags[size_t(i)].sending_bags[size_t(bag - 1)])
+            b200::srs_sparsify(row[size_t(pos)], budget, self, on_discard);
+        }
+      }
+  }
+  std::vector<std::vector<SparseBlock>> out(teams.size());
+  for (size_t t = 0; t < teams.size(); ++t)
+    for (int i = 0; i < m; ++i) {
+      auto& kept = held[t][size_t(i)][size_t(bags[size_t(i)].preservation)];
+      if (!kept) throw error("preservation block missing after reduce-scatter");
+      b200::srs_sparsify(kept, budget, teams[t].workers[size_t(i)], on_discard);
+      out[t].push_back(std::move(*kept));
+    }
+  return out;
+}
+
+inline std::vector<SparseBlock> run_srs(Fabric& fabric, std::vector<WorkerId> workers,
+                                        std::vector<std::vector<SparseBlock>> blocks,
+                                        Index budget, SrsTiming timing = SrsTiming::optimized,
+                                        const DiscardSink& on_discard = null_discard_sink()) {
+  std::vector<SrsTeam> teams{{std::move(workers), std::move(blocks)}};
+  return run_srs_teams(fabric, std::move(teams), budget, timing, on_discard)[0];
 }
 
 // ---------------------------------------------------------------- inc/sag.hpp
@@ -444,11 +646,130 @@ inline CostRange topka_cost(std::int64_t workers, std::int64_t k) {
   return c;
 }
 
+// inc/sag.hpp:98-270: the team synchronisations as components (host
+// Fabric, GPU merges and selections; see run_srs_teams).
+struct PositionGroup {
+  std::vector<WorkerId> workers;
+  std::vector<SparseBlock> blocks;   // blocks[i] belongs to workers[i]
+};
+
+// R-SAG: log2 d rounds of XOR-partner swaps; each side merges the partner's
+// block into its own and selects back to the budget, the discard shared
+// 1/(2 dist) ways (inc/sag.hpp:125-173).
+inline std::vector<std::vector<SparseBlock>> rsag_groups(
+    Fabric& fabric, std::vector<PositionGroup> groups, Index budget,
+    const DiscardSink& on_discard = null_discard_sink()) {
+  if (groups.empty()) throw group_size_error("rsag with no groups");
+  const int d = static_cast<int>(groups[0].workers.size());
+  if (d < 2 || !is_power_of_two(d))
+    throw group_size_error("rsag requires a power-of-two team count >= 2");
+  for (const PositionGroup& g : groups)
+    if (static_cast<int>(g.workers.size()) != d || g.blocks.size() != g.workers.size())
+      throw group_size_error("rsag groups must share one size");
+  for (int dist = 1; dist < d; dist <<= 1) {
+    Fabric::RoundPlan plan(size_t(fabric.worker_count()));
+    for (const PositionGroup& g : groups)
+      for (int i = 0; i < d; ++i) {
+        Fabric::Send snd;
+        snd.target = g.workers[size_t(i ^ dist)];
+        snd.payload = {g.blocks[size_t(i)]};
+        plan[size_t(g.workers[size_t(i)])] = std::move(snd);
+      }
+    auto inbox = fabric.exchange(std::move(plan));
+    const double share = 1.0 / static_cast<double>(2 * dist);
+    for (PositionGroup& g : groups)
+      for (int i = 0; i < d; ++i) {
+        const WorkerId self = g.workers[size_t(i)];
+        SparseBlock merged = merge_add(g.blocks[size_t(i)], inbox[size_t(self)].at(0));
+        if (merged.nnz() > budget) {
+          TopKResult r = top_k_select(merged, budget);
+          on_discard(self, r.discarded.block_id, r.discarded, share);
+          merged = std::move(r.selected);
+        }
+        g.blocks[size_t(i)] = std::move(merged);
+      }
+  }
+  std::vector<std::vector<SparseBlock>> out;
+  for (PositionGroup& g : groups) out.push_back(std::move(g.blocks));
+  return out;
+}
+
+struct BsagGroupResult {
+  std::vector<SparseBlock> blocks;   // identical on every member
+  std::int64_t union_size = 0;       // N_t before the final selection
+};
+
+// B-SAG: every member pre-selects its block to h (the rest its own
+// discard), the h-blocks are Bruck-gathered unmerged, every member folds
+// them in source order and selects the identical union to the budget with
+// its dyadic share of the discard (inc/sag.hpp:189-249).
+inline std::vector<BsagGroupResult> bsag_groups(
+    Fabric& fabric, std::vector<PositionGroup> groups, const std::vector<Index>& pre_budgets,
+    Index budget, const DiscardSink& on_discard = null_discard_sink()) {
+  if (groups.empty()) throw group_size_error("bsag with no groups");
+  if (pre_budgets.size() != groups.size())
+    throw config_error("bsag: one pre-selection budget per group");
+  const int d = static_cast<int>(groups[0].workers.size());
+  if (d < 2) throw group_size_error("bsag requires >= 2 teams");
+  for (const PositionGroup& g : groups)
+    if (static_cast<int>(g.workers.size()) != d || g.blocks.size() != g.workers.size())
+      throw group_size_error("bsag groups must share one size");
+  std::vector<GroupGather> gathers;
+  for (size_t q = 0; q < groups.size(); ++q) {
+    GroupGather gg;
+    gg.workers = groups[q].workers;
+    for (int i = 0; i < d; ++i) {
+      SparseBlock& blk = groups[q].blocks[size_t(i)];
+      if (blk.nnz() > pre_budgets[q]) {
+        TopKResult r = top_k_select(blk, pre_budgets[q]);
+        on_discard(groups[q].workers[size_t(i)], r.discarded.block_id, r.discarded, 1.0);
+        blk = std::move(r.selected);
+      }
+      gg.blocks.push_back(std::move(blk));
+    }
+    gathers.push_back(std::move(gg));
+  }
+  auto got = detail::bruck_all_gather_multi(fabric, gathers);
+  const std::vector<double> shares = dyadic_shares(d);
+  std::vector<BsagGroupResult> out(groups.size());
+  for (size_t q = 0; q < groups.size(); ++q)
+    for (int i = 0; i < d; ++i) {
+      SparseBlock acc = got[q][size_t(i)][0];
+      for (int src = 1; src < d; ++src) acc = merge_add(acc, got[q][size_t(i)][size_t(src)]);
+      out[q].union_size = acc.nnz();
+      if (acc.nnz() > budget) {
+        TopKResult r = top_k_select(acc, budget);
+        on_discard(groups[q].workers[size_t(i)], r.discarded.block_id, r.discarded,
+                   shares[size_t(i)]);
+        acc = std::move(r.selected);
+      }
+      out[q].blocks.push_back(std::move(acc));
+    }
+  return out;
+}
+
+inline std::vector<SparseBlock> rsag(Fabric& fabric, std::vector<WorkerId> workers,
+                                     std::vector<SparseBlock> blocks, Index budget,
+                                     const DiscardSink& on_discard = null_discard_sink()) {
+  std::vector<PositionGroup> groups{{std::move(workers), std::move(blocks)}};
+  return rsag_groups(fabric, std::move(groups), budget, on_discard)[0];
+}
+
+inline BsagGroupResult bsag(Fabric& fabric, std::vector<WorkerId> workers,
+                            std::vector<SparseBlock> blocks, Index pre_budget, Index budget,
+                            const DiscardSink& on_discard = null_discard_sink()) {
+  std::vector<PositionGroup> groups{{std::move(workers), std::move(blocks)}};
+  return bsag_groups(fabric, std::move(groups), {pre_budget}, budget, on_discard)[0];
+}
+
 // ---------------------------------------------------------------- inc/residual.hpp
 enum class ResidualMode { gres, pres, lres };
 
-// Host view of a worker's residual; the authoritative copy lives on the GPU
-// and is mirrored here after every spardl_all_reduce.
+// inc/residual.hpp:52-177: a worker's residual state.  The pipeline keeps
+// the authoritative carry on the GPU (in place: the carry buffer is G_copy)
+// and mirrors it here after every spardl_all_reduce; the member functions
+// are the reference's per-iteration protocol for callers that run the
+// phases themselves (merges on the GPU in double, spardl_merge_add_f64).
 class ResidualStore {
  public:
   ResidualStore(ResidualMode mode, Index n) : mode_(mode), n_(n), carry_(n) {}
@@ -457,11 +778,102 @@ class ResidualStore {
   const GradientVector& carry() const { return carry_; }
   GradientVector& mutable_carry() { return carry_; }
 
+  // combined = g + carry; the carry is consumed (inc/residual.hpp:63-71)
+  GradientVector apply(const GradientVector& gradients) {
+    if (gradients.size() != n_) throw config_error("apply_residual: dimension mismatch");
+    GradientVector combined = gradients;
+    for (Index i = 0; i < n_; ++i) combined[i] += carry_[i];
+    carry_ = GradientVector(n_);
+    return combined;
+  }
+
+  // G_copy := combined, per-block discard accumulators reset (:75-92)
+  void begin_iteration(const GradientVector& combined, const BlockPartition& part) {
+    if (in_iteration_) throw state_error("begin_iteration called twice without finalize");
+    if (combined.size() != n_ || part.n != n_)
+      throw config_error("begin_iteration: dimension mismatch");
+    g_copy_ = combined;
+    part_ = part;
+    xi_.assign(size_t(part.block_count), SparseBlock{});
+    for (int b = 0; b < part.block_count; ++b) {
+      xi_[size_t(b)].block_id = b;
+      xi_[size_t(b)].range = part.range_of(b);
+    }
+    remainder_ = GradientVector(n_);
+    in_iteration_ = true;
+  }
+
+  // the dividing selection's leftovers, the lres carry (:96-99)
+  void record_dividing_remainder(const SparseBlock& remainder) {
+    require("record_dividing_remainder");
+    for (const Entry& e : remainder.entries) remainder_[e.index] = e.value;
+  }
+
+  // xi[b] += weight * discarded (:104-124)
+  void record_inproc(int block_id, const SparseBlock& discarded, double weight) {
+    require("record_inproc");
+    if (block_id < 0 || block_id >= part_.block_count)
+      throw config_error("record_inproc: unknown block id");
+    if (weight <= 0.0 || weight > 1.0)
+      throw config_error("record_inproc: weight must be in (0, 1]");
+    SparseBlock& acc = xi_[size_t(block_id)];
+    for (const Entry& e : discarded.entries)
+      if (!acc.range.contains(e.index))
+        throw config_error("record_inproc: index " + std::to_string(e.index) +
+                           " outside block range");
+    SparseBlock w = scale(discarded, weight);
+    w.block_id = block_id;
+    w.range = acc.range;
+    acc = merge_add(acc, w);
+  }
+
+  // the carry of the next iteration (:128-150)
+  const GradientVector& finalize(const GlobalSparseGradient& final_global) {
+    require("finalize");
+    if (mode_ == ResidualMode::lres) {
+      carry_ = remainder_;
+    } else {
+      carry_ = g_copy_;
+      for (const Entry& e : final_global.entries)
+        carry_[e.index] = mode_ == ResidualMode::gres ? xi_value(e.index) : 0.0;
+    }
+    in_iteration_ = false;
+    return carry_;
+  }
+
+  // the in-procedure accumulator at one index, 0 when absent (:153-160)
+  double xi_value(Index index) const {
+    const SparseBlock& acc = xi_[size_t(part_.block_of(index))];
+    auto it = std::lower_bound(acc.entries.begin(), acc.entries.end(), index,
+                               [](const Entry& e, Index i) { return e.index < i; });
+    return it != acc.entries.end() && it->index == index ? it->value : 0.0;
+  }
+
  private:
+  void require(const char* op) const {
+    if (!in_iteration_) throw state_error(std::string(op) + " outside an iteration");
+  }
   ResidualMode mode_;
   Index n_;
   GradientVector carry_;
+  GradientVector g_copy_;
+  GradientVector remainder_;
+  std::vector<SparseBlock> xi_;
+  BlockPartition part_;
+  bool in_iteration_ = false;
 };
+
+inline GradientVector apply_residual(const GradientVector& gradients, ResidualStore& store) {
+  return store.apply(gradients);
+}
+inline void record_inproc(ResidualStore& store, int block_id, const SparseBlock& discarded,
+                          double weight) {
+  store.record_inproc(block_id, discarded, weight);
+}
+inline const GradientVector& finalize(ResidualStore& store,
+                                      const GlobalSparseGradient& final_global) {
+  return store.finalize(final_global);
+}
 
 // ---------------------------------------------------------------- inc/pipeline.hpp
 struct ClusterConfig {
@@ -687,10 +1099,10 @@ inline void write_controller_trace_row(std::ostream& os, std::int64_t iter, cons
      << c.target() << '\n';
 }
 
-// inc/collectives.hpp:185-216: the Top-k All-Gather baseline.  Local top-k
-// and the source-ordered merge fold run on the GPU (spardl_topk_select_slice,
-// spardl_merge_add); the ledger is the Bruck all-gather's: every worker
-// receives the P-1 other selections in ceil(log2 P) rounds.
+// inc/collectives.hpp:185-216: the Top-k All-Gather baseline -- local top-k
+// on the GPU, Bruck all-gather over the Fabric, source-ordered merge fold on
+// the GPU (a worker receives 2(P-1)k scalars in ceil(log2 P) rounds).  The
+// GPU-resident form for real gradients is paper_2304_00737_b200.topka.
 inline std::vector<GlobalSparseGradient> topka_baseline(Fabric& fabric,
                                                         const std::vector<GradientVector>& gradients,
                                                         Index k) {
@@ -699,27 +1111,36 @@ inline std::vector<GlobalSparseGradient> topka_baseline(Fabric& fabric,
     throw config_error("topka: gradient count != worker count");
   const Index n = gradients[0].size();
   if (k > n) throw config_error("topka: k must satisfy k <= N");
-  std::vector<SparseBlock> locals(static_cast<size_t>(p));
-  for (int w = 0; w < p; ++w)
-    locals[size_t(w)] = top_k_select_slice(gradients[size_t(w)], 0, {0, n}, k).selected;
-  SparseBlock acc;
-  acc.block_id = 0;
-  acc.range = {0, n};
-  for (int s = 0; s < p; ++s) acc = merge_add(acc, locals[size_t(s)]);
-  int rounds = 0;
-  while ((1 << rounds) < p) ++rounds;
-  auto& led = fabric.mutable_ledger();
+  std::vector<WorkerId> group;
+  std::vector<SparseBlock> locals;
   for (int w = 0; w < p; ++w) {
-    led[size_t(w)].rounds += rounds;
-    for (int s = 0; s < p; ++s)
-      if (s != w) led[size_t(w)].scalars_received += 2 * locals[size_t(s)].nnz();
+    group.push_back(w);
+    locals.push_back(top_k_select_slice(gradients[size_t(w)], 0, {0, n}, k).selected);
   }
+  const GatherResult got = bruck_all_gather(fabric, group, locals);
   std::vector<GlobalSparseGradient> out(static_cast<size_t>(p));
-  for (auto& o : out) {
-    o.n = n;
-    o.entries = acc.entries;
+  for (int w = 0; w < p; ++w) {
+    SparseBlock acc;
+    acc.block_id = 0;
+    acc.range = {0, n};
+    for (int s = 0; s < p; ++s) acc = merge_add(acc, got[size_t(w)][size_t(s)]);
+    out[size_t(w)].n = n;
+    out[size_t(w)].entries = std::move(acc.entries);
   }
   return out;
+}
+
+// inc/collectives.hpp:221-234: the dense element-wise sum in worker order,
+// the reference's correctness oracle and dense baseline (no Fabric cost).
+// A test utility: the dense all-reduce on B200 is NCCL's (bench.py context).
+inline GradientVector dense_all_reduce_reference(const std::vector<GradientVector>& gradients) {
+  if (gradients.empty()) throw group_size_error("all-reduce on empty group");
+  GradientVector sum(gradients[0].size());
+  for (const GradientVector& g : gradients) {
+    if (g.size() != sum.size()) throw config_error("dense all-reduce: dimension mismatch");
+    for (Index i = 0; i < sum.size(); ++i) sum[i] += g[i];
+  }
+  return sum;
 }
 
 }  // namespace spardl

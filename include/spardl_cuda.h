@@ -148,6 +148,22 @@ int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* const* v
 
 /* The same three components on HOST buffers (staged through the device by
  * the library; synchronous).  Used by the C++ drop-in shim. */
+/* fp64 forms (the C++ drop-in surface, include/spardl/): the reference's
+ * double semantics.  top_k_select: flag[i] = 1 for the min(budget, n)
+ * entries first in (|val| desc, idx asc), inc/sparse.hpp:136-162; merge_add
+ * of two index-sorted lists, coinciding indices summed a + b,
+ * inc/sparse.hpp:182-208.  Device pointers (stream-ordered, synchronising)
+ * and host-buffer variants. */
+int spardl_topk_select_f64(const int64_t* idx, const double* val, int64_t n, int64_t budget,
+                           uint8_t* flag, void* stream);
+int spardl_merge_add_f64(const int64_t* ai, const double* av, int64_t na, const int64_t* bi,
+                         const double* bv, int64_t nb, int64_t* oi, double* ov, int64_t* n_out,
+                         void* stream);
+int spardl_topk_select_f64_hostbuf(const int64_t* idx, const double* val, int64_t n,
+                                   int64_t budget, uint8_t* flag);
+int spardl_merge_add_f64_hostbuf(const int64_t* ai, const double* av, int64_t na,
+                                 const int64_t* bi, const double* bv, int64_t nb, int64_t* oi,
+                                 double* ov, int64_t* n_out);
 int spardl_topk_select_hostbuf(const int32_t* idx, const float* val, int64_t n, int64_t budget,
                                int32_t* sel_idx, float* sel_val, int64_t* n_sel,
                                int32_t* dis_idx, float* dis_val, int64_t* n_dis);

@@ -133,7 +133,8 @@ EXPORTS = [
     "spardl_expected_cost_sag", "spardl_bsag_phase_cost", "spardl_topka_cost",
     "spardl_dyadic_shares", "spardl_hctrl_init", "spardl_hctrl_observe", "spardl_hctrl_budget",
     "spardl_topk_select", "spardl_topk_select_slice", "spardl_merge_add",
-    "spardl_topk_select_hostbuf", "spardl_topk_select_slice_hostbuf", "spardl_merge_add_hostbuf",
+    "spardl_topk_select_f64", "spardl_merge_add_f64", "spardl_topk_select_f64_hostbuf",
+    "spardl_merge_add_f64_hostbuf", "spardl_topk_select_hostbuf", "spardl_topk_select_slice_hostbuf", "spardl_merge_add_hostbuf",
     "spardl_nccl_unique_id", "spardl_ctx_create", "spardl_ctx_destroy", "spardl_plan_ops",
     "spardl_ctx_local_workers", "spardl_ctx_set_graph", "spardl_ctx_set_audit",
     "spardl_allreduce", "spardl_allreduce_host", "spardl_profile", "spardl_sync",

@@ -541,6 +541,84 @@ EXPORT int spardl_merge_add_hostbuf(int32_t r, const int32_t* const* idx, const 
 }
 
 // ---------------------------------------------------------------------------
+// fp64 components (the C++ drop-in surface keeps the reference's double
+// semantics for its one-shot component calls; components64.cu)
+EXPORT int spardl_topk_select_f64(const int64_t* idx, const double* val, int64_t n,
+                                  int64_t budget, uint8_t* flag, void* stream) {
+  return guarded([&] {   // inc/sparse.hpp:136-162
+    require_device();
+    if (budget < 0) sdlh::fail(SPARDL_E_ERROR, "top_k_select: negative budget");
+    if (n < 0 || n >= (int64_t(1) << 31)) sdlh::fail(SPARDL_E_ARG, "n out of range");
+    DeviceOf on(val);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    sdl::launch_topk64(idx, val, static_cast<int>(n), budget, flag, s);
+    CK(sdl::take_launch_error());
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+EXPORT int spardl_merge_add_f64(const int64_t* ai, const double* av, int64_t na,
+                                const int64_t* bi, const double* bv, int64_t nb, int64_t* oi,
+                                double* ov, int64_t* n_out, void* stream) {
+  return guarded([&] {   // inc/sparse.hpp:182-208
+    require_device();
+    if (na < 0 || nb < 0 || na + nb >= (int64_t(1) << 31)) sdlh::fail(SPARDL_E_ARG, "n out of range");
+    DeviceOf on(oi);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DevBuf buf(s);
+    const size_t n = static_cast<size_t>(na + nb) + 1;
+    int64_t* ti = buf.get<int64_t>(n);
+    double* tv = buf.get<double>(n);
+    int64_t* no = buf.get<int64_t>(1);
+    sdl::launch_merge64(ai, av, static_cast<int>(na), bi, bv, static_cast<int>(nb), ti, tv, oi,
+                        ov, no, s);
+    CK(sdl::take_launch_error());
+    CK(cudaMemcpyAsync(n_out, no, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+EXPORT int spardl_topk_select_f64_hostbuf(const int64_t* idx, const double* val, int64_t n,
+                                          int64_t budget, uint8_t* flag) {
+  int rc = SPARDL_OK;
+  const int outer = guarded([&] {
+    require_device();
+    DevBuf buf(nullptr);
+    const size_t un = static_cast<size_t>(n < 0 ? 0 : n);
+    const int64_t* di = to_dev(buf, idx, un);
+    const double* dv = to_dev(buf, val, un);
+    uint8_t* df = buf.get<uint8_t>(un + 1);
+    rc = spardl_topk_select_f64(di, dv, n, budget, df, nullptr);
+    if (rc != SPARDL_OK) return;
+    to_host(flag, df, un);
+  });
+  return rc != SPARDL_OK ? rc : outer;
+}
+
+EXPORT int spardl_merge_add_f64_hostbuf(const int64_t* ai, const double* av, int64_t na,
+                                        const int64_t* bi, const double* bv, int64_t nb,
+                                        int64_t* oi, double* ov, int64_t* n_out) {
+  int rc = SPARDL_OK;
+  const int outer = guarded([&] {
+    require_device();
+    DevBuf buf(nullptr);
+    const int64_t* dai = to_dev(buf, ai, static_cast<size_t>(na));
+    const double* dav = to_dev(buf, av, static_cast<size_t>(na));
+    const int64_t* dbi = to_dev(buf, bi, static_cast<size_t>(nb));
+    const double* dbv = to_dev(buf, bv, static_cast<size_t>(nb));
+    int64_t* doi = buf.get<int64_t>(static_cast<size_t>(na + nb) + 1);
+    double* dov = buf.get<double>(static_cast<size_t>(na + nb) + 1);
+    int64_t no = 0;
+    rc = spardl_merge_add_f64(dai, dav, na, dbi, dbv, nb, doi, dov, &no, nullptr);
+    if (rc != SPARDL_OK) return;
+    to_host(oi, doi, static_cast<size_t>(no));
+    to_host(ov, dov, static_cast<size_t>(no));
+    *n_out = no;
+  });
+  return rc != SPARDL_OK ? rc : outer;
+}
+
+// ---------------------------------------------------------------------------
 // pipeline context
 struct spardl_ctx {
   std::unique_ptr<sdle::Engine> eng;

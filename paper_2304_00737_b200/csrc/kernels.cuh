@@ -458,6 +458,13 @@ struct CtlTask {
 int launch_controller(const CtlTask* tasks_dev, int ntask, int observe, const int32_t* abort,
                       cudaStream_t s);
 
+// fp64 components of the C++ drop-in surface (components64.cu)
+int launch_topk64(const int64_t* idx, const double* val, int n, long long budget, uint8_t* flag,
+                  cudaStream_t s);
+int launch_merge64(const int64_t* ai, const double* av, int na, const int64_t* bi,
+                   const double* bv, int nb, int64_t* ti, double* tv, int64_t* oi, double* ov,
+                   int64_t* no, cudaStream_t s);
+
 // peer-memory transport (transport.cu): iteration epoch, readiness flags
 int launch_begin(long long* epoch, const long long* const* done, int n, int32_t* err,
                  unsigned long long timeout_ns, cudaStream_t s);

@@ -30,3 +30,22 @@ def test_cpp_dropin(built):
     print(r.stdout[-3000:], r.stderr[-2000:])
     assert r.returncode == 0
     assert "0 failed" in r.stdout
+
+
+REF_BIN = os.path.join(ROOT, "oracle", "_ref")
+
+
+@pytest.mark.parametrize("name", ["sparse", "fabric", "collectives"])
+def test_reference_unit_tests_unmodified(built, name):
+    """The reference's own unit tests (/root/reference/proj/tests/test_*.cpp,
+    unmodified) compiled against include/spardl with the GoogleTest
+    stand-in (tests/cpp/gtest_shim) by oracle/Makefile, run on the B200:
+    every case passes (17 + 9 + 16 = 42)."""
+    exe = os.path.join(REF_BIN, f"ref_test_{name}")
+    if not os.path.exists(exe):
+        pytest.skip("reference unit tests not built (no /root/reference where built)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    expect = {"sparse": 17, "fabric": 9, "collectives": 16}[name]
+    assert f"{expect} passed, 0 failed" in r.stdout

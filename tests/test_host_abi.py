@@ -160,3 +160,16 @@ def test_plan_ops_pair_up_for_every_world(sd):
                         s = [(o[0], o[3], o[4]) for o in ops[a] if o[1] == b and o[2] == 1]
                         rcv = [(o[0], o[3], o[4]) for o in ops[b] if o[1] == a and o[2] == 0]
                         assert s == rcv, (P, d, sag, world, a, b)
+
+
+def test_reference_fabric_unit_tests_on_host(built):
+    """The reference's test_fabric.cpp (unmodified; the Fabric and its ledger
+    are host-side) against the drop-in surface, no GPU needed: 9/9."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle",
+                       "_ref", "ref_test_fabric")
+    if not os.path.exists(exe):
+        pytest.skip("reference unit tests not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:]
+    assert "9 passed, 0 failed" in r.stdout
