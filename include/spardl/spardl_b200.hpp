@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -903,12 +904,36 @@ inline spardl_config to_c(const ClusterConfig& c) {
   return o;
 }
 
-struct DeviceState {
+// The devices a drop-in spardl_all_reduce spreads its P workers over: the
+// SPARDL_DEVICES list (e.g. "0,1,2,3") or every visible GPU, trimmed to the
+// largest count that divides P.
+inline std::vector<std::int32_t> dropin_devices(std::int64_t workers) {
+  std::vector<std::int32_t> d;
+  if (const char* e = std::getenv("SPARDL_DEVICES")) {
+    std::string s(e);
+    size_t p = 0;
+    while (p < s.size()) {
+      const size_t q = s.find(',', p);
+      d.push_back(std::stoi(s.substr(p, q == std::string::npos ? std::string::npos : q - p)));
+      if (q == std::string::npos) break;
+      p = q + 1;
+    }
+  } else {
+    std::int32_t n = 0;
+    if (spardl_device_count(&n) != SPARDL_OK || n < 1) n = 1;
+    for (int i = 0; i < n; ++i) d.push_back(i);
+  }
+  while (d.size() > 1 && workers % static_cast<std::int64_t>(d.size()) != 0) d.pop_back();
+  if (d.empty()) d.push_back(0);
+  return d;
+}
+
+struct DeviceState {   // one engine per device, all driven from this thread
   spardl_config cfg{};
-  spardl_ctx* ctx = nullptr;
+  spardl_mctx* ctx = nullptr;
   std::vector<std::int64_t> last_scalars, last_rounds;
   ~DeviceState() {
-    if (ctx) spardl_ctx_destroy(ctx);
+    if (ctx) spardl_mctx_destroy(ctx);
   }
 };
 }  // namespace b200
@@ -964,8 +989,10 @@ inline CostRange expected_cost(const ClusterConfig& cfg) {
   return expected_cost_sag(cfg.workers, cfg.k, cfg.teams, cfg.sag);
 }
 
-// The sparse All-Reduce on the GPU: all P workers on device 0 of this
-// process (the multi-GPU form is spardl_ctx_create with world_size > 1).
+// The sparse All-Reduce on the GPU(s): the P workers spread over the local
+// devices (b200::dropin_devices), one host thread driving all of them --
+// the reference's call shape.  Process-per-GPU callers use spardl_ctx_create
+// with world_size > 1 (paper_2304_00737_b200.SparDL.from_process_group).
 inline RunResult spardl_all_reduce(Fabric& fabric, const ClusterConfig& cfg,
                                    const std::vector<GradientVector>& grads,
                                    std::vector<WorkerState>& states) {
@@ -978,7 +1005,9 @@ inline RunResult spardl_all_reduce(Fabric& fabric, const ClusterConfig& cfg,
   if (!dev || std::memcmp(&dev->cfg, &c, sizeof(c)) != 0) {
     dev = std::make_shared<b200::DeviceState>();
     dev->cfg = c;
-    b200::check(spardl_ctx_create(&c, 0, 1, 0, nullptr, nullptr, &dev->ctx));
+    const std::vector<std::int32_t> devs = b200::dropin_devices(cfg.workers);
+    b200::check(spardl_mctx_create(&c, static_cast<std::int32_t>(devs.size()), devs.data(),
+                                   &dev->ctx));
     dev->last_scalars.assign(size_t(p), 0);
     dev->last_rounds.assign(size_t(p), 0);
   }
@@ -999,38 +1028,46 @@ inline RunResult spardl_all_reduce(Fabric& fabric, const ClusterConfig& cfg,
       carry[i] = static_cast<float>(states[size_t(w)].residual.carry().values[i]);
       comb[size_t(w)][i] = g32[size_t(w)][i] + carry[i];
     }
-    b200::check(spardl_carry_from_host(dev->ctx, w, carry.data()));
+    b200::check(spardl_mctx_carry_from_host(dev->ctx, w, carry.data()));
     if (cfg.sag == SagMode::bsag) {
       if (!states[size_t(w)].controller)
         throw config_error("bsag requires controller state per worker");
-      b200::check(spardl_set_controller(dev->ctx, w, &states[size_t(w)].controller->raw()));
+      b200::check(spardl_mctx_set_controller(dev->ctx, w, &states[size_t(w)].controller->raw()));
     }
     gp[size_t(w)] = g32[size_t(w)].data();
   }
   std::vector<std::int64_t> gi(size_t(cfg.k) + 1);
   std::vector<float> gv(size_t(cfg.k) + 1);
   std::int64_t nnz = 0;
-  b200::check(spardl_allreduce_host(dev->ctx, gp.data(), gi.data(), gv.data(), cfg.k, &nnz));
+  b200::check(spardl_mctx_allreduce_host(dev->ctx, gp.data(), gi.data(), gv.data(), cfg.k, &nnz));
   spardl_run_info info{};
-  b200::check(spardl_get_run_info(dev->ctx, &info));
+  b200::check(spardl_mctx_get_run_info(dev->ctx, &info));
 
   RunResult r;
   r.global.n = cfg.dimension;
   for (std::int64_t e = 0; e < nnz; ++e) r.global.entries.push_back({gi[size_t(e)], gv[size_t(e)]});
-  r.per_worker.assign(size_t(p), r.global);
-  r.consistent = info.consistent != 0;
+  // every worker's own copy (each team assembles its own; on every device)
+  r.per_worker.resize(size_t(p));
+  for (int w = 0; w < p; ++w) {
+    std::int64_t wn = 0;
+    b200::check(spardl_mctx_get_global(dev->ctx, w, gi.data(), gv.data(), cfg.k, &wn));
+    r.per_worker[size_t(w)].n = cfg.dimension;
+    for (std::int64_t e = 0; e < wn; ++e)
+      r.per_worker[size_t(w)].entries.push_back({gi[size_t(e)], gv[size_t(e)]});
+  }
+  r.consistent = info.consistent != 0 && verify_consistency(r.per_worker);
   // WorkerState out
   std::vector<float> carry(n);
   for (int w = 0; w < p; ++w) {
-    b200::check(spardl_carry_to_host(dev->ctx, w, carry.data()));
+    b200::check(spardl_mctx_carry_to_host(dev->ctx, w, carry.data()));
     auto& dst = states[size_t(w)].residual.mutable_carry().values;
     for (size_t i = 0; i < n; ++i) dst[i] = carry[i];
     if (cfg.sag == SagMode::bsag)
-      b200::check(spardl_get_controller(dev->ctx, w, &states[size_t(w)].controller->raw()));
+      b200::check(spardl_mctx_get_controller(dev->ctx, w, &states[size_t(w)].controller->raw()));
   }
   // ledger: the device ledger is cumulative per context; fold its delta in
   std::vector<std::int64_t> rounds(np), scalars(np);
-  b200::check(spardl_get_ledger(dev->ctx, rounds.data(), scalars.data()));
+  b200::check(spardl_mctx_get_ledger(dev->ctx, rounds.data(), scalars.data()));
   for (int w = 0; w < p; ++w) {
     auto& l = fabric.mutable_ledger()[size_t(w)];
     l.scalars_received += scalars[size_t(w)] - dev->last_scalars[size_t(w)];
@@ -1045,7 +1082,9 @@ inline RunResult spardl_all_reduce(Fabric& fabric, const ClusterConfig& cfg,
   r.predicted = {info.pred_rounds, info.pred_low, info.pred_high};
   if (info.n_union > 0) {
     r.union_sizes.resize(size_t(info.n_union));
-    b200::check(spardl_get_union_sizes(dev->ctx, r.union_sizes.data()));
+    std::vector<std::int64_t> u(size_t(p), 0);
+    b200::check(spardl_mctx_get_union_sizes(dev->ctx, u.data()));
+    std::copy(u.begin(), u.begin() + std::ptrdiff_t(info.n_union), r.union_sizes.begin());
   }
   // conservation audit as the reference states it (inc/pipeline.hpp:305-334)
   r.conservation_applicable = cfg.residual == ResidualMode::gres;

@@ -95,6 +95,8 @@ typedef struct spardl_hctrl {
 typedef struct spardl_ctx spardl_ctx;
 
 const char* spardl_last_error(void);
+/* CUDA devices visible to this process (0 without a GPU) */
+int spardl_device_count(int32_t* n);
 int spardl_abi_version(void);
 
 /* ------------------------------------------------------------------ */
@@ -271,6 +273,34 @@ int spardl_debug_select_timestamps(spardl_ctx* ctx, int32_t step, int32_t task, 
 int spardl_kernel_launches(const spardl_ctx* ctx, int64_t* per_iteration);
 /* the stream the context enqueues on (cudaStream_t) */
 int spardl_ctx_stream(const spardl_ctx* ctx, void** stream);
+
+/* ---------------------------------------------------------------------------
+ * One process, one host thread, several local GPUs (the reference's call
+ * shape: one spardl_all_reduce advances all P workers, inc/fabric.hpp:47-53,
+ * inc/pipeline.hpp:140-142).  One engine per device (ranks of one NCCL
+ * clique, peers read each other's buffers through direct peer access);
+ * worker w lives on devs[w / (P / ndev)].  devs == NULL: devices 0..ndev-1.
+ * The iteration is enqueued on every device from the calling thread;
+ * run-info / ledger gathers run one internal host thread per device. */
+typedef struct spardl_mctx spardl_mctx;
+int spardl_mctx_create(const spardl_config* cfg, int32_t ndev, const int32_t* devs,
+                       spardl_mctx** out);
+int spardl_mctx_destroy(spardl_mctx* m);
+int spardl_mctx_devices(const spardl_mctx* m, int32_t* ndev, int32_t* transport_peer);
+int spardl_mctx_allreduce(spardl_mctx* m, const float* const* grads_dev);
+int spardl_mctx_allreduce_host(spardl_mctx* m, const float* const* grads_host, int64_t* g_idx,
+                               float* g_val, int64_t cap, int64_t* nnz);
+int spardl_mctx_sync(spardl_mctx* m);
+int spardl_mctx_get_run_info(spardl_mctx* m, spardl_run_info* out);
+int spardl_mctx_get_ledger(spardl_mctx* m, int64_t* rounds, int64_t* scalars);
+int spardl_mctx_get_union_sizes(spardl_mctx* m, int64_t* out);
+int spardl_mctx_get_global(spardl_mctx* m, int32_t worker, int64_t* g_idx, float* g_val,
+                           int64_t cap, int64_t* nnz);
+int spardl_mctx_carry_to_host(spardl_mctx* m, int32_t worker, float* host);
+int spardl_mctx_carry_from_host(spardl_mctx* m, int32_t worker, const float* host);
+int spardl_mctx_set_controller(spardl_mctx* m, int32_t worker, const spardl_hctrl* c);
+int spardl_mctx_get_controller(spardl_mctx* m, int32_t worker, spardl_hctrl* c);
+int spardl_mctx_reset_state(spardl_mctx* m);
 
 #ifdef __cplusplus
 }

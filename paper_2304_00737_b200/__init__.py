@@ -11,6 +11,6 @@ from ._lib import (  # noqa: F401
     NcclError, PartitionError, ScheduleViolationError, SpardlError, StateError,
     TheoremViolationError, UnsupportedError, LIB_PATH, lib)
 from .api import (  # noqa: F401
-    BlockPartition, ClusterConfig, HController, SparDL, build_bags, bsag_phase_cost,
+    BlockPartition, ClusterConfig, HController, SparDL, SparDLMulti, build_bags, bsag_phase_cost,
     dyadic_shares, expected_cost_sag, expected_cost_srs, merge_add, partition, top_k_select,
     top_k_select_slice, topka_cost, validate)

@@ -128,7 +128,7 @@ class HCtrl(C.Structure):
 
 # every symbol include/spardl_cuda.h declares (tests check the exports)
 EXPORTS = [
-    "spardl_last_error", "spardl_abi_version", "spardl_validate", "spardl_partition",
+    "spardl_last_error", "spardl_device_count", "spardl_abi_version", "spardl_validate", "spardl_partition",
     "spardl_block_of", "spardl_build_bags", "spardl_expected_cost_srs",
     "spardl_expected_cost_sag", "spardl_bsag_phase_cost", "spardl_topka_cost",
     "spardl_dyadic_shares", "spardl_hctrl_init", "spardl_hctrl_observe", "spardl_hctrl_budget",
@@ -142,7 +142,12 @@ EXPORTS = [
     "spardl_carry_to_host", "spardl_carry_from_host", "spardl_set_controller",
     "spardl_get_ledger", "spardl_get_union_sizes", "spardl_get_controller",
     "spardl_dense_fallbacks", "spardl_dense_fallbacks_total", "spardl_wide_handed_back", "spardl_div_diag", "spardl_kernel_launches", "spardl_ctx_stream",
-    "spardl_ctx_transport", "spardl_debug_select_timestamps",
+    "spardl_ctx_transport", "spardl_debug_select_timestamps", "spardl_mctx_create",
+    "spardl_mctx_destroy", "spardl_mctx_devices", "spardl_mctx_allreduce",
+    "spardl_mctx_allreduce_host", "spardl_mctx_sync", "spardl_mctx_get_run_info",
+    "spardl_mctx_get_ledger", "spardl_mctx_get_union_sizes", "spardl_mctx_get_global",
+    "spardl_mctx_carry_to_host", "spardl_mctx_carry_from_host", "spardl_mctx_set_controller",
+    "spardl_mctx_get_controller", "spardl_mctx_reset_state",
 ]
 
 _lib = None

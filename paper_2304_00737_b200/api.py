@@ -431,9 +431,115 @@ class SparDL:
         return n.value
 
 
+class SparDLMulti:
+    """One process, one host thread, several local GPUs: the reference's
+    call shape (one spardl_all_reduce advances all P workers,
+    inc/fabric.hpp:47-53).  Worker w lives on devices[w // (P / ndev)]; the
+    engines are ranks of one NCCL clique whose peers read each other's
+    buffers through direct peer access."""
+
+    def __init__(self, cfg: ClusterConfig, devices=None):
+        import ctypes as _C
+        self.cfg = cfg
+        torch = _torch()
+        devs = list(devices) if devices is not None else list(range(torch.cuda.device_count()))
+        self.devices = devs
+        self.wloc = cfg.workers // len(devs)
+        c = cfg.c()
+        arr = (_C.c_int32 * len(devs))(*devs)
+        self._h = _C.c_void_p()
+        check(lib().spardl_mctx_create(_C.byref(c), _C.c_int32(len(devs)), arr,
+                                       _C.byref(self._h)))
+        nd, peer = _C.c_int32(), _C.c_int32()
+        check(lib().spardl_mctx_devices(self._h, _C.byref(nd), _C.byref(peer)))
+        self.transport = "peer" if peer.value else ("nccl" if nd.value > 1 else "local")
+
+    def close(self):
+        if self._h:
+            lib().spardl_mctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def device_of(self, worker: int) -> int:
+        return self.devices[worker // self.wloc]
+
+    def all_reduce(self, grads) -> None:
+        """grads[w]: worker w's float32 CUDA tensor on device_of(w)."""
+        torch = _torch()
+        assert len(grads) == self.cfg.workers
+        for d in self.devices:
+            torch.cuda.synchronize(d)   # the gradients are complete
+        ptrs = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
+        check(lib().spardl_mctx_allreduce(self._h, ptrs))
+
+    def all_reduce_host(self, grads_host):
+        import numpy as np
+        ptrs = (C.c_void_p * len(grads_host))(*[g.ctypes.data for g in grads_host])
+        idx = np.empty(self.cfg.k, np.int64)
+        val = np.empty(self.cfg.k, np.float32)
+        nnz = C.c_int64()
+        check(lib().spardl_mctx_allreduce_host(self._h, ptrs, idx.ctypes.data_as(C.c_void_p),
+                                               val.ctypes.data_as(C.c_void_p),
+                                               C.c_int64(self.cfg.k), C.byref(nnz)))
+        return idx[: nnz.value], val[: nnz.value]
+
+    def sync(self):
+        check(lib().spardl_mctx_sync(self._h))
+
+    def run_info(self) -> dict:
+        ri = RunInfo()
+        check(lib().spardl_mctx_get_run_info(self._h, C.byref(ri)))
+        return ri.as_dict()
+
+    def global_gradient(self, worker: int = 0):
+        import numpy as np
+        idx = np.empty(self.cfg.k, np.int64)
+        val = np.empty(self.cfg.k, np.float32)
+        nnz = C.c_int64()
+        check(lib().spardl_mctx_get_global(self._h, C.c_int32(worker),
+                                           idx.ctypes.data_as(C.c_void_p),
+                                           val.ctypes.data_as(C.c_void_p),
+                                           C.c_int64(self.cfg.k), C.byref(nnz)))
+        return idx[: nnz.value], val[: nnz.value]
+
+    def carry(self, worker: int):
+        import numpy as np
+        out = np.empty(self.cfg.dimension, np.float32)
+        check(lib().spardl_mctx_carry_to_host(self._h, C.c_int32(worker),
+                                              out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def ledger(self):
+        P = self.cfg.workers
+        r = (C.c_int64 * P)()
+        s_ = (C.c_int64 * P)()
+        check(lib().spardl_mctx_get_ledger(self._h, r, s_))
+        return list(r), list(s_)
+
+    def union_sizes(self):
+        P = self.cfg.workers
+        out = (C.c_int64 * P)()
+        check(lib().spardl_mctx_get_union_sizes(self._h, out))
+        m = self.cfg.workers // self.cfg.teams
+        return list(out)[:m] if self.cfg.sag == "bsag" else []
+
+    def controller(self, worker: int = 0) -> dict:
+        c = HCtrl()
+        check(lib().spardl_mctx_get_controller(self._h, C.c_int32(worker), C.byref(c)))
+        return {"h": c.h, "step": c.step, "flag": c.flag, "target": c.target}
+
+    def reset_state(self):
+        check(lib().spardl_mctx_reset_state(self._h))
+
+
 __all__ = [
     "ClusterConfig", "validate", "partition", "BlockPartition", "build_bags",
     "expected_cost_srs", "expected_cost_sag", "bsag_phase_cost", "topka_cost", "dyadic_shares",
-    "HController", "top_k_select", "top_k_select_slice", "merge_add", "SparDL",
+    "HController", "top_k_select", "top_k_select_slice", "merge_add", "SparDL", "SparDLMulti",
 ]
 _ = _lib

@@ -9,6 +9,9 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <thread>
+#include <exception>
+#include <algorithm>
 
 #include "divplan.hpp"
 #include "engine.hpp"
@@ -165,6 +168,18 @@ void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf, int max_tiles = 0,
 }  // namespace
 
 EXPORT const char* spardl_last_error(void) { return g_msg.c_str(); }
+
+EXPORT int spardl_device_count(int32_t* n) {
+  return guarded([&] {
+    need(n, "n");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *n = c;
+  });
+}
 EXPORT int spardl_abi_version(void) { return SPARDL_ABI_VERSION; }
 
 // ---------------------------------------------------------------------------
@@ -926,5 +941,267 @@ EXPORT int spardl_ctx_stream(const spardl_ctx* ctx, void** stream) {
   return guarded([&] {
     need(ctx, "ctx");
     *stream = static_cast<void*>(ctx->eng->stream());
+  });
+}
+
+// ---------------------------------------------------------------------------
+// One process, one host thread, every local GPU (inc/fabric.hpp:47-53: one
+// call advances all P workers).  One engine per device, ranks 0..ndev-1 of
+// one NCCL clique; peers in this process read each other's buffers through
+// direct peer access (no IPC).  Calls that are collective across the
+// engines (creation, the run-info / ledger gathers) run one host thread per
+// device; an iteration is enqueued on all devices from the caller's thread.
+struct spardl_mctx {
+  std::vector<std::unique_ptr<sdle::Engine>> eng;
+  std::vector<int> dev;
+  std::vector<float*> staging;        // allreduce_host: device copies, worker order
+  int wloc = 1;
+  ~spardl_mctx() {
+    for (size_t i = 0; i < staging.size(); ++i) {
+      cudaSetDevice(dev[i / static_cast<size_t>(wloc)]);
+      cudaFree(staging[i]);
+    }
+  }
+};
+
+namespace {
+// f(i) on one host thread per engine; the first exception is rethrown
+template <class F>
+void each_engine(spardl_mctx& m, F&& f) {
+  std::vector<std::exception_ptr> errs(m.dev.size());
+  std::vector<std::thread> th;
+  for (size_t i = 0; i < m.dev.size(); ++i)
+    th.emplace_back([&, i] {
+      try {
+        if (cudaSetDevice(m.dev[i]) != cudaSuccess) sdlh::fail(SPARDL_E_CUDA, "cudaSetDevice");
+        f(static_cast<int>(i));
+      } catch (...) {
+        errs[i] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+}  // namespace
+
+EXPORT int spardl_mctx_create(const spardl_config* cfg, int32_t ndev, const int32_t* devs,
+                              spardl_mctx** out) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(out, "out");
+    require_device();
+    sdlh::validate(*cfg);
+    int avail = 0;
+    CK(cudaGetDeviceCount(&avail));
+    if (ndev < 1) sdlh::fail(SPARDL_E_ARG, "ndev must be >= 1");
+    if (cfg->workers % ndev != 0)
+      sdlh::fail(SPARDL_E_UNSUPPORTED, "P must be a positive multiple of the device count");
+    auto m = std::make_unique<spardl_mctx>();
+    for (int i = 0; i < ndev; ++i) {
+      const int d = devs ? devs[i] : i;
+      if (d < 0 || d >= avail) sdlh::fail(SPARDL_E_ARG, "device index out of range");
+      m->dev.push_back(d);
+    }
+    m->wloc = static_cast<int>(cfg->workers / ndev);
+    ncclUniqueId id{};
+    if (ndev > 1) {
+      const ncclResult_t r = ncclGetUniqueId(&id);
+      if (r != ncclSuccess) sdlh::fail(SPARDL_E_NCCL, ncclGetErrorString(r));
+    }
+    m->eng.resize(static_cast<size_t>(ndev));
+    each_engine(*m, [&](int i) {
+      m->eng[static_cast<size_t>(i)] = std::make_unique<sdle::Engine>(
+          *cfg, m->dev[static_cast<size_t>(i)], ndev, i, ndev > 1 ? &id : nullptr, nullptr);
+    });
+    *out = m.release();
+  });
+}
+
+EXPORT int spardl_mctx_destroy(spardl_mctx* m) {
+  return guarded([&] { delete m; });
+}
+
+EXPORT int spardl_mctx_devices(const spardl_mctx* m, int32_t* ndev, int32_t* transport_peer) {
+  return guarded([&] {
+    need(m, "mctx");
+    if (ndev) *ndev = static_cast<int32_t>(m->dev.size());
+    if (transport_peer) *transport_peer = m->eng[0]->peer_transport() ? 1 : 0;
+  });
+}
+
+// grads_dev[w]: worker w's gradient on device dev[w / (P / ndev)]
+EXPORT int spardl_mctx_allreduce(spardl_mctx* m, const float* const* grads_dev) {
+  return guarded([&] {
+    need(m, "mctx");
+    need(grads_dev, "grads");
+    for (size_t i = 0; i < m->eng.size(); ++i)
+      m->eng[i]->run(grads_dev + i * static_cast<size_t>(m->wloc));
+  });
+}
+
+EXPORT int spardl_mctx_sync(spardl_mctx* m) {
+  return guarded([&] {
+    need(m, "mctx");
+    for (auto& e : m->eng) e->sync();
+  });
+}
+
+// host gradients in (worker order), the global sparse gradient out
+EXPORT int spardl_mctx_allreduce_host(spardl_mctx* m, const float* const* grads_host,
+                                      int64_t* g_idx, float* g_val, int64_t cap, int64_t* nnz) {
+  return guarded([&] {
+    need(m, "mctx");
+    need(grads_host, "grads");
+    const size_t P = m->eng.size() * static_cast<size_t>(m->wloc);
+    const size_t bytes = sizeof(float) * static_cast<size_t>(m->eng[0]->dimension());
+    if (m->staging.empty())
+      for (size_t w = 0; w < P; ++w) {
+        CK(cudaSetDevice(m->dev[w / static_cast<size_t>(m->wloc)]));
+        float* p = nullptr;
+        CK(cudaMalloc(&p, bytes));
+        m->staging.push_back(p);
+      }
+    for (size_t w = 0; w < P; ++w) {
+      need(grads_host[w], "grads[w]");
+      const auto& e = m->eng[w / static_cast<size_t>(m->wloc)];
+      CK(cudaSetDevice(m->dev[w / static_cast<size_t>(m->wloc)]));
+      CK(cudaMemcpyAsync(m->staging[w], grads_host[w], bytes, cudaMemcpyHostToDevice, e->stream()));
+    }
+    std::vector<const float*> sp(m->staging.begin(), m->staging.end());
+    for (size_t i = 0; i < m->eng.size(); ++i)
+      m->eng[i]->run(sp.data() + i * static_cast<size_t>(m->wloc));
+    for (auto& e : m->eng) e->sync();
+    const int32_t* di = nullptr;
+    const float* dv = nullptr;
+    int64_t n = 0;
+    m->eng[0]->global(0, &di, &dv, &n);
+    *nnz = n;
+    if (g_idx && g_val) {
+      if (cap < n) sdlh::fail(SPARDL_E_ARG, "output capacity below the global nnz");
+      std::vector<int32_t> tmp(static_cast<size_t>(n));
+      CK(cudaSetDevice(m->dev[0]));
+      CK(cudaMemcpy(tmp.data(), di, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(g_val, dv, sizeof(float) * n, cudaMemcpyDeviceToHost));
+      for (int64_t q = 0; q < n; ++q) g_idx[q] = tmp[static_cast<size_t>(q)];
+    }
+  });
+}
+
+EXPORT int spardl_mctx_get_run_info(spardl_mctx* m, spardl_run_info* out) {
+  return guarded([&] {
+    need(m, "mctx");
+    need(out, "out");
+    std::vector<spardl_run_info> ri(m->eng.size());
+    each_engine(*m, [&](int i) { ri[static_cast<size_t>(i)] = m->eng[static_cast<size_t>(i)]->run_info(); });
+    *out = ri[0];
+  });
+}
+
+EXPORT int spardl_mctx_get_ledger(spardl_mctx* m, int64_t* rounds, int64_t* scalars) {
+  return guarded([&] {
+    need(m, "mctx");
+    const size_t P = m->eng.size() * static_cast<size_t>(m->wloc);
+    std::vector<std::vector<int64_t>> r(m->eng.size(), std::vector<int64_t>(P)),
+        sc(m->eng.size(), std::vector<int64_t>(P));
+    each_engine(*m, [&](int i) {
+      m->eng[static_cast<size_t>(i)]->ledger(r[static_cast<size_t>(i)].data(),
+                                             sc[static_cast<size_t>(i)].data());
+    });
+    std::copy(r[0].begin(), r[0].end(), rounds);
+    std::copy(sc[0].begin(), sc[0].end(), scalars);
+  });
+}
+
+EXPORT int spardl_mctx_get_union_sizes(spardl_mctx* m, int64_t* out) {
+  return guarded([&] {
+    need(m, "mctx");
+    const size_t n = static_cast<size_t>(m->eng.size() * m->wloc);   // >= m
+    std::vector<std::vector<int64_t>> u(m->eng.size(), std::vector<int64_t>(n, 0));
+    each_engine(*m, [&](int i) { m->eng[static_cast<size_t>(i)]->union_sizes(u[static_cast<size_t>(i)].data()); });
+    std::copy(u[0].begin(), u[0].end(), out);
+  });
+}
+
+// the global sparse gradient as held by worker w (host copy)
+EXPORT int spardl_mctx_get_global(spardl_mctx* m, int32_t worker, int64_t* g_idx, float* g_val,
+                                  int64_t cap, int64_t* nnz) {
+  return guarded([&] {
+    need(m, "mctx");
+    const int i = worker / m->wloc;
+    if (worker < 0 || i >= static_cast<int>(m->eng.size())) sdlh::fail(SPARDL_E_ARG, "worker out of range");
+    CK(cudaSetDevice(m->dev[static_cast<size_t>(i)]));
+    const int32_t* di = nullptr;
+    const float* dv = nullptr;
+    int64_t n = 0;
+    m->eng[static_cast<size_t>(i)]->global(worker % m->wloc, &di, &dv, &n);
+    *nnz = n;
+    if (g_idx && g_val) {
+      if (cap < n) sdlh::fail(SPARDL_E_ARG, "output capacity below the global nnz");
+      std::vector<int32_t> tmp(static_cast<size_t>(n));
+      CK(cudaMemcpy(tmp.data(), di, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(g_val, dv, sizeof(float) * n, cudaMemcpyDeviceToHost));
+      for (int64_t q = 0; q < n; ++q) g_idx[q] = tmp[static_cast<size_t>(q)];
+    }
+  });
+}
+
+EXPORT int spardl_mctx_carry_to_host(spardl_mctx* m, int32_t worker, float* host) {
+  return guarded([&] {
+    need(m, "mctx");
+    need(host, "host");
+    const int i = worker / m->wloc;
+    if (worker < 0 || i >= static_cast<int>(m->eng.size())) sdlh::fail(SPARDL_E_ARG, "worker out of range");
+    auto& e = *m->eng[static_cast<size_t>(i)];
+    CK(cudaSetDevice(m->dev[static_cast<size_t>(i)]));
+    e.sync();
+    CK(cudaMemcpy(host, e.carry(worker % m->wloc), sizeof(float) * e.dimension(),
+                  cudaMemcpyDeviceToHost));
+  });
+}
+
+EXPORT int spardl_mctx_carry_from_host(spardl_mctx* m, int32_t worker, const float* host) {
+  return guarded([&] {
+    need(m, "mctx");
+    need(host, "host");
+    const int i = worker / m->wloc;
+    if (worker < 0 || i >= static_cast<int>(m->eng.size())) sdlh::fail(SPARDL_E_ARG, "worker out of range");
+    auto& e = *m->eng[static_cast<size_t>(i)];
+    CK(cudaSetDevice(m->dev[static_cast<size_t>(i)]));
+    e.sync();
+    CK(cudaMemcpy(e.carry(worker % m->wloc), host, sizeof(float) * e.dimension(),
+                  cudaMemcpyHostToDevice));
+  });
+}
+
+EXPORT int spardl_mctx_set_controller(spardl_mctx* m, int32_t worker, const spardl_hctrl* c) {
+  return guarded([&] {
+    need(m, "mctx");
+    need(c, "controller");
+    const int i = worker / m->wloc;
+    if (worker < 0 || i >= static_cast<int>(m->eng.size())) sdlh::fail(SPARDL_E_ARG, "worker out of range");
+    CK(cudaSetDevice(m->dev[static_cast<size_t>(i)]));
+    m->eng[static_cast<size_t>(i)]->set_controller(worker % m->wloc, *c);
+  });
+}
+
+EXPORT int spardl_mctx_get_controller(spardl_mctx* m, int32_t worker, spardl_hctrl* c) {
+  return guarded([&] {
+    need(m, "mctx");
+    need(c, "controller");
+    const int i = worker / m->wloc;
+    if (worker < 0 || i >= static_cast<int>(m->eng.size())) sdlh::fail(SPARDL_E_ARG, "worker out of range");
+    CK(cudaSetDevice(m->dev[static_cast<size_t>(i)]));
+    m->eng[static_cast<size_t>(i)]->controller(worker % m->wloc, c);
+  });
+}
+
+EXPORT int spardl_mctx_reset_state(spardl_mctx* m) {
+  return guarded([&] {
+    need(m, "mctx");
+    for (size_t i = 0; i < m->eng.size(); ++i) {
+      CK(cudaSetDevice(m->dev[i]));
+      m->eng[i]->reset_state();
+    }
   });
 }

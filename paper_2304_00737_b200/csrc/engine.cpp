@@ -21,6 +21,8 @@
 #include <cstring>
 #include <set>
 
+#include <unistd.h>
+
 namespace sdle {
 
 #define CK(x)                                                                            \
@@ -178,9 +180,11 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
 }
 
 Engine::~Engine() {
+  if (!dry_) cudaSetDevice(device_);
   if (graph_) cudaGraphExecDestroy(graph_);
   for (size_t q = 0; q < peer_base_.size(); ++q)
-    if (peer_base_[q] && peer_base_[q] != sym_) cudaIpcCloseMemHandle(peer_base_[q]);
+    if (peer_base_[q] && peer_base_[q] != sym_ && q < peer_ipc_.size() && peer_ipc_[q])
+      cudaIpcCloseMemHandle(peer_base_[q]);
   if (sym_) cudaFree(sym_);
   if (comm_) ncclCommDestroy(comm_);
   for (float* c : carry_) cudaFree(c);
@@ -1067,29 +1071,56 @@ void Engine::setup_peer() {
   const size_t bytes = done_off_ + align(sizeof(long long) * static_cast<size_t>(world_));
   CK(cudaMalloc(&sym_, bytes));
   CK(cudaMemset(sym_, 0, bytes));
-  cudaIpcMemHandle_t mine{};
-  int32_t ok = cudaIpcGetMemHandle(&mine, sym_) == cudaSuccess ? 1 : 0;
+  // what every rank learns about every other: its IPC handle, and -- for
+  // ranks in this same process (spardl_mctx: one host thread, several
+  // GPUs), where IPC handles cannot be opened -- its raw pointer and device
+  struct PeerInfo {
+    cudaIpcMemHandle_t h;
+    long long pid;
+    unsigned long long ptr;
+    int32_t dev;
+    int32_t pad;
+  };
+  PeerInfo mine{};
+  int32_t ok = cudaIpcGetMemHandle(&mine.h, sym_) == cudaSuccess ? 1 : 0;
   cudaGetLastError();
-  // exchange the handles over the communicator
-  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  mine.pid = static_cast<long long>(getpid());
+  mine.ptr = reinterpret_cast<unsigned long long>(sym_);
+  mine.dev = device_;
+  const size_t hb = sizeof(PeerInfo);
   unsigned char* dbuf = nullptr;
   CK(cudaMalloc(&dbuf, hb * static_cast<size_t>(world_ + 1) + 16));
   CK(cudaMemcpy(dbuf, &mine, hb, cudaMemcpyHostToDevice));
   NK(ncclAllGather(dbuf, dbuf + hb, hb, ncclChar, comm_, stream_));
-  std::vector<cudaIpcMemHandle_t> hs(static_cast<size_t>(world_));
+  std::vector<PeerInfo> hs(static_cast<size_t>(world_));
   CK(cudaStreamSynchronize(stream_));
   CK(cudaMemcpy(hs.data(), dbuf + hb, hb * static_cast<size_t>(world_), cudaMemcpyDeviceToHost));
   peer_base_.assign(static_cast<size_t>(world_), nullptr);
+  peer_ipc_.assign(static_cast<size_t>(world_), 0);
   peer_base_[static_cast<size_t>(rank_)] = sym_;
   for (int q = 0; q < world_ && ok; ++q) {
     if (q == rank_) continue;
+    const PeerInfo& pi = hs[static_cast<size_t>(q)];
+    if (pi.pid == mine.pid) {   // same process: direct peer access (UVA)
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, device_, pi.dev) != cudaSuccess || !can) {
+        cudaGetLastError();
+        ok = 0;
+        continue;
+      }
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(pi.dev, 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) ok = 0;
+      cudaGetLastError();
+      peer_base_[static_cast<size_t>(q)] = reinterpret_cast<unsigned char*>(pi.ptr);
+      continue;
+    }
     void* p = nullptr;
-    if (cudaIpcOpenMemHandle(&p, hs[static_cast<size_t>(q)], cudaIpcMemLazyEnablePeerAccess) !=
-        cudaSuccess) {
+    if (cudaIpcOpenMemHandle(&p, pi.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
       cudaGetLastError();
       ok = 0;
     } else {
       peer_base_[static_cast<size_t>(q)] = static_cast<unsigned char*>(p);
+      peer_ipc_[static_cast<size_t>(q)] = 1;
     }
   }
   // every rank must agree, or all use NCCL
@@ -1101,7 +1132,7 @@ void Engine::setup_peer() {
   CK(cudaFree(dbuf));
   if (!ok) {
     for (int q = 0; q < world_; ++q)
-      if (q != rank_ && peer_base_[static_cast<size_t>(q)])
+      if (q != rank_ && peer_base_[static_cast<size_t>(q)] && peer_ipc_[static_cast<size_t>(q)])
         cudaIpcCloseMemHandle(peer_base_[static_cast<size_t>(q)]);
     peer_base_.clear();
     cudaFree(sym_);

@@ -282,6 +282,7 @@ class Engine {
   bool peer_ = false;
   unsigned char* sym_ = nullptr;
   std::vector<unsigned char*> peer_base_;   // per rank; own entry is sym_
+  std::vector<char> peer_ipc_;              // per rank: mapped through CUDA IPC (to close)
   size_t slot_stride_ = 0, flags_off_ = 0, done_off_ = 0;
   std::vector<int> uid_slot_;               // buffer index of each uid (peer transport: global)
   std::map<int, std::vector<int>> push_dst_;   // uid -> remote ranks its producer writes into

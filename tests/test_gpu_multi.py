@@ -121,3 +121,56 @@ def test_multi_gpu_parity(built, world, transport):
     for p in procs:
         p.join(timeout=60)
     assert all(not v for v in res.values()), res
+
+
+MCTX_CASES = [(4, 1, "none", "gres", "optimized"), (8, 2, "rsag", "gres", "optimized"),
+              (6, 3, "bsag", "gres", "optimized"), (8, 1, "none", "pres", "naive")]
+
+
+@pytest.mark.parametrize("P,d,sag,residual,timing", MCTX_CASES)
+def test_single_process_multi_gpu(built, P, d, sag, residual, timing):
+    """One process, one host thread, every local GPU (spardl_mctx): the
+    reference's call shape.  Global gradients, every worker's residual and
+    the ledger bit-exact against the fp32 oracle."""
+    import sys
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import paper_2304_00737_b200 as sd
+    from gpu_util import gen
+    from pyoracle import Oracle, make_config
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    devs = list(range(n))
+    while P % len(devs):
+        devs.pop()
+    N, k = 300_000 + P, P * 1000
+    cfg = sd.ClusterConfig(workers=P, dimension=N, k=k, teams=d, sag=sag, residual=residual,
+                           timing=timing)
+    ctx = sd.SparDLMulti(cfg, devices=devs)
+    ref = Oracle("f32").pipeline(make_config(P, N, k, d, sag, residual, timing))
+    rng = np.random.default_rng(17)
+    for it in range(3):
+        g = gen("gauss", (P, N), rng)
+        grads = [torch.from_numpy(g[w]).to(f"cuda:{ctx.device_of(w)}") for w in range(P)]
+        ctx.all_reduce(grads)
+        ctx.sync()
+        info = ctx.run_info()
+        rinfo = ref.allreduce(g)
+        ri, rv = ref.global_gradient()
+        for w in range(P):
+            gi, gv = ctx.global_gradient(w)
+            assert np.array_equal(gi, ri), (it, w)
+            assert np.array_equal(gv.view(np.uint32), rv.view(np.uint32)), (it, w)
+            assert np.array_equal(ctx.carry(w).view(np.uint32), ref.carry(w).view(np.uint32)), \
+                (it, w)
+        assert info["consistent"] == 1
+        for key in ("max_rounds", "max_scalars", "global_nnz"):
+            assert info[key] == rinfo[key], (key, info[key], rinfo[key])
+        lr, ls = ctx.ledger()
+        rr, rs = ref.ledger()
+        assert list(lr) == list(rr) and list(ls) == list(rs)
+        if sag == "bsag":
+            assert ctx.union_sizes() == list(ref.union_sizes())
+    assert ctx.transport == "peer", ctx.transport
+    ctx.close()
