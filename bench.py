@@ -253,8 +253,9 @@ def reference_arm(args, cfg):
 
 def bench_config(cfg, world):
     P = cfg["P"]
-    return {"workload": cfg["name"], "N": cfg["N"], "P": P, "k": cfg["k"], "teams": 1,
-            "sag": "none", "residual": "gres", "timing": "optimized",
+    return {"workload": cfg["name"], "N": cfg["N"], "P": P, "k": cfg["k"],
+            "teams": cfg.get("teams", 1), "sag": cfg.get("sag", "none"), "residual": "gres",
+            "timing": "optimized",
             "workers_per_gpu": P // max(1, world),
             "parallelism": f"{P} SparDL workers over {world} GPU(s)",
             "data_sets": f"{NSETS} gradient sets rotated (fresh data every step)",
@@ -302,8 +303,26 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=1)
     ap.add_argument("--profile-only", action="store_true", help="ncu helper: short run, no extras")
+    # sweeps: team count / SAG mode, density, P, correlated inputs
+    ap.add_argument("--teams", type=int, default=1)
+    ap.add_argument("--sag", default="none", choices=["none", "rsag", "bsag"])
+    ap.add_argument("--density", type=float, default=None)
+    ap.add_argument("--workers", type=int, default=None)
+    ap.add_argument("--gen", default="iid", choices=["iid", "corr"],
+                    help="corr: g_w = 0.8 s + 0.6 e_w with s shared per gradient set")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.workers:
+        cfg["P"] = args.workers
+    if args.density is not None or args.workers:
+        dens = args.density if args.density is not None else cfg["k"] / cfg["N"]
+        cfg["k"] = cfg["P"] * int(dens * cfg["N"] / cfg["P"])
+    cfg["teams"], cfg["sag"], cfg["gen"] = args.teams, args.sag, args.gen
+    if args.teams != 1 or args.sag != "none" or args.density is not None or args.workers or \
+            args.gen != "iid":
+        cfg["name"] = (f"{cfg['name'].split(':')[0]} sweep: N={cfg['N']}, P={cfg['P']}, "
+                       f"k={cfg['k']} ({cfg['k'] / cfg['N']:.4%}), d={args.teams}, "
+                       f"sag={args.sag}, inputs={args.gen}")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -337,7 +356,8 @@ def main():
     if P % world:
         raise SystemExit(f"P={P} is not divisible by {world} GPUs")
     wloc = P // world
-    ccfg = sd.ClusterConfig(workers=P, dimension=N, k=k)
+    ccfg = sd.ClusterConfig(workers=P, dimension=N, k=k, teams=cfg.get("teams", 1),
+                            sag=cfg.get("sag", "none"))
     ctx = (sd.SparDL.from_process_group(ccfg, device=local_rank) if world > 1
            else sd.SparDL(ccfg, device=0))
     gen = torch.Generator(device="cuda")
@@ -346,7 +366,12 @@ def main():
         grads = []
         for i in range(wloc):
             gen.manual_seed(1000 + 97 * s_ + ctx.first_worker + i)
-            grads.append(torch.randn(N, device="cuda", dtype=torch.float32, generator=gen))
+            g_ = torch.randn(N, device="cuda", dtype=torch.float32, generator=gen)
+            if cfg.get("gen") == "corr":   # shared signal per set (identical on every rank)
+                gen.manual_seed(777 + 97 * s_)
+                g_.mul_(0.6).add_(torch.randn(N, device="cuda", dtype=torch.float32,
+                                              generator=gen), alpha=0.8)
+            grads.append(g_)
         sets.append(grads)
     stream = torch.cuda.ExternalStream(ctx.stream_handle())
     steps, warmup = args.steps, args.warmup
@@ -368,6 +393,7 @@ def main():
         sampler.start()
         time.sleep(0.3)
     fb0 = ctx.dense_fallbacks_total()
+    led0 = ctx.ledger()
     nvl0 = nvlink_tx_kib(phys[:world]) if (world > 1 and local_rank == 0) else None
     barrier()
     if sampler:
@@ -381,6 +407,9 @@ def main():
     ms = allmax(e0.elapsed_time(e1) / steps)
     nvl1 = nvlink_tx_kib(phys[:world]) if nvl0 is not None else None
     fallbacks = int(allmax(ctx.dense_fallbacks_total() - fb0))
+    led1 = ctx.ledger()
+    led_step = {"max_rounds": max(b - a for a, b in zip(led0[0], led1[0])) / steps,
+                "max_scalars": max(b - a for a, b in zip(led0[1], led1[1])) / steps}
     # keep every GPU loaded (the iterations are collective: all ranks in
     # lockstep) until the clock sampler has seen >= ~1.5 s of load
     soak = max(0, min(4000, int((1500.0 - ms * steps) / max(ms, 1e-3))))
@@ -457,7 +486,9 @@ def main():
     t_hbm_ms = 12 * N * wloc / (peak * 1e9) * 1e3   # HBM bound of the whole step
     # fabric bytes: the ledger's scalars received per worker per iteration x 4 B
     # (SURVEY 8d B_NVL, closed form of inc/sag.hpp:295-340); t_roof = max of both
-    _, _, nvl_scalars = sd.expected_cost_sag(P, k, 1, "none")
+    pred = sd.expected_cost_sag(P, k, cfg.get("teams", 1), cfg.get("sag", "none"))
+    # bsag: the measured ledger (the closed form is an interval)
+    nvl_scalars = pred[2] if cfg.get("sag", "none") != "bsag" else led_step["max_scalars"]
     b_nvl = 4 * nvl_scalars
     # per GPU only the workers of other GPUs send over NVLink
     b_nvl_gpu = b_nvl * wloc * (world - 1) / max(1, P - 1) if world > 1 else 0
@@ -505,7 +536,9 @@ def main():
                              "GPUs" if world > 1 else "one GPU holds the single team assembly: "
                              "cross-worker identity is checked by the parity tests instead"),
         "dense_fallbacks_timed_steps": fallbacks,
-        "ledger": {"max_rounds": info["max_rounds"], "max_scalars": info["max_scalars"]},
+        "ledger_per_step": {"measured": led_step,
+                            "expected_cost_sag": {"rounds": pred[0], "scalars_low": pred[1],
+                                                  "scalars_high": pred[2]}},
         "north_star": {"target": "C4 (138M, P=8, 1%) on 8 B200 within 2x of its HBM/NVLink "
                                  "roofline", "t_roof_ms": round(t_roof, 4),
                        "frac_of_roof": round(t_roof / ms, 4), "workers_per_gpu": wloc,

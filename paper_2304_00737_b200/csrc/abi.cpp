@@ -157,8 +157,7 @@ void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf, int max_tiles = 0,
   t.seg_valid = segs + 5 * nck;
   sdl::SelTask* td = buf.get<sdl::SelTask>(1);
   CK(cudaMemcpyAsync(td, &t, sizeof(t), cudaMemcpyHostToDevice, s));
-  (void)dividing;
-  if (t.ws) sdl::launch_wselect(td, 1, max_tiles, true, s);
+  if (t.ws) sdl::launch_wselect(td, 1, max_tiles, !dividing, s);
   sdl::launch_select(td, 1, std::max(1, sdl::sel_scratch_segments(t)), s);
   CK(sdl::take_launch_error());
   CK(cudaGetLastError());

@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "wsel_common.cuh"
 
 #ifndef SPARDL_DIV_MINB
 #define SPARDL_DIV_MINB 3
@@ -166,7 +167,9 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
 // (warp * 32 * ITER + it * 32 + lane) * 4 + e of the chunk, value in s_comb)
 // compacted in index order into the chunk's candidate segment.
 __device__ __forceinline__ void cand_compact(const DivTask& t, int c, int64_t A, uint32_t mask,
-                                             const float* s_comb) {
+                                             const float* s_comb, uint32_t* s_wh = nullptr,
+                                             uint32_t* s_wab = nullptr, uint32_t hbase = 0,
+                                             uint32_t hshift = 0) {
   constexpr int ITER = kChunk / (kThreads * 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // order: (warp, it, lane, e) == index order inside the chunk
@@ -218,13 +221,47 @@ __device__ __forceinline__ void cand_compact(const DivTask& t, int c, int64_t A,
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (mask & (1u << (it * 4 + e))) {
+        const float x = s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e];
         ci[p] = (int32_t)(i0 + e);
-        cv[p] = s_comb[(warp * (32 * ITER) + it * 32 + lane) * 4 + e];
+        cv[p] = x;
         ++p;
+        if (s_wh) {   // the wide select's window histogram (shared, flushed per CTA)
+          const uint32_t d = (mag_key(x) - hbase) >> hshift;
+          atomicAdd(d < (uint32_t)kWBins ? &s_wh[d] : s_wab, 1u);
+        }
       }
     }
   }
   if (threadIdx.x == 0) t.cand_cnt[c] = total;
+}
+
+// The dividing select's level-1 histogram, filled by the candidate pass
+// itself: every CTA flushes its shared histogram (once, non-empty bins only)
+// and the CTA that completes the task decides the wide select's run
+// (wsel_common.cuh).  Every CTA of the grid arrives, with or without work.
+__device__ void div_wsel_epilogue(const DivTask& t, const uint32_t* s_wh, const uint32_t* s_wab,
+                                  bool flush) {
+  WScratch* ws = t.ws;
+  __shared__ int s_last;
+  __shared__ int scratch[40];
+  __shared__ long long lsh[3 * 32];
+  __syncthreads();
+  if (flush) {
+    for (int b = threadIdx.x; b < kWBins; b += kThreads)
+      if (s_wh[b]) atomicAdd(&ws->hist[b], s_wh[b]);
+    if (threadIdx.x == 0 && *s_wab) atomicAdd(&ws->above, *s_wab);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = (int)(atomicAdd(&ws->harrive, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const long long total = w_hist_total(ws, lsh) + __ldcg(&ws->above);
+  const bool bad = __ldcg(t.cand_bad) != 0 || total < t.budget;
+  w_decide(ws, total, bad, t.budget, kWWindow, ws->base, ws->shift, scratch, lsh);
 }
 
 // ---------------------------------------------------------------------------
@@ -246,7 +283,20 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand_bulk(con
   pdl_enter();
   const DivTask& t = tasks[blockIdx.y];
   const int c = blockIdx.x;
-  if (c >= t.nchunks) return;
+  __shared__ uint32_t s_wh[kWBins];
+  __shared__ uint32_t s_wab;
+  const bool wf = t.ws != nullptr;
+  if (c >= t.nchunks) {
+    if (wf) div_wsel_epilogue(t, s_wh, &s_wab, false);
+    return;
+  }
+  uint32_t wb = 0, wsh = 0;
+  if (wf) {
+    for (int b = threadIdx.x; b < kWBins; b += kThreads) s_wh[b] = 0;
+    if (threadIdx.x == 0) s_wab = 0;
+    wb = t.ws->base;
+    wsh = t.ws->shift;
+  }
   extern __shared__ __align__(128) unsigned char dsm[];
   float* s_c = reinterpret_cast<float*>(dsm);        // carry -> combined
   float* s_g = s_c + kChunk;                          // gradient
@@ -370,7 +420,8 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand_bulk(con
     }
   }
   if (nan) *t.err = 1;
-  if (cand) cand_compact(t, c, A, mask, s_c);
+  if (cand) cand_compact(t, c, A, mask, s_c, wf ? s_wh : nullptr, &s_wab, wb, wsh);
+  if (wf) div_wsel_epilogue(t, s_wh, &s_wab, cand);
 }
 
 // FIN: the deferred finalize of the previous iteration (records, see
@@ -379,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand_bulk(con
 // order) are loaded while the chunk streams in and marked in a bitmap of the
 // chunk's positions; the carry stays in registers, and an element whose bit
 // is set takes its record (its rank among the set bits) as it is combined.
-constexpr int kFinRecMax = 1024;   // records per chunk handled in place (else: staged)
+constexpr int kFinRecMax = 256;    // records per chunk handled in place (else: staged)
 #ifndef SPARDL_DIV_FIN_MINB
 #define SPARDL_DIV_FIN_MINB 3
 #endif
@@ -390,7 +441,21 @@ __global__ void __launch_bounds__(kThreads, FIN ? SPARDL_DIV_FIN_MINB : SPARDL_D
   pdl_enter();
   const DivTask& t = tasks[blockIdx.y];
   const int c = blockIdx.x;
-  if (c >= t.nchunks) return;
+  // the wide select's window histogram of the candidates (t.ws)
+  __shared__ uint32_t s_wh[kWBins];
+  __shared__ uint32_t s_wab;
+  const bool wf = t.ws != nullptr;
+  if (c >= t.nchunks) {
+    if (wf) div_wsel_epilogue(t, s_wh, &s_wab, false);
+    return;
+  }
+  uint32_t wb = 0, wsh = 0;
+  if (wf) {
+    for (int b = threadIdx.x; b < kWBins; b += kThreads) s_wh[b] = 0;
+    if (threadIdx.x == 0) s_wab = 0;
+    wb = t.ws->base;
+    wsh = t.ws->shift;
+  }
   // participation in the look-back is decided by the pre-threshold kernel
   // only (bit 0), never by an overflow seen later in this kernel (bit 1)
   const bool cand = !(*t.cand_bad & 1);
@@ -554,8 +619,8 @@ __global__ void __launch_bounds__(kThreads, FIN ? SPARDL_DIV_FIN_MINB : SPARDL_D
     }
   }
   if (nan) *t.err = 1;
-  if (!cand) return;
-  cand_compact(t, c, A, mask, s_comb);
+  if (cand) cand_compact(t, c, A, mask, s_comb, wf ? s_wh : nullptr, &s_wab, wb, wsh);
+  if (wf) div_wsel_epilogue(t, s_wh, &s_wab, cand);
 }
 
 // One CTA per task: the work list of the dividing select -- every chunk

@@ -1253,11 +1253,11 @@ int Engine::exec_stage(const Stage& st, bool dividing) {
   if (!st.merges.empty() && !st.fused)
     n += sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts,
                            st.max_rT, st.max_r, stream_);
-  // wide path first; the cluster select then runs only the tasks handed back
-  (void)dividing;
+  // wide path first (the dividing histogram and decision come from the
+  // candidate pass); the cluster select then runs only the tasks handed back
   if (st.wide)
     n += sdl::launch_wselect(st.sels_dev, static_cast<int>(st.sels.size()), st.w_max_tiles,
-                             true, stream_);
+                             !dividing, stream_);
   if (!st.sels.empty())
     n += sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_,
                             st.fused ? st.cl : 0, st.fused ? st.win_cap : 0);

@@ -39,6 +39,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "wsel_common.cuh"
 
 namespace sdl {
 
@@ -151,49 +152,6 @@ __device__ __forceinline__ int tile_src(const TileMap& tm, int p) {
     lo = (mid < tm.nseg && tm.pre[mid] <= p) ? mid : lo;
   }
   return tm.off[lo] + (p - tm.pre[lo]);
-}
-
-// The bin holding the need-th largest key of the level-1 histogram (every
-// thread of the CTA gets the result).  Returns false if the histogram (plus
-// `above`) holds fewer than `need` entries.  *before = entries in higher bins
-// (including `above`).
-__device__ bool w_locate(const uint32_t* __restrict__ hist, long long above, long long need,
-                         int* bin, long long* before, int* scratch, long long* sh) {
-  constexpr int BPT = kWBins / kWThreads;   // 8 bins per thread
-  __shared__ int s_bin;
-  __shared__ long long s_before;
-  const int tid = threadIdx.x;
-  const int g = kWThreads - 1 - tid;        // this thread's bin group, top groups first
-  uint32_t hb[BPT];
-  long long mine = 0;
-#pragma unroll
-  for (int q = 0; q < BPT; ++q) {
-    hb[q] = __ldcg(hist + g * BPT + q);
-    mine += hb[q];
-  }
-  if (tid == 0) {
-    s_bin = -1;
-    s_before = 0;
-  }
-  // exclusive scan over descending groups (counts fit in int: < 2^31 entries)
-  int tot = 0;
-  const long long ex = above + block_exscan((int)mine, scratch, &tot);
-  if (ex < need && need <= ex + mine) {
-    long long cum = ex;
-    for (int q = BPT - 1; q >= 0; --q) {
-      if (cum + (long long)hb[q] >= need) {
-        s_bin = g * BPT + q;
-        s_before = cum;
-        break;
-      }
-      cum += hb[q];
-    }
-  }
-  __syncthreads();
-  *bin = s_bin;
-  *before = s_before;
-  (void)sh;
-  return s_bin >= 0;
 }
 
 // The need-th largest composite value among c[0, n) (1 <= need <= n), by a
@@ -345,42 +303,13 @@ __global__ void __launch_bounds__(kWThreads) k_wsel_hist(const SelTask* __restri
   if (!s_last) return;
   __threadfence();
   const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
-  const long long above = __ldcg(&ws->above), below = __ldcg(&ws->below);
-  long long part = 0;
-  for (int b = tid; b < kWBins; b += kWThreads) part += __ldcg(ws->hist + b);
-  {
-    long long u0 = 0, u1 = 0;
-    block_sum3_ll(part, u0, u1, lsh);
-  }
-  long long total = part + above + below;
+  long long total = w_hist_total(ws, lsh) + __ldcg(&ws->above) + __ldcg(&ws->below);
   bool bad = false;
   if (ws->is_div) {
     total = *t.cand_total;
     bad = *t.cand_bad != 0 || total < budget;   // incomplete: dense fallback in k_select
   }
-  int state, bstar = -1;
-  long long before = 0;
-  if (bad) state = kWFallback;
-  else if (total <= budget) state = kWAll;
-  else if (budget <= 0) state = kWNone;
-  else if (above >= budget) state = kWFallback;   // threshold above the window
-  else state = w_locate(ws->hist, above, budget, &bstar, &before, scratch, lsh) ? kWOk : kWFallback;
-  const uint32_t expect = bstar >= 0 ? __ldcg(ws->hist + bstar) : 0u;
-  __syncthreads();
-  for (int b = tid; b < kWBins; b += kWThreads) ws->hist[b] = 0;
-  if (tid == 0) {
-    ws->state = state;
-    ws->run_mode = mode;
-    ws->run_base = base;
-    ws->run_shift = shift;
-    ws->bstar = bstar;
-    ws->before = before;
-    ws->bin_expect = expect;
-    ws->total_in = total;
-    ws->above = 0;
-    ws->below = 0;
-    ws->harrive = 0;
-  }
+  w_decide(ws, total, bad, budget, mode, base, shift, scratch, lsh);
 }
 
 // ---------------------------------------------------------------------------
@@ -672,11 +601,14 @@ __global__ void __launch_bounds__(kWThreads, 3) k_wsel_write(const SelTask* __re
 int launch_wselect(const SelTask* tasks_dev, int ntask, int max_tiles, bool histogram,
                    cudaStream_t s) {
   if (ntask <= 0 || max_tiles <= 0) return 0;
-  (void)histogram;
-  launch_pdl(k_wsel_hist, dim3(max_tiles, ntask), dim3(kWThreads), 0, s, tasks_dev);
+  int n = 0;
+  if (histogram) {   // (the dividing selects' histogram comes from k_div_cand)
+    launch_pdl(k_wsel_hist, dim3(max_tiles, ntask), dim3(kWThreads), 0, s, tasks_dev);
+    ++n;
+  }
   launch_pdl(k_wsel_gather, dim3(max_tiles, ntask), dim3(kWThreads), 0, s, tasks_dev);
   launch_pdl(k_wsel_write, dim3(max_tiles, ntask), dim3(kWThreads), 0, s, tasks_dev);
-  return 3;
+  return n + 2;
 }
 
 int wsel_max_group() { return kWMaxGroup; }
