@@ -535,9 +535,26 @@ void Engine::finish_stage(Stage& st) {
   st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size();
   if (!st.wide)
     for (auto& t : st.sels) t.ws = nullptr;   // (cluster selects only)
-  if (!st.merges.empty()) {
+  if (!st.sels.empty())
+    st.sels_dev =
+        static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));
+  if (!st.merges.empty())
     st.merges_dev = static_cast<sdl::MergeTask*>(
         arena_.alloc(sizeof(sdl::MergeTask) * st.merges.size()));
+  // a wide select fed by a merge: the merge histograms its output and
+  // decides (no histogram pass for that select)
+  if (st.wide && !st.merges.empty())
+    for (size_t i = 0; i < st.sels.size(); ++i) {
+      sdl::SelTask& t = st.sels[i];
+      if (!t.merge_slot) continue;
+      sdl::MergeTask& mt = st.merges[static_cast<size_t>(t.merge_slot - 1)];
+      mt.ws = t.ws;
+      mt.sel = st.sels_dev + i;
+      const int32_t one = 1;
+      CK(mcpy(reinterpret_cast<unsigned char*>(t.ws) + offsetof(sdl::WScratch, by_merge), &one,
+              sizeof(one), cudaMemcpyHostToDevice));
+    }
+  if (!st.merges.empty()) {
     CK(mcpy(st.merges_dev, st.merges.data(), sizeof(sdl::MergeTask) * st.merges.size(),
                   cudaMemcpyHostToDevice));
     if (!st.fused) launches_ += 2;
@@ -549,8 +566,6 @@ void Engine::finish_stage(Stage& st) {
         t.nseg = 1;
       }
   if (!st.sels.empty()) {
-    st.sels_dev =
-        static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));
     CK(mcpy(st.sels_dev, st.sels.data(), sizeof(sdl::SelTask) * st.sels.size(),
                   cudaMemcpyHostToDevice));
     launches_ += 9;

@@ -205,6 +205,8 @@ struct WScratch {
   int32_t max_tiles;
   int32_t mode;               // kWWindow (dividing: window set by k_div_prethr) / kWAuto
   int32_t is_div;             // dividing select (candidates + history)
+  int32_t by_merge;           // the feeding merge histograms and decides (no hist pass)
+  int32_t pad2_;
   // level-1 histogram (zeroed by the decider after use)
   uint32_t hist[kWBins];
   uint32_t above;             // window mode: keys past the last bin
@@ -269,6 +271,10 @@ struct MergeTask {
   int32_t* seg_off;                 // [max_parts]
   int32_t* seg_cnt;                 // [max_parts]
   long long* dbg;                   // diagnostics: phase stamps of partitions 0..7, or null
+  // the wide select consuming this merge (nullable): every partition CTA
+  // histograms its output, the last one decides (wsel_common.cuh)
+  WScratch* ws;
+  const SelTask* sel;
 };
 
 // ---------------------------------------------------------------------------

@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "wsel_common.cuh"
 
 namespace sdl {
 
@@ -321,13 +322,7 @@ __device__ __forceinline__ void merge_body(const MergeTask& t, int q, int32_t v_
 }
 
 template <bool PATH>
-__global__ void __launch_bounds__(kMergeThreads, PATH ? SPARDL_MERGE_PATH_MINB : SPARDL_MERGE_MINB) k_merge_part(const MergeTask* __restrict__ tasks) {
-  pdl_enter();
-  // grid (task, partition): partitions of every task come first in launch
-  // order, so the live ones (q < nparts, usually far fewer than max_parts)
-  // all start in the first wave
-  const MergeTask& t = tasks[blockIdx.x];
-  const int q = blockIdx.y;
+__device__ __forceinline__ void merge_part_body(const MergeTask& t, int q) {
   const int S = *t.nparts;
   if (q >= t.max_parts) return;
   if (q >= S) {
@@ -360,10 +355,7 @@ __global__ void __launch_bounds__(kMergeThreads, PATH ? SPARDL_MERGE_PATH_MINB :
 constexpr int kOneShotSamples = 4 * kMergeThreads;
 
 template <bool PATH>
-__global__ void __launch_bounds__(kMergeThreads, PATH ? SPARDL_MERGE_PATH_MINB : SPARDL_MERGE_MINB) k_merge_one(const MergeTask* __restrict__ tasks) {
-  pdl_enter();
-  const MergeTask& t = tasks[blockIdx.x];
-  const int q = blockIdx.y;
+__device__ __forceinline__ void merge_one_body(const MergeTask& t, int q) {
   if (q >= t.max_parts) return;
   mstamp(t, q, 0);
   peer_wait(t.ps);   // remote input lists published
@@ -434,6 +426,81 @@ __global__ void __launch_bounds__(kMergeThreads, PATH ? SPARDL_MERGE_PATH_MINB :
     return;
   }
   merge_body<PATH>(t, q, v_lo, v_hi, win);
+}
+
+static_assert(kMergeThreads == kWDecideThreads, "the merge CTA runs the wide-select decider");
+
+// The consuming wide select's level-1 histogram (MergeTask::ws): every
+// partition CTA histograms the segment it just wrote (shared bins, one
+// flush); the CTA completing the task decides the select's run.  Every CTA
+// of the grid arrives, with or without a partition.
+__device__ void merge_wsel_epilogue(const MergeTask& t, int q) {
+  WScratch* ws = t.ws;
+  const SelTask& ts = *t.sel;
+  int mode;
+  uint32_t base, shift;
+  w_geometry(ts, *ws, mode, base, shift);
+  __shared__ uint32_t h[kWBins];
+  __shared__ uint32_t s_ab[2];
+  __shared__ int s_last;
+  __shared__ int scratch[40];
+  __shared__ long long lsh[3 * 32];
+  for (int b = threadIdx.x; b < kWBins; b += kMergeThreads) h[b] = 0;
+  if (threadIdx.x < 2) s_ab[threadIdx.x] = 0;
+  __syncthreads();   // (and the segment written by this CTA is visible to it)
+  uint32_t nb = 0, na = 0;
+  if (q < t.max_parts) {
+    const int off = t.seg_off[q], cnt = t.seg_cnt[q];
+    for (int j = threadIdx.x; j < cnt; j += kMergeThreads) {
+      const int b = w_bin(mode, base, shift, mag_key(t.out_val[off + j]));
+      if (b < 0) ++nb;
+      else if (b >= kWBins) ++na;
+      else atomicAdd(&h[b], 1u);
+    }
+  }
+  nb = __reduce_add_sync(0xffffffffu, nb);
+  na = __reduce_add_sync(0xffffffffu, na);
+  if ((threadIdx.x & 31) == 0 && (nb | na)) {
+    atomicAdd(&s_ab[0], nb);
+    atomicAdd(&s_ab[1], na);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kWBins; b += kMergeThreads)
+    if (h[b]) atomicAdd(&ws->hist[b], h[b]);
+  if (threadIdx.x == 0) {
+    if (s_ab[0]) atomicAdd(&ws->below, s_ab[0]);
+    if (s_ab[1]) atomicAdd(&ws->above, s_ab[1]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = (int)(atomicAdd(&ws->harrive, 1u) == gridDim.y - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t budget = ts.budget_dev ? *ts.budget_dev : ts.budget;
+  const long long total = w_hist_total(ws, lsh) + __ldcg(&ws->above) + __ldcg(&ws->below);
+  w_decide(ws, total, false, budget, mode, base, shift, scratch, lsh);
+}
+
+// grid (task, partition): partitions of every task come first in launch
+// order, so the live ones (q < nparts, usually far fewer than max_parts)
+// all start in the first wave
+template <bool PATH>
+__global__ void __launch_bounds__(kMergeThreads, PATH ? SPARDL_MERGE_PATH_MINB : SPARDL_MERGE_MINB) k_merge_part(const MergeTask* __restrict__ tasks) {
+  pdl_enter();
+  const MergeTask& t = tasks[blockIdx.x];
+  merge_part_body<PATH>(t, blockIdx.y);
+  if (t.ws) merge_wsel_epilogue(t, blockIdx.y);
+}
+
+template <bool PATH>
+__global__ void __launch_bounds__(kMergeThreads, PATH ? SPARDL_MERGE_PATH_MINB : SPARDL_MERGE_MINB) k_merge_one(const MergeTask* __restrict__ tasks) {
+  pdl_enter();
+  const MergeTask& t = tasks[blockIdx.x];
+  merge_one_body<PATH>(t, blockIdx.y);
+  if (t.ws) merge_wsel_epilogue(t, blockIdx.y);
 }
 
 bool merge_path_on() {

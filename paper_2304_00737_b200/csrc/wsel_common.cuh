@@ -13,6 +13,40 @@ namespace {
 
 constexpr int kWDecideThreads = 256;
 
+// level-1 bin of a key: 0..kWBins-1, kWBins = above the window, -1 = below
+__device__ __forceinline__ int w_bin(int mode, uint32_t base, uint32_t shift, uint32_t key) {
+  if (mode == kWFull) return (int)(key >> 20);
+  if (key < base) return -1;
+  const uint32_t d = (key - base) >> shift;
+  return d >= (uint32_t)kWBins ? kWBins : (int)d;
+}
+
+// this run's histogram geometry of a task (identical in every CTA of the
+// histogram and gather kernels: the previous threshold is only rewritten by
+// the finisher, after every gather CTA has classified its tile)
+__device__ __forceinline__ void w_geometry(const SelTask& t, const WScratch& w, int& mode,
+                                           uint32_t& base, uint32_t& shift) {
+  if (w.mode == kWWindow) {
+    mode = kWWindow;
+    base = w.base;
+    shift = w.shift;
+    return;
+  }
+  const SelScratch* sc = t.scr;
+  const uint32_t prev = sc->prefix;
+  if (sc->all == 0 && prev != 0) {
+    mode = kWWindow;
+    shift = kWAutoShift;
+    const uint32_t half = (uint32_t)(kWBins / 2) << kWAutoShift;
+    base = prev > half ? prev - half : 0u;
+  } else {
+    mode = kWFull;
+    base = 0;
+    shift = 20;
+  }
+}
+
+
 // The bin holding the need-th largest key of the level-1 histogram (every
 // thread of the CTA gets the result).  Returns false if the histogram (plus
 // `above`) holds fewer than `need` entries.  *before = entries in higher bins

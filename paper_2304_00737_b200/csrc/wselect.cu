@@ -64,39 +64,6 @@ __device__ __forceinline__ void w_seg(const WScratch& w, int s, int& off, int& c
   cnt = c < 0 ? 0 : c;
 }
 
-// level-1 bin of a key: 0..kWBins-1, kWBins = above the window, -1 = below
-__device__ __forceinline__ int w_bin(int mode, uint32_t base, uint32_t shift, uint32_t key) {
-  if (mode == kWFull) return (int)(key >> 20);
-  if (key < base) return -1;
-  const uint32_t d = (key - base) >> shift;
-  return d >= (uint32_t)kWBins ? kWBins : (int)d;
-}
-
-// this run's histogram geometry of a task (identical in every CTA of the
-// histogram and gather kernels: the previous threshold is only rewritten by
-// the finisher, after every gather CTA has classified its tile)
-__device__ __forceinline__ void w_geometry(const SelTask& t, const WScratch& w, int& mode,
-                                           uint32_t& base, uint32_t& shift) {
-  if (w.mode == kWWindow) {
-    mode = kWWindow;
-    base = w.base;
-    shift = w.shift;
-    return;
-  }
-  const SelScratch* sc = t.scr;
-  const uint32_t prev = sc->prefix;
-  if (sc->all == 0 && prev != 0) {
-    mode = kWWindow;
-    shift = kWAutoShift;
-    const uint32_t half = (uint32_t)(kWBins / 2) << kWAutoShift;
-    base = prev > half ? prev - half : 0u;
-  } else {
-    mode = kWFull;
-    base = 0;
-    shift = 20;
-  }
-}
-
 __device__ __forceinline__ unsigned long long w_comp(uint32_t key, int32_t idx) {
   return ((unsigned long long)key << 32) | (unsigned long long)(0x7fffffffu - (uint32_t)idx);
 }
@@ -243,6 +210,7 @@ __global__ void __launch_bounds__(kWThreads) k_wsel_hist(const SelTask* __restri
   pdl_enter();
   const SelTask& t = tasks[blockIdx.y];
   WScratch* __restrict__ ws = t.ws;
+  if (ws->by_merge) return;   // histogrammed and decided by the merge feeding it
   const int nseg = w_nseg(*ws);
   const int q = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
