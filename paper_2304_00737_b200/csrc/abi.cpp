@@ -157,7 +157,8 @@ void run_select(sdl::SelTask t, cudaStream_t s, DevBuf& buf, int max_tiles = 0,
   t.seg_valid = segs + 5 * nck;
   sdl::SelTask* td = buf.get<sdl::SelTask>(1);
   CK(cudaMemcpyAsync(td, &t, sizeof(t), cudaMemcpyHostToDevice, s));
-  if (t.ws) sdl::launch_wselect(td, 1, max_tiles, !dividing, s);
+  (void)dividing;   // (the one-shot slice histograms in the histogram pass)
+  if (t.ws) sdl::launch_wselect(td, 1, max_tiles, true, s);
   sdl::launch_select(td, 1, std::max(1, sdl::sel_scratch_segments(t)), s);
   CK(sdl::take_launch_error());
   CK(cudaGetLastError());

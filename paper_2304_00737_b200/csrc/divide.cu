@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, SPARDL_DIV_MINB) k_div_cand_bulk(con
   const int c = blockIdx.x;
   __shared__ uint32_t s_wh[kWBins];
   __shared__ uint32_t s_wab;
-  const bool wf = t.ws != nullptr;
+  const bool wf = t.ws != nullptr && t.ws_fused;
   if (c >= t.nchunks) {
     if (wf) div_wsel_epilogue(t, s_wh, &s_wab, false);
     return;
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, FIN ? SPARDL_DIV_FIN_MINB : SPARDL_D
   // the wide select's window histogram of the candidates (t.ws)
   __shared__ uint32_t s_wh[kWBins];
   __shared__ uint32_t s_wab;
-  const bool wf = t.ws != nullptr;
+  const bool wf = t.ws != nullptr && t.ws_fused;
   if (c >= t.nchunks) {
     if (wf) div_wsel_epilogue(t, s_wh, &s_wab, false);
     return;

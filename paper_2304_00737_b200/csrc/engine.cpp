@@ -87,6 +87,7 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   if (world < 1 || rank < 0 || rank >= world || P_ % world != 0)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "P must be a positive multiple of the process count");
   if (const char* we = std::getenv("SPARDL_WSEL")) wide_on_ = we[0] != '0';
+  if (const char* wf = std::getenv("SPARDL_WSEL_FUSE")) wsel_fuse_ = wf[0] == '1';
   if (cfg.sag == SPARDL_SAG_BSAG && d_ > sdl::kMaxR)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "bsag on the device supports d <= 16");
   wloc_ = P_ / world;
@@ -542,8 +543,10 @@ void Engine::finish_stage(Stage& st) {
     st.merges_dev = static_cast<sdl::MergeTask*>(
         arena_.alloc(sizeof(sdl::MergeTask) * st.merges.size()));
   // a wide select fed by a merge: the merge histograms its output and
-  // decides (no histogram pass for that select)
-  if (st.wide && !st.merges.empty())
+  // decides (no histogram pass for that select; opt-in SPARDL_WSEL_FUSE=1:
+  // measured slower on B200, every small merge CTA flushes a 2048-bin
+  // histogram)
+  if (st.wide && wsel_fuse_ && !st.merges.empty())
     for (size_t i = 0; i < st.sels.size(); ++i) {
       sdl::SelTask& t = st.sels[i];
       if (!t.merge_slot) continue;
@@ -618,10 +621,12 @@ void Engine::plan() {
       max_chunks = std::max(max_chunks, dt.nchunks);
       t.dval = dt.carry + lo;
       t.fallbacks = fallbacks_dev_;
-      if (wide_on_ && dt.use_cand && div_split_ <= 1)
-        div_tasks_.back().ws = make_wide(div_stage_, t, dt.cand_idx, dt.cand_val, nullptr, dt.cand_cnt, nullptr,
-                          dt.cap, dt.nchunks, 64, sdl::kWWindow, 1,
-                          std::max<int64_t>(16384, L_ / 8));
+      if (wide_on_ && dt.use_cand && div_split_ <= 1) {
+        div_tasks_.back().ws_fused = wsel_fuse_ ? 1 : 0;
+        div_tasks_.back().ws = make_wide(div_stage_, t, dt.cand_idx, dt.cand_val, nullptr,
+                                         dt.cand_cnt, nullptr, dt.cap, dt.nchunks, 64,
+                                         sdl::kWWindow, 1, std::max<int64_t>(16384, L_ / 8));
+      }
       t.sel_idx = out.idx;
       t.sel_val = out.val;
       t.sel_cnt = out.cnt;
@@ -1268,11 +1273,12 @@ int Engine::exec_stage(const Stage& st, bool dividing) {
   if (!st.merges.empty() && !st.fused)
     n += sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts,
                            st.max_rT, st.max_r, stream_);
-  // wide path first (the dividing histogram and decision come from the
-  // candidate pass); the cluster select then runs only the tasks handed back
+  // wide path first (with SPARDL_WSEL_FUSE=1 the dividing histogram and
+  // decision come from the candidate pass); the cluster select then runs
+  // only the tasks handed back
   if (st.wide)
     n += sdl::launch_wselect(st.sels_dev, static_cast<int>(st.sels.size()), st.w_max_tiles,
-                             !dividing, stream_);
+                             !(dividing && wsel_fuse_), stream_);
   if (!st.sels.empty())
     n += sdl::launch_select(st.sels_dev, static_cast<int>(st.sels.size()), st.max_nseg, stream_,
                             st.fused ? st.cl : 0, st.fused ? st.win_cap : 0);

@@ -325,6 +325,8 @@ struct DivTask {
   int32_t use_cand;        // 0: candidate path disabled (dense select)
   int32_t* err;            // NaN flag
   WScratch* ws;            // nullable: the wide select of this block (window histogram)
+  int32_t ws_fused;        // k_div_cand histograms the candidates and decides (opt-in)
+  int32_t pad_ws_;
   // deferred finalize (nullable): the previous iteration's records of this
   // block, applied to the carry before the gradient is added when *fin_apply
   const int32_t* rec_idx;
