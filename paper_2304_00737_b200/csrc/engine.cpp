@@ -86,7 +86,11 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
     sdlh::fail(SPARDL_E_UNSUPPORTED, "device path supports N < 2^31 - 1");
   if (world < 1 || rank < 0 || rank >= world || P_ % world != 0)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "P must be a positive multiple of the process count");
-  if (const char* we = std::getenv("SPARDL_WSEL")) wide_on_ = we[0] != '0';
+  if (const char* we = std::getenv("SPARDL_WSEL")) {
+    wide_on_ = we[0] != '0';
+    wsel_force_ = we[0] == '1';
+  }
+  if (const char* wm = std::getenv("SPARDL_WSEL_MAXTASKS")) wsel_max_tasks_ = std::atoi(wm);
   if (const char* wf = std::getenv("SPARDL_WSEL_FUSE")) wsel_fuse_ = wf[0] == '1';
   if (cfg.sag == SPARDL_SAG_BSAG && d_ > sdl::kMaxR)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "bsag on the device supports d <= 16");
@@ -533,7 +537,12 @@ void Engine::plan_fused(Stage& st) {
 
 void Engine::finish_stage(Stage& st) {
   plan_fused(st);
-  st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size();
+  // the wide select where the cluster select cannot fill the GPU: a stage of
+  // few selections (one worker per GPU: one or two per stage); with many
+  // tasks the cluster select already has every SM busy and measured faster
+  // (SPARDL_WSEL_MAXTASKS, default 12; SPARDL_WSEL=1 forces the wide path)
+  st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size() &&
+            (wsel_force_ || static_cast<int>(st.sels.size()) <= wsel_max_tasks_);
   if (!st.wide)
     for (auto& t : st.sels) t.ws = nullptr;   // (cluster selects only)
   if (!st.sels.empty())

@@ -169,6 +169,8 @@ class Engine {
                            const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* count,
                            int stride, int nseg, int group, int mode, int is_div, int64_t bin_cap);
   bool wide_on_ = true;      // SPARDL_WSEL=0: cluster selects only
+  bool wsel_force_ = false;  // SPARDL_WSEL=1: the wide select in every stage
+  int wsel_max_tasks_ = 12;  // otherwise: stages of at most this many selections
   bool wsel_fuse_ = false;   // SPARDL_WSEL_FUSE=1: producers histogram for the wide select
   sdl::SelTask select_from_slot(const Slot& in);
   sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);
