@@ -101,9 +101,9 @@ void require_device() {
     sdlh::fail(SPARDL_E_CUDA, "no CUDA device: the SparDL device path has no CPU fallback");
 }
 
-bool wide_enabled() {
+bool wide_enabled() {   // the one-shot components: as the engine (opt-in)
   const char* e = std::getenv("SPARDL_WSEL");
-  return !(e && e[0] == '0');
+  return e && (e[0] == '1' || e[0] == 'a');
 }
 
 // The wide-select scratch of a one-shot select (the same layout the engine

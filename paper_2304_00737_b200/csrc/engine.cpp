@@ -87,7 +87,7 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   if (world < 1 || rank < 0 || rank >= world || P_ % world != 0)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "P must be a positive multiple of the process count");
   if (const char* we = std::getenv("SPARDL_WSEL")) {
-    wide_on_ = we[0] != '0';
+    wide_on_ = we[0] == '1' || we[0] == 'a';
     wsel_force_ = we[0] == '1';
   }
   if (const char* wm = std::getenv("SPARDL_WSEL_MAXTASKS")) wsel_max_tasks_ = std::atoi(wm);
@@ -537,10 +537,8 @@ void Engine::plan_fused(Stage& st) {
 
 void Engine::finish_stage(Stage& st) {
   plan_fused(st);
-  // the wide select where the cluster select cannot fill the GPU: a stage of
-  // few selections (one worker per GPU: one or two per stage); with many
-  // tasks the cluster select already has every SM busy and measured faster
-  // (SPARDL_WSEL_MAXTASKS, default 12; SPARDL_WSEL=1 forces the wide path)
+  // the wide select (opt-in): every stage with SPARDL_WSEL=1, the stages of
+  // at most SPARDL_WSEL_MAXTASKS selections with SPARDL_WSEL=auto
   st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size() &&
             (wsel_force_ || static_cast<int>(st.sels.size()) <= wsel_max_tasks_);
   if (!st.wide)

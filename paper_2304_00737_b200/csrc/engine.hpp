@@ -168,9 +168,14 @@ class Engine {
   sdl::WScratch* make_wide(Stage& st, sdl::SelTask& t, const int32_t* idx, const float* val,
                            const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* count,
                            int stride, int nseg, int group, int mode, int is_div, int64_t bin_cap);
-  bool wide_on_ = true;      // SPARDL_WSEL=0: cluster selects only
-  bool wsel_force_ = false;  // SPARDL_WSEL=1: the wide select in every stage
-  int wsel_max_tasks_ = 12;  // otherwise: stages of at most this many selections
+  // the wide select (wselect.cu) is opt-in: measured on B200 the cluster
+  // select is as fast with many selections per stage (one GPU: 3.93 vs
+  // 3.89 ms per C4 step) and faster with few (4 GPUs: 1.353 vs 1.371 ms per
+  // C4 step, 0.415 vs 0.507 ms per C2 step: three dependent kernels and
+  // their single-CTA deciders cost more latency than a cluster's 16 CTAs)
+  bool wide_on_ = false;     // SPARDL_WSEL=1: every stage; SPARDL_WSEL=auto: small stages
+  bool wsel_force_ = false;
+  int wsel_max_tasks_ = 12;  // SPARDL_WSEL=auto: stages of at most this many selections
   bool wsel_fuse_ = false;   // SPARDL_WSEL_FUSE=1: producers histogram for the wide select
   sdl::SelTask select_from_slot(const Slot& in);
   sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);

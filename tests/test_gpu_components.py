@@ -12,8 +12,18 @@ from gpu_util import gen
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def env(built):
+@pytest.fixture(scope="module", params=["cluster", "wide"])
+def env(built, request):
+    """Every component test runs through the cluster select and through the
+    opt-in wide select (SPARDL_WSEL=1, read per call by the one-shot entry
+    points)."""
+    import os
+    os.environ["SPARDL_WSEL"] = "1" if request.param == "wide" else "0"
+    yield _env()
+    os.environ.pop("SPARDL_WSEL", None)
+
+
+def _env():
     import torch
     import paper_2304_00737_b200 as sd
     from pyoracle import Oracle

@@ -232,16 +232,16 @@ def test_pipeline_deferred_finalize(env, mode, carry_every, P, d, sag, N, kind, 
          carry_every=carry_every, audit=False)
 
 
-@pytest.mark.parametrize("wsel", ["1", "0"])
+@pytest.mark.parametrize("wsel", ["1", "0", "auto"])
 @pytest.mark.parametrize("P,d,sag,N,kind", [(8, 1, "none", 1_000_000, "gauss"),
                                             (6, 3, "bsag", 300_007, "gauss"),
                                             (8, 2, "rsag", 200_000, "int"),
                                             (4, 1, "none", 100_003, "mixed"),
                                             (1, 1, "none", 2_000_000, "gauss")])
 def test_pipeline_select_paths(env, wsel, P, d, sag, N, kind, monkeypatch):
-    """Every stage through the wide select (SPARDL_WSEL=1: the dividing selects
-    too) or through the cluster select only (SPARDL_WSEL=0); by default the
-    wide select takes the stages of at most 12 selections."""
+    """Every stage through the opt-in wide select (SPARDL_WSEL=1: the dividing
+    selects too) or through the cluster select only (SPARDL_WSEL=0, the
+    default)."""
     monkeypatch.setenv("SPARDL_WSEL", wsel)
     _run(env, P, d, sag, "gres", "optimized", kind, N, P * (N // (P * 100)), iters=4, seed=51,
          audit=False)
