@@ -544,6 +544,17 @@ def main():
                        "frac_of_roof": round(t_roof / ms, 4), "workers_per_gpu": wloc,
                        "within_2x": bool(ms <= 2 * t_roof)},
     }
+    if world > 1 and (nvl0 is None or nvl1 is None):
+        # the NVLink Tx/Rx counters read N/A on this box: the pushes' algorithmic
+        # bytes over the phases that carry them (a lower bound of the link rate:
+        # the pushes overlap the selects that produce them)
+        xch_ms = ph[3] + ph[4]
+        line["nvlink_measured"] = {
+            "source": "algorithmic pushed bytes per GPU / (SRS+SAG + gather phases, device "
+                      "events); nvidia-smi nvlink -gt d counters read N/A here",
+            "algorithmic_bytes_per_gpu_step": int(b_nvl_gpu),
+            "avg_gbs_over_exchange_phases": round(b_nvl_gpu / (xch_ms * 1e-3) / 1e9, 2),
+            "peak_gbs_per_direction": 900.0}
     if nvl0 is not None and nvl1 is not None:
         tx = sum(nvl1[g] - nvl0[g] for g in nvl0) * 1024 / steps / world
         line["nvlink_measured"] = {

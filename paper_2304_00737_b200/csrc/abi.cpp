@@ -427,6 +427,7 @@ EXPORT int spardl_merge_add(int32_t r, const int32_t* const* idx, const float* c
     mt.nparts = buf.get<int32_t>(1);
     mt.out_idx = buf.get<int32_t>(std::max<int64_t>(capsum, 1));
     mt.out_val = buf.get<float>(std::max<int64_t>(capsum, 1));
+    mt.out_cap = std::max<int64_t>(capsum, 1);
     mt.seg_off = buf.get<int32_t>(parts);
     mt.seg_cnt = buf.get<int32_t>(parts);
     sdl::MergeTask* mtd = buf.get<sdl::MergeTask>(1);

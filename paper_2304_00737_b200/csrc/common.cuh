@@ -1,6 +1,7 @@
 // Small device helpers shared by the kernels.
 #pragma once
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <cuda_runtime.h>
@@ -9,6 +10,33 @@
 #include "kernels.cuh"
 
 namespace sdl {
+
+// Device bounds assertions (the sanitizer stand-in: compute-sanitizer is
+// closed on the GPU pool).  Compiled in with make EXTRA=-DSPARDL_CHECKED=1:
+// a violated bound prints the site and traps (the launch fails loudly).
+#ifndef SPARDL_CHECKED
+#define SPARDL_CHECKED 0
+#endif
+#if SPARDL_CHECKED
+#define SPARDL_BOUND(i, n)                                                                  \
+  do {                                                                                      \
+    const long long i_ = (long long)(i), n_ = (long long)(n);                               \
+    if (i_ < 0 || i_ >= n_) {                                                               \
+      printf("SPARDL_BOUND %s:%d: %s = %lld outside [0, %s = %lld)\n", __FILE__, __LINE__,  \
+             #i, i_, #n, n_);                                                               \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define SPARDL_BOUND(i, n) \
+  do {                     \
+  } while (0)
+#endif
+// (a capacity of 0 means "not recorded": unchecked)
+#define SPARDL_BOUND_CAP(i, cap) \
+  do {                           \
+    if ((cap) > 0) SPARDL_BOUND(i, cap); \
+  } while (0)
 
 // Magnitude key: |v| ordering == unsigned ordering of the low 31 bits for
 // every non-NaN float; +0 and -0 share key 0 (inc/sparse.hpp:122-127 compares

@@ -401,6 +401,7 @@ sdl::SelTask Engine::select_from_merge(Stage& st, const std::vector<int>& pieces
   mt.nparts = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
   mt.out_idx = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * capsum));
   mt.out_val = static_cast<float*>(arena_.alloc(sizeof(float) * capsum));
+  mt.out_cap = capsum;
   mt.seg_off = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * parts));
   mt.seg_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * parts));
   st.merges.push_back(mt);
@@ -454,6 +455,8 @@ int Engine::materialize(int w, int pos, std::vector<int> pieces, int64_t budget,
   for (int u : pieces) capsum += local_slot(u).cap;
   t.dis_idx = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * capsum));
   t.dis_val = static_cast<float*>(arena_.alloc(sizeof(float) * capsum));
+  t.sel_cap = static_cast<int32_t>(out.cap);
+  t.dis_cap = static_cast<int32_t>(capsum);
   t.dis_cnt = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
   xi_[static_cast<size_t>(li)][static_cast<size_t>(xi_block)].push_back(
       {t.dis_idx, t.dis_val, t.dis_cnt});
@@ -628,6 +631,7 @@ void Engine::plan() {
       max_chunks = std::max(max_chunks, dt.nchunks);
       t.dval = dt.carry + lo;
       t.fallbacks = fallbacks_dev_;
+      t.sel_cap = static_cast<int32_t>(out.cap);
       if (wide_on_ && dt.use_cand && div_split_ <= 1) {
         div_tasks_.back().ws_fused = wsel_fuse_ ? 1 : 0;
         div_tasks_.back().ws = make_wide(div_stage_, t, dt.cand_idx, dt.cand_val, nullptr,
@@ -1433,10 +1437,14 @@ void Engine::profile(const float* const* grads, int iters, double* phase_ms) {
     }
   }
   if (!step_ev_.empty()) {   // stage / publish / wait of every step, us
-    std::fprintf(stderr, "rank %d steps:", rank_);
-    for (size_t q = 0; q < step_acc.size(); ++q)
-      std::fprintf(stderr, "%s%.1f", q % 3 == 0 ? " | " : " ", 1e3 * step_acc[q] / std::max(iters, 1));
-    std::fprintf(stderr, "\n");
+    std::string line = "rank " + std::to_string(rank_) + " steps (stage, controller, round us):";
+    char buf[48];
+    for (size_t q = 0; q < step_acc.size(); ++q) {
+      std::snprintf(buf, sizeof(buf), "%s%.1f", q % 3 == 0 ? " | " : " ",
+                    1e3 * step_acc[q] / std::max(iters, 1));
+      line += buf;
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());   // one write per rank
   }
   for (auto& e : ev) cudaEventDestroy(e);
   for (int p = 0; p < 5; ++p) phase_ms[p] = acc[p] / std::max(iters, 1);

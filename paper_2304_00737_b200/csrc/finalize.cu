@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB)
     const int e = tid + q * kThreads;
     if (e < nloc) {
       const float r = present[q] ? acc[q] : 0.f;
+      SPARDL_BOUND(gi[e], t.n);
       carry[gi[e]] = r;
       if (t.aud_comb) {
         t.aud_comb[s_off + c0 + e] = x[q];

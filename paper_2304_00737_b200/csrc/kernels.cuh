@@ -138,6 +138,8 @@ struct SelTask {
   float* dis_val;
   int32_t* dis_cnt;
   float weight;          // discard share (inc/residual.hpp:104-124)
+  int32_t sel_cap;       // capacity of sel_idx/sel_val (bounds checks; 0: unchecked)
+  int32_t dis_cap;       // capacity of dis_idx/dis_val
   int32_t pad0_;
   int64_t* total_out;    // nullable: B-SAG union size N_t
   // scratch
@@ -268,8 +270,9 @@ struct MergeTask {
   // output: segmented list
   int32_t* out_idx;                 // capacity sum of input capacities
   float* out_val;
+  int64_t out_cap;                  // capacity of out_idx/out_val (bounds checks)
   int32_t* seg_off;                 // [max_parts]
-  int32_t* seg_cnt;                 // [max_parts]
+ int32_t* seg_cnt;                 // [max_parts]
   long long* dbg;                   // diagnostics: phase stamps of partitions 0..7, or null
   // the wide select consuming this merge (nullable): every partition CTA
   // histograms its output, the last one decides (wsel_common.cuh)

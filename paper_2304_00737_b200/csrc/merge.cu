@@ -258,10 +258,12 @@ __device__ __forceinline__ void merge_body(const MergeTask& t, int q, int32_t v_
     // pass writes the segment, the others ping-pong between two buffers
     int32_t* const q_idx = reinterpret_cast<int32_t*>(m_val + r * T);   // second buffer
     float* const q_val = reinterpret_cast<float*>(q_idx + r * T);
+    SPARDL_BOUND(seg_base + sz_pref[r] - 1, t.out_cap + (sz_pref[r] == 0));
     Run acc{w_idx + a_[0], w_val + a_[0], b_[0] - a_[0]};
     int out = acc.n;
     if (r == 1) {
       for (int e = threadIdx.x; e < acc.n; e += blockDim.x) {
+        SPARDL_BOUND(seg_base + e, t.out_cap);
         t.out_idx[seg_base + e] = acc.idx[e];
         t.out_val[seg_base + e] = acc.val[e];
       }
@@ -310,6 +312,7 @@ __device__ __forceinline__ void merge_body(const MergeTask& t, int q, int32_t v_
       const int32_t x = m_idx[e];
       float acc = m_val[e];
       for (int f = e + 1; f < M && m_idx[f] == x; ++f) acc = __fadd_rn(acc, m_val[f]);
+      SPARDL_BOUND(seg_base + rk, t.out_cap);
       t.out_idx[seg_base + rk] = x;
       t.out_val[seg_base + rk] = acc;
     }

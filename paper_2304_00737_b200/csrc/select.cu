@@ -304,6 +304,7 @@ __device__ long long merge_prologue(const MergeTask& mt, int cr, int32_t* w_idx,
     for (int b = 0; b < kMB; ++b) {
       if (q[b] < 0) continue;
       heads += head[b];
+      SPARDL_BOUND(base + rank[b], mt.out_cap);
       mt.out_idx[base + rank[b]] = x[b];
       mt.out_val[base + rank[b]] = head[b] ? acc[b] : __uint_as_float(kHoleBits);
     }
@@ -956,18 +957,21 @@ __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
           val_seen += __popc(bv);
         }
         if (is_sel) {
+          SPARDL_BOUND_CAP(sel_base + sel_rank, t.sel_cap);
           t.sel_idx[sel_base + sel_rank] = ix;
           t.sel_val[sel_base + sel_rank] = v;
           if (npush > 0) {
 #pragma unroll
             for (int p = 0; p < kMaxPush; ++p)
               if (p < npush) {
+                SPARDL_BOUND_CAP(sel_base + sel_rank, t.push_cap);
                 pidx[p][sel_base + sel_rank] = ix;
                 pval[p][sel_base + sel_rank] = v;
               }
           }
         } else if (valid && want_dis) {
           const int p = dis_base + (val_rank - sel_rank);
+          SPARDL_BOUND_CAP(p, t.dis_cap);
           t.dis_idx[p] = ix;
           t.dis_val[p] = __fmul_rn(v, w);
         }

@@ -526,8 +526,10 @@ __global__ void __launch_bounds__(kWThreads, 3) k_wsel_write(const SelTask* __re
         const uint32_t bd = __ballot_sync(0xffffffffu, ix[i] >= 0 && !kp);
         if (kp) {
           const int p = bs + __popc(bk & lt);
+          SPARDL_BOUND_CAP(p, t.sel_cap);
           sel_idx[p] = ix[i];
           sel_val[p] = v[i];
+          if (npush > 0) SPARDL_BOUND_CAP(p, t.push_cap);
           for (int pp = 0; pp < npush; ++pp) {   // peers' copies (slot layout)
             unsigned char* b = push_base[pp];
             reinterpret_cast<int32_t*>(b + 16)[p] = ix[i];
@@ -535,6 +537,7 @@ __global__ void __launch_bounds__(kWThreads, 3) k_wsel_write(const SelTask* __re
           }
         } else if (dis_idx && ix[i] >= 0) {
           const int p = bdd + __popc(bd & lt);
+          SPARDL_BOUND_CAP(p, t.dis_cap);
           dis_idx[p] = ix[i];
           dis_val[p] = __fmul_rn(v[i], w);
         }

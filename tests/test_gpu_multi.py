@@ -174,3 +174,72 @@ def test_single_process_multi_gpu(built, P, d, sag, residual, timing):
             assert ctx.union_sizes() == list(ref.union_sizes())
     assert ctx.transport == "peer", ctx.transport
     ctx.close()
+
+
+def _timeout_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    import paper_2304_00737_b200 as sd
+    os.environ["SPARDL_PEER_TIMEOUT_MS"] = "1500"
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    try:
+        cfg = sd.ClusterConfig(workers=2, dimension=100_000, k=1000)
+        ctx = sd.SparDL.from_process_group(cfg, device=rank)
+        out["transport"] = ctx.transport
+        g = [torch.randn(100_000, device="cuda")]
+        ctx.all_reduce(g)
+        ctx.sync()
+        dist.barrier()
+        if rank == 0:   # rank 1 never joins this iteration: rank 0 must time out
+            ctx.all_reduce(g)
+            try:
+                ctx.sync()
+                out["timeout_reported"] = False
+            except sd.CudaError as e:
+                out["timeout_reported"] = "did not arrive" in str(e)
+            try:
+                ctx.all_reduce(g)   # poisoned: refused until reset_state()
+                out["poisoned"] = False
+            except sd.StateError:
+                out["poisoned"] = True
+            ctx.reset_state()
+            out["reset_ok"] = True
+        dist.barrier()
+    except Exception as e:
+        out["exception"] = repr(e)
+    q.put((rank, out))
+    try:
+        dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+@pytest.mark.timeout(300)
+def test_peer_timeout_poisons_context(built):
+    """A peer that never arrives: the waiting rank's iteration
+    drains within the timeout instead of hanging, sync() reports it, and the
+    context refuses further iterations until reset_state()."""
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_timeout_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0].get("transport") == "peer", res
+    assert res[0].get("timeout_reported") is True, res
+    assert res[0].get("poisoned") is True, res
+    assert res[0].get("reset_ok") is True, res
+    assert "exception" not in res[1], res
