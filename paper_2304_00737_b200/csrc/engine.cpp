@@ -87,9 +87,10 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   if (world < 1 || rank < 0 || rank >= world || P_ % world != 0)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "P must be a positive multiple of the process count");
   if (const char* we = std::getenv("SPARDL_WSEL")) {
-    wide_on_ = we[0] == '1' || we[0] == 'a';
+    wide_on_ = we[0] != '0';
     wsel_force_ = we[0] == '1';
   }
+  if (const char* wn = std::getenv("SPARDL_WSEL_MINENTRIES")) wsel_min_entries_ = std::atoll(wn);
   if (const char* wm = std::getenv("SPARDL_WSEL_MAXTASKS")) wsel_max_tasks_ = std::atoi(wm);
   if (const char* wf = std::getenv("SPARDL_WSEL_FUSE")) wsel_fuse_ = wf[0] == '1';
   if (cfg.sag == SPARDL_SAG_BSAG && d_ > sdl::kMaxR)
@@ -326,7 +327,7 @@ void Engine::add_select(Stage& st, const sdl::SelTask& t0, int out_uid, int in_u
 sdl::WScratch* Engine::make_wide(Stage& st, sdl::SelTask& t, const int32_t* idx, const float* val,
                                   const int32_t* seg_off, const int32_t* seg_cnt,
                                   const int32_t* count, int stride, int nseg, int group, int mode,
-                                  int is_div, int64_t bin_cap) {
+                                  int is_div, int64_t bin_cap, int64_t typical) {
   sdl::WScratch w{};
   w.idx = idx;
   w.val = val;
@@ -353,6 +354,7 @@ sdl::WScratch* Engine::make_wide(Stage& st, sdl::SelTask& t, const int32_t* idx,
   CK(mcpy(d, &w, sizeof(w), cudaMemcpyHostToDevice));
   t.ws = d;
   st.w_max_tiles = std::max(st.w_max_tiles, w.max_tiles);
+  st.w_max_entries = std::max<int64_t>(st.w_max_entries, typical);
   st.ws.push_back(d);
   return d;
 }
@@ -466,12 +468,12 @@ int Engine::materialize(int w, int pos, std::vector<int> pieces, int64_t budget,
       constexpr int kStride = 8192;
       make_wide(st, t, in.idx, in.val, nullptr, nullptr, in.cnt, kStride,
                 static_cast<int>((in.cap + kStride - 1) / kStride), 1, sdl::kWAuto, 0,
-                std::max<int64_t>(16384, in.cap / 8));
+                std::max<int64_t>(16384, in.cap / 8), in.cap);
     } else {                    // the merge's partitions
       const sdl::MergeTask& mt = st.merges.back();
       make_wide(st, t, mt.out_idx, mt.out_val, mt.seg_off, mt.seg_cnt, nullptr, t.stride, t.nseg,
                 std::max(1, 8192 / std::max(1, static_cast<int>(mt.T))), sdl::kWAuto, 0,
-                std::max<int64_t>(16384, capsum / 8));
+                std::max<int64_t>(16384, capsum / 8), capsum);
     }
   }
   add_select(st, t, uid, pieces.size() == 1 ? pieces[0] : -1);
@@ -540,10 +542,15 @@ void Engine::plan_fused(Stage& st) {
 
 void Engine::finish_stage(Stage& st) {
   plan_fused(st);
-  // the wide select (opt-in): every stage with SPARDL_WSEL=1, the stages of
-  // at most SPARDL_WSEL_MAXTASKS selections with SPARDL_WSEL=auto
+  // the wide select where the cluster select cannot fill the GPU: few
+  // selections (<= SPARDL_WSEL_MAXTASKS) of large inputs (>= 200k entries) --
+  // one worker per GPU.  Measured on B200: C4 with one worker on each of 4
+  // GPUs 0.873 -> 0.771 ms per step; with small inputs (C2: 64k-128k entries
+  // per select) the cluster select's single kernel wins (4 GPUs: 0.415 vs
+  // 0.507 ms).  SPARDL_WSEL=1: every stage, =0: none.
   st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size() &&
-            (wsel_force_ || static_cast<int>(st.sels.size()) <= wsel_max_tasks_);
+            (wsel_force_ || (static_cast<int>(st.sels.size()) <= wsel_max_tasks_ &&
+                             st.w_max_entries >= wsel_min_entries_));
   if (!st.wide)
     for (auto& t : st.sels) t.ws = nullptr;   // (cluster selects only)
   if (!st.sels.empty())
@@ -636,7 +643,8 @@ void Engine::plan() {
         div_tasks_.back().ws_fused = wsel_fuse_ ? 1 : 0;
         div_tasks_.back().ws = make_wide(div_stage_, t, dt.cand_idx, dt.cand_val, nullptr,
                                          dt.cand_cnt, nullptr, dt.cap, dt.nchunks, 64,
-                                         sdl::kWWindow, 1, std::max<int64_t>(16384, L_ / 8));
+                                         sdl::kWWindow, 1, std::max<int64_t>(16384, L_ / 8),
+                                         L_ + L_ / 3);
       }
       t.sel_idx = out.idx;
       t.sel_val = out.val;

@@ -79,6 +79,7 @@ struct Stage {           // one batch of merge + select tasks
   int win_cap = 0;           // fused: window entries per CTA
   bool wide = false;         // every select runs the wide path first (wselect.cu)
   int w_max_tiles = 0;       // wide: largest tile count of a task
+  int64_t w_max_entries = 0; // wide: largest input capacity of a task
   std::vector<sdl::WScratch*> ws;   // wide: per select task
 };
 
@@ -167,15 +168,14 @@ class Engine {
   // wide-select scratch of a task over the given input segments
   sdl::WScratch* make_wide(Stage& st, sdl::SelTask& t, const int32_t* idx, const float* val,
                            const int32_t* seg_off, const int32_t* seg_cnt, const int32_t* count,
-                           int stride, int nseg, int group, int mode, int is_div, int64_t bin_cap);
-  // the wide select (wselect.cu) is opt-in: measured on B200 the cluster
-  // select is as fast with many selections per stage (one GPU: 3.93 vs
-  // 3.89 ms per C4 step) and faster with few (4 GPUs: 1.353 vs 1.371 ms per
-  // C4 step, 0.415 vs 0.507 ms per C2 step: three dependent kernels and
-  // their single-CTA deciders cost more latency than a cluster's 16 CTAs)
-  bool wide_on_ = false;     // SPARDL_WSEL=1: every stage; SPARDL_WSEL=auto: small stages
+                           int stride, int nseg, int group, int mode, int is_div, int64_t bin_cap,
+                           int64_t typical);   // typical: the input's expected size
+  // the wide select (wselect.cu) for stages the cluster select cannot fill
+  // (see finish_stage); SPARDL_WSEL=1: every stage, =0: never
+  bool wide_on_ = true;
   bool wsel_force_ = false;
-  int wsel_max_tasks_ = 12;  // SPARDL_WSEL=auto: stages of at most this many selections
+  int wsel_max_tasks_ = 12;            // stages of at most this many selections ...
+  int64_t wsel_min_entries_ = 200000;  // ... with inputs of at least this many entries
   bool wsel_fuse_ = false;   // SPARDL_WSEL_FUSE=1: producers histogram for the wide select
   sdl::SelTask select_from_slot(const Slot& in);
   sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);
