@@ -542,14 +542,15 @@ void Engine::plan_fused(Stage& st) {
 
 void Engine::finish_stage(Stage& st) {
   plan_fused(st);
-  // the wide select where the cluster select cannot fill the GPU: few
-  // selections (<= SPARDL_WSEL_MAXTASKS) of large inputs (>= 200k entries) --
-  // one worker per GPU.  Measured on B200: C4 with one worker on each of 4
-  // GPUs 0.873 -> 0.771 ms per step; with small inputs (C2: 64k-128k entries
-  // per select) the cluster select's single kernel wins (4 GPUs: 0.415 vs
-  // 0.507 ms).  SPARDL_WSEL=1: every stage, =0: none.
+  // the wide select where the cluster select cannot fill the GPU: one worker
+  // per GPU (the north-star split), few selections (<= SPARDL_WSEL_MAXTASKS)
+  // of large inputs (>= 200k entries).  Measured on B200 (C4, 4 GPUs): one
+  // worker per GPU 0.873 -> 0.771 ms per step; two per GPU 1.349 -> 1.370
+  // (the cluster selects of 4-16 tasks already fill the GPU); C2's 64k-128k
+  // entry selects favour the cluster select's single kernel (0.415 vs 0.507).
+  // SPARDL_WSEL=1: every stage, =0: none.
   st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size() &&
-            (wsel_force_ || (static_cast<int>(st.sels.size()) <= wsel_max_tasks_ &&
+            (wsel_force_ || (wloc_ == 1 && static_cast<int>(st.sels.size()) <= wsel_max_tasks_ &&
                              st.w_max_entries >= wsel_min_entries_));
   if (!st.wide)
     for (auto& t : st.sels) t.ws = nullptr;   // (cluster selects only)
