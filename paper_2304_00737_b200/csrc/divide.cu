@@ -260,7 +260,7 @@ __device__ void div_wsel_epilogue(const DivTask& t, const uint32_t* s_wh, const 
   if (!s_last) return;
   __threadfence();
   const long long total = w_hist_total(ws, lsh) + __ldcg(&ws->above);
-  const bool bad = __ldcg(t.cand_bad) != 0 || total < t.budget;
+  const bool bad = (__ldcg(t.cand_bad) & 3) != 0 || total < t.budget;
   w_decide(ws, total, bad, t.budget, kWWindow, ws->base, ws->shift, scratch, lsh);
 }
 
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(1024) k_div_tiles(const DivTask* __restrict__ 
   if (threadIdx.x == 0) {
     *t.cand_total = cand_carry;
     *t.ntiles = min(tile_carry, t.max_tiles);
-    if (tile_carry > t.max_tiles) *t.cand_bad |= 2;   // work list capacity: dense fallback
+    if (tile_carry > t.max_tiles) *t.cand_bad |= 4;   // work list capacity: dense fallback
   }
 }
 

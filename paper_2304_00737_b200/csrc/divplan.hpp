@@ -26,8 +26,19 @@ void div_plan(DivTask& dt, SelTask& t, int64_t lo, int64_t hi, int64_t budget, A
   // per-task work-item bound
   const int64_t cand_cap = std::min<int64_t>(nb, 4 * budget + 4096);
   int tile_len = kTile;
-  while (nch + (cand_cap + tile_len - 1) / tile_len > kMaxSegPerTask) tile_len += kTile;
-  const int max_tiles = nch + static_cast<int>((cand_cap + tile_len - 1) / tile_len);
+  int max_tiles;
+  if (nch + 1 < kMaxSegPerTask) {
+    while (nch + (cand_cap + tile_len - 1) / tile_len > kMaxSegPerTask) tile_len += kTile;
+    max_tiles = nch + static_cast<int>((cand_cap + tile_len - 1) / tile_len);
+  } else {
+    // more chunks than the cluster select's work items (a block of > 64M
+    // elements): the work list overflows (bit 2 of cand_bad: the cluster
+    // select takes the dense path) and the wide select, which reads the
+    // chunk segments directly, selects the candidates
+    tile_len = kTile * 64;
+    max_tiles = kMaxSegPerTask;
+  }
+  dt.huge = nch + 1 >= kMaxSegPerTask ? 1 : 0;
   dt.tile_len = tile_len;
   dt.lo = static_cast<int32_t>(lo);
   dt.hi = static_cast<int32_t>(hi);

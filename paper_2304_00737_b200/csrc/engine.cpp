@@ -550,8 +550,9 @@ void Engine::finish_stage(Stage& st) {
   // entry selects favour the cluster select's single kernel (0.415 vs 0.507).
   // SPARDL_WSEL=1: every stage, =0: none.
   st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size() &&
-            (wsel_force_ || (wloc_ == 1 && static_cast<int>(st.sels.size()) <= wsel_max_tasks_ &&
-                             st.w_max_entries >= wsel_min_entries_));
+            (wsel_force_ || st.need_wide ||
+             (wloc_ == 1 && static_cast<int>(st.sels.size()) <= wsel_max_tasks_ &&
+              st.w_max_entries >= wsel_min_entries_));
   if (!st.wide)
     for (auto& t : st.sels) t.ws = nullptr;   // (cluster selects only)
   if (!st.sels.empty())
@@ -640,7 +641,8 @@ void Engine::plan() {
       t.dval = dt.carry + lo;
       t.fallbacks = fallbacks_dev_;
       t.sel_cap = static_cast<int32_t>(out.cap);
-      if (wide_on_ && dt.use_cand && div_split_ <= 1) {
+      if (dt.huge) div_stage_.need_wide = true;   // (the cluster select would go dense)
+      if (dt.use_cand && div_split_ <= 1 && (wide_on_ || dt.huge)) {
         div_tasks_.back().ws_fused = wsel_fuse_ ? 1 : 0;
         div_tasks_.back().ws = make_wide(div_stage_, t, dt.cand_idx, dt.cand_val, nullptr,
                                          dt.cand_cnt, nullptr, dt.cap, dt.nchunks, 64,

@@ -80,6 +80,7 @@ struct Stage {           // one batch of merge + select tasks
   bool wide = false;         // every select runs the wide path first (wselect.cu)
   int w_max_tiles = 0;       // wide: largest tile count of a task
   int64_t w_max_entries = 0; // wide: largest input capacity of a task
+  bool need_wide = false;    // a dividing block too large for the cluster select's work list
   std::vector<sdl::WScratch*> ws;   // wide: per select task
 };
 

@@ -320,7 +320,8 @@ struct DivTask {
   int32_t tile_len;        // candidates per work-list tile (multiple of kTile)
   int32_t* ntiles;         // tiles in use (written by k_div_tiles)
   int64_t* cand_total;
-  int32_t* cand_bad;       // bit 0: candidate path off for this run, bit 1: overflow
+  int32_t* cand_bad;       // bit 0: candidate path off for this run, bit 1: chunk overflow,
+                           // bit 2: select work-list overflow (the wide select still applies)
   uint32_t* pre_key;       // candidate threshold (key >= pre_key)
   uint32_t* samp_hist;     // [kSampBins]
   struct DivHistory* hist;  // threshold carried over from the previous iteration
@@ -329,7 +330,7 @@ struct DivTask {
   int32_t* err;            // NaN flag
   WScratch* ws;            // nullable: the wide select of this block (window histogram)
   int32_t ws_fused;        // k_div_cand histograms the candidates and decides (opt-in)
-  int32_t pad_ws_;
+  int32_t huge;            // more chunks than select work items (wide select only)
   // deferred finalize (nullable): the previous iteration's records of this
   // block, applied to the carry before the gradient is added when *fin_apply
   const int32_t* rec_idx;

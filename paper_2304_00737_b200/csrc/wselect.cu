@@ -275,7 +275,9 @@ __global__ void __launch_bounds__(kWThreads) k_wsel_hist(const SelTask* __restri
   bool bad = false;
   if (ws->is_div) {
     total = *t.cand_total;
-    bad = *t.cand_bad != 0 || total < budget;   // incomplete: dense fallback in k_select
+    // incomplete candidates: dense fallback in k_select (bit 2, the cluster
+    // select's work list, does not concern the wide select)
+    bad = (*t.cand_bad & 3) != 0 || total < budget;
   }
   w_decide(ws, total, bad, budget, mode, base, shift, scratch, lsh);
 }

@@ -103,6 +103,12 @@ def test_c3_gaussian_vs_f32_oracle(env):
     _f32_run(env, 6, 25_600_000, 255_996, iters=2, seed=2025, name="c3_f32")
 
 
+def test_huge_block_vs_f32_oracle(env):
+    """One block of 70M elements (more chunks than the cluster select's work
+    items): the dividing select goes through the wide select, bit-exact."""
+    _f32_run(env, 1, 70_000_000, 700_000, iters=2, seed=2027, name="huge_block_f32")
+
+
 @pytest.mark.slow
 @pytest.mark.skipif(not SLOW, reason="SPARDL_SLOW=1 (the oracle needs minutes)")
 def test_c4_one_iteration_vs_f32_oracle(env):

@@ -173,3 +173,19 @@ def test_reference_fabric_unit_tests_on_host(built):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:]
     assert "9 passed, 0 failed" in r.stdout
+
+
+@pytest.mark.parametrize("P,N,k,d,sag,world", [(8, 138_000_000, 1_380_000, 4, 1, 4),
+                                               (8, 138_000_000, 1_380_000, 8, 2, 1),
+                                               (2, 340_000_000, 3_400_000, 1, 0, 2)])
+def test_plan_huge_blocks(built, P, N, k, d, sag, world):
+    """Blocks of more chunks than the cluster select's work items (> 64M
+    elements: C4 with d = 4 / 8, C5 on 2 GPUs) plan in bounded time (a round-1
+    sizing loop never terminated there)."""
+    import time
+    from paper_2304_00737_b200._lib import Config, lib
+    cfg = Config(P, N, k, d, sag, 0, 0, 0, 0)
+    n = C.c_int64()
+    t0 = time.time()
+    assert lib().spardl_plan_ops(C.byref(cfg), world, 0, None, 0, C.byref(n)) == 0
+    assert time.time() - t0 < 30
