@@ -22,5 +22,9 @@ case "${SWEEP:-all}" in
     run --config c4 --gen corr ;;
 esac
 case "${SWEEP:-all}" in
-  c5|all) for dens in 0.001 0.0025 0.005 0.01; do run --config c5 --density $dens; done ;;
+  c4d2) for d in 4 8; do for s in rsag bsag; do run --config c4 --teams $d --sag $s; done; done
+        run --config c4 --teams 8 --sag bsag --gen corr ;;
+esac
+case "${SWEEP:-all}" in
+  c5|all) for dens in ${DENS:-0.001 0.0025 0.005 0.01}; do run --config c5 --density $dens; done ;;
 esac
