@@ -11,8 +11,9 @@ P = 8 workers, d = 1 (Spar-Reduce-Scatter + final gather), global residual
 collection, optimized SRS timing.  The P = 8 logical workers are spread over
 the N GPUs (8/N per GPU; at N = 8 one worker per GPU), so the total work is
 fixed: scaling "strong".  One step = one spardl_all_reduce over all 8
-workers' gradients, resident in HBM; every step reads a fresh gradient set
-(4 sets rotate, each larger than L2: no flush needed).
+workers' gradients, resident in HBM; every step reads a fresh i.i.d.
+gradient (a new 16-byte-aligned window of a per-worker N(0,1) buffer larger
+than L2: no flush needed).
 
 metric: effective dense-gradient bandwidth = P * 4 * N bytes of gradient
 synchronised per second (whole job), plus ms per step.
@@ -43,7 +44,7 @@ CONFIGS = {
                N=340_000_000, P=8, k=3_400_000),
 }
 METRIC = "sparse-allreduce effective dense-grad GB/s (P*4N bytes per step / time)"
-NSETS = 4            # gradient sets rotated over the timed steps (fresh data every step)
+WINDOWS = 1024       # gradient windows per worker buffer (a fresh i.i.d. gradient every step)
 
 
 def peaks():
@@ -258,7 +259,7 @@ def bench_config(cfg, world):
             "timing": "optimized",
             "workers_per_gpu": P // max(1, world),
             "parallelism": f"{P} SparDL workers over {world} GPU(s)",
-            "data_sets": f"{NSETS} gradient sets rotated (fresh data every step)",
+            "data_sets": f"fresh i.i.d. gradient every step ({WINDOWS} windows of one buffer per worker)",
             "l2": "inputs larger than L2 (no flush)", "graph": "CUDA graph per iteration"}
 
 
@@ -360,27 +361,37 @@ def main():
                             sag=cfg.get("sag", "none"))
     ctx = (sd.SparDL.from_process_group(ccfg, device=local_rank) if world > 1
            else sd.SparDL(ccfg, device=0))
+    # fresh gradients every step without storing one set per step: one N(0,1)
+    # buffer of N + 4 * WINDOWS floats per worker; step i reads the window at
+    # offset 4 * (i mod WINDOWS) (16-byte aligned), so every step's gradient is
+    # a new i.i.d. vector at every index -- independent of the residual the
+    # earlier steps left there (a rotation of a few stored sets would re-add
+    # the same gradient every few steps and the residual would grow coherently)
     gen = torch.Generator(device="cuda")
-    sets = []
-    for s_ in range(NSETS):
-        grads = []
-        for i in range(wloc):
-            gen.manual_seed(1000 + 97 * s_ + ctx.first_worker + i)
-            g_ = torch.randn(N, device="cuda", dtype=torch.float32, generator=gen)
-            if cfg.get("gen") == "corr":   # shared signal per set (identical on every rank)
-                gen.manual_seed(777 + 97 * s_)
-                g_.mul_(0.6).add_(torch.randn(N, device="cuda", dtype=torch.float32,
-                                              generator=gen), alpha=0.8)
-            grads.append(g_)
-        sets.append(grads)
+    bufs = []
+    for i in range(wloc):
+        gen.manual_seed(1000 + ctx.first_worker + i)
+        b_ = torch.randn(N + 4 * WINDOWS, device="cuda", dtype=torch.float32, generator=gen)
+        if cfg.get("gen") == "corr":   # shared signal (identical on every rank)
+            gen.manual_seed(777)
+            b_.mul_(0.6).add_(torch.randn(N + 4 * WINDOWS, device="cuda", dtype=torch.float32,
+                                          generator=gen), alpha=0.8)
+        bufs.append(b_)
+    step_no = [0]
+
+    def fresh():
+        o = 4 * (step_no[0] % WINDOWS)
+        step_no[0] += 1
+        return [b_[o:o + N] for b_ in bufs]
+
     stream = torch.cuda.ExternalStream(ctx.stream_handle())
     steps, warmup = args.steps, args.warmup
     for i in range(warmup):
-        ctx.all_reduce(sets[i % NSETS])
+        ctx.all_reduce(fresh())
     ctx.sync()
     if args.profile_only:
         for i in range(steps):
-            ctx.all_reduce(sets[i % NSETS])
+            ctx.all_reduce(fresh())
         ctx.sync()
         if rank == 0:
             print(json.dumps({"profile_only": True}))
@@ -393,6 +404,7 @@ def main():
         sampler.start()
         time.sleep(0.3)
     fb0 = ctx.dense_fallbacks_total()
+    rt0 = ctx.candidate_retries()
     led0 = ctx.ledger()
     nvl0 = nvlink_tx_kib(phys[:world]) if (world > 1 and local_rank == 0) else None
     barrier()
@@ -401,12 +413,13 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(steps):
-        ctx.all_reduce(sets[i % NSETS])
+        ctx.all_reduce(fresh())
     e1.record(stream)
     e1.synchronize()
     ms = allmax(e0.elapsed_time(e1) / steps)
     nvl1 = nvlink_tx_kib(phys[:world]) if nvl0 is not None else None
     fallbacks = int(allmax(ctx.dense_fallbacks_total() - fb0))
+    retries = int(allmax(ctx.candidate_retries() - rt0))
     led1 = ctx.ledger()
     led_step = {"max_rounds": max(b - a for a, b in zip(led0[0], led1[0])) / steps,
                 "max_scalars": max(b - a for a, b in zip(led0[1], led1[1])) / steps}
@@ -414,7 +427,7 @@ def main():
     # lockstep) until the clock sampler has seen >= ~1.5 s of load
     soak = max(0, min(4000, int((1500.0 - ms * steps) / max(ms, 1e-3))))
     for i in range(soak):
-        ctx.all_reduce(sets[i % NSETS])
+        ctx.all_reduce(fresh())
     ctx.sync()
     clocks = None
     if sampler:
@@ -423,31 +436,43 @@ def main():
         clocks = sampler.summary()
     launches = ctx.kernel_launches()
     info = ctx.run_info()
-    ph = ctx.profile(sets[0], iters=min(20, max(3, steps)))
-    ph = [allmax(x) for x in ph]
+    # phases: one profiled iteration per call, each on the next fresh window
+    nprof = min(20, max(3, steps))
+    acc = [0.0] * 5
+    for _ in range(nprof):
+        for q, x in enumerate(ctx.profile(fresh(), iters=1)):
+            acc[q] += x / nprof
+    ph = [allmax(x) for x in acc]
 
     e2e = None
     if not args.no_e2e:
-        host_sets = [[g.cpu().pin_memory().numpy() for g in sets[q]] for q in range(2)]
+        # pinned host copies of the same buffers, read through the same windows
+        hbufs = [b_.cpu().pin_memory().numpy() for b_ in bufs]
+
+        def fresh_host():
+            o = 4 * (step_no[0] % WINDOWS)
+            step_no[0] += 1
+            return [h_[o:o + N] for h_ in hbufs]
+
         for q in range(2):
-            ctx.all_reduce_host(host_sets[q])
+            ctx.all_reduce_host(fresh_host())
         e2e_steps = max(3, min(20, steps))
         barrier()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h0.record(stream)
         nnz = 0
         for i in range(e2e_steps):
-            gi, gv = ctx.all_reduce_host(host_sets[i % 2])
+            gi, gv = ctx.all_reduce_host(fresh_host())
             nnz = len(gi)
         h1.record(stream)
         h1.synchronize()
         e2e = {"ms": allmax(h0.elapsed_time(h1) / e2e_steps), "d2h": nnz * 8 * world,
                "steps": e2e_steps}
-        del host_sets
+        del hbufs
 
     dense_ms = None
     if world > 1:
-        dense = sets[0][0]
+        dense = bufs[0][:N]
         for _ in range(3):
             dist.all_reduce(dense)
         barrier()
@@ -461,9 +486,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        host0 = np.stack([g.cpu().numpy() for g in sets[0]])
+        host0 = np.stack([g.cpu().numpy() for g in fresh()])
         ctx.close()
-        del sets
+        del bufs
         torch.cuda.empty_cache()
         try:
             cpu = cpu_baseline_full(cfg, host0, iters=args.cpu_iters)
@@ -514,8 +539,10 @@ def main():
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": (f"synthetic: N(0,1) fp32 gradients generated on device (torch.randn), {NSETS} "
-                 "sets seeded per set and worker, rotated so every step reads fresh data"),
+        "data": ("synthetic: N(0,1) fp32 gradients generated on device (torch.randn), one "
+                 f"buffer of N + {4 * WINDOWS} floats per worker (seeded per worker); step i "
+                 f"reads the window at offset 4 * (i mod {WINDOWS}): a fresh i.i.d. gradient "
+                 "at every index every step"),
         "config": bench_config(cfg, world),
         "roofline": {"bound": "hbm", "kernel": "k_div_cand (fused residual add + candidate compaction)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -536,6 +563,7 @@ def main():
                              "GPUs" if world > 1 else "one GPU holds the single team assembly: "
                              "cross-worker identity is checked by the parity tests instead"),
         "dense_fallbacks_timed_steps": fallbacks,
+        "candidate_retries_timed_steps": retries,
         "ledger_per_step": {"measured": led_step,
                             "expected_cost_sag": {"rounds": pred[0], "scalars_low": pred[1],
                                                   "scalars_high": pred[2]}},
@@ -568,7 +596,8 @@ def main():
                        "h2d_bytes_per_step": P * 4 * N, "d2h_bytes_per_step": e2e["d2h"],
                        "steps": e2e["steps"],
                        "path": "spardl_allreduce_host (C ABI, pinned host gradients in, "
-                               "global sparse gradient out; 2 host sets rotated)"}
+                               "global sparse gradient out; pinned host windows, a fresh "
+                               "gradient every step)"}
     if cpu is not None:
         line["cpu_baseline"] = cpu
     if dense_ms is not None:

@@ -258,6 +258,11 @@ int spardl_dense_fallbacks_total(spardl_ctx* ctx, int64_t* count);
  * cluster select (threshold outside the dividing window, massive key ties),
  * summed since creation / reset_state (synchronises) */
 int spardl_wide_handed_back(spardl_ctx* ctx, int64_t* count);
+/* diagnostics: dividing blocks whose carried pre-threshold missed (too few
+ * candidates, a chunk overflow) and whose candidates were redone from a fresh
+ * sample instead of the dense path, summed since creation / reset_state
+ * (synchronises) */
+int spardl_candidate_retries(spardl_ctx* ctx, int64_t* count);
 /* diagnostics of local dividing task i (= local_worker * m + block):
  * [resolved mode, candidate flags, candidate total, list length, pre-key, capacity,
  *  selection threshold key, carried next pre-key (-1: none), carried margin] */

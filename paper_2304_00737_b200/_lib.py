@@ -141,7 +141,7 @@ EXPORTS = [
     "spardl_get_run_info", "spardl_get_global", "spardl_get_carry", "spardl_ctx_reset_state",
     "spardl_carry_to_host", "spardl_carry_from_host", "spardl_set_controller",
     "spardl_get_ledger", "spardl_get_union_sizes", "spardl_get_controller",
-    "spardl_dense_fallbacks", "spardl_dense_fallbacks_total", "spardl_wide_handed_back", "spardl_div_diag", "spardl_kernel_launches", "spardl_ctx_stream",
+    "spardl_dense_fallbacks", "spardl_dense_fallbacks_total", "spardl_wide_handed_back", "spardl_candidate_retries", "spardl_div_diag", "spardl_kernel_launches", "spardl_ctx_stream",
     "spardl_ctx_transport", "spardl_debug_select_timestamps", "spardl_mctx_create",
     "spardl_mctx_destroy", "spardl_mctx_devices", "spardl_mctx_allreduce",
     "spardl_mctx_allreduce_host", "spardl_mctx_sync", "spardl_mctx_get_run_info",

@@ -425,6 +425,14 @@ class SparDL:
         check(lib().spardl_wide_handed_back(self._h, C.byref(n)))
         return n.value
 
+    def candidate_retries(self) -> int:
+        """Dividing blocks whose carried pre-threshold missed and whose
+        candidates were redone from a fresh sample (the second chance, not the
+        dense path), summed since creation / reset_state()."""
+        n = C.c_int64()
+        check(lib().spardl_candidate_retries(self._h, C.byref(n)))
+        return n.value
+
     def kernel_launches(self) -> int:
         n = C.c_int64()
         check(lib().spardl_kernel_launches(self._h, C.byref(n)))

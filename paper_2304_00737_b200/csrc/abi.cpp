@@ -908,6 +908,14 @@ EXPORT int spardl_dense_fallbacks_total(spardl_ctx* ctx, int64_t* count) {
   });
 }
 
+EXPORT int spardl_candidate_retries(spardl_ctx* ctx, int64_t* count) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(count, "count");
+    *count = ctx->eng->candidate_retries();
+  });
+}
+
 EXPORT int spardl_wide_handed_back(spardl_ctx* ctx, int64_t* count) {
   return guarded([&] {
     need(ctx, "ctx");

@@ -216,10 +216,10 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* scratc
 }
 
 #ifndef SPARDL_DIV_EXTRAP
-#define SPARDL_DIV_EXTRAP 0.5
+#define SPARDL_DIV_EXTRAP 0.75
 #endif
 #ifndef SPARDL_DIV_TARGET
-#define SPARDL_DIV_TARGET 1.2
+#define SPARDL_DIV_TARGET 1.15
 #endif
 // Dividing select epilogue: the pre-threshold of the next iteration.
 __device__ inline void update_history(DivHistory* h, int mode, int all, uint32_t T, uint32_t pre,

@@ -19,6 +19,7 @@
 // candidates are complete (>= L of them, no chunk overflow); otherwise it
 // selects from the dense slice instead, so the result never depends on the
 // sample.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -626,11 +627,7 @@ __global__ void __launch_bounds__(kThreads, FIN ? SPARDL_DIV_FIN_MINB : SPARDL_D
 // One CTA per task: the work list of the dividing select -- every chunk
 // segment cut into tiles of <= kTile candidates, in chunk (= index) order --
 // and the candidate total.  Unused tile slots get count 0.
-__global__ void __launch_bounds__(1024) k_div_tiles(const DivTask* __restrict__ tasks) {
-  pdl_enter();
-  const DivTask& t = tasks[blockIdx.x];
-  __shared__ int scratch[40];
-  if (*t.cand_bad & 1) return;
+__device__ void div_tiles_body(const DivTask& t, int* scratch) {
   int tile_carry = 0, cand_carry = 0;
   for (int c0 = 0; c0 < t.nchunks; c0 += blockDim.x) {
     const int c = c0 + threadIdx.x;
@@ -655,6 +652,136 @@ __global__ void __launch_bounds__(1024) k_div_tiles(const DivTask* __restrict__ 
     *t.cand_total = cand_carry;
     *t.ntiles = min(tile_carry, t.max_tiles);
     if (tile_carry > t.max_tiles) *t.cand_bad |= 4;   // work list capacity: dense fallback
+  }
+  __syncthreads();
+}
+
+// Second chance.  A block whose carried pre-threshold missed -- fewer than L
+// candidates, a chunk segment overflowing, or (cluster select) more tiles
+// than its work list -- would otherwise go down the exact dense path (a
+// select over the whole block: ~270 us per block at C4).  Instead this CTA
+// samples the block's combined values (now in the carry) as k_div_sample
+// does, puts the pre-threshold at a wider margin (1.5 L + 6 sigma of the
+// sample), resets the block's history (the select re-fits it from this run)
+// and marks the block (bit 3) for k_div_recand, which recompacts its
+// candidates from the carry.  Only a second miss takes the dense path.
+__device__ void div_resample(const DivTask& t, uint32_t* h, int* scratch) {
+  constexpr int BPT = kSampBins / 1024;   // bins per thread (blockDim.x == 1024)
+  for (int b = threadIdx.x; b < kSampBins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (int c = 0; c < t.nchunks; c += t.sample_every) {
+    const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
+    const int64_t s = A > t.lo ? A : t.lo;
+    const int64_t e = (A + kChunk) < t.hi ? (A + kChunk) : t.hi;
+    for (int64_t i = s + threadIdx.x; i < e; i += blockDim.x)
+      atomicAdd(&h[mag_key(__ldcg(t.carry + i)) >> kSampShift], 1u);
+  }
+  __syncthreads();
+  // thread r holds bins [(1023 - r) * BPT, +BPT): thread order = key order, descending
+  const int r = blockDim.x - 1 - threadIdx.x;
+  int mine = 0;
+  for (int q = 0; q < BPT; ++q) mine += (int)h[r * BPT + q];
+  int ns = 0;
+  const int above = block_exscan(mine, scratch, &ns);
+  const double expect = (double)t.budget / (double)((int64_t)t.hi - t.lo) * (double)ns;
+  const long long target = (long long)(1.5 * expect + 6.0 * sqrt(expect + 1.0) + 16.0);
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 0;
+  __syncthreads();
+  if (target < ns && above < target && target <= above + mine) {
+    long long cum = above;
+    for (int q = BPT - 1; q >= 0; --q) {
+      const uint32_t cq = h[r * BPT + q];
+      if (cum + (long long)cq >= target) {
+        const uint32_t pre = (uint32_t)(r * BPT + q) << kSampShift;
+        *t.pre_key = pre;
+        if (t.ws) {   // the wide select's window (as k_div_prethr sets it)
+          uint32_t sh = 0;
+          while (sh < 31 && ((unsigned long long)kWBins << sh) < 4ull * (8u << kSampShift)) ++sh;
+          t.ws->base = pre;
+          t.ws->shift = sh;
+        }
+        s_ok = 1;
+        break;
+      }
+      cum += cq;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_ok) {
+    *t.cand_bad = 8;
+    *t.cand_total = 0;
+    t.hist->valid = 0;   // re-fitted by this run's select from the new pre-threshold
+    if (t.retries) atomicAdd(t.retries, 1ull);
+  }
+}
+
+// PHASE 0 (after k_div_cand): the work list, or the second chance on a
+// miss.  PHASE 1 (after k_div_recand): the work list of the blocks redone.
+template <int PHASE>
+__global__ void __launch_bounds__(1024) k_div_tiles(const DivTask* __restrict__ tasks) {
+  pdl_enter();
+  const DivTask& t = tasks[blockIdx.x];
+  __shared__ int scratch[40];
+  if (PHASE == 1) {
+    if (!(*t.cand_bad & 8)) return;
+    div_tiles_body(t, scratch);
+    if (threadIdx.x == 0) *t.cand_bad &= ~8;
+    return;
+  }
+  if (*t.cand_bad & 1) return;
+  div_tiles_body(t, scratch);
+  const int bad = *t.cand_bad;
+  const bool miss = t.use_cand &&
+                    ((bad & 2) || *t.cand_total < t.budget || (!t.huge && (bad & 4)));
+  if (!miss) return;   // (uniform: every thread read the same words after the barrier)
+  __shared__ uint32_t h[kSampBins];
+  div_resample(t, h, scratch);
+}
+
+// The candidates of the blocks marked by the second chance (bit 3),
+// recompacted from the carry (the combined values, written by k_div_cand)
+// with the new pre-threshold.  A persistent grid over (block, chunk); with
+// no block marked -- the normal case -- every CTA exits after reading the
+// flags.
+__global__ void __launch_bounds__(kThreads) k_div_recand(const DivTask* __restrict__ tasks,
+                                                         int ntask, int max_chunks) {
+  pdl_enter();
+  int any = 0;
+  for (int q = threadIdx.x; q < ntask; q += blockDim.x) any |= (*tasks[q].cand_bad & 8);
+  if (!__syncthreads_or(any)) return;
+  __shared__ __align__(16) float s_comb[kChunk];
+  constexpr int ITER = kChunk / (kThreads * 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long items = (long long)ntask * max_chunks;
+  for (long long w = blockIdx.x; w < items; w += gridDim.x) {
+    const DivTask& t = tasks[w / max_chunks];
+    const int c = (int)(w % max_chunks);
+    if (c >= t.nchunks || !(*t.cand_bad & 8)) continue;   // uniform per CTA
+    const uint32_t pre = *t.pre_key;
+    const int64_t A = chunk_origin(t) + (int64_t)c * kChunk;
+    const int64_t lo = t.lo, hi = t.hi;
+    uint32_t mask = 0;
+    __syncthreads();   // s_comb of the previous item fully consumed
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int sp0 = (warp * (32 * ITER) + it * 32 + lane) * 4;
+      const int64_t i0 = A + sp0;
+      float v[4];
+      if (i0 >= lo && i0 + 4 <= hi) {
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(t.carry + i0));
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (i0 + e >= lo && i0 + e < hi) ? t.carry[i0 + e] : 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        s_comb[sp0 + e] = v[e];
+        if (i0 + e >= lo && i0 + e < hi && mag_key(v[e]) >= pre) mask |= 1u << (it * 4 + e);
+      }
+    }
+    cand_compact(t, c, A, mask, s_comb);
   }
 }
 
@@ -702,8 +829,20 @@ int launch_divide(const DivTask* tasks_dev, int ntask, int max_chunks, int sampl
     } else {
       launch_pdl(k_div_cand<0, 0>, dim3(max_chunks, ntask), dim3(kThreads), 0, s, tasks_dev);
     }
-    launch_pdl(k_div_tiles, dim3(ntask), dim3(1024), 0, s, tasks_dev);
-    n += 2;
+    launch_pdl(k_div_tiles<0>, dim3(ntask), dim3(1024), 0, s, tasks_dev);
+    // the second chance (no-ops unless a block's pre-threshold missed)
+    static int recand_grid[kMaxDevices] = {};
+    const int dev = cur_device();
+    if (!recand_grid[dev]) {
+      int sms = 0, per = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_div_recand, kThreads, 0);
+      recand_grid[dev] = std::max(1, sms) * std::max(1, per);
+    }
+    launch_pdl(k_div_recand, dim3(recand_grid[dev]), dim3(kThreads), 0, s, tasks_dev, ntask,
+               max_chunks);
+    launch_pdl(k_div_tiles<1>, dim3(ntask), dim3(1024), 0, s, tasks_dev);
+    n += 4;
   }
   return n;
 }

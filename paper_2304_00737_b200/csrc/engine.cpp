@@ -170,6 +170,7 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   err_dev_ = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t)));
   fallbacks_dev_ = static_cast<unsigned long long*>(arena_.alloc(sizeof(unsigned long long)));
   wide_back_dev_ = static_cast<unsigned long long*>(arena_.alloc(sizeof(unsigned long long)));
+  retries_dev_ = static_cast<unsigned long long*>(arena_.alloc(sizeof(unsigned long long)));
   hash_dev_ = static_cast<int64_t*>(arena_.alloc(sizeof(int64_t) * d_));
   rb_dev_ = static_cast<int64_t*>(
       arena_.alloc(sizeof(int64_t) * (static_cast<size_t>(P_ + wloc_) + static_cast<size_t>(d_) * (world_ + 1))));
@@ -592,6 +593,17 @@ void Engine::finish_stage(Stage& st) {
                   cudaMemcpyHostToDevice));
     launches_ += 9;
   }
+  if (std::getenv("SPARDL_PLAN_DEBUG") && rank_ == 0) {   // the stage's shape (diagnostics)
+    std::string line = "stage: " + std::to_string(st.merges.size()) + " merges r/T/out_cap:";
+    for (const auto& mt : st.merges)
+      line += " " + std::to_string(mt.r) + "/" + std::to_string(mt.T) + "/" +
+              std::to_string(mt.out_cap);
+    line += " | " + std::to_string(st.sels.size()) + " selects budget/nseg:";
+    for (const auto& t : st.sels)
+      line += " " + std::to_string(t.budget) + "/" + std::to_string(t.nseg);
+    line += st.wide ? " (wide)" : (st.fused ? " (fused)" : "");
+    std::fprintf(stderr, "%s\n", line.c_str());
+  }
 }
 
 // the wide scratch of every task of a stage back to its idle state
@@ -661,7 +673,10 @@ void Engine::plan() {
   // ~8 sampled chunks (65k elements) per block: ~650 expected top-L samples
   // at 1% density whatever the block size (the 4-sigma margin is ~15%)
   div_sample_every_ = std::max(1, max_chunks / 8);
-  for (auto& dt : div_tasks_) dt.sample_every = div_sample_every_;
+  for (auto& dt : div_tasks_) {
+    dt.sample_every = div_sample_every_;
+    dt.retries = retries_dev_;
+  }
   div_max_chunks_ = max_chunks;
   if (!div_tasks_.empty()) {
     div_dev_ = static_cast<sdl::DivTask*>(arena_.alloc(sizeof(sdl::DivTask) * div_tasks_.size()));
@@ -1418,8 +1433,9 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
 }
 
 void Engine::profile(const float* const* grads, int iters, double* phase_ms) {
-  CK(cudaSetDevice(device_));
-  run(grads);   // refresh pointer table + warm
+  // the pointer table only: every profiled iteration is a fresh one on these
+  // gradients (no extra warm iteration re-adding the same gradient)
+  set_grads(grads);
   const char* se = std::getenv("SPARDL_STEP_EVENTS");
   if (se && se[0] == '1' && step_ev_.empty()) {
     step_ev_.resize(3 * steps_.size());
@@ -1461,7 +1477,7 @@ void Engine::profile(const float* const* grads, int iters, double* phase_ms) {
   for (int p = 0; p < 5; ++p) phase_ms[p] = acc[p] / std::max(iters, 1);
 }
 
-void Engine::run(const float* const* grads) {
+void Engine::set_grads(const float* const* grads) {
   CK(cudaSetDevice(device_));
   if (poisoned_)
     sdlh::fail(SPARDL_E_STATE, "peer transport: an earlier iteration timed out waiting for a "
@@ -1488,6 +1504,10 @@ void Engine::run(const float* const* grads) {
     tab_used_[tab_next_] = true;
     tab_next_ = (tab_next_ + 1) % kTabRing;
   }
+}
+
+void Engine::run(const float* const* grads) {
+  set_grads(grads);
   for (int w = 0; w < P_; ++w)
     for (int p = 0; p < 3; ++p)
       rounds_[static_cast<size_t>(w)] += phase_rounds_[static_cast<size_t>(w)][static_cast<size_t>(p)];
@@ -1545,6 +1565,7 @@ void Engine::reset_state() {
   CK(cudaMemset(fallbacks_dev_, 0, sizeof(unsigned long long)));
   if (fin_apply_) CK(cudaMemset(fin_apply_, 0, sizeof(int32_t)));
   CK(cudaMemset(wide_back_dev_, 0, sizeof(unsigned long long)));
+  CK(cudaMemset(retries_dev_, 0, sizeof(unsigned long long)));
   reset_wide(div_stage_);
   for (const Step& stp : steps_) reset_wide(stp.stage);
   for (const auto& dt : div_tasks_) CK(cudaMemset(dt.hist, 0, sizeof(sdl::DivHistory)));
@@ -1704,6 +1725,13 @@ int64_t Engine::wide_handed_back() {
   sync();
   unsigned long long n = 0;
   if (wide_back_dev_) CK(mcpy(&n, wide_back_dev_, sizeof(n), cudaMemcpyDeviceToHost));
+  return static_cast<int64_t>(n);
+}
+
+int64_t Engine::candidate_retries() {
+  sync();
+  unsigned long long n = 0;
+  CK(mcpy(&n, retries_dev_, sizeof(n), cudaMemcpyDeviceToHost));
   return static_cast<int64_t>(n);
 }
 

@@ -108,6 +108,8 @@ class Engine {
   ~Engine();
 
   void run(const float* const* grads_dev);
+  // upload a new gradient pointer table in stream order when it changed
+  void set_grads(const float* const* grads);
   // per-phase device time of `iters` profiled (non-graph) iterations, ms:
   // [sample+prethr, candidate pass, dividing select, SRS/SAG, gather+finalize]
   void profile(const float* const* grads_dev, int iters, double* phase_ms);
@@ -120,6 +122,9 @@ class Engine {
   int64_t dense_fallbacks();
   // dividing selects that fell back to the dense path since reset_state()
   int64_t dense_fallbacks_total();
+  // dividing blocks whose carried pre-threshold missed and whose candidates
+  // were redone from a fresh sample (k_div_recand) since reset_state()
+  int64_t candidate_retries();
   // wide-path selects handed back to the cluster select since reset_state()
   int64_t wide_handed_back();
   // device timestamps (ns) of the phases of one select of the last run
@@ -240,6 +245,7 @@ class Engine {
   int32_t* err_dev_ = nullptr;           // NaN flag
   unsigned long long* fallbacks_dev_ = nullptr;   // dense fallbacks since reset_state()
   unsigned long long* wide_back_dev_ = nullptr;   // wide selects handed back since reset_state()
+  unsigned long long* retries_dev_ = nullptr;     // dividing candidate passes redone since reset_state()
   int64_t* hash_dev_ = nullptr;          // [d] consistency hashes
   int64_t* rb_dev_ = nullptr;            // readback scratch
   std::vector<int64_t> rounds_;          // host, per global worker (cumulative)

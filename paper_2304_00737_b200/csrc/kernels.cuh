@@ -321,7 +321,8 @@ struct DivTask {
   int32_t* ntiles;         // tiles in use (written by k_div_tiles)
   int64_t* cand_total;
   int32_t* cand_bad;       // bit 0: candidate path off for this run, bit 1: chunk overflow,
-                           // bit 2: select work-list overflow (the wide select still applies)
+                           // bit 2: select work-list overflow (the wide select still applies),
+                           // bit 3: candidates being redone (second chance, k_div_recand)
   uint32_t* pre_key;       // candidate threshold (key >= pre_key)
   uint32_t* samp_hist;     // [kSampBins]
   struct DivHistory* hist;  // threshold carried over from the previous iteration
@@ -339,6 +340,7 @@ struct DivTask {
   const int32_t* chunk_off;
   const int32_t* fin_apply;
   const SelScratch* prev_sel; // the previous iteration's dividing selection (membership)
+  unsigned long long* retries;  // nullable: += 1 per block whose candidates were redone
 };
 
 // ---------------------------------------------------------------------------

@@ -81,7 +81,9 @@ def _run(env, P, d, sag, residual, timing, kind, N, k, iters, seed, graph=True, 
             for w in range(P):
                 c, rc = ctx.controller(w), ref.controller(w)
                 assert (c["h"], c["step"], c["flag"]) == (rc.h, rc.step, rc.flag), tag
+    counts = {"retries": ctx.candidate_retries(), "fallbacks": ctx.dense_fallbacks_total()}
     ctx.close()
+    return counts
 
 
 @pytest.mark.parametrize("P,d,sag", configs())
@@ -119,6 +121,19 @@ def test_pipeline_distribution_shift(env):
     (through the dense fallback when the carried threshold is off)."""
     _run(env, 8, 1, "none", "gres", "optimized", "gauss", 1_000_000, 10_000, iters=6, seed=9,
          scales=[1.0, 1e3, 1e-3, 1.0, 1e-6, 1e6])
+
+
+@pytest.mark.parametrize("wsel", ["0", "1"])
+def test_pipeline_second_chance(env, wsel, monkeypatch):
+    """A carried pre-threshold that misses (the gradient scale halves: too
+    few candidates; doubles: chunk segments overflow) is repaired by the
+    second chance -- a fresh sample and a recompaction of that block's
+    candidates -- not by the dense path; the result stays bit-exact."""
+    monkeypatch.setenv("SPARDL_WSEL", wsel)
+    c = _run(env, 8, 1, "none", "gres", "optimized", "gauss", 1_000_000, 10_000, iters=6,
+             seed=12, scales=[1.0, 1.0, 0.5, 2.0, 1.0, 0.7], audit=False)
+    assert c["retries"] >= 8, c
+    assert c["fallbacks"] == 0, c
 
 
 def test_pipeline_no_graph(env):
