@@ -194,6 +194,36 @@ __global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB)
   __shared__ float svl[kFinLists][kFinChunk];   // late mode: list li's value per entry
   __syncthreads();
   const int32_t jlo = gi[0], jhi = gi[nloc - 1];
+  // Late mode without the audit: the dividing-selection membership comes from
+  // joining the chunk with this worker's dividing selection of block b (the
+  // list the select wrote, exactly the entries the threshold test accepts)
+  // instead of reading the carry.  The carry is then touched only where the
+  // residual changes: a member is overwritten (its residual is its discards,
+  // no read), a non-member with discards is read, folded and written, a
+  // non-member without discards keeps its combined value (no access) -- most
+  // global entries come from other workers' selections.
+  const bool join_div = late && !t.aud_comb;
+  __shared__ unsigned char s_mem[kFinChunk];
+  __shared__ int s_drange[2];
+  if (join_div) {
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) s_mem[tid + q * kThreads] = 0;
+    const GatherSrc D = t.div[b];
+    if (tid < 64) {
+      const int dn = *D.cnt;
+      const bool upper = tid >= 32;
+      const int r = warp_bound(D.idx, dn, upper ? jhi : jlo, upper);
+      if ((tid & 31) == 0) s_drange[tid >> 5] = r;
+    }
+    __syncthreads();
+    const int r0 = s_drange[0], r1 = s_drange[1];
+    for (int p = r0 + tid; p < r1; p += kThreads) {
+      const int32_t x = D.idx[p];
+      const int ps = lower_bound_i32(gi, nloc, x);
+      if (ps < nloc && gi[ps] == x) s_mem[ps] = 1;
+    }
+    __syncthreads();
+  }
   for (int xb = x0; xb < x1; xb += kMaxXiLists) {
     const int nx = min(kMaxXiLists, x1 - xb);
     // the sub-range of each discard list inside [jlo, jhi], in parallel
@@ -261,7 +291,30 @@ __global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB)
       for (int q = 0; q < kFinPer; ++q) nd[q] = sf[tid + q * kThreads];
     }
   }
-  if (late) {   // read, fold and write back each entry's carry together
+  bool skip[kFinPer];
+#pragma unroll
+  for (int q = 0; q < kFinPer; ++q) skip[q] = false;
+  if (late && join_div) {   // the carry read only where it is kept and folded
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) {
+      const int e = tid + q * kThreads;
+      const bool mem = jj[q] != INT_MAX && s_mem[e];
+      skip[q] = !mem && nd[q] == 0;   // unchanged (or past the chunk)
+      x[q] = (jj[q] != INT_MAX && !mem && nd[q] != 0) ? carry[jj[q]] : 0.f;
+      present[q] = jj[q] != INT_MAX && !mem;
+    }
+#pragma unroll
+    for (int q = 0; q < kFinPer; ++q) {
+      const int e = tid + q * kThreads;
+      acc[q] = present[q] ? x[q] : 0.f;
+      for (int li = 0; li < x1 - x0; ++li)
+        if ((nd[q] >> li) & 1) {
+          const float v = svl[li][e];
+          acc[q] = present[q] ? __fadd_rn(acc[q], v) : v;
+          present[q] = true;
+        }
+    }
+  } else if (late) {   // read, fold and write back each entry's carry together
 #pragma unroll
     for (int q = 0; q < kFinPer; ++q) x[q] = jj[q] != INT_MAX ? carry[jj[q]] : 0.f;
 #pragma unroll
@@ -280,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB)
 #pragma unroll
   for (int q = 0; q < kFinPer; ++q) {
     const int e = tid + q * kThreads;
-    if (e < nloc) {
+    if (e < nloc && !skip[q]) {
       const float r = present[q] ? acc[q] : 0.f;
       SPARDL_BOUND(gi[e], t.n);
       carry[gi[e]] = r;

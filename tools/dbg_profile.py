@@ -3,7 +3,10 @@ import sys, ctypes as C, torch
 sys.path.insert(0, '.')
 import paper_2304_00737_b200 as sd
 from paper_2304_00737_b200._lib import lib
-P, N, k = 8, 25_600_000, 256_000
+import os
+P = 8
+N = int(os.environ.get('DBG_N', '25600000'))
+k = N // 100
 ctx = sd.SparDL(sd.ClusterConfig(workers=P, dimension=N, k=k), device=0, graph=(len(sys.argv) > 1 and sys.argv[1] == 'graph'))
 gen = torch.Generator(device='cuda')
 grads = []
