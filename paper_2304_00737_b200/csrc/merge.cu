@@ -96,8 +96,11 @@ constexpr int kMergeThreads = SPARDL_MERGE_THREADS;   // threads per partition C
 #ifndef SPARDL_MERGE_MINB
 #define SPARDL_MERGE_MINB 6   // 6 CTAs per SM (<= 42 registers): fewer waves for r >= 4
 #endif
-#ifndef SPARDL_MERGE_PATH_MINB   // merge-path variant (8: one wave for r = 2, but spills)
-#define SPARDL_MERGE_PATH_MINB 1
+#ifndef SPARDL_MERGE_PATH_MAXR   // widest merge folded by merge-path passes (else rank scatter)
+#define SPARDL_MERGE_PATH_MAXR 3
+#endif
+#ifndef SPARDL_MERGE_PATH_MINB   // merge-path variant (6: <= 42 registers, no spills; C4 SRS 0.773 -> 0.759 ms; 8 spills)
+#define SPARDL_MERGE_PATH_MINB 6
 #endif
 
 __device__ __forceinline__ void mstamp(const MergeTask& t, int q, int k) {
@@ -533,7 +536,7 @@ int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r
   // rank-scatter fallback 16 B per entry
   const size_t path_bytes = (size_t)max_r_T * 8 * (1 + std::min(std::max(max_r - 2, 0), 2));
   // (r >= 4: two intermediates cost more occupancy than the rank scatter)
-  const bool path = merge_path_on() && max_r <= 3 && path_bytes <= 200 * 1024;
+  const bool path = merge_path_on() && max_r <= SPARDL_MERGE_PATH_MAXR && path_bytes <= 200 * 1024;
   const size_t smem = path ? path_bytes : (size_t)max_r_T * 16;
   const bool one = max_parts <= kOneShotSamples && merge_one_shot();
   auto part = path ? k_merge_part<true> : k_merge_part<false>;

@@ -53,6 +53,13 @@ constexpr int kWarps = kSelThreads / 32;
 #endif
 constexpr int kIlp = SPARDL_SEL_ILP;   // 32-entry groups loaded per warp step (memory-level parallelism)
 constexpr int kChunkE = 32 * kIlp;   // flat entries per work chunk (one warp step)
+// wide clusters (>= 6 CTAs: the Spar-Reduce-Scatter / SAG batches of 8-16
+// selections of 2-4 L merged entries, mostly past the on-chip copy) keep
+// twice as many loads in flight per warp; measured on B200 at C4 (one GPU):
+// SRS 0.808 -> 0.773 ms, while the 2-wide dividing selects lose with 8
+#ifndef SPARDL_SEL_ILP_WIDE
+#define SPARDL_SEL_ILP_WIDE 8
+#endif
 
 __device__ __forceinline__ int resolve_mode(const SelTask& t) {
   if (!t.mode_from_cand) return t.mode;
@@ -334,6 +341,8 @@ __device__ long long merge_prologue(const MergeTask& mt, int cr, int32_t* w_idx,
 template <int CL, bool FUSED>
 __global__ void __launch_bounds__(kSelThreads, SPARDL_SEL_MINB)
     k_select(const SelTask* __restrict__ tasks, int tab_cap, int win_cap, int vcap) {
+  constexpr int kIlp = CL >= 6 ? SPARDL_SEL_ILP_WIDE : SPARDL_SEL_ILP;   // (shadows the default)
+  constexpr int kChunkE = 32 * kIlp;
   pdl_enter();
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank();
