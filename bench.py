@@ -141,7 +141,7 @@ def _sub_config(cfg, parts):
 def cpu_ref_leg(argv):
     """Child process (pinned with taskset -c 0): one iteration of the
     unmodified reference (oracle/_ref) on the FULL workload, fed the GPU run's
-    own first gradient set (fp32, widened to double inside the wrapper)."""
+    own gradient window of one step (fp32, widened to double inside the wrapper)."""
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import LIBS, Oracle, make_config
@@ -193,7 +193,7 @@ def cpu_baseline_full(cfg, grads_host, iters=1):
     return {"value": round(P * 4 * N / sec / 1e9, 5), "unit": "GB/s", "cores": 1, "kind": r["kind"],
             "ms_per_step": round(sec * 1e3, 1),
             "sample": f"the full workload (P={P}, N={N}, k={k}), {len(r['seconds'])} iteration(s) "
-                      f"of spardl_all_reduce incl. its audit on the GPU run's first gradient set, "
+                      f"of spardl_all_reduce incl. its audit on one step's gradient window of the GPU run, "
                       f"1 thread pinned with taskset -c 0 (cpus {r['affinity']})",
             "host": info}
 

@@ -97,11 +97,6 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
   constexpr int BPT = kSampBins / kThreads;
   __shared__ long long suf[kThreads];
   __shared__ long long lscr[32];
-  uint32_t* hist = t.samp_hist + threadIdx.x * BPT;
-  long long mine = 0;
-  for (int q = 0; q < BPT; ++q) mine += hist[q];
-  const long long ns = block_sum_ll(mine, lscr);
-  const int64_t nb = (int64_t)t.hi - t.lo;
   // the wide select's histogram window (wselect.cu): 2048 bins from the
   // pre-threshold up, together ~4x the expected distance to the threshold
   auto set_window = [&](uint32_t pre, uint32_t w) {
@@ -113,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
     }
   };
   if (t.use_cand && t.hist->valid) {   // threshold carried from the last iteration
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {           // (before touching the histogram: the common case)
       *t.cand_total = 0;
       *t.cand_bad = 0;
       *t.pre_key = t.hist->next_pre;
@@ -121,6 +116,11 @@ __global__ void __launch_bounds__(kThreads) k_div_prethr(const DivTask* __restri
     }
     return;   // the sample histogram was not touched: still zero
   }
+  uint32_t* hist = t.samp_hist + threadIdx.x * BPT;
+  long long mine = 0;
+  for (int q = 0; q < BPT; ++q) mine += hist[q];
+  const long long ns = block_sum_ll(mine, lscr);
+  const int64_t nb = (int64_t)t.hi - t.lo;
   if (threadIdx.x == 0) {
     *t.cand_total = 0;
     *t.cand_bad = t.use_cand ? 0 : 1;
