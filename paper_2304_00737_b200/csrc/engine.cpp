@@ -1305,11 +1305,12 @@ void Engine::plan_peer() {
 
 // ---------------------------------------------------------------------------
 // execution
-int Engine::exec_stage(const Stage& st, bool dividing) {
+int Engine::exec_stage(const Stage& st, bool dividing, cudaEvent_t after_merge) {
   int n = 0;
   if (!st.merges.empty() && !st.fused)
     n += sdl::launch_merge(st.merges_dev, static_cast<int>(st.merges.size()), st.max_parts,
                            st.max_rT, st.max_r, stream_);
+  if (after_merge) CK(cudaEventRecord(after_merge, stream_));
   // wide path first (with SPARDL_WSEL_FUSE=1 the dividing histogram and
   // decision come from the candidate pass); the cluster select then runs
   // only the tasks handed back
@@ -1389,20 +1390,21 @@ void Engine::enqueue_iteration(cudaEvent_t* ev) {
   }
   mark(3);
   // optional per-step events (profiling diagnostics, SPARDL_STEP_EVENTS=1)
+  const bool sev = ev && !step_ev_.empty();
   auto step_mark = [&](size_t i, int what) {
-    if (ev && !step_ev_.empty()) CK(cudaEventRecord(step_ev_[3 * i + what], stream_));
+    if (sev) CK(cudaEventRecord(step_ev_[4 * i + what], stream_));
   };
   for (size_t i = 0; i < steps_.size(); ++i) {
     const Step& s = steps_[i];
-    n += exec_stage(s.stage, false);
-    step_mark(i, 0);
+    n += exec_stage(s.stage, false, sev ? step_ev_[4 * i] : nullptr);
+    step_mark(i, 1);
     if (s.controller_after)
       n += sdl::launch_controller(ctl_tasks_dev_, static_cast<int>(ctl_tasks_.size()), 1, abort,
                                   stream_);
-    step_mark(i, 1);
+    step_mark(i, 2);
     if (i + 1 == steps_.size()) mark(4);
     exec_round(s.xfers);   // NCCL transport only: peers wait per task
-    step_mark(i, 2);
+    step_mark(i, 3);
   }
   if (steps_.empty()) mark(4);
   // the assembled global gradient and the ledger only read the gathered
@@ -1438,10 +1440,10 @@ void Engine::profile(const float* const* grads, int iters, double* phase_ms) {
   set_grads(grads);
   const char* se = std::getenv("SPARDL_STEP_EVENTS");
   if (se && se[0] == '1' && step_ev_.empty()) {
-    step_ev_.resize(3 * steps_.size());
+    step_ev_.resize(4 * steps_.size());
     for (auto& e : step_ev_) CK(cudaEventCreate(&e));
   }
-  std::vector<double> step_acc(3 * steps_.size(), 0.0);
+  std::vector<double> step_acc(4 * steps_.size(), 0.0);
   cudaEvent_t ev[6];
   for (auto& e : ev) CK(cudaEventCreate(&e));
   double acc[5] = {0, 0, 0, 0, 0};
@@ -1464,10 +1466,11 @@ void Engine::profile(const float* const* grads, int iters, double* phase_ms) {
     }
   }
   if (!step_ev_.empty()) {   // stage / publish / wait of every step, us
-    std::string line = "rank " + std::to_string(rank_) + " steps (stage, controller, round us):";
+    std::string line =
+        "rank " + std::to_string(rank_) + " steps (merge, select, controller, round us):";
     char buf[48];
     for (size_t q = 0; q < step_acc.size(); ++q) {
-      std::snprintf(buf, sizeof(buf), "%s%.1f", q % 3 == 0 ? " | " : " ",
+      std::snprintf(buf, sizeof(buf), "%s%.1f", q % 4 == 0 ? " | " : " ",
                     1e3 * step_acc[q] / std::max(iters, 1));
       line += buf;
     }

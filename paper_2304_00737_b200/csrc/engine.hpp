@@ -196,7 +196,7 @@ class Engine {
   bool is_local(int w) const { return w >= first_ && w < first_ + wloc_; }
   int rank_of(int w) const { return w / wloc_; }
   void exec_round(const std::vector<Xfer>& xs);
-  int exec_stage(const Stage& st, bool dividing);
+  int exec_stage(const Stage& st, bool dividing, cudaEvent_t after_merge = nullptr);
   void reset_wide(const Stage& st);
   cudaError_t mcpy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
     return dry_ ? cudaSuccess : cudaMemcpy(dst, src, bytes, kind);
