@@ -93,6 +93,7 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   if (const char* wn = std::getenv("SPARDL_WSEL_MINENTRIES")) wsel_min_entries_ = std::atoll(wn);
   if (const char* wm = std::getenv("SPARDL_WSEL_MAXTASKS")) wsel_max_tasks_ = std::atoi(wm);
   if (const char* wf = std::getenv("SPARDL_WSEL_FUSE")) wsel_fuse_ = wf[0] == '1';
+  if (const char* wc = std::getenv("SPARDL_WSEL_COOP")) wsel_coop_ = wc[0] != '0';
   if (cfg.sag == SPARDL_SAG_BSAG && d_ > sdl::kMaxR)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "bsag on the device supports d <= 16");
   wloc_ = P_ / world;
@@ -355,6 +356,7 @@ sdl::WScratch* Engine::make_wide(Stage& st, sdl::SelTask& t, const int32_t* idx,
   CK(mcpy(d, &w, sizeof(w), cudaMemcpyHostToDevice));
   t.ws = d;
   st.w_max_tiles = std::max(st.w_max_tiles, w.max_tiles);
+  st.w_max_nseg = std::max(st.w_max_nseg, nseg);
   st.w_max_entries = std::max<int64_t>(st.w_max_entries, typical);
   st.ws.push_back(d);
   return d;
@@ -556,6 +558,11 @@ void Engine::finish_stage(Stage& st) {
               st.w_max_entries >= wsel_min_entries_));
   if (!st.wide)
     for (auto& t : st.sels) t.ws = nullptr;   // (cluster selects only)
+  // the single-kernel form when every task's segment table and entries fit
+  // (the tiled form otherwise; producer-fused dividing histograms need it)
+  st.coop = st.wide && wsel_coop_ && !dry_ && st.w_max_nseg <= sdl::wsel_coop_max_seg() &&
+            !(&st == &div_stage_ && wsel_fuse_) &&
+            st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size()));
   if (!st.sels.empty())
     st.sels_dev =
         static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));
@@ -612,6 +619,11 @@ void Engine::reset_wide(const Stage& st) {
     // hist .. ntiles (the run state); the input descriptor and buffers stay
     const size_t a = offsetof(sdl::WScratch, hist), b = offsetof(sdl::WScratch, total);
     CK(cudaMemset(reinterpret_cast<unsigned char*>(w) + a, 0, b - a));
+    // the cooperative form's histograms, barrier and counts (in the bin buffer)
+    unsigned long long* bc = nullptr;
+    CK(mcpy(&bc, reinterpret_cast<unsigned char*>(w) + offsetof(sdl::WScratch, bin_c), sizeof(bc),
+            cudaMemcpyDeviceToHost));
+    if (bc) CK(cudaMemset(bc, 0, sizeof(uint32_t) * sdl::wsel_coop_words()));
   }
 }
 
@@ -1314,7 +1326,9 @@ int Engine::exec_stage(const Stage& st, bool dividing, cudaEvent_t after_merge) 
   // wide path first (with SPARDL_WSEL_FUSE=1 the dividing histogram and
   // decision come from the candidate pass); the cluster select then runs
   // only the tasks handed back
-  if (st.wide)
+  if (st.wide && st.coop)
+    n += sdl::launch_wselect_coop(st.sels_dev, static_cast<int>(st.sels.size()), stream_);
+  else if (st.wide)
     n += sdl::launch_wselect(st.sels_dev, static_cast<int>(st.sels.size()), st.w_max_tiles,
                              !(dividing && wsel_fuse_), stream_);
   if (!st.sels.empty())

@@ -81,6 +81,8 @@ struct Stage {           // one batch of merge + select tasks
   int w_max_tiles = 0;       // wide: largest tile count of a task
   int64_t w_max_entries = 0; // wide: largest input capacity of a task
   bool need_wide = false;    // a dividing block too large for the cluster select's work list
+  bool coop = false;         // wide: the single-kernel cooperative form (k_wsel_coop)
+  int w_max_nseg = 0;        // wide: most input segments of a task
   std::vector<sdl::WScratch*> ws;   // wide: per select task
 };
 
@@ -183,6 +185,7 @@ class Engine {
   int wsel_max_tasks_ = 12;            // stages of at most this many selections ...
   int64_t wsel_min_entries_ = 200000;  // ... with inputs of at least this many entries
   bool wsel_fuse_ = false;   // SPARDL_WSEL_FUSE=1: producers histogram for the wide select
+  bool wsel_coop_ = true;    // SPARDL_WSEL_COOP=0: the tiled wide select (three kernels)
   sdl::SelTask select_from_slot(const Slot& in);
   sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);
   void finish_stage(Stage& st);

@@ -34,6 +34,7 @@
 // threshold outside the dividing window, bin buffer overflow (massive key
 // ties) -- is marked kWFallback and k_select (launched right after) selects
 // it; every other task makes k_select return at once.
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 
@@ -569,7 +570,457 @@ __global__ void __launch_bounds__(kWThreads, 3) k_wsel_write(const SelTask* __re
   peer_publish(t.ps);   // (fences at system scope first)
 }
 
+// ---------------------------------------------------------------------------
+// Cooperative form: the whole select of a task in ONE kernel, G CTAs per task
+// (all co-resident: the grid never exceeds one wave), every CTA holding a
+// contiguous 1/G of the task's entries (index order) in shared memory.
+//   stage     the CTA's entries (4-byte cp.async, all in flight) into shared
+//             memory -- the only global read of the input
+//   3 levels  exact radix select of the magnitude key (11 / 11 / 9 bits):
+//             shared histogram of the entries inside the prefix, flushed to a
+//             per-task global histogram; task barrier; every CTA reads the
+//             global histogram and finds the digit holding the rank itself
+//   counts    #(key > T), #(key == T) per CTA; task barrier; every CTA takes
+//             the exclusive prefix over the lower CTAs: its output offsets
+//             and its share of the tie quota (ties go to the smaller index,
+//             i.e. the earlier CTA)
+//   write     ordered compaction from shared memory (warp ballots)
+// The last CTA (arrival counter) records the selection, writes the counts,
+// leaves the scratch zeroed and publishes.  Three kernel boundaries, the
+// serial finisher and two re-reads of the input of the tiled form go away.
+// A task whose entries do not fit (or a dividing select with incomplete
+// candidates) is handed to k_select (kWFallback), as in the tiled form.
+constexpr int kCoopThreads = 512;
+constexpr int kCoopWarps = kCoopThreads / 32;
+constexpr int kCoopMaxSeg = 4096;    // input segments per task (shared prefix table)
+constexpr int kCoopMaxG = 512;       // CTAs per task
+// coop scratch in the bin buffer (uint32 view): level-2 / level-3 histograms,
+// the task barrier, per-CTA counts
+constexpr int kCoopH2 = 0, kCoopH3 = 2048, kCoopBar = 2560, kCoopGt = 2564,
+              kCoopEq = kCoopGt + kCoopMaxG, kCoopWords = kCoopEq + kCoopMaxG;
+
+__device__ __forceinline__ uint32_t ld_acq_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// every CTA of the task: arrive, wait for all G (counter never reset mid-run)
+__device__ __forceinline__ void coop_barrier(uint32_t* ctr, uint32_t target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const unsigned long long t0 = gtime();
+    unsigned ns = 32;
+    while (ld_acq_u32(ctr) < target) {
+      __nanosleep(ns);
+      if (ns < 256) ns <<= 1;
+      if (gtime() - t0 > 5000000000ull) __trap();   // a CTA never became resident
+    }
+  }
+  __syncthreads();
+}
+
+// the digit of `nb` bins (descending) holding rank `rank` in the global
+// histogram gh; returns it, *above = entries in higher bins (same in every CTA)
+__device__ int coop_digit(const uint32_t* gh, int nb, long long rank, long long* above,
+                          int* scratch) {
+  __shared__ int s_d;
+  __shared__ long long s_ab;
+  const int per = nb / kCoopThreads;   // 4 (2048 bins) or 1 (512)
+  // thread i: bins nb-1-i*per .. nb-per-i*per (descending order = thread order)
+  uint32_t c[4];
+  int mine = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    c[u] = u < per ? __ldcg(gh + nb - 1 - ((int)threadIdx.x * per + u)) : 0u;
+    mine += (int)c[u];
+  }
+  int tot;
+  const int ex = block_exscan(mine, scratch, &tot);
+  if (ex < rank && rank <= (long long)ex + mine) {
+    long long cum = ex;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u < per) {
+        if (cum + c[u] >= rank) {
+          s_d = nb - 1 - ((int)threadIdx.x * per + u);
+          s_ab = cum;
+          break;
+        }
+        cum += c[u];
+      }
+  }
+  __syncthreads();
+  *above = s_ab;
+  const int d = s_d;
+  __syncthreads();
+  return d;
+}
+
+__global__ void __launch_bounds__(kCoopThreads, 1)
+    k_wsel_coop(const SelTask* __restrict__ tasks, int cap) {
+  pdl_enter();
+  const SelTask& t = tasks[blockIdx.y];
+  WScratch* __restrict__ ws = t.ws;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  int32_t* pre = reinterpret_cast<int32_t*>(dsm);               // [kCoopMaxSeg + 1]
+  int32_t* soff = pre + kCoopMaxSeg + 1;                        // [kCoopMaxSeg]
+  float* sv = reinterpret_cast<float*>(soff + kCoopMaxSeg);     // [cap]
+  int32_t* si = reinterpret_cast<int32_t*>(sv + cap);           // [cap]
+  __shared__ uint32_t h[kWBins];
+  __shared__ int scratch[40];
+  __shared__ int wcnt[3][kCoopWarps];
+  __shared__ int s_flag;
+  uint32_t* cs = reinterpret_cast<uint32_t*>(ws->bin_c);        // coop scratch
+  uint32_t* bar = cs + kCoopBar;
+  peer_wait(t.ps);
+  const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
+  // ---- the task's segments: offsets and the exclusive prefix of the counts
+  const int nseg = w_nseg(*ws);
+  int carry = 0;
+  for (int s0 = 0; s0 < nseg; s0 += kCoopThreads) {
+    const int s = s0 + tid;
+    int off = 0, cnt = 0;
+    if (s < nseg) w_seg(*ws, s, off, cnt);
+    int tt;
+    const int e = carry + block_exscan(cnt, scratch, &tt);
+    if (s < nseg) {
+      pre[s] = e;
+      soff[s] = off;
+    }
+    carry += tt;
+  }
+  if (tid == 0) pre[nseg] = carry;
+  __syncthreads();
+  const long long total = carry;
+  // run state (identical in every CTA)
+  int state;
+  bool bad = false;
+  if (ws->is_div) bad = (*t.cand_bad & 3) != 0 || total < budget;
+  if (bad) state = kWFallback;
+  else if (total <= budget) state = kWAll;
+  else if (budget <= 0) state = kWNone;
+  else state = (total + G - 1) / G > cap ? kWFallback : kWOk;
+  if (state == kWFallback) {   // k_select selects this task (no barrier was entered)
+    if (c == 0 && tid == 0) {
+      ws->state = kWFallback;
+      if (ws->handed_back) atomicAdd(ws->handed_back, 1ull);
+    }
+    return;
+  }
+  const int e0 = (int)(total * c / G), e1 = (int)(total * (c + 1) / G);
+  const int n = state == kWOk ? e1 - e0 : 0;
+  // ---- stage this CTA's entries (flat positions e0..e1, index order)
+  if (n > 0) {
+    for (int p0 = 0; p0 < n; p0 += kCoopThreads * 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = p0 + u * kCoopThreads + tid;
+        if (q < n) {
+          const int p = e0 + q;
+          int lo = 0, hi = nseg - 1;   // last segment with pre[s] <= p
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pre[mid] <= p) lo = mid;
+            else hi = mid - 1;
+          }
+          const int src = soff[lo] + (p - pre[lo]);
+          const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sv + q));
+          const unsigned si_a = static_cast<unsigned>(__cvta_generic_to_shared(si + q));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(ws->val + src)
+                       : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(si_a), "l"(ws->idx + src)
+                       : "memory");
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();
+  // ---- exact threshold: three radix levels over the global histograms
+  uint32_t T = 0;
+  long long need_eq = 0;
+  uint32_t nbar = 0;
+  if (state == kWOk) {
+    uint32_t prefix = 0, pmask = 0;
+    long long rank = budget;
+    for (int lvl = 0; lvl < 3; ++lvl) {
+      const int shift = lvl == 0 ? 20 : (lvl == 1 ? 9 : 0);
+      const int nb = lvl == 2 ? 512 : kWBins;
+      uint32_t* gh = lvl == 0 ? ws->hist : cs + (lvl == 1 ? kCoopH2 : kCoopH3);
+      for (int b = tid; b < nb; b += kCoopThreads) h[b] = 0;
+      __syncthreads();
+      for (int q = tid; q < n; q += kCoopThreads) {
+        const uint32_t key = mag_key(sv[q]);
+        if ((key & pmask) == prefix) atomicAdd(&h[(key >> shift) & (nb - 1)], 1u);
+      }
+      __syncthreads();
+      for (int b = tid; b < nb; b += kCoopThreads)
+        if (h[b]) atomicAdd(gh + b, h[b]);
+      coop_barrier(bar, (uint32_t)G * ++nbar);
+      long long above = 0;
+      const int d = coop_digit(gh, nb, rank, &above, scratch);
+      prefix |= (uint32_t)d << shift;
+      pmask |= (uint32_t)(nb - 1) << shift;
+      rank -= above;
+    }
+    T = prefix;
+    need_eq = rank;   // entries with key == T still to take (>= 1)
+  }
+  // ---- per-CTA counts -> offsets and tie quota
+  int gt = 0, eq = 0;
+  if (state == kWOk)
+    for (int q = tid; q < n; q += kCoopThreads) {
+      const uint32_t key = mag_key(sv[q]);
+      gt += key > T;
+      eq += key == T;
+    }
+  {
+    int tt;
+    block_exscan(gt, scratch, &tt);
+    gt = tt;
+    block_exscan(eq, scratch, &tt);
+    eq = tt;
+  }
+  long long base_gt = 0, base_eq = 0;
+  if (state == kWOk) {
+    if (tid == 0) {
+      cs[kCoopGt + c] = (uint32_t)gt;
+      cs[kCoopEq + c] = (uint32_t)eq;
+    }
+    coop_barrier(bar, (uint32_t)G * ++nbar);
+    long long a = 0, b = 0;
+    for (int q = tid; q < c; q += kCoopThreads) {
+      a += __ldcg(cs + kCoopGt + q);
+      b += __ldcg(cs + kCoopEq + q);
+    }
+    __shared__ long long lsh3[3 * 32];
+    long long z = 0;
+    block_sum3_ll(a, b, z, lsh3);
+    base_gt = a;
+    base_eq = b;
+  }
+  // ---- write: selected (and pushed) / discarded, in index order
+  const long long q_take = need_eq - base_eq;
+  const int take = state != kWOk ? 0 : (int)(q_take <= 0 ? 0 : (q_take >= eq ? eq : q_take));
+  const long long sel_before =
+      state == kWAll ? e0 : (state == kWOk ? base_gt + (base_eq < need_eq ? base_eq : need_eq) : 0);
+  // (kWAll / kWNone: every CTA sweeps its flat range straight from memory)
+  const int nn = state == kWOk ? n : e1 - e0;
+  int ks = (int)sel_before;
+  int kd = e0 - (int)sel_before;
+  int eqs = 0;   // ties of this CTA seen
+  int cutv = -1;
+  const uint32_t lt = lanemask_lt();
+  const int npush = t.npush;
+  const size_t push_voff = 16 + 4 * (size_t)t.push_cap;
+  const float w = t.weight;
+  for (int r0 = 0; r0 < nn; r0 += kCoopThreads * 4) {
+    float v[4];
+    int32_t ix[4];
+    bool val[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = r0 + warp * 128 + u * 32 + lane;   // warp-major: index order
+      val[u] = q < nn;
+      v[u] = 0.f;
+      ix[u] = 0;
+      if (val[u]) {
+        if (state == kWOk) {
+          v[u] = sv[q];
+          ix[u] = si[q];
+        } else {
+          const int p = e0 + q;
+          int lo = 0, hi = nseg - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pre[mid] <= p) lo = mid;
+            else hi = mid - 1;
+          }
+          const int src = soff[lo] + (p - pre[lo]);
+          v[u] = __ldcg(ws->val + src);
+          ix[u] = __ldcg(ws->idx + src);
+        }
+      }
+    }
+    // ties in order: warp tie counts -> CTA prefix
+    int we = 0;
+    uint32_t beq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      beq[u] = __ballot_sync(0xffffffffu, state == kWOk && val[u] && mag_key(v[u]) == T);
+      we += __popc(beq[u]);
+    }
+    if (lane == 0) wcnt[0][warp] = we;
+    __syncthreads();
+    int eb = eqs, etot = 0;
+    for (int u = 0; u < kCoopWarps; ++u) {
+      const int x = wcnt[0][u];
+      if (u < warp) eb += x;
+      etot += x;
+    }
+    bool sel[4];
+    int ws_ = 0, wd = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t key = mag_key(v[u]);
+      const bool is_eq = (beq[u] >> lane) & 1u;
+      const int er = eb + __popc(beq[u] & lt);
+      eb += __popc(beq[u]);
+      sel[u] = val[u] && (state == kWAll || (state == kWOk && (key > T || (is_eq && er < take))));
+      if (sel[u] && is_eq) cutv = max(cutv, ix[u]);
+      ws_ += __popc(__ballot_sync(0xffffffffu, sel[u]));
+      wd += __popc(__ballot_sync(0xffffffffu, val[u] && !sel[u]));
+    }
+    if (lane == 0) {
+      wcnt[1][warp] = ws_;
+      wcnt[2][warp] = wd;
+    }
+    __syncthreads();
+    int bs = ks, bd = kd, ts = 0, td = 0;
+    for (int u = 0; u < kCoopWarps; ++u) {
+      const int a0 = wcnt[1][u], a1 = wcnt[2][u];
+      if (u < warp) {
+        bs += a0;
+        bd += a1;
+      }
+      ts += a0;
+      td += a1;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t bk = __ballot_sync(0xffffffffu, sel[u]);
+      const uint32_t bdd = __ballot_sync(0xffffffffu, val[u] && !sel[u]);
+      if (sel[u]) {
+        const int p = bs + __popc(bk & lt);
+        SPARDL_BOUND_CAP(p, t.sel_cap);
+        t.sel_idx[p] = ix[u];
+        t.sel_val[p] = v[u];
+        if (npush > 0) SPARDL_BOUND_CAP(p, t.push_cap);
+        for (int pp = 0; pp < npush; ++pp) {
+          unsigned char* b = t.push_base[pp];
+          reinterpret_cast<int32_t*>(b + 16)[p] = ix[u];
+          reinterpret_cast<float*>(b + push_voff)[p] = v[u];
+        }
+      } else if (val[u] && t.dis_idx) {
+        const int p = bd + __popc(bdd & lt);
+        SPARDL_BOUND_CAP(p, t.dis_cap);
+        t.dis_idx[p] = ix[u];
+        t.dis_val[p] = __fmul_rn(v[u], w);
+      }
+      bs += __popc(bk);
+      bd += __popc(bdd);
+    }
+    ks += ts;
+    kd += td;
+    eqs += etot;
+    __syncthreads();   // wcnt reused
+  }
+  // the CTA holding the last tie taken knows the cut index (ties in index order)
+  cutv = __reduce_max_sync(0xffffffffu, cutv);
+  __shared__ int s_cut;
+  if (tid == 0) s_cut = -1;
+  __syncthreads();
+  if (lane == 0 && cutv >= 0) atomicMax(&s_cut, cutv);
+  __syncthreads();
+  if (tid == 0 && state == kWOk && base_eq < need_eq && need_eq <= base_eq + eq) ws->cut = s_cut;
+  // ---- completion: the last CTA records, counts, cleans up and publishes
+  __syncthreads();
+  if (tid == 0) {
+    if (npush > 0) __threadfence_system();
+    else __threadfence();
+    s_flag = (int)(atomicAdd(&ws->wdone, 1u) == (unsigned)G - 1);
+  }
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+  if (state == kWOk) {   // leave the histograms zeroed for the next run
+    for (int b = tid; b < kWBins; b += kCoopThreads) {
+      ws->hist[b] = 0;
+      cs[kCoopH2 + b] = 0;
+    }
+    for (int b = tid; b < 512; b += kCoopThreads) cs[kCoopH3 + b] = 0;
+  }
+  if (tid != 0) return;
+  const long long ns = state == kWAll ? total : (state == kWOk ? budget : 0);
+  const int32_t cut = state == kWOk ? __ldcg(&ws->cut) : -1;
+  *bar = 0;
+  ws->wdone = 0;
+  ws->state = state;
+  ws->T = T;
+  ws->total = total;
+  ws->total_sel = ns;
+  SelScratch* sc = t.scr;
+  const int all = state == kWAll ? 1 : (state == kWNone ? 2 : 0);
+  sc->mode = 0;
+  sc->total = total;
+  sc->prefix = state == kWOk ? T : 0;
+  sc->cut_idx = cut;
+  sc->all = all;
+  if (ws->is_div) {
+    if (all == 1) {
+      sc->all = 0;
+      sc->prefix = *t.pre_key_dev;
+      sc->cut_idx = INT_MAX;
+    }
+    if (t.div_hist)
+      update_history(t.div_hist, 0, all, state == kWOk ? T : 0u, *t.pre_key_dev, total, budget);
+  }
+  *t.sel_cnt = (int32_t)ns;
+  for (int p = 0; p < npush; ++p) *reinterpret_cast<int32_t*>(t.push_base[p]) = (int32_t)ns;
+  if (t.dis_cnt) *t.dis_cnt = (int32_t)(total - ns);
+  if (t.total_out) *t.total_out = total;
+  peer_publish(t.ps);   // (fences at system scope first)
+}
+
 }  // namespace
+
+int wsel_coop_words() { return kCoopWords; }
+int wsel_coop_max_seg() { return kCoopMaxSeg; }
+
+// CTAs of the cooperative select resident at once on this device, and the
+// entries one CTA can hold
+static void coop_geometry(int* resident, int* cap) {
+  static int res[kMaxDevices] = {}, cp[kMaxDevices] = {};
+  const int dev = cur_device();
+  if (!res[dev]) {
+    int optin = 0, sms = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_wsel_coop);
+    const int dyn = optin - (int)fa.sharedSizeBytes - 1024;
+    cudaFuncSetAttribute(k_wsel_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    const int table = (2 * kCoopMaxSeg + 1) * 4;
+    cp[dev] = std::max(0, (dyn - table) / 8) & ~31;
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wsel_coop, kCoopThreads, dyn);
+    res[dev] = std::max(1, sms * std::max(1, per));
+  }
+  *resident = res[dev];
+  *cap = cp[dev];
+}
+
+long long wsel_coop_capacity(int ntask) {
+  int resident = 0, cap = 0;
+  coop_geometry(&resident, &cap);
+  const int G = std::max(1, std::min(kCoopMaxG, resident / std::max(1, ntask)));
+  return (long long)G * cap;
+}
+
+int launch_wselect_coop(const SelTask* tasks_dev, int ntask, cudaStream_t s) {
+  if (ntask <= 0) return 0;
+  int resident = 0, cap = 0;
+  coop_geometry(&resident, &cap);
+  const int G = std::max(1, std::min(kCoopMaxG, resident / ntask));
+  const size_t smem = (size_t)(2 * kCoopMaxSeg + 1) * 4 + (size_t)cap * 8;
+  launch_pdl(k_wsel_coop, dim3(G, ntask), dim3(kCoopThreads), smem, s, tasks_dev, cap);
+  return 1;
+}
 
 int launch_wselect(const SelTask* tasks_dev, int ntask, int max_tiles, bool histogram,
                    cudaStream_t s) {
