@@ -714,28 +714,34 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
   }
   const int e0 = (int)(total * c / G), e1 = (int)(total * (c + 1) / G);
   const int n = state == kWOk ? e1 - e0 : 0;
-  // ---- stage this CTA's entries (flat positions e0..e1, index order)
+  // ---- stage this CTA's entries (flat positions e0..e1, index order): warp w
+  // walks its 1/16 of the range segment by segment (one search for the first)
   if (n > 0) {
-    for (int p0 = 0; p0 < n; p0 += kCoopThreads * 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int q = p0 + u * kCoopThreads + tid;
-        if (q < n) {
-          const int p = e0 + q;
-          int lo = 0, hi = nseg - 1;   // last segment with pre[s] <= p
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (pre[mid] <= p) lo = mid;
-            else hi = mid - 1;
-          }
-          const int src = soff[lo] + (p - pre[lo]);
+    const int a = (int)((long long)n * warp / kCoopWarps);
+    const int b = (int)((long long)n * (warp + 1) / kCoopWarps);
+    if (a < b) {
+      int p = e0 + a;
+      int lo = 0, hi = nseg - 1;   // last segment with pre[s] <= p
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (pre[mid] <= p) lo = mid;
+        else hi = mid - 1;
+      }
+      const float* __restrict__ gv = ws->val;
+      const int32_t* __restrict__ gi = ws->idx;
+      for (int sg = lo; p < e0 + b; ++sg) {
+        const int upto = min(pre[sg + 1], e0 + b);
+        const int base = soff[sg] - pre[sg];
+        for (int x = p + lane; x < upto; x += 32) {
+          const int q = x - e0;
           const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sv + q));
-          const unsigned si_a = static_cast<unsigned>(__cvta_generic_to_shared(si + q));
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(ws->val + src)
+          const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(si + q));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gv + base + x)
                        : "memory");
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(si_a), "l"(ws->idx + src)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sb), "l"(gi + base + x)
                        : "memory");
         }
+        p = max(p, upto);
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
