@@ -677,6 +677,14 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
   __shared__ int s_flag;
   uint32_t* cs = reinterpret_cast<uint32_t*>(ws->bin_c);        // coop scratch
   uint32_t* bar = cs + kCoopBar;
+  auto stamp = [&](int i) {   // phase timestamps of CTA 0 (-DSPARDL_STAMPS=1 builds)
+    if (SPARDL_STAMPS && c == 0 && tid == 0) {
+      long long ts;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+      t.scr->tstamp[i] = ts;
+    }
+  };
+  stamp(0);
   peer_wait(t.ps);
   const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
   // ---- the task's segments: offsets and the exclusive prefix of the counts
@@ -747,6 +755,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
     asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncthreads();
+  stamp(1);
   // ---- exact threshold: three radix levels over the global histograms
   uint32_t T = 0;
   long long need_eq = 0;
@@ -768,6 +777,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
       for (int b = tid; b < nb; b += kCoopThreads)
         if (h[b]) atomicAdd(gh + b, h[b]);
       coop_barrier(bar, (uint32_t)G * ++nbar);
+      stamp(2 + lvl);
       long long above = 0;
       const int d = coop_digit(gh, nb, rank, &above, scratch);
       prefix |= (uint32_t)d << shift;
@@ -799,6 +809,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
       cs[kCoopEq + c] = (uint32_t)eq;
     }
     coop_barrier(bar, (uint32_t)G * ++nbar);
+    stamp(5);
     long long a = 0, b = 0;
     for (int q = tid; q < c; q += kCoopThreads) {
       a += __ldcg(cs + kCoopGt + q);
@@ -926,6 +937,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
     eqs += etot;
     __syncthreads();   // wcnt reused
   }
+  stamp(6);
   // the CTA holding the last tie taken knows the cut index (ties in index order)
   cutv = __reduce_max_sync(0xffffffffu, cutv);
   __shared__ int s_cut;
@@ -944,6 +956,11 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
   __syncthreads();
   if (!s_flag) return;
   __threadfence();
+  if (SPARDL_STAMPS && tid == 0) {   // the last CTA's completion
+    long long ts;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+    t.scr->tstamp[7] = ts;
+  }
   if (state == kWOk) {   // leave the histograms zeroed for the next run
     for (int b = tid; b < kWBins; b += kCoopThreads) {
       ws->hist[b] = 0;
