@@ -915,13 +915,18 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
       if (sel[u]) {
         const int p = bs + __popc(bk & lt);
         SPARDL_BOUND_CAP(p, t.sel_cap);
-        t.sel_idx[p] = ix[u];
-        t.sel_val[p] = v[u];
-        if (npush > 0) SPARDL_BOUND_CAP(p, t.push_cap);
-        for (int pp = 0; pp < npush; ++pp) {
-          unsigned char* b = t.push_base[pp];
-          reinterpret_cast<int32_t*>(b + 16)[p] = ix[u];
-          reinterpret_cast<float*>(b + push_voff)[p] = v[u];
+        if (state == kWOk) {   // compacted in place (positions <= this round's), copied out below
+          si[p - (int)sel_before] = ix[u];
+          sv[p - (int)sel_before] = v[u];
+        } else {
+          t.sel_idx[p] = ix[u];
+          t.sel_val[p] = v[u];
+          if (npush > 0) SPARDL_BOUND_CAP(p, t.push_cap);
+          for (int pp = 0; pp < npush; ++pp) {
+            unsigned char* b = t.push_base[pp];
+            reinterpret_cast<int32_t*>(b + 16)[p] = ix[u];
+            reinterpret_cast<float*>(b + push_voff)[p] = v[u];
+          }
         }
       } else if (val[u] && t.dis_idx) {
         const int p = bd + __popc(bdd & lt);
@@ -936,6 +941,43 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
     kd += td;
     eqs += etot;
     __syncthreads();   // wcnt reused
+  }
+  // the CTA's selected entries (contiguous in the output from sel_before) to the
+  // block and every peer's copy: 16-byte stores from the compacted shared copy
+  // (a remote store per 4-byte entry and lane wasted most of the NVLink packet)
+  if (state == kWOk) {
+    __syncthreads();
+    const int ns = ks - (int)sel_before;
+    const int g0 = (int)sel_before;
+    const int head = min(ns, (4 - (g0 & 3)) & 3);
+    const int nbody = (ns - head) >> 2;
+    for (int d = 0; d <= npush; ++d) {
+      int32_t* di = d == 0 ? t.sel_idx : reinterpret_cast<int32_t*>(t.push_base[d - 1] + 16);
+      float* dv = d == 0 ? t.sel_val : reinterpret_cast<float*>(t.push_base[d - 1] + push_voff);
+      if (ns > 0) SPARDL_BOUND_CAP(g0 + ns - 1, d == 0 ? t.sel_cap : t.push_cap);
+      const bool vec = ((reinterpret_cast<uintptr_t>(di) | reinterpret_cast<uintptr_t>(dv)) & 15) == 0;
+      if (!vec) {   // (unaligned destination: plain stores)
+        for (int l = tid; l < ns; l += kCoopThreads) {
+          di[g0 + l] = si[l];
+          dv[g0 + l] = sv[l];
+        }
+        continue;
+      }
+      if (tid < head) {
+        di[g0 + tid] = si[tid];
+        dv[g0 + tid] = sv[tid];
+      }
+      for (int j = tid; j < nbody; j += kCoopThreads) {
+        const int l = head + 4 * j;
+        reinterpret_cast<int4*>(di + g0 + l)[0] = make_int4(si[l], si[l + 1], si[l + 2], si[l + 3]);
+        reinterpret_cast<float4*>(dv + g0 + l)[0] =
+            make_float4(sv[l], sv[l + 1], sv[l + 2], sv[l + 3]);
+      }
+      for (int l = head + 4 * nbody + tid; l < ns; l += kCoopThreads) {
+        di[g0 + l] = si[l];
+        dv[g0 + l] = sv[l];
+      }
+    }
   }
   stamp(6);
   // the CTA holding the last tie taken knows the cut index (ties in index order)
