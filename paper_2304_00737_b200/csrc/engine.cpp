@@ -352,6 +352,11 @@ sdl::WScratch* Engine::make_wide(Stage& st, sdl::SelTask& t, const int32_t* idx,
   w.tile_sel = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * nt));
   w.tile_sel_off = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * nt));
   w.tile_dis_off = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * nt));
+  // the cooperative form's overflow scratch (entries past the CTAs' shared
+  // copies, at their flat position): the task's input capacity
+  w.ov_cap = std::max<int64_t>(1, typical);
+  w.ov_val = static_cast<float*>(arena_.alloc(sizeof(float) * static_cast<size_t>(w.ov_cap)));
+  w.ov_idx = static_cast<int32_t*>(arena_.alloc(sizeof(int32_t) * static_cast<size_t>(w.ov_cap)));
   auto* d = static_cast<sdl::WScratch*>(arena_.alloc(sizeof(sdl::WScratch)));
   CK(mcpy(d, &w, sizeof(w), cudaMemcpyHostToDevice));
   t.ws = d;
@@ -560,9 +565,9 @@ void Engine::finish_stage(Stage& st) {
     for (auto& t : st.sels) t.ws = nullptr;   // (cluster selects only)
   // the single-kernel form when every task's segment table and entries fit
   // (the tiled form otherwise; producer-fused dividing histograms need it)
+  // (entries past the CTAs' shared copies go through the overflow scratch)
   st.coop = st.wide && wsel_coop_ && !dry_ && st.w_max_nseg <= sdl::wsel_coop_max_seg() &&
-            !(&st == &div_stage_ && wsel_fuse_) &&
-            st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size()));
+            !(&st == &div_stage_ && wsel_fuse_);
   if (!st.sels.empty())
     st.sels_dev =
         static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));

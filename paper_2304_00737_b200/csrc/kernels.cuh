@@ -243,6 +243,11 @@ struct WScratch {
   int32_t* tile_sel_off;
   int32_t* tile_dis_off;
   unsigned long long* handed_back;   // nullable: += 1 per run handed to k_select
+  // cooperative form: entries past a CTA's shared-memory copy live here, at
+  // their flat position in the task (nullable: such tasks are handed back)
+  float* ov_val;
+  int32_t* ov_idx;
+  long long ov_cap;
 };
 
 // value bits of a merge hole: its magnitude key is kHoleKey, never a real

@@ -712,7 +712,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
   if (bad) state = kWFallback;
   else if (total <= budget) state = kWAll;
   else if (budget <= 0) state = kWNone;
-  else state = (total + G - 1) / G > cap ? kWFallback : kWOk;
+  else state = ((total + G - 1) / G > cap && (!ws->ov_val || total > ws->ov_cap)) ? kWFallback
+                                                                                 : kWOk;
   if (state == kWFallback) {   // k_select selects this task (no barrier was entered)
     if (c == 0 && tid == 0) {
       ws->state = kWFallback;
@@ -722,6 +723,11 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
   }
   const int e0 = (int)(total * c / G), e1 = (int)(total * (c + 1) / G);
   const int n = state == kWOk ? e1 - e0 : 0;
+  // entry q of this CTA: shared memory below `cap`, the overflow scratch past it
+  float* __restrict__ ovv = ws->ov_val;
+  int32_t* __restrict__ ovi = ws->ov_idx;
+  auto getv = [&](int q) { return q < cap ? sv[q] : __ldcg(ovv + e0 + q); };
+  auto geti = [&](int q) { return q < cap ? si[q] : __ldcg(ovi + e0 + q); };
   // ---- stage this CTA's entries (flat positions e0..e1, index order): warp w
   // walks its 1/16 of the range segment by segment (one search for the first)
   if (n > 0) {
@@ -742,12 +748,17 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
         const int base = soff[sg] - pre[sg];
         for (int x = p + lane; x < upto; x += 32) {
           const int q = x - e0;
-          const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sv + q));
-          const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(si + q));
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gv + base + x)
-                       : "memory");
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sb), "l"(gi + base + x)
-                       : "memory");
+          if (q < cap) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sv + q));
+            const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(si + q));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gv + base + x)
+                         : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sb), "l"(gi + base + x)
+                         : "memory");
+          } else {   // past the shared copy: the contiguous overflow scratch
+            ovv[x] = __ldcg(gv + base + x);
+            ovi[x] = __ldcg(gi + base + x);
+          }
         }
         p = max(p, upto);
       }
@@ -769,9 +780,19 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
       uint32_t* gh = lvl == 0 ? ws->hist : cs + (lvl == 1 ? kCoopH2 : kCoopH3);
       for (int b = tid; b < nb; b += kCoopThreads) h[b] = 0;
       __syncthreads();
-      for (int q = tid; q < n; q += kCoopThreads) {
-        const uint32_t key = mag_key(sv[q]);
-        if ((key & pmask) == prefix) atomicAdd(&h[(key >> shift) & (nb - 1)], 1u);
+      for (int q0 = tid; q0 < n; q0 += 4 * kCoopThreads) {   // (4 loads in flight)
+        float v4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u * kCoopThreads;
+          v4[u] = q < n ? getv(q) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t key = mag_key(v4[u]);
+          if (q0 + u * kCoopThreads < n && (key & pmask) == prefix)
+            atomicAdd(&h[(key >> shift) & (nb - 1)], 1u);
+        }
       }
       __syncthreads();
       for (int b = tid; b < nb; b += kCoopThreads)
@@ -790,10 +811,20 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
   // ---- per-CTA counts -> offsets and tie quota
   int gt = 0, eq = 0;
   if (state == kWOk)
-    for (int q = tid; q < n; q += kCoopThreads) {
-      const uint32_t key = mag_key(sv[q]);
-      gt += key > T;
-      eq += key == T;
+    for (int q0 = tid; q0 < n; q0 += 4 * kCoopThreads) {
+      float v4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * kCoopThreads;
+        v4[u] = q < n ? getv(q) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t key = mag_key(v4[u]);
+        const bool in = q0 + u * kCoopThreads < n;
+        gt += in && key > T;
+        eq += in && key == T;
+      }
     }
   {
     int tt;
@@ -848,8 +879,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
       ix[u] = 0;
       if (val[u]) {
         if (state == kWOk) {
-          v[u] = sv[q];
-          ix[u] = si[q];
+          v[u] = getv(q);
+          ix[u] = geti(q);
         } else {
           const int p = e0 + q;
           int lo = 0, hi = nseg - 1;
@@ -916,8 +947,14 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
         const int p = bs + __popc(bk & lt);
         SPARDL_BOUND_CAP(p, t.sel_cap);
         if (state == kWOk) {   // compacted in place (positions <= this round's), copied out below
-          si[p - (int)sel_before] = ix[u];
-          sv[p - (int)sel_before] = v[u];
+          const int lp = p - (int)sel_before;
+          if (lp < cap) {
+            si[lp] = ix[u];
+            sv[lp] = v[u];
+          } else {
+            ovi[e0 + lp] = ix[u];
+            ovv[e0 + lp] = v[u];
+          }
         } else {
           t.sel_idx[p] = ix[u];
           t.sel_val[p] = v[u];
@@ -958,24 +995,25 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
       const bool vec = ((reinterpret_cast<uintptr_t>(di) | reinterpret_cast<uintptr_t>(dv)) & 15) == 0;
       if (!vec) {   // (unaligned destination: plain stores)
         for (int l = tid; l < ns; l += kCoopThreads) {
-          di[g0 + l] = si[l];
-          dv[g0 + l] = sv[l];
+          di[g0 + l] = geti(l);
+          dv[g0 + l] = getv(l);
         }
         continue;
       }
       if (tid < head) {
-        di[g0 + tid] = si[tid];
-        dv[g0 + tid] = sv[tid];
+        di[g0 + tid] = geti(tid);
+        dv[g0 + tid] = getv(tid);
       }
       for (int j = tid; j < nbody; j += kCoopThreads) {
         const int l = head + 4 * j;
-        reinterpret_cast<int4*>(di + g0 + l)[0] = make_int4(si[l], si[l + 1], si[l + 2], si[l + 3]);
+        reinterpret_cast<int4*>(di + g0 + l)[0] =
+            make_int4(geti(l), geti(l + 1), geti(l + 2), geti(l + 3));
         reinterpret_cast<float4*>(dv + g0 + l)[0] =
-            make_float4(sv[l], sv[l + 1], sv[l + 2], sv[l + 3]);
+            make_float4(getv(l), getv(l + 1), getv(l + 2), getv(l + 3));
       }
       for (int l = head + 4 * nbody + tid; l < ns; l += kCoopThreads) {
-        di[g0 + l] = si[l];
-        dv[g0 + l] = sv[l];
+        di[g0 + l] = geti(l);
+        dv[g0 + l] = getv(l);
       }
     }
   }
