@@ -94,6 +94,7 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   if (const char* wm = std::getenv("SPARDL_WSEL_MAXTASKS")) wsel_max_tasks_ = std::atoi(wm);
   if (const char* wf = std::getenv("SPARDL_WSEL_FUSE")) wsel_fuse_ = wf[0] == '1';
   if (const char* wc = std::getenv("SPARDL_WSEL_COOP")) wsel_coop_ = wc[0] != '0';
+  if (const char* wf2 = std::getenv("SPARDL_WSEL_FIT")) wsel_fit_ = std::atoi(wf2);
   if (cfg.sag == SPARDL_SAG_BSAG && d_ > sdl::kMaxR)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "bsag on the device supports d <= 16");
   wloc_ = P_ / world;
@@ -557,17 +558,24 @@ void Engine::finish_stage(Stage& st) {
   // (the cluster selects of 4-16 tasks already fill the GPU); C2's 64k-128k
   // entry selects favour the cluster select's single kernel (0.415 vs 0.507).
   // SPARDL_WSEL=1: every stage, =0: none.
+  const bool fits = wsel_fit_ && !dry_ &&
+                   st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size())) &&
+                   (wsel_fit_ == 2 || &st != &div_stage_);
   st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size() &&
-            (wsel_force_ || st.need_wide ||
+            (wsel_force_ || st.need_wide || fits ||
              (wloc_ == 1 && static_cast<int>(st.sels.size()) <= wsel_max_tasks_ &&
               st.w_max_entries >= wsel_min_entries_));
   if (!st.wide)
     for (auto& t : st.sels) t.ws = nullptr;   // (cluster selects only)
   // the single-kernel form when every task's segment table and entries fit
   // (the tiled form otherwise; producer-fused dividing histograms need it)
-  // (entries past the CTAs' shared copies go through the overflow scratch)
+  // (where a stage's typical entries fit the CTAs' shared copies: the
+  // overflow scratch is measured slower than the tiled form when it carries a
+  // large share -- C4 with 8 workers per GPU: SRS 0.955 vs 0.755 ms -- and
+  // only catches runs past the typical size)
   st.coop = st.wide && wsel_coop_ && !dry_ && st.w_max_nseg <= sdl::wsel_coop_max_seg() &&
-            !(&st == &div_stage_ && wsel_fuse_);
+            !(&st == &div_stage_ && wsel_fuse_) &&
+            st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size()));
   if (!st.sels.empty())
     st.sels_dev =
         static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));
