@@ -592,12 +592,13 @@ __global__ void __launch_bounds__(kWThreads, 3) k_wsel_write(const SelTask* __re
 // candidates) is handed to k_select (kWFallback), as in the tiled form.
 constexpr int kCoopThreads = 512;
 constexpr int kCoopWarps = kCoopThreads / 32;
-constexpr int kCoopMaxSeg = 4096;    // input segments per task (shared prefix table)
+constexpr int kCoopMaxSeg = 8192;    // input segments per task (shared prefix table)
 constexpr int kCoopMaxG = 512;       // CTAs per task
 // coop scratch in the bin buffer (uint32 view): level-2 / level-3 histograms,
 // the task barrier, per-CTA counts
 constexpr int kCoopH2 = 0, kCoopH3 = 2048, kCoopBar = 2560, kCoopGt = 2564,
-              kCoopEq = kCoopGt + kCoopMaxG, kCoopWords = kCoopEq + kCoopMaxG;
+              kCoopEq = kCoopGt + kCoopMaxG, kCoopH2g = kCoopEq + kCoopMaxG,
+              kCoopWords = kCoopH2g + 2048;
 
 __device__ __forceinline__ uint32_t ld_acq_u32(const uint32_t* p) {
   uint32_t v;
@@ -774,7 +775,57 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
   if (state == kWOk) {
     uint32_t prefix = 0, pmask = 0;
     long long rank = budget;
-    for (int lvl = 0; lvl < 3; ++lvl) {
+    // Level 1 together with a guessed level 2: the previous run's top digit
+    // d0 (the threshold moves little between iterations).  If level 1 finds
+    // d0 again, the level-2 histogram of the d0 entries is already complete
+    // and one level (a sweep and a task barrier) is skipped.
+    const uint32_t prevT = t.scr->prefix;
+    const bool guess = t.scr->all == 0 && prevT != 0;
+    const uint32_t d0 = prevT >> 20;
+    __shared__ uint32_t hg[kWBins];
+    for (int b = tid; b < kWBins; b += kCoopThreads) {
+      h[b] = 0;
+      hg[b] = 0;
+    }
+    __syncthreads();
+    for (int q0 = tid; q0 < n; q0 += 4 * kCoopThreads) {
+      float v4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * kCoopThreads;
+        v4[u] = q < n ? getv(q) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + u * kCoopThreads < n) {
+          const uint32_t key = mag_key(v4[u]);
+          atomicAdd(&h[key >> 20], 1u);
+          if (guess && (key >> 20) == d0) atomicAdd(&hg[(key >> 9) & (kWBins - 1)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int b = tid; b < kWBins; b += kCoopThreads) {
+      if (h[b]) atomicAdd(ws->hist + b, h[b]);
+      if (hg[b]) atomicAdd(cs + kCoopH2g + b, hg[b]);
+    }
+    coop_barrier(bar, (uint32_t)G * ++nbar);
+    stamp(2);
+    int lvl0 = 1;
+    {
+      long long above = 0;
+      const int d = coop_digit(ws->hist, kWBins, rank, &above, scratch);
+      prefix = (uint32_t)d << 20;
+      pmask = (uint32_t)(kWBins - 1) << 20;
+      rank -= above;
+      if (guess && (uint32_t)d == d0) {   // the guessed level-2 histogram holds the rank
+        const int d2 = coop_digit(cs + kCoopH2g, kWBins, rank, &above, scratch);
+        prefix |= (uint32_t)d2 << 9;
+        pmask |= (uint32_t)(kWBins - 1) << 9;
+        rank -= above;
+        lvl0 = 2;
+      }
+    }
+    for (int lvl = lvl0; lvl < 3; ++lvl) {
       const int shift = lvl == 0 ? 20 : (lvl == 1 ? 9 : 0);
       const int nb = lvl == 2 ? 512 : kWBins;
       uint32_t* gh = lvl == 0 ? ws->hist : cs + (lvl == 1 ? kCoopH2 : kCoopH3);
@@ -1045,6 +1096,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
     for (int b = tid; b < kWBins; b += kCoopThreads) {
       ws->hist[b] = 0;
       cs[kCoopH2 + b] = 0;
+      cs[kCoopH2g + b] = 0;
     }
     for (int b = tid; b < 512; b += kCoopThreads) cs[kCoopH3 + b] = 0;
   }
