@@ -358,7 +358,7 @@ __device__ __forceinline__ void merge_part_body(const MergeTask& t, int q) {
 // shared memory and takes its own splitters and windows -- the ranking that
 // k_merge_rank does once, repeated per CTA, instead of a kernel boundary and
 // two more dependent global round trips.
-constexpr int kOneShotSamples = 8 * kMergeThreads;   // (capacity; see launch_merge)
+constexpr int kOneShotSamples = 4 * kMergeThreads;
 
 template <bool PATH>
 __device__ __forceinline__ void merge_one_body(const MergeTask& t, int q) {
@@ -538,11 +538,7 @@ int launch_merge(const MergeTask* tasks_dev, int ntask, int max_parts, int max_r
   // (r >= 4: two intermediates cost more occupancy than the rank scatter)
   const bool path = merge_path_on() && max_r <= SPARDL_MERGE_PATH_MAXR && path_bytes <= 200 * 1024;
   const size_t smem = path ? path_bytes : (size_t)max_r_T * 16;
-  // one kernel while the per-CTA ranking stays cheap (<= 4 samples per
-  // thread), or up to 8 when the batch is one or two merges (one worker per
-  // GPU: the rank kernel's launch and round trip are the larger cost there)
-  const bool one = merge_one_shot() && (max_parts <= 4 * kMergeThreads ||
-                                        (ntask <= 2 && max_parts <= kOneShotSamples));
+  const bool one = max_parts <= kOneShotSamples && merge_one_shot();
   auto part = path ? k_merge_part<true> : k_merge_part<false>;
   auto single = path ? k_merge_one<true> : k_merge_one<false>;
   // (dynamic + static shared memory above 48 KB needs the opt-in)
