@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+bash tools/scripts/run_ab.sh "" "-DSPARDL_MERGE_MINB=8" "-DSPARDL_MERGE_PATH_MINB=8" "-DSPARDL_MERGE_MINB=8 -DSPARDL_MERGE_PATH_MINB=8"
+make -B -j16 -C paper_2304_00737_b200/csrc > /dev/null 2>&1
