@@ -93,7 +93,10 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
   if (const char* wn = std::getenv("SPARDL_WSEL_MINENTRIES")) wsel_min_entries_ = std::atoll(wn);
   if (const char* wm = std::getenv("SPARDL_WSEL_MAXTASKS")) wsel_max_tasks_ = std::atoi(wm);
   if (const char* wf = std::getenv("SPARDL_WSEL_FUSE")) wsel_fuse_ = wf[0] == '1';
-  if (const char* wc = std::getenv("SPARDL_WSEL_COOP")) wsel_coop_ = wc[0] != '0';
+  if (const char* wc = std::getenv("SPARDL_WSEL_COOP")) {
+    wsel_coop_ = wc[0] != '0';
+    wsel_coop_force_ = wc[0] == '2';   // (tests: also where the overflow scratch carries entries)
+  }
   if (const char* wf2 = std::getenv("SPARDL_WSEL_FIT")) wsel_fit_ = std::atoi(wf2);
   if (cfg.sag == SPARDL_SAG_BSAG && d_ > sdl::kMaxR)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "bsag on the device supports d <= 16");
@@ -575,7 +578,8 @@ void Engine::finish_stage(Stage& st) {
   // only catches runs past the typical size)
   st.coop = st.wide && wsel_coop_ && !dry_ && st.w_max_nseg <= sdl::wsel_coop_max_seg() &&
             !(&st == &div_stage_ && wsel_fuse_) &&
-            st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size()));
+            (wsel_coop_force_ ||
+             st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size())));
   if (!st.sels.empty())
     st.sels_dev =
         static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));

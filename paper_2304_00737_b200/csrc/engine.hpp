@@ -186,6 +186,7 @@ class Engine {
   int64_t wsel_min_entries_ = 200000;  // ... with inputs of at least this many entries
   bool wsel_fuse_ = false;   // SPARDL_WSEL_FUSE=1: producers histogram for the wide select
   bool wsel_coop_ = true;    // SPARDL_WSEL_COOP=0: the tiled wide select (three kernels)
+  bool wsel_coop_force_ = false;   // SPARDL_WSEL_COOP=2: cooperative even past the on-chip copies
   int wsel_fit_ = 0;         // SPARDL_WSEL_FIT=1: the cooperative select wherever a stage fits on chip (2: dividing too)
   sdl::SelTask select_from_slot(const Slot& in);
   sdl::SelTask select_from_merge(Stage& st, const std::vector<int>& pieces);

@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -1152,12 +1153,15 @@ static void coop_geometry(int* resident, int* cap) {
     cudaFuncSetAttribute(k_wsel_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     const int table = (2 * kCoopMaxSeg + 1) * 4;
     cp[dev] = std::max(0, (dyn - table) / 8) & ~31;
+
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wsel_coop, kCoopThreads, dyn);
     res[dev] = std::max(1, sms * std::max(1, per));
   }
   *resident = res[dev];
   *cap = cp[dev];
+  // tests: a smaller shared copy per CTA, so that the overflow scratch runs
+  if (const char* e = getenv("SPARDL_WSEL_COOP_CAP")) *cap = std::max(32, std::min(*cap, atoi(e)));
 }
 
 long long wsel_coop_capacity(int ntask) {

@@ -123,6 +123,21 @@ def test_pipeline_distribution_shift(env):
          scales=[1.0, 1e3, 1e-3, 1.0, 1e-6, 1e6])
 
 
+@pytest.mark.parametrize("P,d,sag,N,kind", [(8, 1, "none", 1_000_000, "gauss"),
+                                            (6, 3, "bsag", 300_007, "gauss"),
+                                            (8, 2, "rsag", 200_000, "int"),
+                                            (1, 1, "none", 2_000_000, "gauss")])
+def test_pipeline_coop_overflow(env, P, d, sag, N, kind, monkeypatch):
+    """The cooperative whole-GPU select with a 256-entry shared copy per CTA:
+    most entries go through the overflow scratch (staging, every radix level,
+    the counts, the in-place compaction and the copy-out), bit-exact."""
+    monkeypatch.setenv("SPARDL_WSEL", "1")
+    monkeypatch.setenv("SPARDL_WSEL_COOP", "2")
+    monkeypatch.setenv("SPARDL_WSEL_COOP_CAP", "256")
+    _run(env, P, d, sag, "gres", "optimized", kind, N, P * (N // (P * 100)), iters=3, seed=61,
+         audit=False)
+
+
 @pytest.mark.parametrize("wsel", ["0", "1"])
 def test_pipeline_second_chance(env, wsel, monkeypatch):
     """A carried pre-threshold that misses (the gradient scale halves: too
