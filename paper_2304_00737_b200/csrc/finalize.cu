@@ -205,10 +205,16 @@ __global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB)
   const bool join_div = late && !t.aud_comb;
   __shared__ unsigned char s_mem[kFinChunk];
   __shared__ int s_drange[2];
+  // with fewer discard lists than bound-search warp pairs, the dividing list's
+  // range is searched by a spare pair beside them (one dependent search phase
+  // less per CTA)
+  const bool d_fused = join_div && x1 > x0 && (x1 - x0) < kMaxXiLists;
+  const GatherSrc D = t.div[b];
   if (join_div) {
 #pragma unroll
     for (int q = 0; q < kFinPer; ++q) s_mem[tid + q * kThreads] = 0;
-    const GatherSrc D = t.div[b];
+  }
+  if (join_div && !d_fused) {
     if (tid < 64) {
       const int dn = *D.cnt;
       const bool upper = tid >= 32;
@@ -235,11 +241,23 @@ __global__ void __launch_bounds__(kThreads, SPARDL_FIN_MINB)
         const bool upper = warp & 1;
         const int r = warp_bound(X.idx, xn, upper ? jhi : jlo, upper);
         if ((tid & 31) == 0) range[warp] = r;
+      } else if (d_fused && xb == x0 && li == nx) {
+        const bool upper = warp & 1;
+        const int r = warp_bound(D.idx, *D.cnt, upper ? jhi : jlo, upper);
+        if ((tid & 31) == 0) s_drange[warp & 1] = r;
       }
     }
 #pragma unroll
     for (int q = 0; q < kFinPer; ++q) sf[tid + q * kThreads] = 0;
     __syncthreads();
+    if (d_fused && xb == x0) {   // the dividing list's entries in this chunk (s_mem only)
+      const int r0 = s_drange[0], r1 = s_drange[1];
+      for (int p = r0 + tid; p < r1; p += kThreads) {
+        const int32_t x = D.idx[p];
+        const int ps = lower_bound_i32(gi, nloc, x);
+        if (ps < nloc && gi[ps] == x) s_mem[ps] = 1;
+      }
+    }
     for (int li = 0; li < nx; ++li) {   // fold in recording order
       const XiList X = t.xi[xb + li];
       const int r0 = range[2 * li], r1 = range[2 * li + 1];

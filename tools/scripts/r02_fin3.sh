@@ -1,0 +1,10 @@
+#!/bin/bash
+mkdir -p gpurun_out
+make -j16 -C paper_2304_00737_b200/csrc > gpurun_out/fn3_build.log 2>&1 || { tail -20 gpurun_out/fn3_build.log; exit 1; }
+timeout 1200 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_scale.py -x -q -m gpu > gpurun_out/fn3_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/fn3_pytest.log
+for rep in 1 2; do
+for c in c4 c2; do
+  timeout 300 python bench.py --no-e2e --no-cpu --steps 50 --warmup 10 --config $c > gpurun_out/fn3_b.log 2>&1
+  echo "$c: $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/fn3_b.log) $(grep -o '"phases_ms": {[^}]*}' gpurun_out/fn3_b.log)"
+done
+done
