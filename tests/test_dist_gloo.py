@@ -8,10 +8,13 @@ rendezvous plumbing used by SparDL.from_process_group (broadcast of the
 128-byte NCCL id) delivers rank 0's bytes to every rank.
 """
 import ctypes as C
+import datetime
 import os
 import socket
 
 import pytest
+
+from spawn_util import init_failed, spawn_ranks
 import torch.multiprocessing as mp
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -32,7 +35,12 @@ def _worker(rank, world, port, cfgs, q):
     from paper_2304_00737_b200._lib import Config, lib
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world,
+                                timeout=datetime.timedelta(seconds=120))
+    except Exception as e:   # (a port taken meanwhile: the launcher retries)
+        init_failed(rank, q, e)
+        return
     try:
         L = lib()
         ok = True
@@ -77,13 +85,5 @@ def _worker(rank, world, port, cfgs, q):
 def test_two_rank_schedule_matches(built):
     world = 2
     cfgs = [(8, 1, 0), (6, 1, 0), (8, 2, 1), (8, 4, 2), (4, 2, 2)]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfgs, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = dict(q.get(timeout=240) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
+    res = spawn_ranks(world, lambda r, port, q: (r, world, port, cfgs, q), _worker, 240)
     assert res == {0: True, 1: True}

@@ -2,11 +2,14 @@
 path, trainer.hpp:180-302: every bucket's synchronised gradient must equal
 the fp32 oracle's global gradient of the ranks' bucket buffers, densified and
 divided by the world size, over several iterations (residual feedback)."""
+import datetime
 import os
 import socket
 
 import numpy as np
 import pytest
+
+from spawn_util import init_failed, spawn_ranks
 
 pytestmark = pytest.mark.gpu
 
@@ -32,7 +35,12 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                timeout=datetime.timedelta(seconds=120))
+    except Exception as e:   # (a port taken meanwhile: the launcher retries)
+        init_failed(rank, q, e)
+        return
     errors = []
     try:
         torch.manual_seed(0)
@@ -101,13 +109,5 @@ def test_ddp_comm_hook(built, world):
     import torch.multiprocessing as mp
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = dict(q.get(timeout=540) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-    assert all(not v for v in res.values()), res
+    res = spawn_ranks(world, lambda r, port, q: (r, world, port, q), _worker, 540)
+    assert len(res) == world and all(not v for v in res.values()), res

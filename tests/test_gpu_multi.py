@@ -6,11 +6,14 @@ own workers' residuals, the global gradient and the full ledger bit-exactly
 against the fp32 oracle.  Skipped with fewer than 2 GPUs (run under
 `gpurun --gpus 2` / `--gpus 4`).
 """
+import datetime
 import os
 import socket
 
 import numpy as np
 import pytest
+
+from spawn_util import init_failed, spawn_ranks
 
 pytestmark = pytest.mark.gpu
 
@@ -45,7 +48,12 @@ def _worker(rank, world, port, q, transport):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world,
+                                timeout=datetime.timedelta(seconds=120))
+    except Exception as e:   # (a port taken meanwhile: the launcher retries)
+        init_failed(rank, q, e)
+        return
     errors = []
     try:
         orc = Oracle("f32")
@@ -111,16 +119,8 @@ def test_multi_gpu_parity(built, world, transport):
     import torch.multiprocessing as mp
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, transport)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = dict(q.get(timeout=840) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-    assert all(not v for v in res.values()), res
+    res = spawn_ranks(world, lambda r, port, q: (r, world, port, q, transport), _worker, 840)
+    assert len(res) == world and all(not v for v in res.values()), res
 
 
 MCTX_CASES = [(4, 1, "none", "gres", "optimized"), (8, 2, "rsag", "gres", "optimized"),
@@ -186,7 +186,12 @@ def _timeout_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world,
+                                timeout=datetime.timedelta(seconds=120))
+    except Exception as e:   # (a port taken meanwhile: the launcher retries)
+        init_failed(rank, q, e)
+        return
     out = {}
     try:
         cfg = sd.ClusterConfig(workers=2, dimension=100_000, k=1000)
@@ -229,15 +234,8 @@ def test_peer_timeout_poisons_context(built):
     import torch.multiprocessing as mp
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_timeout_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = dict(q.get(timeout=240) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
+    res = spawn_ranks(2, lambda r, port, q: (r, 2, port, q), _timeout_worker, 240)
+    assert len(res) == 2 and all(isinstance(v, dict) for v in res.values()), res
     assert res[0].get("transport") == "peer", res
     assert res[0].get("timeout_reported") is True, res
     assert res[0].get("poisoned") is True, res

@@ -2,11 +2,14 @@
 against the oracle restatement of inc/collectives.hpp:185-216 (itself pinned
 to the reference in test_oracle_golden.py): merged union bit-exact, ledger
 equal."""
+import datetime
 import os
 import socket
 
 import numpy as np
 import pytest
+
+from spawn_util import init_failed, spawn_ranks
 
 from gpu_util import gen
 
@@ -49,7 +52,12 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                timeout=datetime.timedelta(seconds=120))
+    except Exception as e:   # (a port taken meanwhile: the launcher retries)
+        init_failed(rank, q, e)
+        return
     errors = []
     try:
         per, N, k = 2, 100_000, 1000
@@ -78,13 +86,5 @@ def test_topka_two_gpus(built):
     import torch.multiprocessing as mp
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = dict(q.get(timeout=280) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-    assert all(not v for v in res.values()), res
+    res = spawn_ranks(2, lambda r, port, q: (r, 2, port, q), _worker, 280)
+    assert len(res) == 2 and all(not v for v in res.values()), res
