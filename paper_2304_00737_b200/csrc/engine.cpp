@@ -97,6 +97,11 @@ Engine::Engine(const spardl_config& cfg, int device, int world, int rank, const 
     wsel_coop_ = wc[0] != '0';
     wsel_coop_force_ = wc[0] == '2';   // (tests: also where the overflow scratch carries entries)
   }
+  // the cooperative select wherever a stage fits on chip, with <= 4 workers
+  // per GPU (measured on B200, C4: 4 GPUs 1.212 -> 1.120 ms per step, 2 GPUs
+  // 1.936 -> 1.916; with 8 workers per GPU it does not pay, C2 SRS 0.236 ->
+  // 0.244 ms); SPARDL_WSEL_FIT=0/1/2 overrides
+  wsel_fit_ = (P_ / world) <= 4 ? 1 : 0;
   if (const char* wf2 = std::getenv("SPARDL_WSEL_FIT")) wsel_fit_ = std::atoi(wf2);
   if (cfg.sag == SPARDL_SAG_BSAG && d_ > sdl::kMaxR)
     sdlh::fail(SPARDL_E_UNSUPPORTED, "bsag on the device supports d <= 16");
