@@ -567,7 +567,7 @@ void Engine::finish_stage(Stage& st) {
   // entry selects favour the cluster select's single kernel (0.415 vs 0.507).
   // SPARDL_WSEL=1: every stage, =0: none.
   const bool fits = wsel_fit_ && !dry_ &&
-                   st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size())) &&
+                   st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size()), st.w_max_nseg) &&
                    (wsel_fit_ == 2 || &st != &div_stage_);
   st.wide = !st.fused && !st.sels.empty() && st.ws.size() == st.sels.size() &&
             (wsel_force_ || st.need_wide || fits ||
@@ -584,7 +584,7 @@ void Engine::finish_stage(Stage& st) {
   st.coop = st.wide && wsel_coop_ && !dry_ && st.w_max_nseg <= sdl::wsel_coop_max_seg() &&
             !(&st == &div_stage_ && wsel_fuse_) &&
             (wsel_coop_force_ ||
-             st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size())));
+             st.w_max_entries <= sdl::wsel_coop_capacity(static_cast<int>(st.sels.size()), st.w_max_nseg));
   if (!st.sels.empty())
     st.sels_dev =
         static_cast<sdl::SelTask*>(arena_.alloc(sizeof(sdl::SelTask) * st.sels.size()));
@@ -1349,7 +1349,8 @@ int Engine::exec_stage(const Stage& st, bool dividing, cudaEvent_t after_merge) 
   // decision come from the candidate pass); the cluster select then runs
   // only the tasks handed back
   if (st.wide && st.coop)
-    n += sdl::launch_wselect_coop(st.sels_dev, static_cast<int>(st.sels.size()), stream_);
+    n += sdl::launch_wselect_coop(st.sels_dev, static_cast<int>(st.sels.size()), st.w_max_nseg,
+                                  stream_);
   else if (st.wide)
     n += sdl::launch_wselect(st.sels_dev, static_cast<int>(st.sels.size()), st.w_max_tiles,
                              !(dividing && wsel_fuse_), stream_);

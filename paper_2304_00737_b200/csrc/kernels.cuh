@@ -364,10 +364,10 @@ int launch_select(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_
 // finisher, write; then launch_select for the tasks handed back
 // the single-kernel cooperative form of the wide select (one wave of CTAs,
 // task barriers in global memory); tasks that do not fit are handed back
-int launch_wselect_coop(const SelTask* tasks_dev, int ntask, cudaStream_t s);
+int launch_wselect_coop(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s);
 int wsel_coop_words();               // uint32 words of its scratch (in the bin buffer)
 int wsel_coop_max_seg();             // most input segments of a task
-long long wsel_coop_capacity(int ntask);   // entries per task that fit on this device
+long long wsel_coop_capacity(int ntask, int max_nseg);   // entries per task that fit on this device
 int launch_wselect(const SelTask* tasks_dev, int ntask, int max_tiles, bool histogram,
                    cudaStream_t s);
 // fused merge+select: smem window capacity (entries) available per CTA, and

@@ -662,16 +662,17 @@ __device__ int coop_digit(const uint32_t* gh, int nb, long long rank, long long*
 }
 
 __global__ void __launch_bounds__(kCoopThreads, 1)
-    k_wsel_coop(const SelTask* __restrict__ tasks, int cap) {
+    k_wsel_coop(const SelTask* __restrict__ tasks, int cap, int tabn) {
   pdl_enter();
   const SelTask& t = tasks[blockIdx.y];
   WScratch* __restrict__ ws = t.ws;
   const int G = gridDim.x, c = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   extern __shared__ __align__(16) unsigned char dsm[];
-  int32_t* pre = reinterpret_cast<int32_t*>(dsm);               // [kCoopMaxSeg + 1]
-  int32_t* soff = pre + kCoopMaxSeg + 1;                        // [kCoopMaxSeg]
-  float* sv = reinterpret_cast<float*>(soff + kCoopMaxSeg);     // [cap]
+  // segment table sized for this launch's tasks (tabn >= every task's segments)
+  int32_t* pre = reinterpret_cast<int32_t*>(dsm);               // [tabn + 1]
+  int32_t* soff = pre + tabn + 1;                               // [tabn]
+  float* sv = reinterpret_cast<float*>(soff + tabn + ((tabn + 1) & 1) + 2);   // [cap], 16 B aligned
   int32_t* si = reinterpret_cast<int32_t*>(sv + cap);           // [cap]
   __shared__ uint32_t h[kWBins];
   __shared__ int scratch[40];
@@ -690,7 +691,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1)
   peer_wait(t.ps);
   const int64_t budget = t.budget_dev ? *t.budget_dev : t.budget;
   // ---- the task's segments: offsets and the exclusive prefix of the counts
-  const int nseg = w_nseg(*ws);
+  const int nseg = min(w_nseg(*ws), tabn);   // (the planner sized tabn for every task)
   int carry = 0;
   for (int s0 = 0; s0 < nseg; s0 += kCoopThreads) {
     const int s = s0 + tid;
@@ -1140,7 +1141,9 @@ int wsel_coop_max_seg() { return kCoopMaxSeg; }
 
 // CTAs of the cooperative select resident at once on this device, and the
 // entries one CTA can hold
-static void coop_geometry(int* resident, int* cap) {
+static int coop_table_bytes(int tabn) { return (2 * tabn + 4) * 4; }
+
+static void coop_geometry(int* resident, int* cap, int tabn = kCoopMaxSeg) {
   static int res[kMaxDevices] = {}, cp[kMaxDevices] = {};
   const int dev = cur_device();
   if (!res[dev]) {
@@ -1151,33 +1154,33 @@ static void coop_geometry(int* resident, int* cap) {
     cudaFuncGetAttributes(&fa, k_wsel_coop);
     const int dyn = optin - (int)fa.sharedSizeBytes - 1024;
     cudaFuncSetAttribute(k_wsel_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-    const int table = (2 * kCoopMaxSeg + 1) * 4;
-    cp[dev] = std::max(0, (dyn - table) / 8) & ~31;
+    cp[dev] = dyn;   // (dynamic shared memory; the entries follow from the table size)
 
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wsel_coop, kCoopThreads, dyn);
     res[dev] = std::max(1, sms * std::max(1, per));
   }
   *resident = res[dev];
-  *cap = cp[dev];
+  *cap = std::max(0, (cp[dev] - coop_table_bytes(tabn)) / 8) & ~31;
   // tests: a smaller shared copy per CTA, so that the overflow scratch runs
   if (const char* e = getenv("SPARDL_WSEL_COOP_CAP")) *cap = std::max(32, std::min(*cap, atoi(e)));
 }
 
-long long wsel_coop_capacity(int ntask) {
+long long wsel_coop_capacity(int ntask, int max_nseg) {
   int resident = 0, cap = 0;
-  coop_geometry(&resident, &cap);
+  coop_geometry(&resident, &cap, std::max(1, max_nseg));
   const int G = std::max(1, std::min(kCoopMaxG, resident / std::max(1, ntask)));
   return (long long)G * cap;
 }
 
-int launch_wselect_coop(const SelTask* tasks_dev, int ntask, cudaStream_t s) {
+int launch_wselect_coop(const SelTask* tasks_dev, int ntask, int max_nseg, cudaStream_t s) {
   if (ntask <= 0) return 0;
+  const int tabn = std::max(1, std::min(max_nseg, kCoopMaxSeg));
   int resident = 0, cap = 0;
-  coop_geometry(&resident, &cap);
+  coop_geometry(&resident, &cap, tabn);
   const int G = std::max(1, std::min(kCoopMaxG, resident / ntask));
-  const size_t smem = (size_t)(2 * kCoopMaxSeg + 1) * 4 + (size_t)cap * 8;
-  launch_pdl(k_wsel_coop, dim3(G, ntask), dim3(kCoopThreads), smem, s, tasks_dev, cap);
+  const size_t smem = (size_t)coop_table_bytes(tabn) + (size_t)cap * 8;
+  launch_pdl(k_wsel_coop, dim3(G, ntask), dim3(kCoopThreads), smem, s, tasks_dev, cap, tabn);
   return 1;
 }
 
